@@ -1,0 +1,308 @@
+"""ctypes bindings for the CPU oracle -- TEST INFRASTRUCTURE ONLY.
+
+Who may import this package: ``tests/``, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py``, only as the
+checker or the timed CPU baseline.  The product package
+``paper_1609_01882_b200`` never imports it.
+
+Two libraries:
+
+* ``oracle/build/libpolyoracle.so`` -- our C restatement (``polyoracle.c``),
+  each function citing the reference file:line it restates.
+* ``oracle/_ref/libpolyref.so`` -- the reference's own C++ sources compiled in
+  place by ``oracle/Makefile`` plus ``ref_driver.cpp`` (C ABI glue).  Used to
+  generate the golden fixtures that pin the restatement, and as the
+  ``--impl reference`` CPU baseline.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "build", "libpolyoracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libpolyref.so")
+
+STRATEGIES = {"adc": 0, "binary": 1, "disidx": 2, "dual": 3}
+
+_P = C.c_void_p
+_u32, _u64, _i32, _f64 = C.c_uint32, C.c_uint64, C.c_int, C.c_double
+
+
+def build() -> None:
+    """Compile the restatement (and the reference when /root/reference exists)."""
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(_P)
+
+
+_lib = None
+_ref = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(ORACLE_SO):
+            build()
+        L = C.CDLL(ORACLE_SO)
+        L.po_gen_centers.argtypes = [_u64, _u32, _u32, _P]
+        L.po_gen_points.argtypes = [_u64, _u32, _u64, _u64, _P, _u32, _u32, _i32, _P]
+        L.po_hash64.argtypes = [_u64]
+        L.po_hash64.restype = _u64
+        L.po_sq_l2.argtypes = [_P, _P, C.c_size_t]
+        L.po_sq_l2.restype = C.c_float
+        L.po_hamming_bytes.argtypes = [_P, _P, C.c_size_t]
+        L.po_hamming_bytes.restype = _u32
+        L.po_disidx.argtypes = [_P, _P, _u32, _u32]
+        L.po_disidx.restype = _u32
+        L.po_topk_select.argtypes = [_P, _P, _u64, _u32, _P, _P]
+        L.po_topk_select.restype = _u32
+        L.po_search_batch.argtypes = [_u32, _u32, _u32, _P, _P, _P, _P, _P, _u64, _P, _u64, _i32, _u32, _u32,
+                                      C.c_uint, _P, _P, _P, _P, _P]
+        L.po_search_batch.restype = _i32
+        L.po_encode_batch.argtypes = [_u32, _u32, _u32, _P, _P, _P, _u64, _P, C.c_uint]
+        L.po_lut_batch.argtypes = [_u32, _u32, _u32, _P, _P, _P, _P, _u64, _P, _P, _P]
+        L.po_hamming_histogram.argtypes = [_u32, _u32, _u32, _P, _P, _P, _u64, _P, _u64, C.c_uint, _P]
+        L.po_calibrate_from_histogram.argtypes = [_P, _u64, _u32, _u64, _f64, C.POINTER(_i32)]
+        L.po_calibrate_from_histogram.restype = _u32
+        L.po_relabel_codes.argtypes = [_u32, _u32, _P, _P, _P, _u64]
+        _lib = L
+    return _lib
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def ref():
+    global _ref
+    if _ref is None:
+        if not ref_available():
+            raise FileNotFoundError(f"{REF_SO} not built (needs /root/reference; run make -C oracle)")
+        L = C.CDLL(REF_SO)
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_train_pq.argtypes = [_P, _u64, _u64, _u32, _u32, _u32, _u64, C.c_uint, _P]
+        L.ref_optimize_pq.argtypes = [_u32, _u32, _u64, _P, _i32, _f64, _u64, _u64, C.c_uint, _P]
+        L.ref_encode.argtypes = [_u32, _u32, _u64, _P, _P, _P, _u64, _P]
+        L.ref_encode_batch.argtypes = [_u32, _u32, _u64, _P, _P, _P, _u64, _P, C.c_uint]
+        L.ref_compute_lut.argtypes = [_u32, _u32, _u64, _P, _P, _P, _u64, _P, _P]
+        L.ref_adc_matrix.argtypes = [_u32, _u32, _u64, _P, _P, _P, _u64, _P, _u64, _P]
+        L.ref_hamming_matrix.argtypes = [_P, _u64, _P, _u64, _u64, _P]
+        L.ref_hamming_matrix.restype = None
+        L.ref_search_batch.argtypes = [_u32, _u32, _u64, _P, _P, _P, _P, _u64, _P, _u64, _i32, _u32, _u32, C.c_uint,
+                                       _P, _P, _P, _P]
+        L.ref_buggy_topk.argtypes = [_P, _P, _u64, _u32, _P, _P]
+        L.ref_buggy_topk.restype = _u32
+        _ref = L
+    return _ref
+
+
+def _check_ref(rc):
+    if rc != 0:
+        raise RuntimeError(f"reference error {rc}: {ref().ref_last_error().decode()}")
+
+
+# --------------------------------------------------------------------------- PQ container
+class PQ:
+    """Codebooks + assignments, mirroring poly::ProductQuantizer (pq.hpp:49-89)."""
+
+    def __init__(self, m, dbits, dim, codebooks, perms):
+        self.m, self.dbits, self.dim = int(m), int(dbits), int(dim)
+        ks = 1 << self.dbits
+        self.codebooks = np.ascontiguousarray(codebooks, dtype=np.float32).reshape(self.m, ks, self.dim // self.m)
+        self.perms = np.ascontiguousarray(perms, dtype=np.uint16).reshape(self.m, ks)
+        inv = np.empty_like(self.perms)
+        for sq in range(self.m):
+            inv[sq, self.perms[sq]] = np.arange(ks, dtype=np.uint16)
+        self.inv_perms = inv
+
+    @property
+    def code_bits(self):
+        return self.m * self.dbits
+
+    @property
+    def code_bytes(self):
+        return (self.code_bits + 7) // 8
+
+    def args(self):
+        return (self.m, self.dbits, self.dim, _ptr(self.codebooks), _ptr(self.perms))
+
+
+# --------------------------------------------------------------------------- generator
+def gen_centers(seed, ncent, dim):
+    out = np.empty((ncent, dim), np.float32)
+    lib().po_gen_centers(seed, ncent, dim, _ptr(out))
+    return out
+
+
+def gen_points(seed, stream, row0, n, centers, normalize=False):
+    centers = np.ascontiguousarray(centers, np.float32)
+    ncent, dim = centers.shape
+    out = np.empty((n, dim), np.float32)
+    lib().po_gen_points(seed, stream, row0, n, _ptr(centers), ncent, dim, int(normalize), _ptr(out))
+    return out
+
+
+# --------------------------------------------------------------------------- restatement
+def encode(pq: PQ, x, threads=8):
+    x = np.ascontiguousarray(x, np.float32)
+    codes = np.empty((x.shape[0], pq.code_bytes), np.uint8)
+    lib().po_encode_batch(*pq.args(), _ptr(x), x.shape[0], _ptr(codes), threads)
+    return codes
+
+
+def lut_batch(pq: PQ, q):
+    q = np.ascontiguousarray(q, np.float32)
+    nq = q.shape[0]
+    ks = 1 << pq.dbits
+    lut = np.empty((nq, pq.m, ks), np.float32)
+    lutp = np.empty((nq, pq.m, ks), np.float32)
+    qc = np.empty((nq, pq.code_bytes), np.uint8)
+    lib().po_lut_batch(*pq.args(), _ptr(pq.inv_perms), _ptr(q), nq, _ptr(lut), _ptr(lutp), _ptr(qc))
+    return lut, lutp, qc
+
+
+def search(pq: PQ, codes, queries, k, tau=None, strategy="dual", ids=None, threads=8):
+    """Two-pass dual search.  Returns ids, scores, counts, survivors, survivor_hash."""
+    codes = np.ascontiguousarray(codes, np.uint8)
+    queries = np.ascontiguousarray(queries, np.float32)
+    n, nq = codes.shape[0], queries.shape[0]
+    if ids is None:
+        ids = np.arange(n, dtype=np.int64)
+    ids = np.ascontiguousarray(ids, np.int64)
+    tau = pq.code_bits if tau is None else tau
+    oi = np.empty((nq, k), np.int64)
+    osc = np.empty((nq, k), np.float32)
+    oc = np.empty(nq, np.uint32)
+    sv = np.empty(nq, np.uint64)
+    sh = np.empty(nq, np.uint64)
+    rc = lib().po_search_batch(*pq.args(), _ptr(pq.inv_perms), _ptr(codes), _ptr(ids), n, _ptr(queries), nq,
+                               STRATEGIES[strategy], k, tau, threads, _ptr(oi), _ptr(osc), _ptr(oc), _ptr(sv), _ptr(sh))
+    if rc != 0:
+        raise ValueError(f"oracle search rejected arguments (rc={rc})")
+    return oi, osc, oc, sv, sh
+
+
+def topk_select(scores, ids, k):
+    scores = np.ascontiguousarray(scores, np.float32)
+    ids = np.ascontiguousarray(ids, np.int64)
+    oi = np.empty(max(k, 1), np.int64)
+    osc = np.empty(max(k, 1), np.float32)
+    n = lib().po_topk_select(_ptr(scores), _ptr(ids), scores.shape[0], k, _ptr(oi), _ptr(osc))
+    return oi[:n], osc[:n]
+
+
+def hamming_histogram(pq: PQ, codes, queries, threads=8):
+    codes = np.ascontiguousarray(codes, np.uint8)
+    queries = np.ascontiguousarray(queries, np.float32)
+    hist = np.empty((queries.shape[0], pq.code_bits + 1), np.uint64)
+    lib().po_hamming_histogram(*pq.args(), _ptr(codes), codes.shape[0], _ptr(queries), queries.shape[0], threads,
+                               _ptr(hist))
+    return hist
+
+
+def calibrate_threshold(pq: PQ, codes, train_queries, rate, threads=8):
+    hist = hamming_histogram(pq, codes, train_queries, threads)
+    w = _i32(0)
+    tau = lib().po_calibrate_from_histogram(_ptr(hist), hist.shape[0], pq.code_bits, codes.shape[0], rate,
+                                            C.byref(w))
+    return int(tau), bool(w.value)
+
+
+def relabel_codes(pq_old: PQ, new_perms, codes):
+    out = np.array(codes, np.uint8, copy=True)
+    new_perms = np.ascontiguousarray(new_perms, np.uint16)
+    lib().po_relabel_codes(pq_old.m, pq_old.dbits, _ptr(pq_old.inv_perms), _ptr(new_perms), _ptr(out), out.shape[0])
+    return out
+
+
+def hamming(a, b):
+    a = np.ascontiguousarray(a, np.uint8)
+    b = np.ascontiguousarray(b, np.uint8)
+    return int(lib().po_hamming_bytes(_ptr(a), _ptr(b), a.shape[-1]))
+
+
+# --------------------------------------------------------------------------- reference
+def ref_train_pq(train, m, dbits=8, iters=25, seed=1234567, threads=0):
+    train = np.ascontiguousarray(train, np.float32)
+    n, dim = train.shape
+    cb = np.empty((m, 1 << dbits, dim // m), np.float32)
+    _check_ref(ref().ref_train_pq(_ptr(train), n, dim, m, dbits, iters, seed, threads, _ptr(cb)))
+    return cb
+
+
+def ref_optimize_pq(codebooks, dim, dbits=8, loss=0, alpha=0.5, n_iter=500000, seed=1234567, threads=0):
+    codebooks = np.ascontiguousarray(codebooks, np.float32)
+    m = codebooks.shape[0]
+    perms = np.empty((m, 1 << dbits), np.uint16)
+    _check_ref(ref().ref_optimize_pq(m, dbits, dim, _ptr(codebooks), loss, alpha, n_iter, seed, threads, _ptr(perms)))
+    return perms
+
+
+def ref_encode(pq: PQ, x):
+    x = np.ascontiguousarray(x, np.float32)
+    codes = np.empty((x.shape[0], pq.code_bytes), np.uint8)
+    _check_ref(ref().ref_encode(*pq.args(), _ptr(x), x.shape[0], _ptr(codes)))
+    return codes
+
+
+def ref_encode_batch(pq: PQ, x, threads=0):
+    x = np.ascontiguousarray(x, np.float32)
+    codes = np.empty((x.shape[0], pq.code_bytes), np.uint8)
+    _check_ref(ref().ref_encode_batch(*pq.args(), _ptr(x), x.shape[0], _ptr(codes), threads))
+    return codes
+
+
+def ref_compute_lut(pq: PQ, q):
+    q = np.ascontiguousarray(q, np.float32)
+    nq = q.shape[0]
+    lut = np.empty((nq, pq.m, 1 << pq.dbits), np.float32)
+    lutp = np.empty_like(lut)
+    _check_ref(ref().ref_compute_lut(*pq.args(), _ptr(q), nq, _ptr(lut), _ptr(lutp)))
+    return lut, lutp
+
+
+def ref_adc_matrix(pq: PQ, q, codes):
+    q = np.ascontiguousarray(q, np.float32)
+    codes = np.ascontiguousarray(codes, np.uint8)
+    out = np.empty((q.shape[0], codes.shape[0]), np.float32)
+    _check_ref(ref().ref_adc_matrix(*pq.args(), _ptr(q), q.shape[0], _ptr(codes), codes.shape[0], _ptr(out)))
+    return out
+
+
+def ref_hamming_matrix(a, b):
+    a = np.ascontiguousarray(a, np.uint8)
+    b = np.ascontiguousarray(b, np.uint8)
+    out = np.empty((a.shape[0], b.shape[0]), np.uint32)
+    ref().ref_hamming_matrix(_ptr(a), a.shape[0], _ptr(b), b.shape[0], a.shape[1], _ptr(out))
+    return out
+
+
+def ref_search(pq: PQ, codes, queries, k, tau=None, strategy="dual", ids=None, threads=0):
+    codes = np.ascontiguousarray(codes, np.uint8)
+    queries = np.ascontiguousarray(queries, np.float32)
+    n, nq = codes.shape[0], queries.shape[0]
+    ids = np.arange(n, dtype=np.int64) if ids is None else np.ascontiguousarray(ids, np.int64)
+    tau = pq.code_bits if tau is None else tau
+    oi = np.empty((nq, k), np.int64)
+    osc = np.empty((nq, k), np.float32)
+    oc = np.empty(nq, np.uint32)
+    sv = np.empty(nq, np.uint64)
+    _check_ref(ref().ref_search_batch(*pq.args(), _ptr(codes), _ptr(ids), n, _ptr(queries), nq, STRATEGIES[strategy],
+                                      k, tau, threads, _ptr(oi), _ptr(osc), _ptr(oc), _ptr(sv)))
+    return oi, osc, oc, sv
+
+
+def ref_buggy_topk(scores, ids, k):
+    scores = np.ascontiguousarray(scores, np.float32)
+    ids = np.ascontiguousarray(ids, np.int64)
+    oi = np.empty(max(k, 1), np.int64)
+    osc = np.empty(max(k, 1), np.float32)
+    n = ref().ref_buggy_topk(_ptr(scores), _ptr(ids), scores.shape[0], k, _ptr(oi), _ptr(osc))
+    return oi[:n], osc[:n]
