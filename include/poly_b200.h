@@ -1,0 +1,167 @@
+/* poly_b200.h -- C ABI of the B200 polysemous-code search path.
+ *
+ * Drop-in boundary for the reference's flat index
+ * (/root/reference/proj/include/poly/flat_index.hpp:99-144, class poly::FlatIndex).
+ * Plain pointers and sizes only; no exceptions cross this boundary.  Every
+ * entry point returns a status from the reference's error space
+ * (common.hpp:13-22, "usable across the C boundary" common.hpp:24) and leaves a
+ * message in poly_b200_last_error().  A C++ mirror of poly::FlatIndex built on
+ * these calls is in include/poly_b200/flat_index.hpp; the Python mirror is
+ * paper_1609_01882_b200.FlatIndex.
+ *
+ * Scope: dbits = 8 (one byte per sub-quantizer field, the layout of
+ * every configuration), m in {8, 16} (64- and 128-bit codes), k <= 2048.
+ * Other shapes are rejected with POLY_B200_INVALID_ARGUMENT.
+ */
+#ifndef POLY_B200_H
+#define POLY_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* poly::errc (common.hpp:13-22) */
+enum poly_b200_status {
+    POLY_B200_OK = 0,
+    POLY_B200_INVALID_ARGUMENT = 1,
+    POLY_B200_IO = 2,
+    POLY_B200_FORMAT = 3,
+    POLY_B200_STATE = 4,
+    POLY_B200_CORRUPT = 5,
+    POLY_B200_VERSION = 6,
+    POLY_B200_INTERNAL = 7
+};
+
+/* poly::Strategy (flat_index.hpp:44) */
+enum poly_b200_strategy { POLY_B200_ADC = 0, POLY_B200_BINARY = 1, POLY_B200_DISIDX = 2, POLY_B200_DUAL = 3 };
+
+/* poly::ProductQuantizer (pq.hpp:49-89): codebooks m x 2^dbits x dim/m fp32,
+ * perms m x 2^dbits (centroid index -> stored field). */
+typedef struct {
+    uint32_t m;
+    uint32_t dbits;
+    uint64_t dim;
+    const float* codebooks;
+    const uint16_t* perms;
+} poly_b200_pq_desc;
+
+/* poly::SearchParams (flat_index.hpp:48-52) */
+typedef struct {
+    int32_t strategy;
+    uint32_t k;
+    uint32_t tau;
+} poly_b200_search_params;
+
+/* poly::SearchStats (flat_index.hpp:54-57) */
+typedef struct {
+    uint64_t scanned;
+    uint64_t survivors;
+} poly_b200_search_stats;
+
+typedef struct poly_b200_index poly_b200_index;
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* poly_b200_last_error(void);
+
+/* FlatIndex(ProductQuantizer) (flat_index.hpp:102).  `device` is the CUDA
+ * ordinal; the PQ tables are copied to it. */
+int poly_b200_create(const poly_b200_pq_desc* pq, int device, poly_b200_index** out);
+int poly_b200_destroy(poly_b200_index* index);
+
+/* size() / code_bytes() / code_bits() (flat_index.hpp:105-107) */
+uint64_t poly_b200_size(const poly_b200_index* index);
+uint32_t poly_b200_code_bytes(const poly_b200_index* index);
+
+/* FlatIndex::add (flat_index.hpp:115-116): encode n host vectors (n x dim fp32)
+ * on the GPU and append.  ids may be NULL (sequential from size()). */
+int poly_b200_add(poly_b200_index* index, const float* x, uint64_t n, const int64_t* ids);
+
+/* FlatIndex::add_codes (flat_index.hpp:118-119): append n pre-encoded host codes
+ * (n x code_bytes) with their ids (NULL = sequential from size()). */
+int poly_b200_add_codes(poly_b200_index* index, const uint8_t* codes, const int64_t* ids, uint64_t n);
+
+/* FlatIndex::search_batch (flat_index.hpp:124-126), host buffers.
+ * queries nq x dim fp32; out_ids / out_scores nq x k (unfilled slots: id -1,
+ * score +inf); out_counts nq (may be NULL); stats summed over queries (may be NULL).
+ * FlatIndex::search (flat_index.hpp:121-122) is the nq = 1 case. */
+int poly_b200_search_batch(poly_b200_index* index, const float* queries, uint64_t nq,
+                           const poly_b200_search_params* params, int64_t* out_ids, float* out_scores,
+                           uint32_t* out_counts, poly_b200_search_stats* stats);
+
+/* Same, with every buffer in device memory of the index's device and work
+ * enqueued on `stream` (a cudaStream_t, NULL = legacy default stream).
+ * Per-query survivor counts go to out_survivors (device, nq, may be NULL).
+ * Returns after enqueueing; `stats` (host, may be NULL) forces a sync. */
+int poly_b200_search_batch_device(poly_b200_index* index, const float* d_queries, uint64_t nq,
+                                  const poly_b200_search_params* params, int64_t* d_out_ids, float* d_out_scores,
+                                  uint32_t* d_out_counts, uint64_t* d_out_survivors, void* stream,
+                                  poly_b200_search_stats* stats);
+
+/* FlatIndex::calibrate_threshold (flat_index.hpp:128-132):
+ * max { tau : mean survivor fraction over the train queries <= 1 - rate };
+ * returns 0 in *tau with *warning = 1 when even tau = 0 keeps too many. */
+int poly_b200_calibrate_threshold(poly_b200_index* index, const float* train_queries, uint64_t nq,
+                                  double target_filter_rate, uint32_t* tau, int* warning);
+
+/* FlatIndex::with_assignments (flat_index.hpp:134-136): new index over the same
+ * codebooks and vectors under new perms (m x 2^dbits); codes are relabeled
+ * field by field exactly as if re-encoded. */
+int poly_b200_with_assignments(const poly_b200_index* index, const uint16_t* perms, poly_b200_index** out);
+
+/* Copy the stored codes (n x code_bytes) / ids back to host (FlatIndex::codes(), ids()). */
+int poly_b200_get_codes(const poly_b200_index* index, uint8_t* codes, int64_t* ids);
+
+/* ---- multi-GPU plumbing ----------------------------
+ * Per-shard search that stops before mapping keys to ids: writes, per query,
+ * up to k 64-bit keys (fp32 score bits << 32 | 32-bit id rank) ascending, and
+ * the key count.  All ranks all-gather these and call poly_b200_merge_keys. */
+int poly_b200_search_keys_device(poly_b200_index* index, const float* d_queries, uint64_t nq,
+                                 const poly_b200_search_params* params, uint64_t* d_out_keys, uint32_t* d_out_counts,
+                                 uint64_t* d_out_survivors, void* stream);
+
+/* Merge `parts` key lists per query (layout parts x nq x k, counts parts x nq)
+ * into the global top-k; keys are mapped to ids by the index's id map
+ * (the shards of one logical index share it). */
+int poly_b200_merge_keys_device(poly_b200_index* index, const uint64_t* d_keys, const uint32_t* d_counts,
+                                uint32_t parts, uint64_t nq, uint32_t k, int64_t* d_out_ids, float* d_out_scores,
+                                uint32_t* d_out_counts, void* stream);
+
+/* Synthetic workload generator used by the benchmark and the large-N tests:
+ * appends rows [row0, row0 + n) of the seeded Gaussian mixture (stream_id),
+ * generated and encoded on the GPU (never materialised); bit-identical to
+ * oracle/polyoracle.c po_gen_points followed by encode (pq.cpp:29-45).
+ * The appended ids are the global row numbers row0 .. row0 + n - 1, so the
+ * shards of one database keep globally consistent ids. */
+int poly_b200_add_synthetic(poly_b200_index* index, uint64_t seed, const float* centers, uint32_t ncent,
+                            uint32_t stream_id, uint64_t row0, uint64_t n, int normalize);
+
+/* Device-side generator of float rows (same stream definition), for tests. */
+int poly_b200_gen_points_device(int device, uint64_t seed, const float* centers, uint32_t ncent, uint32_t dim,
+                                uint32_t stream_id, uint64_t row0, uint64_t n, int normalize, float* d_out,
+                                void* stream);
+
+/* Test hook: K1 only -- stored-field LUTs (nq x m x 256 fp32, permuted_lut
+ * pq.cpp:107-119) and query codes (nq x code_bytes, encode pq.cpp:29-45) for
+ * host queries, copied back to host buffers. */
+int poly_b200_debug_lut(poly_b200_index* index, const float* queries, uint64_t nq, float* lutp, uint8_t* qcodes);
+
+/* Test hook: per-query candidate counts and final thresholds of the last
+ * scanned batch (nq <= 256 entries each). */
+int poly_b200_debug_counts(poly_b200_index* index, uint32_t* ccount, uint64_t* thr, uint32_t nq);
+
+/* Timing hook for bench.py: while enabled, CUDA events bracket every K2 scan
+ * launch on its stream; poly_b200_profile_read waits for them and returns the
+ * summed K2 time (ms) and launch count since the last read. */
+int poly_b200_profile_enable(poly_b200_index* index, int enable);
+int poly_b200_profile_read(poly_b200_index* index, double* scan_ms, uint64_t* scan_launches);
+
+/* Number of kernel launches this library has issued so far (for bench.py). */
+uint64_t poly_b200_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* POLY_B200_H */

@@ -1,0 +1,74 @@
+"""ctypes binding of libpoly_b200.so (include/poly_b200.h).
+
+The library is built in-tree by ``paper_1609_01882_b200.build``.  There is no
+fallback: if the shared library is missing or fails to load, importing the
+package raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libpoly_b200.so")
+
+_P = C.c_void_p
+_u32, _u64, _i32, _f64 = C.c_uint32, C.c_uint64, C.c_int, C.c_double
+
+
+class PqDesc(C.Structure):
+    _fields_ = [("m", _u32), ("dbits", _u32), ("dim", _u64), ("codebooks", _P), ("perms", _P)]
+
+
+class SearchParamsC(C.Structure):
+    _fields_ = [("strategy", C.c_int32), ("k", _u32), ("tau", _u32)]
+
+
+class SearchStatsC(C.Structure):
+    _fields_ = [("scanned", _u64), ("survivors", _u64)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python paper_1609_01882_b200/build.py` "
+                          "(there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    L.poly_b200_last_error.restype = C.c_char_p
+    L.poly_b200_create.argtypes = [C.POINTER(PqDesc), _i32, C.POINTER(_P)]
+    L.poly_b200_destroy.argtypes = [_P]
+    L.poly_b200_size.argtypes = [_P]
+    L.poly_b200_size.restype = _u64
+    L.poly_b200_code_bytes.argtypes = [_P]
+    L.poly_b200_code_bytes.restype = _u32
+    L.poly_b200_add.argtypes = [_P, _P, _u64, _P]
+    L.poly_b200_add_codes.argtypes = [_P, _P, _P, _u64]
+    L.poly_b200_search_batch.argtypes = [_P, _P, _u64, C.POINTER(SearchParamsC), _P, _P, _P,
+                                         C.POINTER(SearchStatsC)]
+    L.poly_b200_search_batch_device.argtypes = [_P, _P, _u64, C.POINTER(SearchParamsC), _P, _P, _P, _P, _P,
+                                                C.POINTER(SearchStatsC)]
+    L.poly_b200_calibrate_threshold.argtypes = [_P, _P, _u64, _f64, C.POINTER(_u32), C.POINTER(_i32)]
+    L.poly_b200_with_assignments.argtypes = [_P, _P, C.POINTER(_P)]
+    L.poly_b200_get_codes.argtypes = [_P, _P, _P]
+    L.poly_b200_search_keys_device.argtypes = [_P, _P, _u64, C.POINTER(SearchParamsC), _P, _P, _P, _P]
+    L.poly_b200_merge_keys_device.argtypes = [_P, _P, _P, _u32, _u64, _u32, _P, _P, _P, _P]
+    L.poly_b200_add_synthetic.argtypes = [_P, _u64, _P, _u32, _u32, _u64, _u64, _i32]
+    L.poly_b200_gen_points_device.argtypes = [_i32, _u64, _P, _u32, _u32, _u32, _u64, _u64, _i32, _P, _P]
+    L.poly_b200_debug_lut.argtypes = [_P, _P, _u64, _P, _P]
+    L.poly_b200_debug_counts.argtypes = [_P, _P, _P, _u32]
+    L.poly_b200_profile_enable.argtypes = [_P, _i32]
+    L.poly_b200_profile_read.argtypes = [_P, C.POINTER(_f64), C.POINTER(_u64)]
+    L.poly_b200_launch_count.restype = _u64
+    return L
+
+
+lib = _load()
+
+# names the C ABI exports (checked by tests/test_capi_symbols.py)
+EXPORTS = [
+    "poly_b200_last_error", "poly_b200_create", "poly_b200_destroy", "poly_b200_size", "poly_b200_code_bytes",
+    "poly_b200_add", "poly_b200_add_codes", "poly_b200_search_batch", "poly_b200_search_batch_device",
+    "poly_b200_calibrate_threshold", "poly_b200_with_assignments", "poly_b200_get_codes",
+    "poly_b200_search_keys_device", "poly_b200_merge_keys_device", "poly_b200_add_synthetic",
+    "poly_b200_gen_points_device", "poly_b200_debug_lut", "poly_b200_debug_counts", "poly_b200_profile_enable", "poly_b200_profile_read",
+    "poly_b200_launch_count",
+]

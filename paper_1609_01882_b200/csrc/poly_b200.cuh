@@ -1,0 +1,126 @@
+// poly_b200.cuh -- shared device helpers and kernel entry points (sm_100a).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pb {
+
+constexpr int KSUB = 256;              // dbits = 8
+constexpr int DSUB = 16;               // every configuration: 128/8 and 256/16
+constexpr int TILE = 2048;             // codes per pipeline stage
+constexpr int STAGES = 4;              // bulk-copy ring depth
+constexpr int BS = 4096;               // candidate block size for threshold selects
+constexpr int KMAX = 2048;             // largest supported k
+constexpr int QCAP = 64;               // per-warp survivor queue entries
+constexpr int MAXREQ = 16;             // pending threshold selects per CTA
+constexpr uint64_t KEY_INF = ~0ull;
+
+enum Strategy { ADC = 0, BINARY = 1, DISIDX = 2, DUAL = 3 };
+enum IdMode { ID_ARITH = 0, ID_TABLE = 1 };  // key low word = id0 + pos, or id32[pos]
+
+// Host/device argument block of the fused scan (K2).
+struct ScanArgs {
+    const uint8_t* codes;        // n x CB bytes, padded to a multiple of TILE codes
+    uint64_t n;                  // codes in this shard
+    const float* lutp;           // nqb x M x 256 (stored-field indexed LUTs)
+    const uint8_t* qcodes;       // nqb x CB
+    uint32_t nqb, tau, k;
+    int id_mode;
+    uint32_t id0;
+    const uint32_t* id32;        // pos -> key low word (ID_TABLE)
+    unsigned long long* cand;    // nqb x cap candidate keys
+    uint32_t cap;
+    uint32_t* ccount;            // nqb
+    uint32_t* bdone;             // nqb x (cap / BS) completion counters
+    unsigned long long* thr;     // nqb running upper bounds of the k-th key
+    unsigned long long* surv;    // nqb survivor counts
+    uint32_t* overflow;          // set when a candidate did not fit
+    uint32_t* work;              // dynamic work-unit counter
+    uint32_t units, ngroups, tiles_per_chunk;
+    uint64_t ntiles;             // logical tiles; physical tile = logical * tile_stride
+    uint64_t tile_stride;
+};
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// 1-D TMA bulk copy global -> shared, completion counted on `bar` (bytes % 16 == 0).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// ---------------------------------------------------------------- kernels
+// K1: LUT build + query code (compute_lut pq.cpp:91-105, permuted_lut :107-119, encode :29-45).
+void launch_lut(const float* queries, uint32_t nq, uint32_t dim, uint32_t m, const float* codebooks,
+                const uint16_t* perms, float* lutp, uint8_t* qcodes, cudaStream_t s);
+
+// K0: DB encoder (encode pq.cpp:29-45 per vector), from device floats or the synthetic generator.
+void launch_encode(const float* x, uint64_t n, uint32_t dim, uint32_t m, const float* codebooks,
+                   const uint16_t* perms, uint8_t* codes, cudaStream_t s);
+void launch_synth_encode(uint64_t seed, uint32_t stream_id, uint64_t row0, uint64_t n, const float* centers,
+                         uint32_t ncent, uint32_t dim, int normalize, uint32_t m, const float* codebooks,
+                         const uint16_t* perms, uint8_t* codes, cudaStream_t s);
+void launch_gen_points(uint64_t seed, uint32_t stream_id, uint64_t row0, uint64_t n, const float* centers,
+                       uint32_t ncent, uint32_t dim, int normalize, float* out, cudaStream_t s);
+
+// K2: fused filter + ADC + candidate scan.
+void launch_scan(const ScanArgs& a, int strategy, uint32_t m, int num_sms, cudaStream_t s);
+int scan_queries_per_cta(uint32_t m);
+
+// K3: per-query exact top-k over candidate keys; K3b: key -> (id, score).
+// cand part p, query q: cand + p * part_stride + q * cap, count ccount[p * count_stride + q].
+void launch_topk(const unsigned long long* cand, const uint32_t* ccount, uint32_t cap, uint32_t parts,
+                 uint64_t part_stride, uint64_t count_stride, uint32_t nq, uint32_t k, unsigned long long* out_keys,
+                 uint32_t* out_counts, cudaStream_t s);
+void launch_keys_to_ids(const unsigned long long* keys, const uint32_t* counts, uint32_t nq, uint32_t k,
+                        const int64_t* rank_to_id, int64_t* out_ids, float* out_scores, uint32_t* out_counts,
+                        cudaStream_t s);
+
+// Calibration: Hamming histograms (nq x (code_bits + 1)).
+void launch_hamming_hist(const uint8_t* codes, uint64_t n, uint32_t cb, const uint8_t* qcodes, uint32_t nq,
+                         unsigned long long* hist, cudaStream_t s);
+// with_assignments: relabel fields through a per-sub-quantizer byte map.
+void launch_relabel(uint8_t* codes, uint64_t n, uint32_t m, const uint8_t* maps, cudaStream_t s);
+
+void launch_or_flag(uint32_t* dst, const uint32_t* src, cudaStream_t s);
+void count_launch();
+
+}  // namespace pb

@@ -1,0 +1,218 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+vectors and the CPU oracle on identical bytes.
+
+Bar (BASELINE.json north_star): bit-exact Hamming distances, survivor sets,
+query codes, database codes and top-k ids (ties included -- keys order by
+(score, id) exactly); ADC scores are compared bit-exactly (tolerance 0), which
+is stricter than the stated 1e-5 relative.
+"""
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+TAUS8 = (0, 20, 24, 28, 32, 64)
+TAUS16 = (0, 48, 56, 64, 128)
+
+
+@pytest.fixture(scope="module")
+def pb():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_1609_01882_b200 as pb
+    return pb
+
+
+def _index(pb, pq, codes=None, ids=None):
+    ix = pb.FlatIndex(pb.ProductQuantizer(pq.m, pq.dbits, pq.dim, pq.codebooks, pq.perms))
+    if codes is not None:
+        ix.add_codes(codes, ids)
+    return ix
+
+
+def _same(a, b):
+    return np.array_equal(np.asarray(a), np.asarray(b))
+
+
+def _bits(x):
+    return np.ascontiguousarray(x, np.float32).view(np.uint32)
+
+
+@pytest.mark.parametrize("which", ["8", "16"])
+def test_lut_and_query_codes_bit_exact(pb, which, pq8, pq16, g8, g16):
+    pq, g = (pq8, g8) if which == "8" else (pq16, g16)
+    ix = _index(pb, pq)
+    lutp, qc = pb.flat_index.debug_lut(ix, g["queries"])
+    assert _same(qc, g["qcodes"])                                  # encode, pq.cpp:29-45
+    assert _same(_bits(lutp[:4]), _bits(g["lutp"]))                # permuted_lut, pq.cpp:107-119
+
+
+@pytest.mark.parametrize("which", ["8", "16"])
+def test_gpu_encoder_matches_reference_encode(pb, which, pq8, pq16, g8, g16):
+    pq, g = (pq8, g8) if which == "8" else (pq16, g16)
+    centers = oracle.gen_centers(int(g["data_seed"]), int(g["ncent"]), pq.dim)
+    base = oracle.gen_points(int(g["data_seed"]), 2, 0, int(g["n"]), centers)
+    ix = _index(pb, pq)
+    ix.add(base)
+    assert ix.size() == base.shape[0]
+    assert _same(ix.codes(), g["codes"])
+    ix2 = _index(pb, pq)  # generated + encoded on the GPU, never materialised
+    ix2.add_synthetic(int(g["data_seed"]), centers, 0, int(g["n"]))
+    assert _same(ix2.codes(), g["codes"])
+    assert _same(ix2.ids(), np.arange(int(g["n"])))
+
+
+@pytest.mark.parametrize("strategy", ["adc", "binary", "disidx"])
+@pytest.mark.parametrize("which", ["8", "16"])
+def test_strategies_match_reference(pb, strategy, which, pq8, pq16, g8, g16):
+    pq, g = (pq8, g8) if which == "8" else (pq16, g16)
+    ix = _index(pb, pq, g["codes"])
+    ids, sc, cnt = ix.search_batch(g["queries"], pb.SearchParams(pb.strategy_from_string(strategy), 100, 0))
+    assert _same(ids, g[f"{strategy}_ids"])
+    assert _same(_bits(sc), _bits(g[f"{strategy}_scores"]))
+    assert _same(cnt, g[f"{strategy}_counts"])
+
+
+@pytest.mark.parametrize("which", ["8", "16"])
+def test_dual_matches_reference(pb, which, pq8, pq16, g8, g16):
+    pq, g, taus = (pq8, g8, TAUS8) if which == "8" else (pq16, g16, TAUS16)
+    ix = _index(pb, pq, g["codes"])
+    nq = g["queries"].shape[0]
+    for tau in taus:
+        st = pb.SearchStats()
+        ids, sc, cnt = ix.search_batch(g["queries"], pb.SearchParams(pb.Strategy.dual, 100, tau), st)
+        assert _same(ids, g[f"dual{tau}_ids"]), tau
+        assert _same(_bits(sc), _bits(g[f"dual{tau}_scores"])), tau
+        assert _same(cnt, g[f"dual{tau}_counts"]), tau
+        assert st.scanned == nq * g["codes"].shape[0]
+        assert st.survivors == int(g[f"dual{tau}_surv"].sum()), tau
+
+
+@pytest.mark.parametrize("which", ["8", "16"])
+def test_ties_shortage_and_arbitrary_ids(pb, which, pq8, pq16, g8, g16):
+    pq, g, taus = (pq8, g8, TAUS8) if which == "8" else (pq16, g16, TAUS16)
+    tie_codes = np.repeat(g["codes"][:500], 4, axis=0)
+    ix = _index(pb, pq, tie_codes, g["tie_ids_in"])
+    for tau in (taus[1], pq.code_bits):
+        ids, sc, cnt = ix.search_batch(g["queries"], pb.SearchParams(pb.Strategy.dual, 7, tau))
+        assert _same(ids, g[f"tie{tau}_ids"])
+        assert _same(cnt, g[f"tie{tau}_counts"])
+    # ids beyond 32 bits and negative ids go through the rank table
+    big = g["tie_ids_in"] * 1_000_000_007 - 5_000_000_000
+    ixb = _index(pb, pq, tie_codes, big)
+    ids_o, sc_o, cnt_o, _, _ = oracle.search(pq, tie_codes, g["queries"], 9, tau=taus[2], ids=big)
+    ids, sc, cnt = ixb.search_batch(g["queries"], pb.SearchParams(pb.Strategy.dual, 9, taus[2]))
+    assert _same(ids, ids_o) and _same(_bits(sc), _bits(sc_o)) and _same(cnt, cnt_o)
+
+
+def test_edge_cases(pb, pq8, g8):
+    q = g8["queries"][:5]
+    ix = _index(pb, pq8, g8["codes"])
+    ids, sc, cnt = ix.search_batch(q, pb.SearchParams(pb.Strategy.dual, 0, 24))   # k = 0 -> empty
+    assert ids.shape == (5, 0) and cnt.tolist() == [0] * 5
+    empty = _index(pb, pq8)                                                         # empty index -> empty
+    ids, sc, cnt = empty.search_batch(q, pb.SearchParams(pb.Strategy.dual, 10, 24))
+    assert cnt.tolist() == [0] * 5 and (ids == -1).all() and np.isinf(sc).all()
+    with pytest.raises(pb.PolyError) as e:                                          # tau > code_bits
+        ix.search_batch(q, pb.SearchParams(pb.Strategy.dual, 10, 65))
+    assert e.value.code == pb.Errc.invalid_argument
+    # k > n, and a single-query search() returns Neighbor objects
+    small = _index(pb, pq8, g8["codes"][:37])
+    ids, sc, cnt = small.search_batch(q, pb.SearchParams(pb.Strategy.adc, 50, 0))
+    oi, os_, oc, _, _ = oracle.search(pq8, g8["codes"][:37], q, 50, strategy="adc")
+    assert _same(ids, oi) and _same(cnt, oc) and (cnt == 37).all()
+    res = ix.search(q[0], pb.SearchParams(pb.Strategy.dual, 5, 24))
+    assert [r.id for r in res] == g8["dual24_ids"][0, :5].tolist()
+    # a query equal to a stored code's reconstruction ranks that code first
+    recon = np.concatenate([pq8.codebooks[sq, pq8.inv_perms[sq, g8["codes"][123, sq]]] for sq in range(8)])
+    res = ix.search(recon, pb.SearchParams(pb.Strategy.dual, 3, 0))
+    assert res[0].score == 0.0 and g8["codes"][res[0].id].tobytes() == g8["codes"][123].tobytes()
+
+
+def test_calibrate_and_with_assignments(pb, pq8, g8):
+    ix = _index(pb, pq8, g8["codes"])
+    for rate in (0.5, 0.9, 0.95, 0.99, 1e-9):
+        assert ix.calibrate_threshold(g8["queries"], rate) == oracle.calibrate_threshold(pq8, g8["codes"],
+                                                                                         g8["queries"], rate)
+    ident = np.tile(np.arange(256, dtype=np.uint16), (8, 1))
+    ix2 = ix.with_assignments(ident)
+    assert _same(ix2.codes(), oracle.relabel_codes(pq8, ident, g8["codes"]))
+    pq_id = oracle.PQ(8, 8, 128, pq8.codebooks, ident)
+    # adc is pi-invariant: same ids and scores under the new assignment
+    a = ix.search_batch(g8["queries"], pb.SearchParams(pb.Strategy.adc, 20, 0))
+    b = ix2.search_batch(g8["queries"], pb.SearchParams(pb.Strategy.adc, 20, 0))
+    assert _same(a[0], b[0]) and _same(_bits(a[1]), _bits(b[1]))
+    oi, _, _, _, _ = oracle.search(pq_id, ix2.codes(), g8["queries"], 20, tau=20)
+    assert _same(ix2.search_batch(g8["queries"], pb.SearchParams(pb.Strategy.dual, 20, 20))[0], oi)
+
+
+@pytest.fixture(scope="module")
+def big8(pb, pq8):
+    """1M-code database generated + encoded on the GPU, checked against the CPU oracle."""
+    seed = 160901882
+    centers = oracle.gen_centers(seed, 1000, 128)
+    ix = _index(pb, pq8)
+    ix.add_synthetic(seed, centers, 0, 1_000_000)
+    codes = ix.codes()
+    sample = np.random.default_rng(0).choice(1_000_000, 2000, replace=False)
+    rows = np.stack([oracle.gen_points(seed, 2, int(r), 1, centers)[0] for r in sample])
+    assert _same(codes[sample], oracle.encode(pq8, rows))
+    queries = oracle.gen_points(seed, 3, 0, 300, centers)
+    return ix, codes, queries
+
+
+@pytest.mark.parametrize("tau", [20, 24, 28, 32, 64])
+def test_million_codes_match_oracle(pb, pq8, big8, tau):
+    ix, codes, queries = big8
+    oi, osc, oc, osv, _ = oracle.search(pq8, codes, queries, 100, tau=tau, threads=16)
+    st = pb.SearchStats()
+    ids, sc, cnt = ix.search_batch(queries, pb.SearchParams(pb.Strategy.dual, 100, tau), st)
+    assert _same(ids, oi)
+    assert _same(_bits(sc), _bits(osc))
+    assert _same(cnt, oc)
+    assert st.survivors == int(osv.sum())
+
+
+def test_device_api_and_sharded_merge(pb, pq8, big8):
+    """Shards searched separately and merged by K3 == the unsharded search
+    (the multi-GPU exchange, run on one device)."""
+    import torch
+    ix, codes, queries = big8
+    k, tau, G = 100, 24, 4
+    p = pb.SearchParams(pb.Strategy.dual, k, tau)
+    want = ix.search_batch(queries, p)
+    dq = torch.from_numpy(queries).cuda()
+    n = codes.shape[0]
+    keys = torch.empty((G, len(queries), k), dtype=torch.int64, device="cuda")
+    cnts = torch.empty((G, len(queries)), dtype=torch.int32, device="cuda")
+    surv = torch.zeros((G, len(queries)), dtype=torch.int64, device="cuda")
+    bounds = np.linspace(0, n, G + 1).astype(np.int64)
+    shards = []
+    for s in range(G):
+        sh = _index(pb, pq8, codes[bounds[s]:bounds[s + 1]], np.arange(bounds[s], bounds[s + 1]))
+        sh.search_keys_device(dq, p, keys[s], cnts[s], surv[s])
+        shards.append(sh)
+    oid = torch.empty((len(queries), k), dtype=torch.int64, device="cuda")
+    osc = torch.empty((len(queries), k), dtype=torch.float32, device="cuda")
+    ocnt = torch.empty(len(queries), dtype=torch.int32, device="cuda")
+    shards[0].merge_keys_device(keys, cnts, G, len(queries), k, oid, osc, ocnt)
+    torch.cuda.synchronize()
+    assert _same(oid.cpu().numpy(), want[0])
+    assert _same(_bits(osc.cpu().numpy()), _bits(want[1]))
+    assert _same(ocnt.cpu().numpy().astype(np.uint32), want[2])
+    # device-resident search == host search
+    did = torch.empty((len(queries), k), dtype=torch.int64, device="cuda")
+    dsc = torch.empty((len(queries), k), dtype=torch.float32, device="cuda")
+    ix.search_batch_device(dq, p, did, dsc)
+    torch.cuda.synchronize()
+    assert _same(did.cpu().numpy(), want[0])
+
+
+def test_launches_are_counted(pb, pq8, g8):
+    ix = _index(pb, pq8, g8["codes"])
+    before = pb.launch_count()
+    ix.search_batch(g8["queries"], pb.SearchParams(pb.Strategy.dual, 10, 24))
+    assert pb.launch_count() - before >= 4  # K1, K2, K3, ids
