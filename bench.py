@@ -1,0 +1,377 @@
+#!/usr/bin/env python
+"""Polysemous dual search on B200 -- the BASELINE.json headline metric.
+
+Workload (BASELINE.json configs[1], "cfg1"): flat polysemous PQ, d = 128
+mixture, m = 8 x 8-bit codes (64-bit), N = 100,000,000 codes (800 MB) sharded
+over the ranks, nq = 10,000 queries in batches of 256, k = 100, headline
+ht = 24 (the Table 1 calibration rule: tau filters >= ~94% of the codes);
+ht = 28 and 32 are reported under "per_ht".  Data are synthetic (the seeded
+mixture of BASELINE.json).
+
+One step = one 256-query batch through the whole path: K1 LUT + query code,
+K0 warm-up + K2 fused filter/ADC/candidate scan, K3 exact top-k, key -> id;
+at N > 1 plus the NCCL all-gather of per-shard top-k keys and the K3 merge.
+`value` = codes scanned per second over the whole job (256 * N_total per
+step), queries and codes resident in HBM; `e2e` = the same with the queries
+copied from pinned host memory and the results (ids, scores, counts,
+survivors) copied back inside the timed region.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "DB codes scanned/sec (filter+ADC+top-k)"
+UNIT = "codes/s"
+SEED = 160901882
+NCENT = 1000
+DIM = 128
+BATCH = 256
+NQ = 10_000
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=100_000_000, help="total database codes")
+    ap.add_argument("--k", type=int, default=100)
+    ap.add_argument("--ht", type=int, default=24)
+    ap.add_argument("--per-ht", default="28,32")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-queries", type=int, default=256, help="queries in the CPU-baseline sample")
+    ap.add_argument("--ref-n", type=int, default=8_000_000, help="codes in the --impl reference sample")
+    return ap.parse_args()
+
+
+def config(args, world):
+    return {
+        "workload": f"cfg1 flat polysemous: N={args.n} 64-bit codes (m=8, nbits=8, d=128 mixture), "
+                    f"nq={NQ} in batches of {BATCH}, k={args.k}, ht={args.ht}",
+        "n_codes": args.n, "m": 8, "nbits": 8, "dim": DIM, "k": args.k, "ht": args.ht, "batch": BATCH, "nq": NQ,
+        "strategy": "dual", "parallelism": f"db-shard{world}",
+        "l2": "inputs larger than L2 (800 MB of codes vs 126 MB L2); no flush needed",
+    }
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpus):
+        self.path = tempfile.mktemp(suffix=".csv")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                       "-i", ",".join(str(g) for g in gpus), "-lms", "100"],
+                                      stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args, rank):
+    """The reference's own CPU search (oracle/_ref: reference sources compiled in
+    place; FlatIndex::search restated per SPEC from its primitives) on the host."""
+    if rank != 0:
+        return
+    import oracle
+    from paper_1609_01882_b200 import synth
+    threads = os.cpu_count()
+    z = np.load(os.path.join(ROOT, "tests", "golden", "pq_d128_m8.npz"))
+    pq = oracle.PQ(8, 8, DIM, z["codebooks"], z["perms"])
+    kind = "reference" if oracle.ref_available() else "port"
+    centers = synth.gen_centers(SEED, NCENT, DIM)
+    t = time.time()
+    codes = np.empty((args.ref_n, 8), np.uint8)
+    step = 1 << 20
+    for r0 in range(0, args.ref_n, step):
+        x = oracle.gen_points(SEED, 2, r0, min(step, args.ref_n - r0), centers)
+        codes[r0:r0 + len(x)] = oracle.ref_encode_batch(pq, x, threads) if kind == "reference" else oracle.encode(pq, x, threads)
+    setup = time.time() - t
+    queries = synth.gen_points(SEED, 3, 0, NQ, centers)
+
+    def step_fn(i):
+        q = queries[(i * BATCH) % (NQ - NQ % BATCH):][:BATCH]
+        if kind == "reference":
+            oracle.ref_search(pq, codes, q, args.k, tau=args.ht, threads=threads)
+        else:
+            oracle.search(pq, codes, q, args.k, tau=args.ht, threads=threads)
+
+    for i in range(args.warmup):
+        step_fn(i)
+    t = time.perf_counter()
+    for i in range(args.steps):
+        step_fn(args.warmup + i)
+    dt = time.perf_counter() - t
+    value = args.steps * BATCH * args.ref_n / dt
+    sample = (f"each step: {BATCH} queries x {args.ref_n} codes of the cfg1 mixture (encoded by the reference's "
+              f"encode_batch), two-pass dual search, ht={args.ht}, k={args.k}; {threads} threads")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u8/f32", "data": "synthetic",
+            "config": config(args, args.gpus), "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "setup_s": round(setup, 1)}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def cpu_baseline(args, index, dq_host):
+    """Reference CPU search (oracle/_ref) on one full step of the workload:
+    256 queries over all N codes, every host thread."""
+    import oracle
+    z = np.load(os.path.join(ROOT, "tests", "golden", "pq_d128_m8.npz"))
+    pq = oracle.PQ(8, 8, DIM, z["codebooks"], z["perms"])
+    codes = index.codes()
+    q = dq_host[:args.cpu_queries]
+    threads = os.cpu_count()
+    kind = "reference" if oracle.ref_available() else "port"
+    t = time.perf_counter()
+    if kind == "reference":
+        oracle.ref_search(pq, codes, q, args.k, tau=args.ht, threads=threads)
+    else:
+        oracle.search(pq, codes, q, args.k, tau=args.ht, threads=threads)
+    dt = time.perf_counter() - t
+    return {"value": len(q) * codes.shape[0] / dt, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"{len(q)} queries x all {codes.shape[0]} codes (one full step), two-pass dual ht={args.ht}, "
+                      f"k={args.k}, {dt:.1f} s"}
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import paper_1609_01882_b200 as pb
+    from paper_1609_01882_b200 import synth
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    z = np.load(os.path.join(ROOT, "tests", "golden", "pq_d128_m8.npz"))
+    pq = pb.ProductQuantizer(8, 8, DIM, z["codebooks"], z["perms"])
+    centers = synth.gen_centers(SEED, NCENT, DIM)
+    shard = (args.n + world - 1) // world
+    row0 = rank * shard
+    nloc = max(0, min(shard, args.n - row0))
+    t = time.time()
+    index = pb.FlatIndex(pq, device=local)
+    index.add_synthetic(SEED, centers, row0, nloc)   # GPU generator + encoder, ids = global rows
+    setup_s = time.time() - t
+
+    dq = torch.empty((NQ, DIM), dtype=torch.float32, device="cuda")
+    pb.gen_points_device(centers, SEED, 3, 0, NQ, dq, device=local)
+    hq = dq.cpu().pin_memory()
+    nbatches = NQ // BATCH
+    k = args.k
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+
+    o_ids = torch.empty((BATCH, k), dtype=torch.int64, device="cuda")
+    o_sc = torch.empty((BATCH, k), dtype=torch.float32, device="cuda")
+    o_cnt = torch.empty(BATCH, dtype=torch.int32, device="cuda")
+    o_surv = torch.empty(BATCH, dtype=torch.int64, device="cuda")
+    if world > 1:
+        keys = torch.empty((BATCH, k), dtype=torch.int64, device="cuda")
+        kcnt = torch.empty(BATCH, dtype=torch.int32, device="cuda")
+        keys_all = torch.empty((world, BATCH, k), dtype=torch.int64, device="cuda")
+        kcnt_all = torch.empty((world, BATCH), dtype=torch.int32, device="cuda")
+
+    def step(i, ht, q=None):
+        qb = dq[(i % nbatches) * BATCH:][:BATCH] if q is None else q
+        p = pb.SearchParams(pb.Strategy.dual, k, ht)
+        if world == 1:
+            index.search_batch_device(qb, p, o_ids, o_sc, o_cnt, o_surv, stream=sptr)
+        else:
+            index.search_keys_device(qb, p, keys, kcnt, o_surv, stream=sptr)
+            dist.all_gather_into_tensor(keys_all, keys)
+            dist.all_gather_into_tensor(kcnt_all, kcnt)
+            index.merge_keys_device(keys_all, kcnt_all, world, BATCH, k, o_ids, o_sc, o_cnt, stream=sptr)
+
+    def timed(ht, steps, warmup, profile=False):
+        for i in range(warmup):
+            step(i, ht)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        if profile:
+            index.profile_enable(True)
+        surv = 0
+        l0 = pb.launch_count()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(steps):
+            step(warmup + i, ht)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        launches = pb.launch_count() - l0
+        ms = e0.elapsed_time(e1)
+        scan = index.profile_read() if profile else None
+        if profile:
+            index.profile_enable(False)
+        surv = int(o_surv.sum().item())  # last batch's local survivors
+        if dist:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            dist.barrier()
+        return ms, launches, scan, surv
+
+    # ---- headline (device-resident)
+    clocks = ClockSampler([local] if world == 1 else list(range(world))) if rank == 0 else None
+    ms, launches, scan, surv_last = timed(args.ht, args.steps, args.warmup, profile=True)
+    clk = clocks.stop() if clocks else None
+    value = args.steps * BATCH * args.n / (ms / 1e3)
+
+    # ---- e2e: pinned host queries in, results out, inside the timed region
+    h_ids = torch.empty((BATCH, k), dtype=torch.int64).pin_memory()
+    h_sc = torch.empty((BATCH, k), dtype=torch.float32).pin_memory()
+    h_cnt = torch.empty(BATCH, dtype=torch.int32).pin_memory()
+    h_surv = torch.empty(BATCH, dtype=torch.int64).pin_memory()
+    qdev = torch.empty((BATCH, DIM), dtype=torch.float32, device="cuda")
+
+    def e2e_step(i):
+        qdev.copy_(hq[(i % nbatches) * BATCH:][:BATCH], non_blocking=True)
+        step(i, args.ht, q=qdev)
+        if rank == 0:
+            h_ids.copy_(o_ids, non_blocking=True)
+            h_sc.copy_(o_sc, non_blocking=True)
+            h_cnt.copy_(o_cnt, non_blocking=True)
+            h_surv.copy_(o_surv, non_blocking=True)
+
+    for i in range(args.warmup):
+        e2e_step(i)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        e2e_step(args.warmup + i)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e = {"value": args.steps * BATCH * args.n / (e2e_ms / 1e3), "unit": UNIT,
+           "h2d_bytes_per_step": BATCH * DIM * 4,
+           "d2h_bytes_per_step": (BATCH * k * 12 + BATCH * 4 + BATCH * 8) if rank == 0 else 0,
+           "ms_per_step": e2e_ms / args.steps}
+
+    # ---- per-ht sweep (device-resident)
+    per_ht = {str(args.ht): {"value": value, "ms_per_step": ms / args.steps,
+                             "survivor_frac": surv_last / (BATCH * max(nloc, 1))}}
+    for ht in [int(x) for x in args.per_ht.split(",") if x]:
+        m2, _, _, s2 = timed(ht, max(3, args.steps // 2), 1)
+        per_ht[str(ht)] = {"value": max(3, args.steps // 2) * BATCH * args.n / (m2 / 1e3),
+                           "ms_per_step": m2 / max(3, args.steps // 2), "survivor_frac": s2 / (BATCH * max(nloc, 1))}
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (K2 scan), from CUDA events around each launch
+    pk, pk_kind = peaks()
+    scan_ms, scan_n = scan
+    avg = scan_ms / max(scan_n, 1)
+    pairs = BATCH * nloc
+    code_bytes = nloc * 8  # algorithmic: each code read once per 256-query launch
+    hbm_gbs = code_bytes / (avg / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "scan_ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": hbm_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": hbm_gbs / pk["hbm_gbs"], "traffic": traffic, "peak_kind": pk_kind,
+                "kernel": "K2 scan_kernel<8,16,16,DUAL>", "kernel_ms_avg": avg, "kernel_launches": scan_n,
+                "kernel_share_of_step": scan_ms / ms,
+                "algorithmic_bytes_per_launch": code_bytes, "units_per_launch": f"{BATCH} queries x {nloc} codes"}
+    # issue roofline (the binding one for this integer/gather scan):
+    # POPC 16/clk/SM (2 per pair) vs random LUT gathers 13.5/clk/SM (8 per survivor), measured.
+    f_mhz = (clk or {}).get("sm_mhz") or pk.get("sm_max_mhz", 1965.0)
+    s = per_ht[str(args.ht)]["survivor_frac"]
+    clk_per_pair = max(2 / 16.0, s * 8 / 13.5, 8.0 / BATCH / (pk["hbm_gbs"] * 1e3 / f_mhz / 148))
+    peak_pairs = 148 * f_mhz * 1e6 / clk_per_pair
+    roofline_issue = {"bound": "popc/lds issue", "achieved": pairs / (avg / 1e3), "peak": peak_pairs,
+                      "unit": "pairs/s", "frac": pairs / (avg / 1e3) / peak_pairs, "sm_mhz": f_mhz,
+                      "clk_per_pair_bound": clk_per_pair, "survivor_frac": s}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u8/f32", "data": "synthetic (seeded Gaussian mixture, BASELINE cfg1)",
+            "config": config(args, world), "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+            "roofline": roofline, "roofline_issue": roofline_issue, "per_ht": per_ht,
+            "setup_s": round(setup_s, 2)}
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, index, hq.numpy())
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
