@@ -107,8 +107,9 @@ struct poly_b200_index {
     uint32_t* ctrl_w = nullptr;
     uint32_t cand_w_cap = 0;
     unsigned long long* thr = nullptr;
-    unsigned long long* surv = nullptr;
-    unsigned long long* surv_w = nullptr;
+    unsigned long long* surv = nullptr;      // per-query survivors of a batch (per-query mode)
+    unsigned long long* surv_w = nullptr;    // warm-up sink
+    unsigned long long* surv_total = nullptr;  // survivors summed over the whole call
     unsigned long long* keys = nullptr;
     uint32_t keys_k = 0;
     uint32_t* kcounts = nullptr;
@@ -265,6 +266,7 @@ void ensure_scratch(poly_b200_index* ix, uint32_t k) {
         ix->thr = dalloc<unsigned long long>(NQB);
         ix->surv = dalloc<unsigned long long>(NQB);
         ix->surv_w = dalloc<unsigned long long>(NQB);
+        ix->surv_total = dalloc<unsigned long long>(1);
         ix->sticky_overflow = dalloc<uint32_t>(1);
         CK(cudaMallocHost(&ix->h_overflow, sizeof(uint32_t)));
         *ix->h_overflow = 0;
@@ -285,7 +287,7 @@ void ensure_scratch(poly_b200_index* ix, uint32_t k) {
         ix->cand_w_cap = (uint32_t)(WARM_TILES * (16384 / ix->cb));
         ix->cand_w_cap = (ix->cand_w_cap + pb::BS - 1) / pb::BS * pb::BS;
         ix->cand_w = dalloc<unsigned long long>((size_t)NQB * ix->cand_w_cap);
-        ix->ctrl_w = dalloc<uint32_t>(NQB + 4 + (size_t)NQB * (ix->cand_w_cap / pb::BS + 1));
+        ix->ctrl_w = dalloc<uint32_t>(NQB + 4 + (size_t)NQB * (ix->cand_w_cap / 256 + 1));
     }
     if (ix->keys_k < k) {
         dfree(ix->keys);
@@ -318,9 +320,11 @@ void validate_params(const poly_b200_index* ix, const poly_b200_search_params* p
 
 // Core batched search: per batch of <= 256 queries K1 -> K2 -> K3 into keys.
 // emit(b, nqb) consumes ix->keys / ix->kcounts / ix->surv for that batch.
+// perq: per-query survivor counts in ix->surv (else the exact call total
+// accumulates in ix->surv_total at no cost in the scan).
 template <class Emit>
 void run_batches(poly_b200_index* ix, const float* d_queries, uint64_t nq, const poly_b200_search_params* p,
-                 cudaStream_t s, Emit&& emit) {
+                 bool perq, cudaStream_t s, Emit&& emit) {
     const uint32_t k = p->k;
     ensure_scratch(ix, std::max<uint32_t>(k, 1));
     sync_idmap(ix);
@@ -331,11 +335,12 @@ void run_batches(poly_b200_index* ix, const float* d_queries, uint64_t nq, const
     const uint64_t tc = 16384 / ix->cb;
     const uint64_t ntiles = (ix->n + tc - 1) / tc;
     CK(cudaMemsetAsync(ix->sticky_overflow, 0, 4, s));
+    CK(cudaMemsetAsync(ix->surv_total, 0, 8, s));
     for (uint64_t b0 = 0; b0 < nq; b0 += NQB) {
         const uint32_t nqb = (uint32_t)std::min<uint64_t>(NQB, nq - b0);
         CK(cudaMemsetAsync(ix->ctrl, 0, ix->ctrl_words * 4, s));
         CK(cudaMemsetAsync(ix->thr, 0xFF, NQB * 8, s));
-        CK(cudaMemsetAsync(ix->surv, 0, NQB * 8, s));
+        if (perq) CK(cudaMemsetAsync(ix->surv, 0, NQB * 8, s));
         if (k > 0 && ix->n > 0) {
             pb::launch_lut(d_queries + b0 * ix->dim, nqb, ix->dim, ix->m, ix->d_codebooks, ix->d_perms, ix->lutp,
                            ix->qcodes, s);
@@ -352,13 +357,15 @@ void run_batches(poly_b200_index* ix, const float* d_queries, uint64_t nq, const
             a.id32 = ix->d_id32;
             a.thr = ix->thr;
             a.ngroups = (nqb + Q - 1) / Q;
-            // Warm-up: one CTA per query group scans WARM_TILES tiles spread over
-            // the database into a scratch list; its block selects seed thr[] with
-            // valid upper bounds of the k-th key before the full scan starts (keeps
-            // the full scan from flooding the candidate lists while thr = +inf).
-            if (ntiles > 2 * WARM_TILES && ix->n > ix->cand_cap / 4) {
+            // Warm-up: strided samples of 16, 128, 1024, ... tiles spread over the
+            // database, each scanned with the threshold seeded by the exact k-th
+            // key (K3) of the previous sample.  thr[] then admits about
+            // k * N / sample candidates in the full scan, so its in-scan selects
+            // are rare.  The samples are re-scanned by the full scan (their keys
+            // must be in its list); cost ~ 2% of the scan at N = 1e8.
+            for (uint64_t wt = WARM_TILES; ntiles >= 8 * wt && ix->n > ix->cand_cap / 8; wt *= 8) {
                 pb::ScanArgs w = a;
-                const size_t nblk_w = ix->cand_w_cap / pb::BS + 1;
+                const size_t nblk_w = ix->cand_w_cap / 256 + 1;
                 CK(cudaMemsetAsync(ix->ctrl_w, 0, (NQB + 4 + NQB * nblk_w) * 4, s));
                 w.cand = ix->cand_w;
                 w.cap = ix->cand_w_cap;
@@ -367,11 +374,16 @@ void run_batches(poly_b200_index* ix, const float* d_queries, uint64_t nq, const
                 w.work = ix->ctrl_w + NQB + 1;
                 w.bdone = ix->ctrl_w + NQB + 4;
                 w.surv = ix->surv_w;
-                w.ntiles = WARM_TILES;
-                w.tile_stride = ntiles / WARM_TILES;
+                w.ntiles = wt;
+                w.tile_stride = ntiles / wt;
                 w.tiles_per_chunk = (uint32_t)WARM_TILES;
-                w.units = w.ngroups;
-                pb::launch_scan(w, strategy, ix->m, ix->num_sms, s);
+                w.units = (uint32_t)(wt / WARM_TILES) * w.ngroups;
+                w.bs = ix->cand_w_cap;  // no in-scan selects: the whole sample is ranked below
+                pb::launch_scan(w, strategy, ix->m, false, ix->num_sms, s);
+                // an overflowed sample list is only a weaker (still valid) bound: ranks
+                // of a subset of the sample's keys
+                pb::launch_topk(ix->cand_w, ix->ctrl_w, ix->cand_w_cap, 1, 0, 0, nqb, k, ix->keys, ix->kcounts, s);
+                pb::launch_seed_thr(ix->keys, ix->kcounts, nqb, k, ix->thr, s);
             }
             a.cand = ix->cand;
             a.cap = ix->cand_cap;
@@ -379,11 +391,12 @@ void run_batches(poly_b200_index* ix, const float* d_queries, uint64_t nq, const
             a.overflow = ix->ctrl + NQB;
             a.work = ix->ctrl + NQB + 1;
             a.bdone = ix->ctrl + NQB + 4;
-            a.surv = ix->surv;
+            a.surv = perq ? ix->surv : ix->surv_total;
             const uint64_t want = std::max<uint64_t>(1, ntiles * a.ngroups / (8ull * ix->num_sms));
             a.tiles_per_chunk = (uint32_t)std::min<uint64_t>(64, want);
             a.ntiles = ntiles;
             a.tile_stride = 1;
+            a.bs = ix->cand_bs;
             a.units = (uint32_t)((ntiles + a.tiles_per_chunk - 1) / a.tiles_per_chunk) * a.ngroups;
             cudaEvent_t e0 = nullptr, e1 = nullptr;
             if (ix->profiling) {
@@ -398,7 +411,7 @@ void run_batches(poly_b200_index* ix, const float* d_queries, uint64_t nq, const
                 ++ix->prof_used;
                 CK(cudaEventRecord(e0, s));
             }
-            pb::launch_scan(a, strategy, ix->m, ix->num_sms, s);
+            pb::launch_scan(a, strategy, ix->m, perq, ix->num_sms, s);
             if (e1) CK(cudaEventRecord(e1, s));
             CK(cudaGetLastError());
             pb::launch_topk(ix->cand, ix->ctrl, ix->cand_cap, 1, 0, 0, nqb, k, ix->keys, ix->kcounts, s);
@@ -420,6 +433,8 @@ __global__ void surv_out_kernel(const unsigned long long* surv, uint32_t nqb, ui
     if (i < nqb) out[i] = mode == 0 ? 0 : (mode == 1 ? fill : surv[i]);
 }
 
+// Returns the strategy-level survivor semantics: 0 none (adc/binary/disidx),
+// 1 all codes survive (dual at tau = code_bits), 2 counted by the scan.
 int device_search(poly_b200_index* ix, const float* d_queries, uint64_t nq, const poly_b200_search_params* p,
                   int64_t* d_ids, float* d_scores, uint32_t* d_counts, uint64_t* d_surv, cudaStream_t s) {
     validate_params(ix, p);
@@ -433,16 +448,34 @@ int device_search(poly_b200_index* ix, const float* d_queries, uint64_t nq, cons
         return 0;
     }
     const uint32_t k = p->k;
-    run_batches(ix, d_queries, nq, p, s, [&](uint64_t b0, uint32_t nqb, bool dual, bool all_pass) {
+    int mode = 0;
+    run_batches(ix, d_queries, nq, p, d_surv != nullptr, s, [&](uint64_t b0, uint32_t nqb, bool dual, bool all_pass) {
+        mode = dual ? 2 : (all_pass ? 1 : 0);
         pb::launch_keys_to_ids(ix->keys, ix->kcounts, nqb, k, ix->d_rank_to_id, d_ids + b0 * k, d_scores + b0 * k,
                                d_counts ? d_counts + b0 : nullptr, s);
         if (d_surv) {
-            const int mode = dual ? 2 : (all_pass ? 1 : 0);
             surv_out_kernel<<<(nqb + 127) / 128, 128, 0, s>>>(ix->surv, nqb, ix->n, mode, d_surv + b0);
             pb::count_launch();
         }
     });
-    return 0;
+    return mode;
+}
+
+// Exact survivor total of the last device_search (syncs the stream).
+uint64_t survivor_total(poly_b200_index* ix, int mode, uint64_t nq, const uint64_t* d_surv, cudaStream_t s) {
+    if (mode == 0 || nq == 0) return 0;
+    if (mode == 1) return ix->n * nq;
+    uint64_t t = 0;
+    if (d_surv) {
+        std::vector<uint64_t> h(nq);
+        CK(cudaMemcpyAsync(h.data(), d_surv, nq * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        for (uint64_t v : h) t += v;
+    } else {
+        CK(cudaMemcpyAsync(&t, ix->surv_total, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    return t;
 }
 
 void ensure_host_staging(poly_b200_index* ix, uint64_t nq, uint32_t k) {
@@ -514,7 +547,7 @@ int poly_b200_destroy(poly_b200_index* ix) {
             for (void* p : {(void*)ix->d_codebooks, (void*)ix->d_perms, (void*)ix->d_codes, (void*)ix->d_id32,
                             (void*)ix->d_rank_to_id, (void*)ix->lutp, (void*)ix->qcodes, (void*)ix->cand,
                             (void*)ix->ctrl, (void*)ix->thr, (void*)ix->surv,
-                            (void*)ix->surv_w, (void*)ix->cand_w, (void*)ix->ctrl_w, (void*)ix->keys, (void*)ix->kcounts,
+                            (void*)ix->surv_w, (void*)ix->surv_total, (void*)ix->cand_w, (void*)ix->ctrl_w, (void*)ix->keys, (void*)ix->kcounts,
                             (void*)ix->sticky_overflow, (void*)ix->d_q, (void*)ix->d_oid, (void*)ix->d_osc,
                             (void*)ix->d_ocnt, (void*)ix->d_osurv})
                 dfree(p);
@@ -623,21 +656,10 @@ int poly_b200_search_batch_device(poly_b200_index* ix, const float* d_queries, u
         std::lock_guard<std::mutex> lk(ix->mu);
         DeviceGuard dg(ix->device);
         cudaStream_t s = (cudaStream_t)stream;
-        uint64_t* surv = d_surv;
-        if (stats && !surv && nq) {
-            ensure_host_staging(ix, nq, p ? p->k : 1);
-            surv = ix->d_osurv;
-        }
-        device_search(ix, d_queries, nq, p, d_ids, d_scores, d_counts, surv, s);
+        const int mode = device_search(ix, d_queries, nq, p, d_ids, d_scores, d_counts, d_surv, s);
         if (stats) {
             stats->scanned = ix->n * nq;
-            stats->survivors = 0;
-            if (nq) {
-                std::vector<uint64_t> h(nq);
-                CK(cudaMemcpyAsync(h.data(), surv, nq * 8, cudaMemcpyDeviceToHost, s));
-                CK(cudaStreamSynchronize(s));
-                for (uint64_t v : h) stats->survivors += v;
-            }
+            stats->survivors = survivor_total(ix, mode, nq, d_surv, s);
             check_pending(ix, true);
         }
     });
@@ -657,20 +679,14 @@ int poly_b200_search_batch(poly_b200_index* ix, const float* queries, uint64_t n
         ensure_host_staging(ix, nq, k);
         cudaStream_t s = ix->stream;
         CK(cudaMemcpyAsync(ix->d_q, queries, nq * ix->dim * 4, cudaMemcpyHostToDevice, s));
-        device_search(ix, ix->d_q, nq, p, ix->d_oid, ix->d_osc, ix->d_ocnt, ix->d_osurv, s);
+        const int mode = device_search(ix, ix->d_q, nq, p, ix->d_oid, ix->d_osc, ix->d_ocnt, nullptr, s);
         if (k) {
             CK(cudaMemcpyAsync(out_ids, ix->d_oid, nq * k * 8, cudaMemcpyDeviceToHost, s));
             CK(cudaMemcpyAsync(out_scores, ix->d_osc, nq * k * 4, cudaMemcpyDeviceToHost, s));
         }
         if (out_counts) CK(cudaMemcpyAsync(out_counts, ix->d_ocnt, nq * 4, cudaMemcpyDeviceToHost, s));
-        std::vector<uint64_t> h;
-        if (stats) {
-            h.resize(nq);
-            CK(cudaMemcpyAsync(h.data(), ix->d_osurv, nq * 8, cudaMemcpyDeviceToHost, s));
-        }
         CK(cudaStreamSynchronize(s));
-        if (stats)
-            for (uint64_t v : h) stats->survivors += v;
+        if (stats) stats->survivors = survivor_total(ix, mode, nq, nullptr, s);
         check_pending(ix, true);
     });
 }
@@ -687,7 +703,7 @@ int poly_b200_search_keys_device(poly_b200_index* ix, const float* d_queries, ui
         cudaStream_t s = (cudaStream_t)stream;
         check_pending(ix, false);
         const uint32_t k = p->k;
-        run_batches(ix, d_queries, nq, p, s, [&](uint64_t b0, uint32_t nqb, bool dual, bool all_pass) {
+        run_batches(ix, d_queries, nq, p, d_surv != nullptr, s, [&](uint64_t b0, uint32_t nqb, bool dual, bool all_pass) {
             CK(cudaMemcpyAsync(d_keys + b0 * k, ix->keys, (size_t)nqb * k * 8, cudaMemcpyDeviceToDevice, s));
             CK(cudaMemcpyAsync(d_counts + b0, ix->kcounts, nqb * 4, cudaMemcpyDeviceToDevice, s));
             if (d_surv) {

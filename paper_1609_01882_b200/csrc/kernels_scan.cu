@@ -1,28 +1,35 @@
 // kernels_scan.cu -- K2: fused Hamming filter + ADC + candidate scan (sm_100a).
 //
 // One pass over the database per query group replaces the reference's two
-// passes (SPEC.md:336 restated in the oracle):
+// passes (restated in the oracle):
 //   hamming_bytes   flat_index.hpp:14-27   popc(qcode ^ code), kept iff h <= tau
 //   adc_distance    pq.cpp:121-128         acc = 0; acc += LUTp[sq][field_sq] in sq order
-//   TopK::offer     flat_index.hpp:64-76   replaced by key-threshold candidate append; the
+//   TopK::offer     flat_index.hpp:64-76   replaced by a key-threshold candidate append; the
 //                                          exact top-k is taken by K3 (kernels_topk.cu)
 //
-// Work unit = (chunk of tiles, group of Q queries).  A CTA owns one unit at a
-// time (dynamic fetch).  Code tiles stream HBM -> shared memory through a
-// 4-deep ring of 1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx).
-// Each lane holds one code in registers and tests it against the Q query
-// codes; survivors are compacted with a warp ballot into a per-warp queue
-// (code + position + query).  Whenever 32 entries are queued the warp drains
-// them with all lanes busy: 8/16 gathers from the query's stored-field LUT in
-// shared memory, summed in sub-quantizer order with __fadd_rn (bit-exact).
+// CTA = W consumer warps + 1 TMA producer warp.  Work unit = (chunk of tiles,
+// group of Q queries), fetched dynamically.  The producer streams 16 KB code
+// tiles HBM -> shared memory through a STAGES-deep ring of 1-D bulk copies
+// (cp.async.bulk + mbarrier complete_tx) and recycles a stage once all W
+// consumer warps have arrived on its "empty" mbarrier -- no CTA-wide barrier
+// per tile.  Each consumer lane holds one code in registers and tests it
+// against the Q query codes branch-free (xor + 2 POPC + compare per pair),
+// building a per-lane survivor mask; a warp prefix scan compacts survivors
+// into a per-warp ring of 4-byte entries (query | tile index).  Whenever 32
+// entries are queued the warp drains them with all lanes busy: the code is
+// re-read from the tile, 8/16 gathers from the query's stored-field LUT in
+// shared memory are summed in sub-quantizer order with __fadd_rn (bit-exact
+// with the reference), and the key is tested against the query's threshold.
 //
 // Candidates: key = (fp32 score bits << 32) | id-rank (scores are >= 0 so the
 // bits are monotone; ranks are distinct) -- a strict total order equal to the
 // SPEC (score, id) order.  A candidate is appended to its query's global list
 // when key < thr[q].  thr[q] is an upper bound of the final k-th key: whenever
-// a block of BS consecutive list slots completes, the CTA that completed it
-// selects the block's k-th smallest key (radix select) and atomicMin's it
-// into thr[q].  Every final top-k member is therefore in the list.
+// a block of BS consecutive list slots completes, the producer warp of the
+// CTA that completed it selects the block's k-th smallest key (radix select)
+// and atomicMin's it into thr[q].  thr[] starts from the exact k-th key of
+// strided warm-up samples (capi.cu), so these selects are rare.  Every final
+// top-k member is in the list; K3 takes the exact top-k.
 #include "poly_b200.cuh"
 
 namespace pb {
@@ -71,6 +78,10 @@ __device__ __forceinline__ uint32_t key_low(const ScanArgs& a, uint32_t pos) {
     return a.id_mode == ID_ARITH ? a.id0 + pos : __ldg(a.id32 + pos);
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 // Append a candidate key for batch query qg; track block completion.
 __device__ __forceinline__ void append_candidate(const ScanArgs& a, uint32_t qg, unsigned long long key, uint32_t bs,
                                                  uint32_t* nreq_s, uint32_t* req_s) {
@@ -84,93 +95,145 @@ __device__ __forceinline__ void append_candidate(const ScanArgs& a, uint32_t qg,
     const uint32_t nblk = a.cap / bs;
     const uint32_t blk = slot / bs;
     if (atomicAdd(&a.bdone[(size_t)qg * nblk + blk], 1u) == bs - 1) {
+        // request ring served by the producer warp; a full ring drops the request
+        // (thresholds are an optimisation, never needed for correctness)
         const uint32_t r = atomicAdd(nreq_s, 1u);
-        if (r < MAXREQ) req_s[r] = (qg << 16) | blk;
+        req_s[r % MAXREQ] = (qg << 16) | blk;
     }
 }
 
-// k-th smallest (1-based) of n distinct keys in global memory; CTA-cooperative
-// 8-pass radix select, keys streamed from L2 each pass.
-template <int NT>
-__device__ unsigned long long block_select_kth(const unsigned long long* src, uint32_t n, uint32_t kk,
-                                               uint32_t* hist, unsigned long long* prefix_s, uint32_t* k_s) {
+__device__ __forceinline__ void try_candidate(const ScanArgs& a, uint32_t qg, float score, uint32_t pos,
+                                              unsigned long long thr, uint32_t bs, uint32_t* nreq_s, uint32_t* req_s) {
+    const uint32_t sb = __float_as_uint(score);
+    if (sb <= (uint32_t)(thr >> 32)) {
+        const unsigned long long key = ((unsigned long long)sb << 32) | key_low(a, pos);
+        if (key < thr) append_candidate(a, qg, key, bs, nreq_s, req_s);
+    }
+}
+
+// k-th smallest (1-based) of n distinct keys in global memory; one warp,
+// 8-pass radix select over 8-bit digits, keys streamed from L2 each pass.
+__device__ unsigned long long warp_select_kth(const unsigned long long* src, uint32_t n, uint32_t kk, uint32_t* hist) {
+    const int lane = threadIdx.x & 31;
     unsigned long long prefix = 0, mask = 0;
     for (int shift = 56; shift >= 0; shift -= 8) {
-        for (int i = threadIdx.x; i < 256; i += NT) hist[i] = 0;
-        __syncthreads();
-        for (uint32_t i = threadIdx.x; i < n; i += NT) {
+        for (int i = lane; i < 256; i += 32) hist[i] = 0;
+        __syncwarp();
+#pragma unroll 16
+        for (uint32_t i = lane; i < n; i += 32) {
             const unsigned long long v = __ldcg(src + i);
             if ((v & mask) == prefix) atomicAdd(&hist[(v >> shift) & 0xFFu], 1u);
         }
-        __syncthreads();
-        if (threadIdx.x < 32) {
-            const int lane = threadIdx.x;
-            uint32_t c[8], s = 0;
+        __syncwarp();
+        uint32_t c[8], s = 0;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) { c[j] = hist[lane * 8 + j]; s += c[j]; }
-            uint32_t incl = s;
+        for (int j = 0; j < 8; ++j) { c[j] = hist[lane * 8 + j]; s += c[j]; }
+        uint32_t incl = s;
 #pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
-                if (lane >= off) incl += o;
-            }
-            const uint32_t excl = incl - s;
-            if (excl < kk && kk <= incl) {
-                uint32_t r = kk - excl;
-                int digit = lane * 8 + 7;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    if (r <= c[j]) { digit = lane * 8 + j; break; }
-                    r -= c[j];
-                }
-                *prefix_s = prefix | ((unsigned long long)digit << shift);
-                *k_s = r;
-            }
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += o;
         }
-        __syncthreads();
-        prefix = *prefix_s;
-        kk = *k_s;
+        const uint32_t excl = incl - s;
+        const bool mine = excl < kk && kk <= incl;
+        uint32_t r = kk - excl;
+        int digit = lane * 8 + 7;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (r <= c[j]) { digit = lane * 8 + j; break; }
+            r -= c[j];
+        }
+        const int src_lane = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+        digit = __shfl_sync(0xffffffffu, digit, src_lane);
+        kk = __shfl_sync(0xffffffffu, r, src_lane);
+        prefix |= (unsigned long long)digit << shift;
         mask |= 0xFFull << shift;
+        __syncwarp();
     }
     return prefix;
 }
 
-template <int M, int Q, int W, int STRAT>
-__global__ void __launch_bounds__(W * 32, 1) scan_kernel(const ScanArgs a, uint32_t bs) {
+constexpr int RING = 512;  // per-warp survivor ring (4-byte entries)
+
+template <int M, int Q, int W>
+struct ScanSmem {
+    static constexpr int TC = 16384 / M;                    // codes per 16 KB tile
+    // Query q's LUT starts at q * LS floats; the +4 skew puts the same stored
+    // field of different queries in different banks (a drain holds several
+    // queries' entries for the same code).
+    static constexpr int LS = M * KSUB + 4;
+    static constexpr size_t LUT_BYTES = (size_t)Q * LS * 4;
+    static constexpr size_t TILE_BYTES = (size_t)STAGES * 16384;
+    static constexpr size_t RING_BYTES = (size_t)W * RING * 4;
+    static constexpr size_t TOTAL = LUT_BYTES + TILE_BYTES + RING_BYTES;
+};
+
+// PERQ: per-query survivor counts (ballot + popc per query) instead of the
+// free per-batch total.
+template <int M, int Q, int W, int STRAT, bool PERQ>
+__global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a) {
+    const uint32_t bs = a.bs;
     using C = typename CodeT<M>::T;
-    constexpr int NT = W * 32;
-    constexpr int TC = 16384 / M;   // codes per 16 KB tile
-    constexpr int CPW = TC / W;     // codes per warp per tile
+    using SM = ScanSmem<M, Q, W>;
+    constexpr int NT = (W + 1) * 32;
+    constexpr int TC = SM::TC;
+    constexpr int CPW = TC / W;     // codes per consumer warp per tile
     constexpr bool USE_LUT = (STRAT == DUAL || STRAT == ADC);
-    constexpr int LUT_FLOATS = USE_LUT ? Q * M * KSUB : 0;
+    static_assert(CPW % 32 == 0, "tile must split evenly over the consumer warps");
 
     extern __shared__ __align__(128) uint8_t smem[];
     float* lut = reinterpret_cast<float*>(smem);
-    C* tiles = reinterpret_cast<C*>(smem + LUT_FLOATS * 4);
-    C* qu_code = tiles + STAGES * TC;                          // W x QCAP
-    uint2* qu_meta = reinterpret_cast<uint2*>(qu_code + W * QCAP);  // (pos, q)
+    C* tiles = reinterpret_cast<C*>(smem + (USE_LUT ? SM::LUT_BYTES : 0));
+    uint32_t* rings = reinterpret_cast<uint32_t*>(smem + (USE_LUT ? SM::LUT_BYTES : 0) + SM::TILE_BYTES);
 
     __shared__ __align__(8) uint64_t full_bar[STAGES];
+    __shared__ __align__(8) uint64_t empty_bar[STAGES];
     __shared__ unsigned long long thr_s[Q];
     __shared__ C qc_s[Q];
+    __shared__ uint32_t surv_s[Q];
     __shared__ uint32_t unit_s, nreq_s, group_s;
     __shared__ uint32_t req_s[MAXREQ];
     __shared__ uint32_t sel_hist[256];
-    __shared__ unsigned long long sel_prefix_s;
-    __shared__ uint32_t sel_k_s;
+    __shared__ uint32_t req_head_s;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool producer = warp == W;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) mbar_init(&full_bar[s], 1);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], W);
+        }
         fence_mbar_init();
         nreq_s = 0;
+        req_head_s = 0;
         group_s = 0xFFFFFFFFu;
     }
     __syncthreads();
 
-    C* myq_code = qu_code + warp * QCAP;
-    uint2* myq_meta = qu_meta + warp * QCAP;
-    uint32_t seq = 0;  // tiles consumed by this CTA (stage = seq % STAGES, parity = (seq / STAGES) & 1)
+    uint32_t* ring = rings + (producer ? 0 : warp) * RING;
+    uint32_t seq = 0;
+
+    // producer warp: serve threshold selects requested by the consumers' appends
+    auto serve_selects = [&]() {
+        for (;;) {
+            uint32_t req = 0xFFFFFFFFu;
+            if (lane == 0) {
+                const uint32_t tail = *(volatile uint32_t*)&nreq_s;
+                if (req_head_s != tail) {
+                    if (tail - req_head_s > MAXREQ) req_head_s = tail - MAXREQ;  // dropped requests
+                    req = *(volatile uint32_t*)&req_s[req_head_s % MAXREQ];
+                    ++req_head_s;
+                }
+            }
+            req = __shfl_sync(0xffffffffu, req, 0);
+            if (req == 0xFFFFFFFFu) break;
+            const uint32_t qg = req >> 16, blk = req & 0xFFFFu;
+            __threadfence();
+            const unsigned long long kth =
+                warp_select_kth(a.cand + (size_t)qg * a.cap + (size_t)blk * bs, bs, a.k, sel_hist);
+            if (lane == 0) atomicMin(a.thr + qg, kth);
+        }
+    };  // tiles consumed so far: stage = seq % STAGES, parity = (seq / STAGES) & 1
 
     for (;;) {
         if (threadIdx.x == 0) unit_s = atomicAdd(a.work, 1u);
@@ -183,180 +246,194 @@ __global__ void __launch_bounds__(W * 32, 1) scan_kernel(const ScanArgs a, uint3
         const uint64_t t0 = (uint64_t)chunk * a.tiles_per_chunk;
         const uint32_t ntile = (uint32_t)min((uint64_t)a.tiles_per_chunk, a.ntiles - t0);
 
-        // producer prologue: fill the ring
-        auto issue = [&](uint32_t s_seq, uint64_t t) {
-            const uint32_t s = s_seq % STAGES;
-            const uint64_t first = t * a.tile_stride * TC;
-            const uint64_t cnt = min((uint64_t)TC, a.n - first);
-            const uint32_t bytes = (uint32_t)((cnt * M + 15) & ~15ull);
-            mbar_arrive_expect_tx(&full_bar[s], bytes);
-            bulk_g2s(tiles + s * TC, a.codes + first * M, bytes, &full_bar[s]);
-        };
-        if (threadIdx.x == 0) {
-            for (uint32_t j = 0; j < min((uint32_t)STAGES, ntile); ++j) issue(seq + j, t0 + j);
-        }
         // per-group state: LUTs (only when the group changes), query codes, thresholds
         if (group_s != g) {
             if (USE_LUT) {
                 const float4* src = reinterpret_cast<const float4*>(a.lutp + (size_t)q0 * M * KSUB);
-                float4* dst = reinterpret_cast<float4*>(lut);
-                const uint32_t n4 = nqh * M * KSUB / 4;
-                for (uint32_t i = threadIdx.x; i < n4; i += NT) dst[i] = __ldg(src + i);
+                constexpr uint32_t PER_Q = M * KSUB / 4;
+                const uint32_t n4 = nqh * PER_Q;
+                for (uint32_t i = threadIdx.x; i < n4; i += NT) {
+                    const uint32_t q = i / PER_Q, r = i % PER_Q;
+                    reinterpret_cast<float4*>(lut + q * SM::LS)[r] = __ldg(src + i);
+                }
             }
             if (threadIdx.x < Q)
                 qc_s[threadIdx.x] = threadIdx.x < nqh ? reinterpret_cast<const C*>(a.qcodes)[q0 + threadIdx.x] : C{};
         }
-        if (threadIdx.x < Q) thr_s[threadIdx.x] = threadIdx.x < nqh ? __ldcg(a.thr + q0 + threadIdx.x) : 0ull;
+        if (threadIdx.x < Q) {
+            thr_s[threadIdx.x] = threadIdx.x < nqh ? __ldcg(a.thr + q0 + threadIdx.x) : 0ull;
+            surv_s[threadIdx.x] = 0;
+        }
         __syncthreads();
         if (threadIdx.x == 0) group_s = g;
 
-        C qc[Q];
-#pragma unroll
-        for (int q = 0; q < Q; ++q) qc[q] = qc_s[q];
-        uint32_t surv[Q];
-#pragma unroll
-        for (int q = 0; q < Q; ++q) surv[q] = 0;
-        uint32_t qn = 0;  // entries in this warp's queue
-
-        // drain `cnt` queued survivors (lanes < cnt busy): ADC + candidate test
-        auto drain = [&](uint32_t cnt) {
-            __syncwarp();
-            if ((uint32_t)lane < cnt) {
-                const C code = myq_code[lane];
-                const uint2 meta = myq_meta[lane];
-                const float* L = lut + meta.y * (M * KSUB);
-                const float score = adc<M>(L, code);
-                const uint32_t sb = __float_as_uint(score);
-                const unsigned long long thr = thr_s[meta.y];
-                if (sb <= (uint32_t)(thr >> 32)) {
-                    const unsigned long long key = ((unsigned long long)sb << 32) | key_low(a, meta.x);
-                    if (key < thr) append_candidate(a, q0 + meta.y, key, bs, &nreq_s, req_s);
+        if (producer) {
+            for (uint32_t j = 0; j < ntile; ++j) {
+                if (lane == 0) {
+                    const uint32_t sq_ = seq + j, s = sq_ % STAGES;
+                    if (sq_ >= STAGES) mbar_wait(&empty_bar[s], ((sq_ / STAGES) - 1) & 1u);
+                    const uint64_t first = (t0 + j) * a.tile_stride * TC;
+                    const uint64_t cnt = min((uint64_t)TC, a.n - first);
+                    const uint32_t bytes = (uint32_t)((cnt * M + 15) & ~15ull);
+                    mbar_arrive_expect_tx(&full_bar[s], bytes);
+                    bulk_g2s(tiles + s * TC, a.codes + first * M, bytes, &full_bar[s]);
                 }
+                serve_selects();
+                // keep the consumers' thresholds fresh (benign race: aligned 64-bit stores)
+                if (lane < nqh) {
+                    const unsigned long long t = __ldcg(a.thr + q0 + lane);
+                    if (t < thr_s[lane]) thr_s[lane] = t;
+                }
+                __syncwarp();
             }
-            __syncwarp();
-        };
-
-        for (uint32_t j = 0; j < ntile; ++j) {
-            const uint32_t s = (seq + j) % STAGES;
-            mbar_wait(&full_bar[s], ((seq + j) / STAGES) & 1u);
-            const C* T = tiles + s * TC;
-            const uint64_t tfirst = (t0 + j) * a.tile_stride * TC;
-            const uint32_t tcnt = (uint32_t)min((uint64_t)TC, a.n - tfirst);
-#pragma unroll 1
-            for (int i = 0; i < CPW / 32; ++i) {
-                const uint32_t li = warp * CPW + i * 32 + lane;
-                const bool in = li < tcnt;
-                const C code = T[li];
-                const uint32_t pos = (uint32_t)(tfirst + li);
-                if constexpr (STRAT == DUAL) {
+        } else {
+            C qc[Q];
 #pragma unroll
-                    for (int q = 0; q < Q; ++q) {
-                        if (q >= (int)nqh) break;
-                        const bool pass = in && ham(code, qc[q]) <= a.tau;
-                        const uint32_t b = __ballot_sync(0xffffffffu, pass);
-                        if (b) {
-                            const uint32_t nb = __popc(b);
-                            surv[q] += nb;
-                            if (pass) {
-                                const uint32_t at = qn + __popc(b & lanemask_lt());
-                                myq_code[at] = code;
-                                myq_meta[at] = make_uint2(pos, (uint32_t)q);
+            for (int q = 0; q < Q; ++q) qc[q] = qc_s[q];
+            const uint32_t vmask = nqh >= 32 ? 0xFFFFFFFFu : ((1u << nqh) - 1u);
+            uint32_t head = 0, qn = 0;  // ring: entries [head, head + qn)
+            uint32_t tot = 0;           // survivors seen by this warp (warp-uniform)
+            uint32_t survq[PERQ ? Q : 1];
+#pragma unroll
+            for (int q = 0; q < (PERQ ? Q : 1); ++q) survq[q] = 0;
+
+            // ADC + candidate test for `cnt` queued survivors (lanes < cnt busy)
+            auto drain = [&](const C* T, uint64_t tfirst, uint32_t cnt) {
+                if ((uint32_t)lane < cnt) {
+                    const uint32_t e = ring[(head + lane) & (RING - 1)];
+                    const uint32_t q = e >> 16, li = e & 0xFFFFu;
+                    const C code = T[li];
+                    const float score = adc<M>(lut + q * SM::LS, code);
+                    try_candidate(a, q0 + q, score, (uint32_t)(tfirst + li), thr_s[q], bs, &nreq_s, req_s);
+                }
+                head += cnt;
+                qn -= cnt;
+                __syncwarp();
+            };
+
+            for (uint32_t j = 0; j < ntile; ++j) {
+                const uint32_t sq_ = seq + j, s = sq_ % STAGES;
+                mbar_wait(&full_bar[s], (sq_ / STAGES) & 1u);
+                const C* T = tiles + s * TC;
+                const uint64_t tfirst = (t0 + j) * a.tile_stride * TC;
+                const uint32_t tcnt = (uint32_t)min((uint64_t)TC, a.n - tfirst);
+#pragma unroll 1
+                for (int i = 0; i < CPW / 32; ++i) {
+                    const uint32_t li = warp * CPW + i * 32 + lane;
+                    const bool in = li < tcnt;
+                    const C code = T[li];
+                    if constexpr (STRAT == DUAL) {
+                        // filter in halves of Q/2 queries so one half adds <= 32*Q/2 ring entries
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            uint32_t m = 0;
+#pragma unroll
+                            for (int q = h * (Q / 2); q < (h + 1) * (Q / 2); ++q)
+                                m |= (ham(code, qc[q]) <= a.tau ? 1u : 0u) << q;
+                            m &= in ? vmask : 0u;
+                            if constexpr (PERQ) {
+#pragma unroll
+                                for (int q = h * (Q / 2); q < (h + 1) * (Q / 2); ++q)
+                                    survq[q] += __popc(__ballot_sync(0xffffffffu, (m >> q) & 1u));
                             }
-                            qn += nb;
-                            if (qn >= 32) {
-                                drain(32);
-                                qn -= 32;
-                                if ((uint32_t)lane < qn) {
-                                    myq_code[lane] = myq_code[32 + lane];
-                                    myq_meta[lane] = myq_meta[32 + lane];
+                            if (__any_sync(0xffffffffu, m != 0)) {
+                                const uint32_t cnt = __popc(m);
+                                uint32_t incl = cnt;
+#pragma unroll
+                                for (int off = 1; off < 32; off <<= 1) {
+                                    const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
+                                    if (lane >= off) incl += o;
                                 }
+                                const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+                                uint32_t at = head + qn + incl - cnt;
+                                while (m) {
+                                    const uint32_t q = __ffs(m) - 1;
+                                    m &= m - 1;
+                                    ring[at & (RING - 1)] = (q << 16) | li;
+                                    ++at;
+                                }
+                                qn += total;
+                                tot += total;
                                 __syncwarp();
+                                while (qn >= 32) drain(T, tfirst, 32);
                             }
                         }
-                    }
-                } else {
-                    // adc / binary / disidx: every code is scored for every query
-#pragma unroll 1
-                    for (int q = 0; q < (int)nqh; ++q) {
-                        float score;
-                        if constexpr (STRAT == ADC) score = adc<M>(lut + q * (M * KSUB), code);
-                        else if constexpr (STRAT == BINARY) score = (float)ham(code, qc_s[q]);
-                        else score = (float)disidx(code, qc_s[q]);
+                    } else {
+                        // adc / binary / disidx: every code is scored for every query
                         if (in) {
-                            const uint32_t sb = __float_as_uint(score);
-                            const unsigned long long thr = thr_s[q];
-                            if (sb <= (uint32_t)(thr >> 32)) {
-                                const unsigned long long key = ((unsigned long long)sb << 32) | key_low(a, pos);
-                                if (key < thr) append_candidate(a, q0 + q, key, bs, &nreq_s, req_s);
+#pragma unroll 1
+                            for (int q = 0; q < (int)nqh; ++q) {
+                                float score;
+                                if constexpr (STRAT == ADC) score = adc<M>(lut + q * SM::LS, code);
+                                else if constexpr (STRAT == BINARY) score = (float)ham(code, qc[q]);
+                                else score = (float)disidx(code, qc[q]);
+                                try_candidate(a, q0 + q, score, (uint32_t)(tfirst + li), thr_s[q], bs, &nreq_s,
+                                              req_s);
                             }
                         }
                     }
                 }
+                if constexpr (STRAT == DUAL) {
+                    if (qn) drain(T, tfirst, qn);  // entries point into this stage: flush before release
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty_bar[s]);
             }
-            __syncthreads();  // stage s fully consumed (queued survivors hold copies of their codes)
-            if (threadIdx.x == 0 && j + STAGES < ntile) issue(seq + j + STAGES, t0 + j + STAGES);
-            // threshold maintenance: selects requested by appends of this CTA
-            const uint32_t nr = min(nreq_s, (uint32_t)MAXREQ);
-            for (uint32_t r = 0; r < nr; ++r) {
-                const uint32_t qg = req_s[r] >> 16, blk = req_s[r] & 0xFFFFu;
-                __threadfence();
-                const unsigned long long kth = block_select_kth<NT>(a.cand + (size_t)qg * a.cap + (size_t)blk * bs,
-                                                                    bs, a.k, sel_hist, &sel_prefix_s, &sel_k_s);
-                if (threadIdx.x == 0) atomicMin(a.thr + qg, kth);
+            if (STRAT == DUAL && lane == 0) {
+                if constexpr (PERQ) {
+                    for (int q = 0; q < Q; ++q)
+                        if (survq[q]) atomicAdd(&surv_s[q], survq[q]);
+                } else if (tot) {
+                    atomicAdd(&surv_s[0], tot);
+                }
             }
-            __syncthreads();
-            if (threadIdx.x == 0) nreq_s = 0;
-            if (threadIdx.x < nqh) thr_s[threadIdx.x] = __ldcg(a.thr + q0 + threadIdx.x);
-            __syncthreads();
         }
         seq += ntile;
-        if constexpr (STRAT == DUAL) {
-            if (qn) drain(qn);
-            if (lane == 0)
-                for (int q = 0; q < Q; ++q)
-                    if (q < (int)nqh && surv[q]) atomicAdd(a.surv + q0 + q, (unsigned long long)surv[q]);
-        }
+        __syncthreads();
+        if (producer) serve_selects();  // blocks completed during the unit's last tiles
+        // unit boundary: survivor stats flush
+        // per-query counts -> surv[q]; totals -> surv[0] (the batch total)
+        if (STRAT == DUAL && threadIdx.x < (PERQ ? nqh : 1u) && surv_s[threadIdx.x])
+            atomicAdd(a.surv + (PERQ ? q0 + threadIdx.x : 0u), (unsigned long long)surv_s[threadIdx.x]);
         __syncthreads();
     }
 }
 
-template <int M, int Q, int W, int STRAT>
+template <int M, int Q, int W, int STRAT, bool PERQ>
 static void launch_one(const ScanArgs& a, int num_sms, cudaStream_t s) {
-    constexpr int TC = 16384 / M;
+    using SM = ScanSmem<M, Q, W>;
     constexpr bool USE_LUT = (STRAT == DUAL || STRAT == ADC);
-    const size_t smem = (USE_LUT ? (size_t)Q * M * KSUB * 4 : 0) + (size_t)STAGES * TC * M +
-                        (size_t)W * QCAP * (M + 8);
-    auto kfn = scan_kernel<M, Q, W, STRAT>;
+    const size_t smem = USE_LUT ? SM::TOTAL : SM::TOTAL - SM::LUT_BYTES;
+    auto kfn = scan_kernel<M, Q, W, STRAT, PERQ>;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    const uint32_t bs = a.k * 4 > (uint32_t)BS ? a.k * 4 : (uint32_t)BS;
     const unsigned grid = (unsigned)((uint64_t)num_sms < (uint64_t)a.units ? (uint64_t)num_sms : (uint64_t)a.units);
-    kfn<<<grid, W * 32, smem, s>>>(a, bs);
+    kfn<<<grid, (W + 1) * 32, smem, s>>>(a);
     count_launch();
 }
 
 int scan_queries_per_cta(uint32_t m) { return m == 8 ? 16 : 8; }
 
-void launch_scan(const ScanArgs& a, int strategy, uint32_t m, int num_sms, cudaStream_t s) {
-    // Q queries per CTA: Q x m x 1 KB of LUTs must fit next to the tile ring.
-    if (m == 8) {
-        switch (strategy) {
-            case DUAL: launch_one<8, 16, 16, DUAL>(a, num_sms, s); break;
-            case ADC: launch_one<8, 16, 16, ADC>(a, num_sms, s); break;
-            case BINARY: launch_one<8, 16, 16, BINARY>(a, num_sms, s); break;
-            default: launch_one<8, 16, 16, DISIDX>(a, num_sms, s); break;
-        }
-    } else {
-        switch (strategy) {
-            case DUAL: launch_one<16, 8, 16, DUAL>(a, num_sms, s); break;
-            case ADC: launch_one<16, 8, 16, ADC>(a, num_sms, s); break;
-            case BINARY: launch_one<16, 8, 16, BINARY>(a, num_sms, s); break;
-            default: launch_one<16, 8, 16, DISIDX>(a, num_sms, s); break;
-        }
+template <int M, int Q, int W>
+static void launch_m(const ScanArgs& a, int strategy, bool perq, int num_sms, cudaStream_t s) {
+    switch (strategy) {
+        case DUAL:
+            if (perq) launch_one<M, Q, W, DUAL, true>(a, num_sms, s);
+            else launch_one<M, Q, W, DUAL, false>(a, num_sms, s);
+            break;
+        case ADC: launch_one<M, Q, W, ADC, false>(a, num_sms, s); break;
+        case BINARY: launch_one<M, Q, W, BINARY, false>(a, num_sms, s); break;
+        default: launch_one<M, Q, W, DISIDX, false>(a, num_sms, s); break;
     }
+}
+
+void launch_scan(const ScanArgs& a, int strategy, uint32_t m, bool per_query_stats, int num_sms, cudaStream_t s) {
+    // Q queries per CTA: Q x m x 1 KB of LUTs must fit next to the tile ring.
+    if (m == 8) launch_m<8, 16, 16>(a, strategy, per_query_stats, num_sms, s);
+    else launch_m<16, 8, 16>(a, strategy, per_query_stats, num_sms, s);
 }
 
 }  // namespace pb

@@ -183,3 +183,22 @@ void launch_or_flag(uint32_t* dst, const uint32_t* src, cudaStream_t s) {
     count_launch();
 }
 }  // namespace pb
+
+namespace pb {
+// thr[q] = min(thr[q], k-th key of the warm-up sample + 1) -- +1 so that key
+// itself is appended again by the full scan; unchanged when the sample held
+// fewer than k candidates.
+__global__ void seed_thr_kernel(const unsigned long long* keys, const uint32_t* counts, uint32_t nq, uint32_t k,
+                                unsigned long long* thr) {
+    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < nq && counts[q] >= k) {
+        const unsigned long long t = keys[(size_t)q * k + k - 1] + 1;
+        if (t < thr[q]) thr[q] = t;
+    }
+}
+void launch_seed_thr(const unsigned long long* keys, const uint32_t* counts, uint32_t nq, uint32_t k,
+                     unsigned long long* thr, cudaStream_t s) {
+    seed_thr_kernel<<<(nq + 127) / 128, 128, 0, s>>>(keys, counts, nq, k, thr);
+    count_launch();
+}
+}  // namespace pb

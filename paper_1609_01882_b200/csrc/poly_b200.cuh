@@ -13,7 +13,7 @@ constexpr int STAGES = 4;              // bulk-copy ring depth
 constexpr int BS = 4096;               // candidate block size for threshold selects
 constexpr int KMAX = 2048;             // largest supported k
 constexpr int QCAP = 64;               // per-warp survivor queue entries
-constexpr int MAXREQ = 16;             // pending threshold selects per CTA
+constexpr int MAXREQ = 32;             // pending threshold selects per CTA (ring)
 constexpr uint64_t KEY_INF = ~0ull;
 
 enum Strategy { ADC = 0, BINARY = 1, DISIDX = 2, DUAL = 3 };
@@ -34,12 +34,13 @@ struct ScanArgs {
     uint32_t* ccount;            // nqb
     uint32_t* bdone;             // nqb x (cap / BS) completion counters
     unsigned long long* thr;     // nqb running upper bounds of the k-th key
-    unsigned long long* surv;    // nqb survivor counts
+    unsigned long long* surv;    // per-query survivor counts (per_query_stats) or [0] = batch total
     uint32_t* overflow;          // set when a candidate did not fit
     uint32_t* work;              // dynamic work-unit counter
     uint32_t units, ngroups, tiles_per_chunk;
     uint64_t ntiles;             // logical tiles; physical tile = logical * tile_stride
     uint64_t tile_stride;
+    uint32_t bs;                 // candidate block size (>= k) for threshold selects
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -102,7 +103,7 @@ void launch_gen_points(uint64_t seed, uint32_t stream_id, uint64_t row0, uint64_
                        uint32_t ncent, uint32_t dim, int normalize, float* out, cudaStream_t s);
 
 // K2: fused filter + ADC + candidate scan.
-void launch_scan(const ScanArgs& a, int strategy, uint32_t m, int num_sms, cudaStream_t s);
+void launch_scan(const ScanArgs& a, int strategy, uint32_t m, bool per_query_stats, int num_sms, cudaStream_t s);
 int scan_queries_per_cta(uint32_t m);
 
 // K3: per-query exact top-k over candidate keys; K3b: key -> (id, score).
@@ -120,6 +121,8 @@ void launch_hamming_hist(const uint8_t* codes, uint64_t n, uint32_t cb, const ui
 // with_assignments: relabel fields through a per-sub-quantizer byte map.
 void launch_relabel(uint8_t* codes, uint64_t n, uint32_t m, const uint8_t* maps, cudaStream_t s);
 
+void launch_seed_thr(const unsigned long long* keys, const uint32_t* counts, uint32_t nq, uint32_t k,
+                     unsigned long long* thr, cudaStream_t s);
 void launch_or_flag(uint32_t* dst, const uint32_t* src, cudaStream_t s);
 void count_launch();
 

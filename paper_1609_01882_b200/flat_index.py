@@ -209,13 +209,19 @@ class FlatIndex:
         return [Neighbor(int(ids[0, i]), float(scores[0, i])) for i in range(int(counts[0]))]
 
     def search_batch_device(self, d_queries, params: SearchParams, d_ids, d_scores, d_counts=None, d_survivors=None,
-                            stream=0):
-        """Device-resident variant: arguments are torch CUDA tensors (or raw pointers)."""
+                            stream=0, stats: SearchStats | None = None):
+        """Device-resident variant: arguments are torch CUDA tensors (or raw pointers).
+        ``d_survivors`` (per-query counts) selects the per-query-stats scan variant;
+        ``stats`` (totals) synchronises the stream."""
         ptr = lambda t: None if t is None else (t if isinstance(t, int) else t.data_ptr())  # noqa: E731
         nq = d_queries.shape[0]
+        st = SearchStatsC()
         _check(lib.poly_b200_search_batch_device(self._h, ptr(d_queries), nq, C.byref(params.c()), ptr(d_ids),
                                                  ptr(d_scores), ptr(d_counts), ptr(d_survivors), C.c_void_p(stream),
-                                                 None))
+                                                 C.byref(st) if stats is not None else None))
+        if stats is not None:
+            stats.scanned += st.scanned
+            stats.survivors += st.survivors
 
     def search_keys_device(self, d_queries, params: SearchParams, d_keys, d_counts, d_survivors=None, stream=0):
         ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731

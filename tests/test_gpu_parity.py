@@ -200,6 +200,9 @@ def test_device_api_and_sharded_merge(pb, pq8, big8):
     ocnt = torch.empty(len(queries), dtype=torch.int32, device="cuda")
     shards[0].merge_keys_device(keys, cnts, G, len(queries), k, oid, osc, ocnt)
     torch.cuda.synchronize()
+    # per-query survivor counts (the per-query-stats scan variant) == oracle
+    _, _, _, osv, _ = oracle.search(pq8, codes, queries, k, tau=tau, threads=16)
+    assert _same(surv.sum(0).cpu().numpy().astype(np.uint64), osv)
     assert _same(oid.cpu().numpy(), want[0])
     assert _same(_bits(osc.cpu().numpy()), _bits(want[1]))
     assert _same(ocnt.cpu().numpy().astype(np.uint32), want[2])
