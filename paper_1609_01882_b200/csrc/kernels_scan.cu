@@ -82,6 +82,47 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// Explicit shared-window accesses on 32-bit addresses: keeps the hot loop free
+// of generic-pointer materialisation (S2R SR_CgaCtaId + LEA per access).
+__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t lds32v(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ float ldsf(uint32_t addr) {
+    float v;
+    asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void lds_code(uint32_t addr, uint2& c) {
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(c.x), "=r"(c.y) : "r"(addr));
+}
+__device__ __forceinline__ void lds_code(uint32_t addr, uint4& c) {
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(c.x), "=r"(c.y), "=r"(c.z), "=r"(c.w) : "r"(addr));
+}
+
+// ADC from a query's stored-field LUT at shared address L (bytes), in sq order.
+template <int M, class C>
+__device__ __forceinline__ float adc_s(uint32_t L, const C& c) {
+    float acc = ldsf(L + 4u * (word(c, 0) & 0xFFu));
+#pragma unroll
+    for (int sq = 1; sq < M; ++sq) {
+        const uint32_t f = (word(c, sq >> 2) >> (8 * (sq & 3))) & 0xFFu;
+        acc = __fadd_rn(acc, ldsf(L + 4u * (sq * KSUB + f)));
+    }
+    return acc;
+}
+
+// Four Hamming distances (each <= 128) packed into the bytes of one word.
+template <class C>
+__device__ __forceinline__ uint32_t ham4(const C& code, const C* qc) {
+    const uint32_t h0 = ham(code, qc[0]), h1 = ham(code, qc[1]), h2 = ham(code, qc[2]), h3 = ham(code, qc[3]);
+    return (h0 + (h1 << 8)) + ((h2 + (h3 << 8)) << 16);
+}
+
 // Append a candidate key for batch query qg; track block completion.
 __device__ __forceinline__ void append_candidate(const ScanArgs& a, uint32_t qg, unsigned long long key, uint32_t bs,
                                                  uint32_t* nreq_s, uint32_t* req_s) {
@@ -290,7 +331,14 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
             C qc[Q];
 #pragma unroll
             for (int q = 0; q < Q; ++q) qc[q] = qc_s[q];
-            const uint32_t vmask = nqh >= 32 ? 0xFFFFFFFFu : ((1u << nqh) - 1u);
+            // survivor mask layout: query q = 4g + j -> bit 8j + g (g < Q/4, j < 4)
+            uint32_t vmask = 0;
+            for (uint32_t q = 0; q < nqh; ++q) vmask |= 1u << (8 * (q & 3) + (q >> 2));
+            // h <= tau  <=>  bit 7 of (h + 127 - tau) clear, four bytes at a time
+            const uint32_t bias = (127u - min(a.tau, 127u)) * 0x01010101u;
+            const uint32_t lut_base = smem_u32(lut);
+            const uint32_t tile_base = smem_u32(tiles);
+            const uint32_t ring_base = smem_u32(ring);
             uint32_t head = 0, qn = 0;  // ring: entries [head, head + qn)
             uint32_t tot = 0;           // survivors seen by this warp (warp-uniform)
             uint32_t survq[PERQ ? Q : 1];
@@ -298,12 +346,13 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
             for (int q = 0; q < (PERQ ? Q : 1); ++q) survq[q] = 0;
 
             // ADC + candidate test for `cnt` queued survivors (lanes < cnt busy)
-            auto drain = [&](const C* T, uint64_t tfirst, uint32_t cnt) {
+            auto drain = [&](uint32_t T, uint64_t tfirst, uint32_t cnt) {
                 if ((uint32_t)lane < cnt) {
-                    const uint32_t e = ring[(head + lane) & (RING - 1)];
+                    const uint32_t e = lds32v(ring_base + 4u * ((head + lane) & (RING - 1)));
                     const uint32_t q = e >> 16, li = e & 0xFFFFu;
-                    const C code = T[li];
-                    const float score = adc<M>(lut + q * SM::LS, code);
+                    C code;
+                    lds_code(T + li * (uint32_t)M, code);
+                    const float score = adc_s<M>(lut_base + 4u * q * SM::LS, code);
                     try_candidate(a, q0 + q, score, (uint32_t)(tfirst + li), thr_s[q], bs, &nreq_s, req_s);
                 }
                 head += cnt;
@@ -314,46 +363,55 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
             for (uint32_t j = 0; j < ntile; ++j) {
                 const uint32_t sq_ = seq + j, s = sq_ % STAGES;
                 mbar_wait(&full_bar[s], (sq_ / STAGES) & 1u);
-                const C* T = tiles + s * TC;
+                const uint32_t T = tile_base + s * 16384u;
                 const uint64_t tfirst = (t0 + j) * a.tile_stride * TC;
                 const uint32_t tcnt = (uint32_t)min((uint64_t)TC, a.n - tfirst);
 #pragma unroll 1
                 for (int i = 0; i < CPW / 32; ++i) {
                     const uint32_t li = warp * CPW + i * 32 + lane;
                     const bool in = li < tcnt;
-                    const C code = T[li];
+                    C code;
+                    lds_code(T + li * (uint32_t)M, code);
                     if constexpr (STRAT == DUAL) {
-                        // filter in halves of Q/2 queries so one half adds <= 32*Q/2 ring entries
+                        uint32_t m = 0;
 #pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            uint32_t m = 0;
+                        for (int g = 0; g < Q / 4; ++g) {
+                            const uint32_t v = ham4(code, qc + 4 * g) + bias;
+                            m |= (~v & 0x80808080u) >> (7 - g);
+                        }
+                        m &= in ? vmask : 0u;
+                        if constexpr (PERQ) {
 #pragma unroll
-                            for (int q = h * (Q / 2); q < (h + 1) * (Q / 2); ++q)
-                                m |= (ham(code, qc[q]) <= a.tau ? 1u : 0u) << q;
-                            m &= in ? vmask : 0u;
-                            if constexpr (PERQ) {
+                            for (int q = 0; q < Q; ++q)
+                                survq[q] += __popc(__ballot_sync(0xffffffffu, (m >> (8 * (q & 3) + (q >> 2))) & 1u));
+                        }
+                        if (__any_sync(0xffffffffu, m != 0)) {
+                            // one step adds <= 32 * Q entries; split it when the ring could overflow
+                            const uint32_t total = __reduce_add_sync(0xffffffffu, __popc(m));
+                            const bool split = qn + total > RING;
+                            const uint32_t parts[2] = {split ? (m & 0x0000FFFFu) : m, split ? (m & 0xFFFF0000u) : 0u};
 #pragma unroll
-                                for (int q = h * (Q / 2); q < (h + 1) * (Q / 2); ++q)
-                                    survq[q] += __popc(__ballot_sync(0xffffffffu, (m >> q) & 1u));
-                            }
-                            if (__any_sync(0xffffffffu, m != 0)) {
-                                const uint32_t cnt = __popc(m);
+                            for (int part = 0; part < 2; ++part) {
+                                uint32_t mm = parts[part];
+                                if (part == 1 && !split) break;
+                                const uint32_t cnt = __popc(mm);
                                 uint32_t incl = cnt;
 #pragma unroll
                                 for (int off = 1; off < 32; off <<= 1) {
                                     const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
                                     if (lane >= off) incl += o;
                                 }
-                                const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+                                const uint32_t ptotal = __shfl_sync(0xffffffffu, incl, 31);
                                 uint32_t at = head + qn + incl - cnt;
-                                while (m) {
-                                    const uint32_t q = __ffs(m) - 1;
-                                    m &= m - 1;
-                                    ring[at & (RING - 1)] = (q << 16) | li;
+                                while (mm) {
+                                    const uint32_t low = mm & (0u - mm);
+                                    const uint32_t p = 31 - __clz(low);
+                                    sts32(ring_base + 4u * (at & (RING - 1)), ((4 * (p & 7) + (p >> 3)) << 16) | li);
                                     ++at;
+                                    mm ^= low;
                                 }
-                                qn += total;
-                                tot += total;
+                                qn += ptotal;
+                                tot += ptotal;
                                 __syncwarp();
                                 while (qn >= 32) drain(T, tfirst, 32);
                             }
@@ -364,7 +422,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
 #pragma unroll 1
                             for (int q = 0; q < (int)nqh; ++q) {
                                 float score;
-                                if constexpr (STRAT == ADC) score = adc<M>(lut + q * SM::LS, code);
+                                if constexpr (STRAT == ADC) score = adc_s<M>(lut_base + 4u * q * SM::LS, code);
                                 else if constexpr (STRAT == BINARY) score = (float)ham(code, qc[q]);
                                 else score = (float)disidx(code, qc[q]);
                                 try_candidate(a, q0 + q, score, (uint32_t)(tfirst + li), thr_s[q], bs, &nreq_s,
