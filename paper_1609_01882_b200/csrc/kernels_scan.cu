@@ -194,7 +194,7 @@ __device__ unsigned long long warp_select_kth(const unsigned long long* src, uin
     return prefix;
 }
 
-constexpr int RING = 512;  // per-warp survivor ring (4-byte entries)
+constexpr int RING = 768;  // per-warp survivor queue (4-byte entries, linear)
 
 template <int M, int Q, int W>
 struct ScanSmem {
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
     constexpr int TC = SM::TC;
     constexpr int CPW = TC / W;     // codes per consumer warp per tile
     constexpr bool USE_LUT = (STRAT == DUAL || STRAT == ADC);
-    static_assert(CPW % 32 == 0, "tile must split evenly over the consumer warps");
+    static_assert(CPW % 64 == 0, "tile must split evenly over the consumer warps (2 codes per lane per step)");
 
     extern __shared__ __align__(128) uint8_t smem[];
     float* lut = reinterpret_cast<float*>(smem);
@@ -339,25 +339,64 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
             const uint32_t lut_base = smem_u32(lut);
             const uint32_t tile_base = smem_u32(tiles);
             const uint32_t ring_base = smem_u32(ring);
-            uint32_t head = 0, qn = 0;  // ring: entries [head, head + qn)
-            uint32_t tot = 0;           // survivors seen by this warp (warp-uniform)
+            uint32_t qn = 0;   // queued survivor entries: ring[0, qn)
+            uint32_t tot = 0;  // survivors seen by this warp (warp-uniform)
             uint32_t survq[PERQ ? Q : 1];
 #pragma unroll
             for (int q = 0; q < (PERQ ? Q : 1); ++q) survq[q] = 0;
 
-            // ADC + candidate test for `cnt` queued survivors (lanes < cnt busy)
-            auto drain = [&](uint32_t T, uint64_t tfirst, uint32_t cnt) {
+            // ADC + candidate test of `cnt` queued survivors starting at ring[off]
+            // (lanes < cnt busy)
+            auto drain_at = [&](uint32_t T, uint64_t tfirst, uint32_t off, uint32_t cnt) {
                 if ((uint32_t)lane < cnt) {
-                    const uint32_t e = lds32v(ring_base + 4u * ((head + lane) & (RING - 1)));
-                    const uint32_t q = e >> 16, li = e & 0xFFFFu;
+                    const uint32_t e = lds32v(ring_base + 4u * (off + lane));
+                    // mask bit p = 8j + 4c + g -> query 4g + j of the lane's code c (tile index li + 32c)
+                    const uint32_t pbit = e >> 16;
+                    const uint32_t q = 4 * (pbit & 3) + (pbit >> 3);
+                    const uint32_t li = (e & 0xFFFFu) + 32u * ((pbit >> 2) & 1u);
                     C code;
                     lds_code(T + li * (uint32_t)M, code);
                     const float score = adc_s<M>(lut_base + 4u * q * SM::LS, code);
                     try_candidate(a, q0 + q, score, (uint32_t)(tfirst + li), thr_s[q], bs, &nreq_s, req_s);
                 }
-                head += cnt;
-                qn -= cnt;
+            };
+            // drain full groups of 32, then move the (< 32) remainder to the front
+            auto drain_full = [&](uint32_t T, uint64_t tfirst) {
+                uint32_t off = 0;
+                while (qn - off >= 32) {
+                    drain_at(T, tfirst, off, 32);
+                    off += 32;
+                }
                 __syncwarp();
+                if (off) {
+                    const uint32_t rem = qn - off;
+                    const uint32_t e = (uint32_t)lane < rem ? lds32v(ring_base + 4u * (off + lane)) : 0u;
+                    __syncwarp();
+                    if ((uint32_t)lane < rem) sts32(ring_base + 4u * lane, e);
+                    qn = rem;
+                }
+                __syncwarp();
+            };
+            // append the lanes' survivor bits (entry = bit position << 16 | tile index)
+            auto append = [&](uint32_t mm, uint32_t li, uint32_t excl) {
+                uint32_t addr = ring_base + 4u * (qn + excl);
+                const uint32_t lo = li;
+                while (mm) {
+                    const uint32_t low = mm & (0u - mm);
+                    sts32(addr, ((31u - __clz(low)) << 16) | lo);
+                    addr += 4;
+                    mm ^= low;
+                }
+            };
+            auto scan = [&](uint32_t cnt, uint32_t& total) {
+                uint32_t incl = cnt;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
+                    if (lane >= off) incl += o;
+                }
+                total = __shfl_sync(0xffffffffu, incl, 31);
+                return incl - cnt;
             };
 
             for (uint32_t j = 0; j < ntile; ++j) {
@@ -366,59 +405,64 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
                 const uint32_t T = tile_base + s * 16384u;
                 const uint64_t tfirst = (t0 + j) * a.tile_stride * TC;
                 const uint32_t tcnt = (uint32_t)min((uint64_t)TC, a.n - tfirst);
+                if constexpr (STRAT == DUAL) {
+                    // two codes per lane per step (li, li + 32): independent filter chains
 #pragma unroll 1
-                for (int i = 0; i < CPW / 32; ++i) {
-                    const uint32_t li = warp * CPW + i * 32 + lane;
-                    const bool in = li < tcnt;
-                    C code;
-                    lds_code(T + li * (uint32_t)M, code);
-                    if constexpr (STRAT == DUAL) {
-                        uint32_t m = 0;
+                    for (int i = 0; i < CPW / 64; ++i) {
+                        const uint32_t li = warp * CPW + i * 64 + lane;
+                        C c0, c1;
+                        lds_code(T + li * (uint32_t)M, c0);
+                        lds_code(T + (li + 32) * (uint32_t)M, c1);
+                        uint32_t m0 = 0, m1 = 0;
 #pragma unroll
                         for (int g = 0; g < Q / 4; ++g) {
-                            const uint32_t v = ham4(code, qc + 4 * g) + bias;
-                            m |= (~v & 0x80808080u) >> (7 - g);
+                            const uint32_t v0 = ham4(c0, qc + 4 * g) + bias;
+                            const uint32_t v1 = ham4(c1, qc + 4 * g) + bias;
+                            m0 |= (~v0 & 0x80808080u) >> (7 - g);
+                            m1 |= (~v1 & 0x80808080u) >> (3 - g);
                         }
-                        m &= in ? vmask : 0u;
+                        const uint32_t m = (li < tcnt ? m0 & vmask : 0u) | (li + 32 < tcnt ? m1 & (vmask << 4) : 0u);
                         if constexpr (PERQ) {
 #pragma unroll
-                            for (int q = 0; q < Q; ++q)
-                                survq[q] += __popc(__ballot_sync(0xffffffffu, (m >> (8 * (q & 3) + (q >> 2))) & 1u));
-                        }
-                        if (__any_sync(0xffffffffu, m != 0)) {
-                            // one step adds <= 32 * Q entries; split it when the ring could overflow
-                            const uint32_t total = __reduce_add_sync(0xffffffffu, __popc(m));
-                            const bool split = qn + total > RING;
-                            const uint32_t parts[2] = {split ? (m & 0x0000FFFFu) : m, split ? (m & 0xFFFF0000u) : 0u};
-#pragma unroll
-                            for (int part = 0; part < 2; ++part) {
-                                uint32_t mm = parts[part];
-                                if (part == 1 && !split) break;
-                                const uint32_t cnt = __popc(mm);
-                                uint32_t incl = cnt;
-#pragma unroll
-                                for (int off = 1; off < 32; off <<= 1) {
-                                    const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
-                                    if (lane >= off) incl += o;
-                                }
-                                const uint32_t ptotal = __shfl_sync(0xffffffffu, incl, 31);
-                                uint32_t at = head + qn + incl - cnt;
-                                while (mm) {
-                                    const uint32_t low = mm & (0u - mm);
-                                    const uint32_t p = 31 - __clz(low);
-                                    sts32(ring_base + 4u * (at & (RING - 1)), ((4 * (p & 7) + (p >> 3)) << 16) | li);
-                                    ++at;
-                                    mm ^= low;
-                                }
-                                qn += ptotal;
-                                tot += ptotal;
-                                __syncwarp();
-                                while (qn >= 32) drain(T, tfirst, 32);
+                            for (int q = 0; q < Q; ++q) {
+                                const int b = 8 * (q & 3) + (q >> 2);
+                                survq[q] += __popc(__ballot_sync(0xffffffffu, (m >> b) & 1u)) +
+                                            __popc(__ballot_sync(0xffffffffu, (m >> (b + 4)) & 1u));
                             }
                         }
-                    } else {
+                        if (__any_sync(0xffffffffu, m != 0)) {
+                            uint32_t total;
+                            const uint32_t excl = scan(__popc(m), total);
+                            if (qn + total <= RING) {
+                                append(m, li, excl);
+                                qn += total;
+                                tot += total;
+                                __syncwarp();
+                                if (qn >= 32) drain_full(T, tfirst);
+                            } else {
+                                // a step adds <= 64 * Q entries: split it by mask byte (<= 256 each)
+#pragma unroll 1
+                                for (int part = 0; part < 4; ++part) {
+                                    const uint32_t mm = m & (0xFFu << (8 * part));
+                                    uint32_t ptotal;
+                                    const uint32_t pex = scan(__popc(mm), ptotal);
+                                    append(mm, li, pex);
+                                    qn += ptotal;
+                                    tot += ptotal;
+                                    __syncwarp();
+                                    if (qn >= 32) drain_full(T, tfirst);
+                                }
+                            }
+                        }
+                    }
+                } else {
+#pragma unroll 1
+                    for (int i = 0; i < CPW / 32; ++i) {
+                        const uint32_t li = warp * CPW + i * 32 + lane;
+                        C code;
+                        lds_code(T + li * (uint32_t)M, code);
                         // adc / binary / disidx: every code is scored for every query
-                        if (in) {
+                        if (li < tcnt) {
 #pragma unroll 1
                             for (int q = 0; q < (int)nqh; ++q) {
                                 float score;
@@ -432,7 +476,11 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
                     }
                 }
                 if constexpr (STRAT == DUAL) {
-                    if (qn) drain(T, tfirst, qn);  // entries point into this stage: flush before release
+                    if (qn) {  // entries point into this stage: flush before release
+                        drain_at(T, tfirst, 0, qn);
+                        qn = 0;
+                        __syncwarp();
+                    }
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty_bar[s]);

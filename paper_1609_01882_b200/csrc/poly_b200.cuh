@@ -9,7 +9,7 @@ namespace pb {
 constexpr int KSUB = 256;              // dbits = 8
 constexpr int DSUB = 16;               // every configuration: 128/8 and 256/16
 constexpr int TILE = 2048;             // codes per pipeline stage
-constexpr int STAGES = 4;              // bulk-copy ring depth
+constexpr int STAGES = 3;              // bulk-copy ring depth
 constexpr int BS = 4096;               // candidate block size for threshold selects
 constexpr int KMAX = 2048;             // largest supported k
 constexpr int QCAP = 64;               // per-warp survivor queue entries
