@@ -199,10 +199,10 @@ constexpr int RING = 768;  // per-warp survivor queue (4-byte entries, linear)
 template <int M, int Q, int W>
 struct ScanSmem {
     static constexpr int TC = 16384 / M;                    // codes per 16 KB tile
-    // Query q's LUT starts at q * LS floats; the +4 skew puts the same stored
-    // field of different queries in different banks (a drain holds several
-    // queries' entries for the same code).
-    static constexpr int LS = M * KSUB + 4;
+    // Query q's LUT starts at q * LS floats; the +1 skew puts the same stored
+    // field of up to 32 different queries in different banks (a drain holds
+    // many queries' entries for the same code).
+    static constexpr int LS = M * KSUB + 1;
     static constexpr size_t LUT_BYTES = (size_t)Q * LS * 4;
     static constexpr size_t TILE_BYTES = (size_t)STAGES * 16384;
     static constexpr size_t RING_BYTES = (size_t)W * RING * 4;
@@ -295,7 +295,9 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
                 const uint32_t n4 = nqh * PER_Q;
                 for (uint32_t i = threadIdx.x; i < n4; i += NT) {
                     const uint32_t q = i / PER_Q, r = i % PER_Q;
-                    reinterpret_cast<float4*>(lut + q * SM::LS)[r] = __ldg(src + i);
+                    const float4 v = __ldg(src + i);
+                    float* d = lut + q * SM::LS + 4 * r;  // rows are not 16-byte aligned
+                    d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
                 }
             }
             if (threadIdx.x < Q)
