@@ -208,9 +208,9 @@ def main():
     z = np.load(os.path.join(ROOT, "tests", "golden", "pq_d128_m8.npz"))
     pq = pb.ProductQuantizer(8, 8, DIM, z["codebooks"], z["perms"])
     centers = synth.gen_centers(SEED, NCENT, DIM)
-    shard = (args.n + world - 1) // world
-    row0 = rank * shard
-    nloc = max(0, min(shard, args.n - row0))
+    from paper_1609_01882_b200.distributed import shard_range
+    row0, row1 = shard_range(args.n, world, rank)
+    nloc = row1 - row0
     t = time.time()
     index = pb.FlatIndex(pq, device=local)
     index.add_synthetic(SEED, centers, row0, nloc)   # GPU generator + encoder, ids = global rows
@@ -229,21 +229,16 @@ def main():
     o_cnt = torch.empty(BATCH, dtype=torch.int32, device="cuda")
     o_surv = torch.empty(BATCH, dtype=torch.int64, device="cuda")
     if world > 1:
-        keys = torch.empty((BATCH, k), dtype=torch.int64, device="cuda")
-        kcnt = torch.empty(BATCH, dtype=torch.int32, device="cuda")
-        keys_all = torch.empty((world, BATCH, k), dtype=torch.int64, device="cuda")
-        kcnt_all = torch.empty((world, BATCH), dtype=torch.int32, device="cuda")
+        from paper_1609_01882_b200.distributed import FlatIndexEngine, ShardedSearch
+        sharded = ShardedSearch(FlatIndexEngine(index, stream), device="cuda")
 
     def step(i, ht, q=None):
         qb = dq[(i % nbatches) * BATCH:][:BATCH] if q is None else q
         p = pb.SearchParams(pb.Strategy.dual, k, ht)
         if world == 1:
             index.search_batch_device(qb, p, o_ids, o_sc, o_cnt, None, stream=sptr)
-        else:
-            index.search_keys_device(qb, p, keys, kcnt, None, stream=sptr)
-            dist.all_gather_into_tensor(keys_all, keys)
-            dist.all_gather_into_tensor(kcnt_all, kcnt)
-            index.merge_keys_device(keys_all, kcnt_all, world, BATCH, k, o_ids, o_sc, o_cnt, stream=sptr)
+        else:  # local shard scan, NCCL all-gather of top-k keys, K3 merge
+            sharded.search_batch(qb, p, out=(o_ids, o_sc, o_cnt))
 
     def timed(ht, steps, warmup, profile=False):
         for i in range(warmup):

@@ -376,8 +376,8 @@ void run_batches(poly_b200_index* ix, const float* d_queries, uint64_t nq, const
                 w.surv = ix->surv_w;
                 w.ntiles = wt;
                 w.tile_stride = ntiles / wt;
-                w.tiles_per_chunk = (uint32_t)WARM_TILES;
-                w.units = (uint32_t)(wt / WARM_TILES) * w.ngroups;
+                w.tiles_per_chunk = 4;  // small units: the first levels would otherwise use few SMs
+                w.units = (uint32_t)(wt / 4) * w.ngroups;
                 w.bs = ix->cand_w_cap;  // no in-scan selects: the whole sample is ranked below
                 pb::launch_scan(w, strategy, ix->m, false, ix->num_sms, s);
                 // an overflowed sample list is only a weaker (still valid) bound: ranks

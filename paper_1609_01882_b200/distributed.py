@@ -1,0 +1,74 @@
+"""Database sharding across ranks (one process per GPU) with an exact top-k merge.
+
+The flat index partitions naturally: rank r holds the
+contiguous id range ``shard_range(N, world, r)`` and scans it; the only exchange
+is one all-gather per query batch of each rank's top-k as 64-bit keys
+(fp32 score bits << 32 | id rank), merged by the K3 kernel.  Keys carry global
+id ranks, so the merge is exact, ties included.
+
+The engine is pluggable so that the rank plumbing (ranges, gather layout,
+merge order) is testable on CPU with gloo: ``FlatIndexEngine`` is the GPU
+engine (C ABI); tests plug an oracle-backed engine.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(n_total: int, world: int, rank: int):
+    """Contiguous [begin, end) of rank's shard; ceil-sized shards, last one shorter."""
+    per = (n_total + world - 1) // world
+    begin = min(rank * per, n_total)
+    return begin, min(begin + per, n_total)
+
+
+class FlatIndexEngine:
+    """GPU engine over one rank's FlatIndex shard (device tensors, caller's stream)."""
+
+    def __init__(self, index, stream=None):
+        self.index = index
+        self.stream = stream
+
+    def _sptr(self):
+        s = self.stream if self.stream is not None else torch.cuda.current_stream()
+        return s.cuda_stream
+
+    def search_keys(self, queries, params, keys, counts):
+        self.index.search_keys_device(queries, params, keys, counts, None, stream=self._sptr())
+
+    def merge(self, keys_all, counts_all, parts, nq, k, ids, scores, counts):
+        self.index.merge_keys_device(keys_all, counts_all, parts, nq, k, ids, scores, counts, stream=self._sptr())
+
+
+class ShardedSearch:
+    """search_batch over all ranks' shards: local scan, all-gather keys, merge."""
+
+    def __init__(self, engine, device="cuda", group=None):
+        self.engine = engine
+        self.device = device
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+
+    def search_batch(self, queries, params, out=None):
+        nq, k = queries.shape[0], int(params.k)
+        dev = self.device
+        if out is None:
+            out = (torch.empty((nq, k), dtype=torch.int64, device=dev),
+                   torch.empty((nq, k), dtype=torch.float32, device=dev),
+                   torch.empty(nq, dtype=torch.int32, device=dev))
+        keys = torch.empty((nq, k), dtype=torch.int64, device=dev)
+        cnt = torch.empty(nq, dtype=torch.int32, device=dev)
+        self.engine.search_keys(queries, params, keys, cnt)
+        if self.world == 1:
+            keys_all, cnt_all = keys.unsqueeze(0), cnt.unsqueeze(0)
+        else:
+            # gathered along dim 0 (rank-major): parts x nq x k, the merge kernel's layout
+            keys_all = torch.empty((self.world * nq, k), dtype=torch.int64, device=dev)
+            cnt_all = torch.empty(self.world * nq, dtype=torch.int32, device=dev)
+            dist.all_gather_into_tensor(keys_all, keys, group=self.group)
+            dist.all_gather_into_tensor(cnt_all, cnt, group=self.group)
+            keys_all = keys_all.view(self.world, nq, k)
+            cnt_all = cnt_all.view(self.world, nq)
+        self.engine.merge(keys_all, cnt_all, self.world, nq, k, *out)
+        return out

@@ -1,0 +1,94 @@
+"""Multi-rank plumbing on CPU: world_size 2 over gloo.
+
+Each rank scans its shard with an oracle-backed engine (the checker stands in
+for the GPU kernels here, since there is no GPU), the product's ShardedSearch
+all-gathers the per-shard top-k keys and merges them; the merged result must
+equal the unsharded oracle search, ties included.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+class OracleEngine:
+    """Per-shard search by the CPU oracle, emitting the same 64-bit keys as K2/K3."""
+
+    def __init__(self, pq, codes, ids):
+        self.pq, self.codes, self.ids = pq, codes, ids
+
+    def search_keys(self, queries, params, keys, counts):
+        import oracle
+        oi, osc, oc, _, _ = oracle.search(self.pq, self.codes, queries.numpy(), int(params.k), tau=int(params.tau),
+                                          ids=self.ids, threads=2)
+        key = (osc.view(np.uint32).astype(np.uint64) << np.uint64(32)) | (oi.astype(np.uint64) & np.uint64(0xFFFFFFFF))
+        key[oi < 0] = np.uint64(0xFFFFFFFFFFFFFFFF)
+        keys.copy_(torch.from_numpy(key.view(np.int64)))
+        counts.copy_(torch.from_numpy(oc.astype(np.int32)))
+
+    def merge(self, keys_all, counts_all, parts, nq, k, ids, scores, counts):
+        for q in range(nq):
+            pool = []
+            for p in range(parts):
+                c = int(counts_all[p, q])
+                pool.extend(int(x) & 0xFFFFFFFFFFFFFFFF for x in keys_all[p, q, :c].tolist())
+            pool.sort()
+            top = pool[:k]
+            counts[q] = len(top)
+            for r in range(k):
+                if r < len(top):
+                    ids[q, r] = top[r] & 0xFFFFFFFF
+                    scores[q, r] = float(np.uint32(top[r] >> 32).view(np.float32))
+                else:
+                    ids[q, r] = -1
+                    scores[q, r] = float("inf")
+
+
+def _worker(rank, world, port, result_path):
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from conftest import load_pq
+    from paper_1609_01882_b200.distributed import ShardedSearch, shard_range
+
+    class P:  # SearchParams without importing the CUDA library
+        k, tau = 30, 24
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    g = np.load(os.path.join(ROOT, "tests", "golden", "golden_m8.npz"))
+    pq = load_pq("pq_d128_m8.npz")
+    codes = np.repeat(g["codes"][:3000], 2, axis=0)  # ties across the shard boundary
+    b, e = shard_range(len(codes), world, rank)
+    eng = OracleEngine(pq, codes[b:e], np.arange(b, e, dtype=np.int64))
+    ids, scores, counts = ShardedSearch(eng, device="cpu").search_batch(torch.from_numpy(g["queries"]), P())
+    if rank == 0:
+        np.savez(result_path, ids=ids.numpy(), scores=scores.numpy(), counts=counts.numpy())
+    dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def test_sharded_search_equals_unsharded(tmp_path, pq8, g8):
+    import oracle
+    from paper_1609_01882_b200.distributed import shard_range
+    assert [shard_range(10, 3, r) for r in range(3)] == [(0, 4), (4, 8), (8, 10)]
+    out = str(tmp_path / "r0.npz")
+    mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    r = np.load(out)
+    codes = np.repeat(g8["codes"][:3000], 2, axis=0)
+    oi, osc, oc, _, _ = oracle.search(pq8, codes, g8["queries"], 30, tau=24)
+    assert np.array_equal(r["ids"], oi)
+    assert np.array_equal(r["scores"].view(np.uint32), osc.view(np.uint32))
+    assert np.array_equal(r["counts"], oc.astype(np.int32))

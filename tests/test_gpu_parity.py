@@ -219,3 +219,27 @@ def test_launches_are_counted(pb, pq8, g8):
     before = pb.launch_count()
     ix.search_batch(g8["queries"], pb.SearchParams(pb.Strategy.dual, 10, 24))
     assert pb.launch_count() - before >= 4  # K1, K2, K3, ids
+
+
+def test_cpp_mirror_matches_reference(pb, pq8, g8, tmp_path):
+    """A C++ caller of include/poly_b200/flat_index.hpp gets the reference's answers."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.join(root, "paper_1609_01882_b200")
+    exe = str(tmp_path / "mirror")
+    subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(root, "include"),
+                    os.path.join(root, "tests", "cpp", "mirror_smoke.cpp"), "-L", libdir, "-lpoly_b200",
+                    f"-Wl,-rpath,{libdir}", "-o", exe], check=True)
+    cb, pm, blob = (str(tmp_path / f) for f in ("cb.bin", "perms.bin", "blob.bin"))
+    pq8.codebooks.tofile(cb)
+    pq8.perms.tofile(pm)
+    with open(blob, "wb") as f:
+        f.write(g8["codes"].tobytes())
+        f.write(g8["queries"].astype(np.float32).tobytes())
+    out = subprocess.run([exe, cb, pm, blob], capture_output=True, text=True, check=True).stdout.split("\n")
+    assert out[0] == f"stats {20000 * 24} {int(g8['dual24_surv'].sum())}"
+    for i in range(24):
+        assert [int(x) for x in out[1 + i].split()] == g8["dual24_ids"][i, :10].tolist()
+    assert out[25] == "error 1"  # errc::invalid_argument for tau > code_bits
+    assert out[26] == f"tau95 {oracle.calibrate_threshold(pq8, g8['codes'], g8['queries'], 0.95)[0]}"
