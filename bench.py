@@ -37,10 +37,17 @@ sys.path.insert(0, ROOT)
 METRIC = "DB codes scanned/sec (filter+ADC+top-k)"
 UNIT = "codes/s"
 SEED = 160901882
-NCENT = 1000
-DIM = 128
 BATCH = 256
 NQ = 10_000
+# BASELINE.json configs: 1 = flat 64-bit codes (headline), 3 = wide 128-bit codes
+CONFIGS = {
+    1: dict(dim=128, ncent=1000, m=8, n=100_000_000, ht=24, per_ht="28,32", pq="pq_d128_m8.npz"),
+    3: dict(dim=256, ncent=4096, m=16, n=200_000_000, ht=56, per_ht="48,64", pq="pq_d256_m16.npz"),
+}
+NCENT = 1000
+DIM = 128
+M = 8
+PQFILE = "pq_d128_m8.npz"
 
 
 def parse():
@@ -49,23 +56,31 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=100_000_000, help="total database codes")
+    ap.add_argument("--config", type=int, default=1, choices=sorted(CONFIGS))
+    ap.add_argument("--n", type=int, default=None, help="total database codes (default: the config's N)")
     ap.add_argument("--k", type=int, default=100)
-    ap.add_argument("--ht", type=int, default=24)
-    ap.add_argument("--per-ht", default="28,32")
+    ap.add_argument("--ht", type=int, default=None)
+    ap.add_argument("--per-ht", default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-queries", type=int, default=256, help="queries in the CPU-baseline sample")
     ap.add_argument("--ref-n", type=int, default=8_000_000, help="codes in the --impl reference sample")
-    return ap.parse_args()
+    args = ap.parse_args()
+    global NCENT, DIM, M, PQFILE
+    c = CONFIGS[args.config]
+    NCENT, DIM, M, PQFILE = c["ncent"], c["dim"], c["m"], c["pq"]
+    args.n = c["n"] if args.n is None else args.n
+    args.ht = c["ht"] if args.ht is None else args.ht
+    args.per_ht = c["per_ht"] if args.per_ht is None else args.per_ht
+    return args
 
 
 def config(args, world):
     return {
-        "workload": f"cfg1 flat polysemous: N={args.n} 64-bit codes (m=8, nbits=8, d=128 mixture), "
-                    f"nq={NQ} in batches of {BATCH}, k={args.k}, ht={args.ht}",
-        "n_codes": args.n, "m": 8, "nbits": 8, "dim": DIM, "k": args.k, "ht": args.ht, "batch": BATCH, "nq": NQ,
+        "workload": f"cfg{args.config} flat polysemous: N={args.n} {8 * M}-bit codes (m={M}, nbits=8, d={DIM} "
+                    f"mixture of {NCENT}), nq={NQ} in batches of {BATCH}, k={args.k}, ht={args.ht}",
+        "n_codes": args.n, "m": M, "nbits": 8, "dim": DIM, "k": args.k, "ht": args.ht, "batch": BATCH, "nq": NQ,
         "strategy": "dual", "parallelism": f"db-shard{world}",
-        "l2": "inputs larger than L2 (800 MB of codes vs 126 MB L2); no flush needed",
+        "l2": f"inputs larger than L2 ({args.n * M / 1e6:.0f} MB of codes vs 126 MB L2); no flush needed",
     }
 
 
@@ -125,12 +140,12 @@ def run_reference(args, rank):
     import oracle
     from paper_1609_01882_b200 import synth
     threads = os.cpu_count()
-    z = np.load(os.path.join(ROOT, "tests", "golden", "pq_d128_m8.npz"))
-    pq = oracle.PQ(8, 8, DIM, z["codebooks"], z["perms"])
+    z = np.load(os.path.join(ROOT, "tests", "golden", PQFILE))
+    pq = oracle.PQ(M, 8, DIM, z["codebooks"], z["perms"])
     kind = "reference" if oracle.ref_available() else "port"
     centers = synth.gen_centers(SEED, NCENT, DIM)
     t = time.time()
-    codes = np.empty((args.ref_n, 8), np.uint8)
+    codes = np.empty((args.ref_n, M), np.uint8)
     step = 1 << 20
     for r0 in range(0, args.ref_n, step):
         x = oracle.gen_points(SEED, 2, r0, min(step, args.ref_n - r0), centers)
@@ -169,8 +184,8 @@ def cpu_baseline(args, index, dq_host):
     """Reference CPU search (oracle/_ref) on one full step of the workload:
     256 queries over all N codes, every host thread."""
     import oracle
-    z = np.load(os.path.join(ROOT, "tests", "golden", "pq_d128_m8.npz"))
-    pq = oracle.PQ(8, 8, DIM, z["codebooks"], z["perms"])
+    z = np.load(os.path.join(ROOT, "tests", "golden", PQFILE))
+    pq = oracle.PQ(M, 8, DIM, z["codebooks"], z["perms"])
     codes = index.codes()
     q = dq_host[:args.cpu_queries]
     threads = os.cpu_count()
@@ -205,8 +220,8 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    z = np.load(os.path.join(ROOT, "tests", "golden", "pq_d128_m8.npz"))
-    pq = pb.ProductQuantizer(8, 8, DIM, z["codebooks"], z["perms"])
+    z = np.load(os.path.join(ROOT, "tests", "golden", PQFILE))
+    pq = pb.ProductQuantizer(M, 8, DIM, z["codebooks"], z["perms"])
     centers = synth.gen_centers(SEED, NCENT, DIM)
     from paper_1609_01882_b200.distributed import shard_range
     row0, row1 = shard_range(args.n, world, rank)
@@ -333,25 +348,26 @@ def main():
     scan_ms, scan_n = scan
     avg = scan_ms / max(scan_n, 1)
     pairs = BATCH * nloc
-    code_bytes = nloc * 8  # algorithmic: each code read once per 256-query launch
+    code_bytes = nloc * M  # algorithmic: each code read once per 256-query launch
     hbm_gbs = code_bytes / (avg / 1e3) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "scan_ncu_summary.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and args.config == 1 and nloc == 100_000_000:
         try:
             traffic = json.load(open(prof)).get("dram_bytes_per_launch")
         except (OSError, ValueError):
             traffic = None
     roofline = {"bound": "hbm", "achieved": hbm_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": hbm_gbs / pk["hbm_gbs"], "traffic": traffic, "peak_kind": pk_kind,
-                "kernel": "K2 scan_kernel<8,16,16,DUAL>", "kernel_ms_avg": avg, "kernel_launches": scan_n,
+                "kernel": f"K2 scan_kernel<{M},{16 if M == 8 else 8},16,DUAL>", "kernel_ms_avg": avg,
+                "kernel_launches": scan_n,
                 "kernel_share_of_step": scan_ms / ms,
                 "algorithmic_bytes_per_launch": code_bytes, "units_per_launch": f"{BATCH} queries x {nloc} codes"}
     # issue roofline (the binding one for this integer/gather scan):
     # POPC 16/clk/SM (2 per pair) vs random LUT gathers 13.5/clk/SM (8 per survivor), measured.
     f_mhz = (clk or {}).get("sm_mhz") or pk.get("sm_max_mhz", 1965.0)
     s = per_ht[str(args.ht)]["survivor_frac"]
-    clk_per_pair = max(2 / 16.0, s * 8 / 13.5, 8.0 / BATCH / (pk["hbm_gbs"] * 1e3 / f_mhz / 148))
+    clk_per_pair = max(M / 4 / 16.0, s * M / 13.5, float(M) / BATCH / (pk["hbm_gbs"] * 1e3 / f_mhz / 148))
     peak_pairs = 148 * f_mhz * 1e6 / clk_per_pair
     roofline_issue = {"bound": "popc/lds issue", "achieved": pairs / (avg / 1e3), "peak": peak_pairs,
                       "unit": "pairs/s", "frac": pairs / (avg / 1e3) / peak_pairs, "sm_mhz": f_mhz,

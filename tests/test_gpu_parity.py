@@ -243,3 +243,30 @@ def test_cpp_mirror_matches_reference(pb, pq8, g8, tmp_path):
         assert [int(x) for x in out[1 + i].split()] == g8["dual24_ids"][i, :10].tolist()
     assert out[25] == "error 1"  # errc::invalid_argument for tau > code_bits
     assert out[26] == f"tau95 {oracle.calibrate_threshold(pq8, g8['codes'], g8['queries'], 0.95)[0]}"
+
+
+@pytest.fixture(scope="module")
+def big16(pb, pq16):
+    """500k 128-bit codes (config-3 mixture) generated + encoded on the GPU."""
+    seed = 160901882
+    centers = oracle.gen_centers(seed, 4096, 256)
+    ix = _index(pb, pq16)
+    ix.add_synthetic(seed, centers, 0, 500_000)
+    codes = ix.codes()
+    sample = np.random.default_rng(1).choice(500_000, 500, replace=False)
+    rows = np.stack([oracle.gen_points(seed, 2, int(r), 1, centers)[0] for r in sample])
+    assert _same(codes[sample], oracle.encode(pq16, rows))
+    return ix, codes, oracle.gen_points(seed, 3, 0, 160, centers)
+
+
+@pytest.mark.parametrize("tau,strategy", [(48, "dual"), (56, "dual"), (64, "dual"), (0, "adc"), (0, "binary")])
+def test_wide_codes_match_oracle(pb, pq16, big16, tau, strategy):
+    ix, codes, queries = big16
+    oi, osc, oc, osv, _ = oracle.search(pq16, codes, queries, 100, tau=tau, strategy=strategy, threads=16)
+    st = pb.SearchStats()
+    ids, sc, cnt = ix.search_batch(queries, pb.SearchParams(pb.strategy_from_string(strategy), 100, tau), st)
+    assert _same(ids, oi)
+    assert _same(_bits(sc), _bits(osc))
+    assert _same(cnt, oc)
+    if strategy == "dual":
+        assert st.survivors == int(osv.sum())
