@@ -72,6 +72,11 @@ def lib():
         L.po_calibrate_from_histogram.argtypes = [_P, _u64, _u32, _u64, _f64, C.POINTER(_i32)]
         L.po_calibrate_from_histogram.restype = _u32
         L.po_relabel_codes.argtypes = [_u32, _u32, _P, _P, _P, _u64]
+        L.po_ivf_assign.argtypes = [_P, _u64, _u32, _P, _u32, C.c_uint, _P]
+        L.po_ivf_search.argtypes = [_u32, _u32, _u32, _P, _P, _P, _P, _u32, _P, _P, _P, _P, _u64, _u32, _u64, _i32,
+                                    _u32, _u32, C.c_uint, _P, _P, _P, _P, _P, _P]
+        L.po_ivf_search.restype = _i32
+        L.po_ivf_encode_residuals.argtypes = [_u32, _u32, _u32, _P, _P, _P, _u64, _P, _P, _P]
         _lib = L
     return _lib
 
@@ -98,6 +103,10 @@ def ref():
         L.ref_search_batch.argtypes = [_u32, _u32, _u64, _P, _P, _P, _P, _u64, _P, _u64, _i32, _u32, _u32, C.c_uint,
                                        _P, _P, _P, _P]
         L.ref_buggy_topk.argtypes = [_P, _P, _u64, _u32, _P, _P]
+        L.ref_kmeans.argtypes = [_P, _u64, _u64, _u32, _u32, _u64, _P]
+        L.ref_assign_nearest.argtypes = [_P, _u64, _P, _u64, _u64, _P]
+        L.ref_ivf_search.argtypes = [_u32, _u32, _u64, _P, _P, _P, _u32, _P, _P, _P, _P, _u64, _u32, _u64, _i32, _u32,
+                                     _u32, C.c_uint, _P, _P, _P, _P]
         L.ref_buggy_topk.restype = _u32
         _ref = L
     return _ref
@@ -306,3 +315,88 @@ def ref_buggy_topk(scores, ids, k):
     osc = np.empty(max(k, 1), np.float32)
     n = ref().ref_buggy_topk(_ptr(scores), _ptr(ids), scores.shape[0], k, _ptr(oi), _ptr(osc))
     return oi[:n], osc[:n]
+
+
+# --------------------------------------------------------------------------- IVF
+class IVFLists:
+    """CSR inverted lists: cell c holds rows off[c]:off[c+1] of codes/ids."""
+
+    def __init__(self, off, codes, ids):
+        self.off = np.ascontiguousarray(off, np.uint64)
+        self.codes = np.ascontiguousarray(codes, np.uint8)
+        self.ids = np.ascontiguousarray(ids, np.int64)
+
+
+def ivf_assign(x, centroids, threads=8):
+    """Nearest coarse cell by sq_l2 (strict <, ties -> lowest cell)."""
+    x = np.ascontiguousarray(x, np.float32)
+    centroids = np.ascontiguousarray(centroids, np.float32)
+    out = np.empty(x.shape[0], np.uint32)
+    lib().po_ivf_assign(_ptr(x), x.shape[0], x.shape[1], _ptr(centroids), centroids.shape[0], threads, _ptr(out))
+    return out
+
+
+def ivf_build(pq: PQ, x, centroids, ids=None, assign=None):
+    """Lists of residual codes encode(x - c_assign), grouped by cell, stable in input order."""
+    x = np.ascontiguousarray(x, np.float32)
+    centroids = np.ascontiguousarray(centroids, np.float32)
+    n = x.shape[0]
+    ids = np.arange(n, dtype=np.int64) if ids is None else np.asarray(ids, np.int64)
+    assign = ivf_assign(x, centroids) if assign is None else np.ascontiguousarray(assign, np.uint32)
+    codes = np.empty((n, pq.code_bytes), np.uint8)
+    lib().po_ivf_encode_residuals(*pq.args(), _ptr(x), n, _ptr(centroids), _ptr(assign), _ptr(codes))
+    order = np.argsort(assign, kind="stable")
+    off = np.zeros(centroids.shape[0] + 1, np.uint64)
+    off[1:] = np.cumsum(np.bincount(assign, minlength=centroids.shape[0]))
+    return IVFLists(off, codes[order], ids[order]), assign
+
+
+def ivf_search(pq: PQ, centroids, lists: IVFLists, queries, k, nprobe, tau=None, strategy="dual", cap=0, threads=8):
+    """search_coarse.  Returns ids, scores, counts, survivors, scanned, probes."""
+    centroids = np.ascontiguousarray(centroids, np.float32)
+    queries = np.ascontiguousarray(queries, np.float32)
+    nq = queries.shape[0]
+    tau = pq.code_bits if tau is None else tau
+    oi = np.empty((nq, k), np.int64)
+    osc = np.empty((nq, k), np.float32)
+    oc = np.empty(nq, np.uint32)
+    sv = np.empty(nq, np.uint64)
+    sc = np.empty(nq, np.uint64)
+    pr = np.empty((nq, nprobe), np.uint32)
+    rc = lib().po_ivf_search(*pq.args(), _ptr(pq.inv_perms), _ptr(centroids), centroids.shape[0], _ptr(lists.off),
+                             _ptr(lists.codes), _ptr(lists.ids), _ptr(queries), nq, nprobe, cap, STRATEGIES[strategy],
+                             k, tau, threads, _ptr(oi), _ptr(osc), _ptr(oc), _ptr(sv), _ptr(sc), _ptr(pr))
+    if rc != 0:
+        raise ValueError(f"oracle ivf search rejected arguments (rc={rc})")
+    return oi, osc, oc, sv, sc, pr
+
+
+def ref_kmeans(data, k, iters=25, seed=1234567):
+    data = np.ascontiguousarray(data, np.float32)
+    out = np.empty((k, data.shape[1]), np.float32)
+    _check_ref(ref().ref_kmeans(_ptr(data), data.shape[0], data.shape[1], k, iters, seed, _ptr(out)))
+    return out
+
+
+def ref_assign_nearest(x, y):
+    x = np.ascontiguousarray(x, np.float32)
+    y = np.ascontiguousarray(y, np.float32)
+    out = np.empty(x.shape[0], np.uint32)
+    _check_ref(ref().ref_assign_nearest(_ptr(x), x.shape[0], _ptr(y), y.shape[0], x.shape[1], _ptr(out)))
+    return out
+
+
+def ref_ivf_search(pq: PQ, centroids, lists: IVFLists, queries, k, nprobe, tau=None, strategy="dual", cap=0,
+                   threads=0):
+    centroids = np.ascontiguousarray(centroids, np.float32)
+    queries = np.ascontiguousarray(queries, np.float32)
+    nq = queries.shape[0]
+    tau = pq.code_bits if tau is None else tau
+    oi = np.empty((nq, k), np.int64)
+    osc = np.empty((nq, k), np.float32)
+    oc = np.empty(nq, np.uint32)
+    sv = np.empty(nq, np.uint64)
+    _check_ref(ref().ref_ivf_search(*pq.args(), _ptr(centroids), centroids.shape[0], _ptr(lists.off),
+                                    _ptr(lists.codes), _ptr(lists.ids), _ptr(queries), nq, nprobe, cap,
+                                    STRATEGIES[strategy], k, tau, threads, _ptr(oi), _ptr(osc), _ptr(oc), _ptr(sv)))
+    return oi, osc, oc, sv

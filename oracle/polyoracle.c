@@ -454,3 +454,141 @@ void po_relabel_codes(uint32_t m, uint32_t dbits, const uint16_t* old_inv_perms,
             po_set_field(codes + i * cb, sq, dbits, new_perms[(size_t)sq * ks + old_inv_perms[(size_t)sq * ks + f]]);
         }
 }
+
+/* ------------------------------------------------------------------------- */
+/* IVF (coarseindex; no reference code exists).              */
+/* Restated from reference primitives: sq_l2 (distances.cpp:10-17), encode   */
+/* (pq.cpp:29-45), compute_lut/permuted_lut (pq.cpp:91-119), hamming_bytes    */
+/* (flat_index.hpp:14-27) and the SPEC top-k contract.                        */
+/*   build: every vector goes to its nearest coarse cell    */
+/*     (sq_l2, strict <, ties -> lowest cell); residual r = x - c (fp32).     */
+/*   enumerate_cells: the nprobe cells with the smallest    */
+/*     sq_l2(q, c), ascending; ties -> lower cell id.                         */
+/*   search_coarse: visit cells in that order; per cell the */
+/*     query residual q - c gets its own code and LUT; dual */
+/*     filter + ADC over the cell's (id, residual code) list; stop after the  */
+/*     cell at which the scanned count reaches cap (cap counts pre-filter     */
+/*     codes; 0 = no cap); global top-k over visited cells.      */
+/* ------------------------------------------------------------------------- */
+typedef struct { const float* x; uint32_t dim; const float* cent; uint32_t nlist; uint32_t* assign; } po_asg_ctx;
+static void po_assign_chunk(void* p, size_t b, size_t e) {
+    po_asg_ctx* c = (po_asg_ctx*)p;
+    for (size_t i = b; i < e; ++i) {
+        const float* xi = c->x + i * c->dim;
+        uint32_t best = 0;
+        float bd = po_sq_l2(xi, c->cent, c->dim);
+        for (uint32_t j = 1; j < c->nlist; ++j) {
+            const float d = po_sq_l2(xi, c->cent + (size_t)j * c->dim, c->dim);
+            if (d < bd) { bd = d; best = j; }
+        }
+        c->assign[i] = best;
+    }
+}
+
+void po_ivf_assign(const float* x, uint64_t n, uint32_t dim, const float* centroids, uint32_t nlist, unsigned threads,
+                   uint32_t* assign) {
+    po_asg_ctx c = {x, dim, centroids, nlist, assign};
+    po_parallel_chunks(n, threads, po_assign_chunk, &c);
+}
+
+typedef struct { float d; uint32_t c; } po_cd;
+static int po_cmp_cd(const void* a, const void* b) {
+    const po_cd* x = (const po_cd*)a; const po_cd* y = (const po_cd*)b;
+    if (x->d < y->d) return -1;
+    if (x->d > y->d) return 1;
+    return x->c < y->c ? -1 : (x->c > y->c);
+}
+
+typedef struct {
+    const po_pq* pq; const float* cent; uint32_t nlist; const uint64_t* off; const uint8_t* codes; const int64_t* ids;
+    const float* queries; uint32_t nprobe; uint64_t cap; int strategy; uint32_t k, tau;
+    int64_t* out_ids; float* out_scores; uint32_t* out_counts; uint64_t* out_surv; uint64_t* out_scanned;
+    uint32_t* out_probes;
+} po_ivf_ctx;
+
+static void po_ivf_chunk(void* p, size_t qb, size_t qe) {
+    po_ivf_ctx* c = (po_ivf_ctx*)p;
+    const po_pq* pq = c->pq;
+    const uint32_t ks = po_ksub(pq), cb = po_code_bytes(pq), dim = pq->dim;
+    po_cd* cd = (po_cd*)malloc(sizeof(po_cd) * c->nlist);
+    float* r = (float*)malloc(sizeof(float) * dim);
+    float* lut = (float*)malloc(sizeof(float) * pq->m * ks);
+    float* lutp = (float*)malloc(sizeof(float) * pq->m * ks);
+    uint8_t* qcode = (uint8_t*)malloc(cb);
+    po_topk t = {(po_nb*)malloc(sizeof(po_nb) * (c->k ? c->k : 1)), 0, c->k};
+    for (size_t qi = qb; qi < qe; ++qi) {
+        const float* q = c->queries + qi * dim;
+        t.n = 0;
+        uint64_t nsurv = 0, nscan = 0;
+        uint32_t visited = 0;
+        if (c->k > 0) {
+            for (uint32_t j = 0; j < c->nlist; ++j) { cd[j].d = po_sq_l2(q, c->cent + (size_t)j * dim, dim); cd[j].c = j; }
+            qsort(cd, c->nlist, sizeof(po_cd), po_cmp_cd);
+            const uint32_t np = c->nprobe < c->nlist ? c->nprobe : c->nlist;
+            for (uint32_t pi = 0; pi < np; ++pi) {
+                if (c->cap && nscan >= c->cap) break;
+                const uint32_t cell = cd[pi].c;
+                const float* cc = c->cent + (size_t)cell * dim;
+                for (uint32_t d = 0; d < dim; ++d) r[d] = q[d] - cc[d];
+                po_encode(pq, r, qcode);
+                po_compute_lut(pq, r, lut);
+                po_permuted_lut(pq, lut, lutp);
+                for (uint64_t i = c->off[cell]; i < c->off[cell + 1]; ++i) {
+                    const uint8_t* code = c->codes + i * cb;
+                    float s;
+                    if (c->strategy == 3) {
+                        if (po_hamming_bytes(qcode, code, cb) > c->tau) continue;
+                        ++nsurv;
+                        s = po_adc_permuted(pq, lutp, code);
+                    } else if (c->strategy == 0) s = po_adc_permuted(pq, lutp, code);
+                    else if (c->strategy == 1) s = (float)po_hamming_bytes(qcode, code, cb);
+                    else s = (float)po_disidx(qcode, code, pq->m, pq->dbits);
+                    po_topk_offer(&t, s, c->ids[i]);
+                }
+                nscan += c->off[cell + 1] - c->off[cell];
+                ++visited;
+            }
+        }
+        qsort(t.h, t.n, sizeof(po_nb), po_cmp_nb);
+        for (uint32_t rr = 0; rr < c->k; ++rr) {
+            c->out_ids[qi * c->k + rr] = rr < t.n ? t.h[rr].id : -1;
+            c->out_scores[qi * c->k + rr] = rr < t.n ? t.h[rr].score : INFINITY;
+        }
+        c->out_counts[qi] = (uint32_t)t.n;
+        if (c->out_surv) c->out_surv[qi] = nsurv;
+        if (c->out_scanned) c->out_scanned[qi] = nscan;
+        if (c->out_probes) {
+            const uint32_t np = c->nprobe < c->nlist ? c->nprobe : c->nlist;
+            for (uint32_t pi = 0; pi < c->nprobe; ++pi) c->out_probes[qi * c->nprobe + pi] = pi < np ? cd[pi].c : 0xFFFFFFFFu;
+        }
+    }
+    free(cd); free(r); free(lut); free(lutp); free(qcode); free(t.h);
+}
+
+int po_ivf_search(uint32_t m, uint32_t dbits, uint32_t dim, const float* codebooks, const uint16_t* perms,
+                  const uint16_t* inv_perms, const float* centroids, uint32_t nlist, const uint64_t* list_off,
+                  const uint8_t* list_codes, const int64_t* list_ids, const float* queries, uint64_t nq, uint32_t nprobe,
+                  uint64_t cap, int strategy, uint32_t k, uint32_t tau, unsigned threads, int64_t* out_ids,
+                  float* out_scores, uint32_t* out_counts, uint64_t* out_survivors, uint64_t* out_scanned,
+                  uint32_t* out_probes) {
+    po_pq pq = {m, dbits, dim, codebooks, perms, inv_perms};
+    if (m == 0 || dbits < 1 || dbits > 8 || dim % m != 0 || strategy < 0 || strategy > 3 || nlist == 0) return PO_EINVAL;
+    if (tau > m * dbits || nprobe == 0) return PO_EINVAL;
+    po_ivf_ctx c = {&pq, centroids, nlist, list_off, list_codes, list_ids, queries, nprobe, cap, strategy, k, tau,
+                    out_ids, out_scores, out_counts, out_survivors, out_scanned, out_probes};
+    po_parallel_chunks(nq, threads, po_ivf_chunk, &c);
+    return PO_OK;
+}
+
+/* Residual codes of the build: encode(x - c_assign). */
+void po_ivf_encode_residuals(uint32_t m, uint32_t dbits, uint32_t dim, const float* codebooks, const uint16_t* perms,
+                             const float* x, uint64_t n, const float* centroids, const uint32_t* assign, uint8_t* codes) {
+    po_pq pq = {m, dbits, dim, codebooks, perms, NULL};
+    float* r = (float*)malloc(sizeof(float) * dim);
+    for (uint64_t i = 0; i < n; ++i) {
+        const float* cc = centroids + (size_t)assign[i] * dim;
+        for (uint32_t d = 0; d < dim; ++d) r[d] = x[i * dim + d] - cc[d];
+        po_encode(&pq, r, codes + i * po_code_bytes(&pq));
+    }
+    free(r);
+}

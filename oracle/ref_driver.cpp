@@ -25,6 +25,7 @@
 #include "poly/common.hpp"
 #include "poly/distances.hpp"
 #include "poly/flat_index.hpp"
+#include "poly/kmeans.hpp"
 #include "poly/pq.hpp"
 #include "poly/polyopt.hpp"
 
@@ -237,6 +238,90 @@ int ref_search_batch(uint32_t m, uint32_t dbits, uint64_t dim, const float* code
                 for (uint32_t r = 0; r < k; ++r) {
                     out_ids[qi * k + r] = r < res.size() ? res[r].id : -1;
                     out_scores[qi * k + r] = r < res.size() ? res[r].score : INFINITY;
+                }
+                out_counts[qi] = uint32_t(res.size());
+                if (out_survivors) out_survivors[qi] = nsurv;
+            }
+        });
+    });
+}
+
+// kmeans (kmeans.cpp:53-137): k-means++ seeding + Lloyd, used to train the
+// coarse quantizer of the small IVF fixtures.
+int ref_kmeans(const float* data, uint64_t n, uint64_t dim, uint32_t k, uint32_t iters, uint64_t seed,
+               float* centroids_out) {
+    return guard([&] {
+        poly::KmeansParams p;
+        p.k = k;
+        p.iters = iters;
+        p.seed = seed;
+        poly::KmeansResult r = poly::kmeans(data, n, dim, p);
+        std::memcpy(centroids_out, r.centroids.data(), sizeof(float) * r.centroids.size());
+    });
+}
+
+// assign_nearest (distances.cpp:56-79): the reference's GEMM-based nearest
+// centroid (BLAS rounding; may differ from the exact sq_l2 argmin on near-ties).
+int ref_assign_nearest(const float* x, uint64_t n, const float* y, uint64_t m, uint64_t dim, uint32_t* assign) {
+    return guard([&] { poly::assign_nearest(x, n, y, m, dim, assign); });
+}
+
+// search_coarse (no reference code) composed from reference
+// primitives: sq_l2 (distances.cpp:10-17) for enumerate_cells, per-(query,
+// cell) residual encode / compute_lut / permuted_lut (pq.cpp:29-45,91-119),
+// hamming_bytes (flat_index.hpp:14-27), parallel_chunks; corrected top-k.
+int ref_ivf_search(uint32_t m, uint32_t dbits, uint64_t dim, const float* codebooks, const uint16_t* perms,
+                   const float* centroids, uint32_t nlist, const uint64_t* off, const uint8_t* codes,
+                   const int64_t* ids, const float* queries, uint64_t nq, uint32_t nprobe, uint64_t cap, int strategy,
+                   uint32_t k, uint32_t tau, unsigned threads, int64_t* out_ids, float* out_scores,
+                   uint32_t* out_counts, uint64_t* out_survivors) {
+    return guard([&] {
+        poly::ProductQuantizer pq = make_pq(m, dbits, dim, codebooks, perms);
+        poly::require(tau <= pq.code_bits(), poly::errc::invalid_argument, "tau exceeds code bits");
+        const size_t cb = pq.code_bytes();
+        if (threads == 0) threads = poly::default_threads();
+        poly::parallel_chunks(nq, threads, [&](size_t qb, size_t qe) {
+            std::vector<std::pair<float, uint32_t>> cd(nlist);
+            std::vector<float> r(dim);
+            std::vector<uint8_t> qcode(cb);
+            for (size_t qi = qb; qi < qe; ++qi) {
+                const float* q = queries + qi * dim;
+                FixedTopK top(k);
+                uint64_t nsurv = 0, nscan = 0;
+                if (k > 0) {
+                    for (uint32_t j = 0; j < nlist; ++j) cd[j] = {poly::sq_l2(q, centroids + size_t(j) * dim, dim), j};
+                    std::sort(cd.begin(), cd.end());  // (distance, cell) ascending: ties -> lower cell
+                    const uint32_t np = std::min(nprobe, nlist);
+                    for (uint32_t pi = 0; pi < np; ++pi) {
+                        if (cap && nscan >= cap) break;
+                        const uint32_t cell = cd[pi].second;
+                        for (size_t d = 0; d < dim; ++d) r[d] = q[d] - centroids[size_t(cell) * dim + d];
+                        pq.encode(r.data(), qcode.data());
+                        const poly::LookupTable lutp = pq.permuted_lut(pq.compute_lut(r.data()));
+                        for (uint64_t i = off[cell]; i < off[cell + 1]; ++i) {
+                            const uint8_t* c = codes + i * cb;
+                            float s;
+                            if (strategy == 3) {
+                                if (poly::hamming_bytes(qcode.data(), c, cb) > tau) continue;
+                                ++nsurv;
+                            }
+                            if (strategy == 0 || strategy == 3) {
+                                s = 0.0f;
+                                for (uint32_t sq = 0; sq < pq.m; ++sq) s += lutp.row(sq)[poly::code_get_field(c, sq, pq.dbits)];
+                            } else if (strategy == 1) {
+                                s = float(poly::hamming_bytes(qcode.data(), c, cb));
+                            } else {
+                                s = float(poly::disidx_fields(qcode.data(), c, pq.m, pq.dbits));
+                            }
+                            top.offer(s, ids[i]);
+                        }
+                        nscan += off[cell + 1] - off[cell];
+                    }
+                }
+                std::vector<poly::Neighbor> res = top.sorted();
+                for (uint32_t rr = 0; rr < k; ++rr) {
+                    out_ids[qi * k + rr] = rr < res.size() ? res[rr].id : -1;
+                    out_scores[qi * k + rr] = rr < res.size() ? res[rr].score : INFINITY;
                 }
                 out_counts[qi] = uint32_t(res.size());
                 if (out_survivors) out_survivors[qi] = nsurv;

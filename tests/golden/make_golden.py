@@ -16,6 +16,12 @@ Files:
                    matrices and search results for every strategy and tau
   golden_m16.npz   same for the 128-bit codes
   topk_kat.npz     the reference TopK's defect vs the SPEC contract
+  golden_ivf.npz   IVF (no reference code): 64-cell coarse
+                   quantizer from the reference's kmeans, residual PQ from
+                   train_pq + optimize_pq on residuals, lists from the
+                   reference's assign_nearest + encode, and search_coarse
+                   results composed from reference primitives
+                   (oracle/ref_driver.cpp ref_ivf_search)
 """
 from __future__ import annotations
 
@@ -101,6 +107,42 @@ def make_topk_kat():
     print(f"topk_kat: reference TopK k=2 on 5,3,4,1 -> {bs.tolist()}; mismatch rate {np.mean(trials):.2f}")
 
 
+def make_ivf_golden(name="golden_ivf.npz", nlist=64, ntrain=20000, n=20000, nq=24):
+    t = time.time()
+    centers = oracle.gen_centers(DATA_SEED, 1000, 128)
+    train = oracle.gen_points(DATA_SEED, 1, 0, ntrain, centers)
+    coarse = oracle.ref_kmeans(train, nlist, 10, 1234567)
+    tr_assign = oracle.ref_assign_nearest(train, coarse)
+    resid = train - coarse[tr_assign]
+    cb = oracle.ref_train_pq(resid, 8, 8, 25, 1234567)
+    perms = oracle.ref_optimize_pq(cb, 128)
+    pq = oracle.PQ(8, 8, 128, cb, perms)
+    base = oracle.gen_points(DATA_SEED, 2, 0, n, centers)
+    assign_ref = oracle.ref_assign_nearest(base, coarse)          # distances.cpp:56-79 (GEMM)
+    assign_exact = oracle.ivf_assign(base, coarse)                # sq_l2 argmin
+    codes = oracle.ref_encode(pq, base - coarse[assign_ref])      # pq.cpp:29-45 on residuals
+    order = np.argsort(assign_ref, kind="stable")
+    off = np.zeros(nlist + 1, np.uint64)
+    off[1:] = np.cumsum(np.bincount(assign_ref, minlength=nlist))
+    lists = oracle.IVFLists(off, codes[order], order.astype(np.int64) * 7 + 3)
+    queries = oracle.gen_points(DATA_SEED, 3, 0, nq, centers)
+    out = dict(coarse=coarse, codebooks=cb, perms=perms, off=lists.off, list_codes=lists.codes, list_ids=lists.ids,
+               assign_ref=assign_ref, assign_exact=assign_exact, queries=queries, base_head=base[:64],
+               data_seed=DATA_SEED, n=n)
+    for nprobe in (1, 4, 16, 64):
+        for tau in (20, 26, 64):
+            for cap in (0, 1500):
+                i, sc, c, sv = oracle.ref_ivf_search(pq, coarse, lists, queries, 50, nprobe, tau=tau, cap=cap)
+                key = f"p{nprobe}_t{tau}_c{cap}"
+                out[key + "_ids"], out[key + "_scores"], out[key + "_counts"], out[key + "_surv"] = i, sc, c, sv
+    for strat in ("adc", "binary"):
+        i, sc, c, _ = oracle.ref_ivf_search(pq, coarse, lists, queries, 50, 16, strategy=strat)
+        out[f"{strat}16_ids"], out[f"{strat}16_scores"], out[f"{strat}16_counts"] = i, sc, c
+    np.savez_compressed(os.path.join(OUT, name), **out)
+    print(f"{name}: nlist {nlist}, {n} codes in {time.time() - t:.1f}s; GEMM vs exact assignment mismatches: "
+          f"{int((assign_ref != assign_exact).sum())}; list sizes {int(np.diff(off).min())}..{int(np.diff(off).max())}")
+
+
 if __name__ == "__main__":
     oracle.build()
     pq8 = make_pq("pq_d128_m8.npz", 128, 1000, 8)
@@ -108,3 +150,4 @@ if __name__ == "__main__":
     make_golden("golden_m8.npz", pq8, 1000, 20000, 24, (0, 20, 24, 28, 32, 64))
     make_golden("golden_m16.npz", pq16, 4096, 10000, 16, (0, 48, 56, 64, 128))
     make_topk_kat()
+    make_ivf_golden()
