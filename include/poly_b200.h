@@ -158,6 +158,63 @@ int poly_b200_debug_counts(poly_b200_index* index, uint32_t* ccount, uint64_t* t
 int poly_b200_profile_enable(poly_b200_index* index, int enable);
 int poly_b200_profile_read(poly_b200_index* index, double* scan_ms, uint64_t* scan_launches);
 
+/* ---- IVF + polysemous (coarseindex; configs 2 and 4) ------
+ * Coarse quantizer of nlist centroids (nlist x dim fp32); inverted lists of
+ * (id, residual code) where the residual PQ (`pq`) encodes x - c_cell.
+ * enumerate_cells: the nprobe cells with the smallest sq_l2(q, c), ascending,
+ * ties -> lower cell.  search_coarse: per probed cell the query residual gets
+ * its own code and LUT; dual filter + ADC over the list; cells are visited in
+ * order and the visit stops after the cell at which `cap` scanned codes is
+ * reached (0 = no cap); global top-k.  The reference ships no IVF code; the
+ * oracle restates SPEC from the reference's primitives. */
+typedef struct poly_b200_ivf poly_b200_ivf;
+
+typedef struct {
+    int32_t strategy;
+    uint32_t k;
+    uint32_t tau;
+    uint32_t nprobe;
+    uint64_t cap;
+} poly_b200_ivf_params;
+
+int poly_b200_ivf_create(const poly_b200_pq_desc* pq, const float* coarse, uint32_t nlist, int device,
+                         poly_b200_ivf** out);
+int poly_b200_ivf_destroy(poly_b200_ivf* ivf);
+uint64_t poly_b200_ivf_size(const poly_b200_ivf* ivf);
+
+/* build: nearest cell by sq_l2 (strict <, lowest cell on
+ * ties) for n host vectors -> cells (n). */
+int poly_b200_ivf_assign(poly_b200_ivf* ivf, const float* x, uint64_t n, uint32_t* cells);
+
+/* Assign, residual-encode and append n host vectors; ids may be NULL
+ * (sequential from size()).  cells may be NULL (computed) or given. */
+int poly_b200_ivf_add(poly_b200_ivf* ivf, const float* x, uint64_t n, const uint32_t* cells, const int64_t* ids);
+
+/* Same for device-resident vectors and cells (cells required), ids
+ * id0 .. id0 + n - 1; used by the benchmark's chunked builder. */
+int poly_b200_ivf_add_device(poly_b200_ivf* ivf, const float* d_x, const uint32_t* d_cells, uint64_t n, int64_t id0,
+                             void* stream);
+
+/* Append pre-encoded residual codes with their cells and ids (serialization). */
+int poly_b200_ivf_add_codes(poly_b200_ivf* ivf, const uint32_t* cells, const uint8_t* codes, const int64_t* ids,
+                            uint64_t n);
+
+/* Lists in CSR form: off (nlist + 1), codes (size x code_bytes), ids (size);
+ * any output may be NULL. */
+int poly_b200_ivf_get_lists(poly_b200_ivf* ivf, uint64_t* off, uint8_t* codes, int64_t* ids);
+
+/* enumerate_cells for host queries: cells (nq x nprobe). */
+int poly_b200_ivf_probes(poly_b200_ivf* ivf, const float* queries, uint64_t nq, uint32_t nprobe, uint32_t* cells);
+
+/* search_coarse, host buffers (ids/scores nq x k; unfilled: -1 / +inf). */
+int poly_b200_ivf_search(poly_b200_ivf* ivf, const float* queries, uint64_t nq, const poly_b200_ivf_params* params,
+                         int64_t* out_ids, float* out_scores, uint32_t* out_counts, poly_b200_search_stats* stats);
+
+/* Device buffers, work enqueued on `stream`; `stats` (host, may be NULL) syncs. */
+int poly_b200_ivf_search_device(poly_b200_ivf* ivf, const float* d_queries, uint64_t nq,
+                                const poly_b200_ivf_params* params, int64_t* d_out_ids, float* d_out_scores,
+                                uint32_t* d_out_counts, void* stream, poly_b200_search_stats* stats);
+
 /* Number of kernel launches this library has issued so far (for bench.py). */
 uint64_t poly_b200_launch_count(void);
 

@@ -8,5 +8,7 @@ kernels in csrc/.  See DESIGN.md.
 from .flat_index import (Errc, FlatIndex, Neighbor, PolyError, ProductQuantizer, SearchParams, SearchStats,
                          Strategy, gen_points_device, launch_count, strategy_from_string, to_string)
 
-__all__ = ["Errc", "FlatIndex", "Neighbor", "PolyError", "ProductQuantizer", "SearchParams", "SearchStats",
+from .ivf_index import CoarseParams, IVFIndex
+
+__all__ = ["CoarseParams", "IVFIndex", "Errc", "FlatIndex", "Neighbor", "PolyError", "ProductQuantizer", "SearchParams", "SearchStats",
            "Strategy", "gen_points_device", "launch_count", "strategy_from_string", "to_string"]

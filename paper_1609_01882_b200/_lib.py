@@ -24,6 +24,10 @@ class SearchParamsC(C.Structure):
     _fields_ = [("strategy", C.c_int32), ("k", _u32), ("tau", _u32)]
 
 
+class IvfParamsC(C.Structure):
+    _fields_ = [("strategy", C.c_int32), ("k", _u32), ("tau", _u32), ("nprobe", _u32), ("cap", _u64)]
+
+
 class SearchStatsC(C.Structure):
     _fields_ = [("scanned", _u64), ("survivors", _u64)]
 
@@ -58,6 +62,19 @@ def _load():
     L.poly_b200_profile_enable.argtypes = [_P, _i32]
     L.poly_b200_profile_read.argtypes = [_P, C.POINTER(_f64), C.POINTER(_u64)]
     L.poly_b200_launch_count.restype = _u64
+    L.poly_b200_ivf_create.argtypes = [C.POINTER(PqDesc), _P, _u32, _i32, C.POINTER(_P)]
+    L.poly_b200_ivf_destroy.argtypes = [_P]
+    L.poly_b200_ivf_size.argtypes = [_P]
+    L.poly_b200_ivf_size.restype = _u64
+    L.poly_b200_ivf_assign.argtypes = [_P, _P, _u64, _P]
+    L.poly_b200_ivf_add.argtypes = [_P, _P, _u64, _P, _P]
+    L.poly_b200_ivf_add_device.argtypes = [_P, _P, _P, _u64, C.c_int64, _P]
+    L.poly_b200_ivf_add_codes.argtypes = [_P, _P, _P, _P, _u64]
+    L.poly_b200_ivf_get_lists.argtypes = [_P, _P, _P, _P]
+    L.poly_b200_ivf_probes.argtypes = [_P, _P, _u64, _u32, _P]
+    L.poly_b200_ivf_search.argtypes = [_P, _P, _u64, C.POINTER(IvfParamsC), _P, _P, _P, C.POINTER(SearchStatsC)]
+    L.poly_b200_ivf_search_device.argtypes = [_P, _P, _u64, C.POINTER(IvfParamsC), _P, _P, _P, _P,
+                                              C.POINTER(SearchStatsC)]
     return L
 
 
@@ -70,5 +87,7 @@ EXPORTS = [
     "poly_b200_calibrate_threshold", "poly_b200_with_assignments", "poly_b200_get_codes",
     "poly_b200_search_keys_device", "poly_b200_merge_keys_device", "poly_b200_add_synthetic",
     "poly_b200_gen_points_device", "poly_b200_debug_lut", "poly_b200_debug_counts", "poly_b200_profile_enable", "poly_b200_profile_read",
-    "poly_b200_launch_count",
+    "poly_b200_launch_count", "poly_b200_ivf_create", "poly_b200_ivf_destroy", "poly_b200_ivf_size",
+    "poly_b200_ivf_assign", "poly_b200_ivf_add", "poly_b200_ivf_add_device", "poly_b200_ivf_add_codes",
+    "poly_b200_ivf_get_lists", "poly_b200_ivf_probes", "poly_b200_ivf_search", "poly_b200_ivf_search_device",
 ]

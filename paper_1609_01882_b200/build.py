@@ -17,7 +17,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libpoly_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["capi.cu", "kernels_encode.cu", "kernels_scan.cu", "kernels_topk.cu"]
+SOURCES = ["capi.cu", "capi_ivf.cu", "kernels_encode.cu", "kernels_scan.cu", "kernels_topk.cu", "kernels_ivf.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
          "-Xptxas", "-v", f"-I{os.path.join(os.path.dirname(HERE), 'include')}"]
 
@@ -28,7 +28,7 @@ def _stale(obj, deps):
 
 def build(verbose: bool = False) -> str:
     os.makedirs(OUT_DIR, exist_ok=True)
-    headers = [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith(".cuh")]
+    headers = [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith((".cuh", ".h"))]
     headers.append(os.path.join(os.path.dirname(HERE), "include", "poly_b200.h"))
     objs = []
     for src in SOURCES:

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "../../include/poly_b200.h"
+#include "host_common.h"
 #include "poly_b200.cuh"
 
 namespace pb {
@@ -23,49 +24,12 @@ static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 }  // namespace pb
 
-namespace {
-
+namespace pbh {
 thread_local std::string g_err;
+}  // namespace pbh
+using namespace pbh;
 
-struct Error : std::runtime_error {
-    int code;
-    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
-};
-
-void require(bool ok, int code, const std::string& msg) {
-    if (!ok) throw Error(code, msg);
-}
-
-void ck(cudaError_t e, const char* what) {
-    if (e != cudaSuccess) throw Error(POLY_B200_INTERNAL, std::string(what) + ": " + cudaGetErrorString(e));
-}
-#define CK(x) ck((x), #x)
-
-template <class F>
-int guard(F&& f) {
-    try {
-        f();
-        g_err.clear();
-        return POLY_B200_OK;
-    } catch (const Error& e) {
-        g_err = e.what();
-        return e.code;
-    } catch (const std::exception& e) {
-        g_err = e.what();
-        return POLY_B200_INTERNAL;
-    }
-}
-
-template <class T>
-T* dalloc(size_t count) {
-    void* p = nullptr;
-    if (count) CK(cudaMalloc(&p, count * sizeof(T)));
-    return static_cast<T*>(p);
-}
-
-void dfree(void* p) {
-    if (p) cudaFree(p);
-}
+namespace {
 
 constexpr uint32_t NQB = 256;  // queries per batch (BASELINE.json config 1: "batches of 256")
 constexpr uint64_t WARM_TILES = 16;  // strided sample that seeds the thresholds
@@ -86,14 +50,7 @@ struct poly_b200_index {
     uint64_t n = 0, cap_codes = 0;
 
     // ids: arithmetic (id0 + pos) until a non-sequential id arrives
-    bool ids_arith = true;
-    int64_t id0 = 0;
-    std::vector<int64_t> h_ids;
-    bool idmap_dirty = true;
-    int id_mode = pb::ID_ARITH;
-    uint32_t key_id0 = 0;
-    uint32_t* d_id32 = nullptr;
-    int64_t* d_rank_to_id = nullptr;
+    pbh::IdMap idm;
 
     // batch scratch
     float* lutp = nullptr;
@@ -141,35 +98,6 @@ struct poly_b200_index {
 
 namespace {
 
-struct DeviceGuard {
-    int prev = 0;
-    explicit DeviceGuard(int dev) {
-        cudaGetDevice(&prev);
-        CK(cudaSetDevice(dev));
-    }
-    ~DeviceGuard() { cudaSetDevice(prev); }
-};
-
-void check_pq(const poly_b200_pq_desc* pq) {
-    require(pq && pq->codebooks && pq->perms, POLY_B200_INVALID_ARGUMENT, "null product quantizer");
-    require(pq->dbits == 8, POLY_B200_INVALID_ARGUMENT, "only dbits = 8 is supported on the GPU path");
-    require(pq->m == 8 || pq->m == 16, POLY_B200_INVALID_ARGUMENT, "m must be 8 or 16 (64- or 128-bit codes)");
-    require(pq->dim == (uint64_t)pq->m * pb::DSUB, POLY_B200_INVALID_ARGUMENT,
-            "dim must be 16 * m (sub-vectors of 16 dimensions)");
-    const size_t ks = 256;
-    for (uint32_t sq = 0; sq < pq->m; ++sq) {  // pq.cpp:11-27: perms must be bijections
-        std::vector<bool> seen(ks, false);
-        for (size_t j = 0; j < ks; ++j) {
-            const uint16_t v = pq->perms[sq * ks + j];
-            require(v < ks && !seen[v], POLY_B200_INVALID_ARGUMENT,
-                    "assignment for sub-quantizer " + std::to_string(sq) + " is not a bijection");
-            seen[v] = true;
-        }
-    }
-    for (size_t i = 0; i < (size_t)pq->m * ks * pb::DSUB; ++i)
-        require(std::isfinite(pq->codebooks[i]), POLY_B200_INVALID_ARGUMENT, "non-finite codebook entry");
-}
-
 void grow_codes(poly_b200_index* ix, uint64_t need) {
     const uint64_t tile = 16384 / ix->cb;
     if (need + tile <= ix->cap_codes) return;
@@ -185,78 +113,15 @@ void grow_codes(poly_b200_index* ix, uint64_t need) {
 }
 
 void append_ids(poly_b200_index* ix, const int64_t* ids, uint64_t n) {
-    const uint64_t base = ix->n;
-    if (ix->ids_arith) {
-        const int64_t id0 = (base == 0 && ids && n) ? ids[0] : ix->id0;
-        bool seq = true;
-        if (ids)
-            for (uint64_t i = 0; i < n && seq; ++i) seq = ids[i] == id0 + (int64_t)(base + i);
-        if (seq) {
-            ix->id0 = id0;
-            ix->idmap_dirty = true;
-            return;
-        }
-        ix->ids_arith = false;
-        ix->h_ids.resize(base);
-        std::iota(ix->h_ids.begin(), ix->h_ids.end(), ix->id0);
-    }
-    const size_t old = ix->h_ids.size();
-    ix->h_ids.resize(old + n);
-    for (uint64_t i = 0; i < n; ++i) ix->h_ids[old + i] = ids ? ids[i] : (int64_t)(base + i);
-    ix->idmap_dirty = true;
+    ix->idm.append(ids, ix->n, n);
 }
 
 void append_id_range(poly_b200_index* ix, int64_t first, uint64_t n) {
-    if (ix->ids_arith && (ix->n == 0 || first == ix->id0 + (int64_t)ix->n)) {
-        if (ix->n == 0) ix->id0 = first;
-        ix->idmap_dirty = true;
-        return;
-    }
-    std::vector<int64_t> ids(n);
-    std::iota(ids.begin(), ids.end(), first);
-    append_ids(ix, ids.data(), n);
+    ix->idm.append_range(first, ix->n, n);
 }
 
-// Key low word: arithmetic ids -> id itself; 32-bit ids -> id32 table;
-// anything else -> rank of the id among all ids, mapped back by rank_to_id.
 void sync_idmap(poly_b200_index* ix) {
-    if (!ix->idmap_dirty) return;
-    dfree(ix->d_id32);
-    dfree(ix->d_rank_to_id);
-    ix->d_id32 = nullptr;
-    ix->d_rank_to_id = nullptr;
-    if (ix->ids_arith && ix->id0 >= 0 && ix->id0 + (int64_t)ix->n <= (int64_t)UINT32_MAX + 1) {
-        ix->id_mode = pb::ID_ARITH;
-        ix->key_id0 = (uint32_t)ix->id0;
-    } else {
-        std::vector<int64_t> ids;
-        if (ix->ids_arith) {
-            ids.resize(ix->n);
-            std::iota(ids.begin(), ids.end(), ix->id0);
-        }
-        const std::vector<int64_t>& I = ix->ids_arith ? ids : ix->h_ids;
-        require(ix->n <= (uint64_t)UINT32_MAX + 1, POLY_B200_INVALID_ARGUMENT, "more than 2^32 codes per device");
-        std::vector<uint32_t> id32(ix->n);
-        bool small = std::all_of(I.begin(), I.end(), [](int64_t v) { return v >= 0 && v <= (int64_t)UINT32_MAX; });
-        if (small) {
-            for (uint64_t i = 0; i < ix->n; ++i) id32[i] = (uint32_t)I[i];
-        } else {
-            std::vector<uint32_t> order(ix->n);
-            std::iota(order.begin(), order.end(), 0u);
-            std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return I[a] < I[b]; });
-            std::vector<int64_t> r2id(ix->n);
-            for (uint64_t r = 0; r < ix->n; ++r) {
-                id32[order[r]] = (uint32_t)r;
-                r2id[r] = I[order[r]];
-            }
-            ix->d_rank_to_id = dalloc<int64_t>(ix->n);
-            CK(cudaMemcpy(ix->d_rank_to_id, r2id.data(), ix->n * 8, cudaMemcpyHostToDevice));
-        }
-        ix->d_id32 = dalloc<uint32_t>(std::max<uint64_t>(ix->n, 1));
-        if (ix->n) CK(cudaMemcpy(ix->d_id32, id32.data(), ix->n * 4, cudaMemcpyHostToDevice));
-        ix->id_mode = pb::ID_TABLE;
-    }
-    ix->idmap_dirty = false;
+    ix->idm.sync(ix->n);
 }
 
 void ensure_scratch(poly_b200_index* ix, uint32_t k) {
@@ -352,9 +217,9 @@ void run_batches(poly_b200_index* ix, const float* d_queries, uint64_t nq, const
             a.nqb = nqb;
             a.tau = p->tau;
             a.k = k;
-            a.id_mode = ix->id_mode;
-            a.id0 = ix->key_id0;
-            a.id32 = ix->d_id32;
+            a.id_mode = ix->idm.mode;
+            a.id0 = ix->idm.key_id0;
+            a.id32 = ix->idm.d_id32;
             a.thr = ix->thr;
             a.ngroups = (nqb + Q - 1) / Q;
             // Warm-up: strided samples of 16, 128, 1024, ... tiles spread over the
@@ -451,7 +316,7 @@ int device_search(poly_b200_index* ix, const float* d_queries, uint64_t nq, cons
     int mode = 0;
     run_batches(ix, d_queries, nq, p, d_surv != nullptr, s, [&](uint64_t b0, uint32_t nqb, bool dual, bool all_pass) {
         mode = dual ? 2 : (all_pass ? 1 : 0);
-        pb::launch_keys_to_ids(ix->keys, ix->kcounts, nqb, k, ix->d_rank_to_id, d_ids + b0 * k, d_scores + b0 * k,
+        pb::launch_keys_to_ids(ix->keys, ix->kcounts, nqb, k, ix->idm.d_rank_to_id, d_ids + b0 * k, d_scores + b0 * k,
                                d_counts ? d_counts + b0 : nullptr, s);
         if (d_surv) {
             surv_out_kernel<<<(nqb + 127) / 128, 128, 0, s>>>(ix->surv, nqb, ix->n, mode, d_surv + b0);
@@ -544,13 +409,13 @@ int poly_b200_destroy(poly_b200_index* ix) {
         {
             DeviceGuard dg(ix->device);
             if (ix->stream) cudaStreamSynchronize(ix->stream);
-            for (void* p : {(void*)ix->d_codebooks, (void*)ix->d_perms, (void*)ix->d_codes, (void*)ix->d_id32,
-                            (void*)ix->d_rank_to_id, (void*)ix->lutp, (void*)ix->qcodes, (void*)ix->cand,
+            for (void* p : {(void*)ix->d_codebooks, (void*)ix->d_perms, (void*)ix->d_codes, (void*)ix->lutp, (void*)ix->qcodes, (void*)ix->cand,
                             (void*)ix->ctrl, (void*)ix->thr, (void*)ix->surv,
                             (void*)ix->surv_w, (void*)ix->surv_total, (void*)ix->cand_w, (void*)ix->ctrl_w, (void*)ix->keys, (void*)ix->kcounts,
                             (void*)ix->sticky_overflow, (void*)ix->d_q, (void*)ix->d_oid, (void*)ix->d_osc,
                             (void*)ix->d_ocnt, (void*)ix->d_osurv})
                 dfree(p);
+            ix->idm.release();
             if (ix->h_overflow) cudaFreeHost(ix->h_overflow);
             for (auto& pe : ix->prof_events) {
                 cudaEventDestroy(pe.first);
@@ -732,7 +597,7 @@ int poly_b200_merge_keys_device(poly_b200_index* ix, const uint64_t* d_keys, con
             // parts x nq x k layout: part p of batch query i at d_keys + (p * nq + b0 + i) * k
             pb::launch_topk(reinterpret_cast<const unsigned long long*>(d_keys) + b0 * k, d_counts + b0, k, parts,
                             nq * k, nq, nqb, k, ix->keys, ix->kcounts, s);
-            pb::launch_keys_to_ids(ix->keys, ix->kcounts, nqb, k, ix->d_rank_to_id, d_ids + b0 * k, d_scores + b0 * k,
+            pb::launch_keys_to_ids(ix->keys, ix->kcounts, nqb, k, ix->idm.d_rank_to_id, d_ids + b0 * k, d_scores + b0 * k,
                                    d_out_counts ? d_out_counts + b0 : nullptr, s);
         }
         CK(cudaGetLastError());
@@ -814,10 +679,10 @@ int poly_b200_with_assignments(const poly_b200_index* src, const uint16_t* perms
             dfree(d_maps);
             CK(e);
             dst->n = src->n;
-            dst->ids_arith = src->ids_arith;
-            dst->id0 = src->id0;
-            dst->h_ids = src->h_ids;
-            dst->idmap_dirty = true;
+            dst->idm.arith = src->idm.arith;
+            dst->idm.id0 = src->idm.id0;
+            dst->idm.h = src->idm.h;
+            dst->idm.dirty = true;
         } catch (...) {
             poly_b200_destroy(dst);
             throw;
@@ -891,12 +756,8 @@ int poly_b200_get_codes(const poly_b200_index* ix, uint8_t* codes, int64_t* ids)
         require(ix != nullptr, POLY_B200_INVALID_ARGUMENT, "null index");
         DeviceGuard dg(ix->device);
         if (codes && ix->n) CK(cudaMemcpy(codes, ix->d_codes, ix->n * ix->cb, cudaMemcpyDeviceToHost));
-        if (ids) {
-            if (ix->ids_arith)
-                for (uint64_t i = 0; i < ix->n; ++i) ids[i] = ix->id0 + (int64_t)i;
-            else
-                std::copy(ix->h_ids.begin(), ix->h_ids.end(), ids);
-        }
+        if (ids)
+            for (uint64_t i = 0; i < ix->n; ++i) ids[i] = ix->idm.at(i);
     });
 }
 

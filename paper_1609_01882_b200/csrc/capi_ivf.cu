@@ -1,0 +1,563 @@
+// capi_ivf.cu -- C ABI of the IVF search path (include/poly_b200.h, poly_b200_ivf_*).
+//
+// Restates the SPEC's coarseindex module (the reference has
+// no code for it) on the GPU: build = exact nearest-cell assignment + residual
+// encode + CSR lists; search_coarse = K5 (coarse keys) -> K3 (nprobe nearest
+// cells) -> K1r (per-(query, cell) residual LUTs and codes) -> rounds of K6
+// list scans over probes [0,1), [1,4), [4,16), ... with the k-th key of the
+// candidates so far (K3) seeding each next round's threshold -> K3 top-k.
+#include <algorithm>
+#include <mutex>
+#include <vector>
+
+#include "../../include/poly_b200.h"
+#include "host_common.h"
+#include "poly_b200.cuh"
+
+using namespace pbh;
+
+namespace {
+constexpr uint32_t IVF_NQB = 256;  // queries per batch
+}
+
+struct poly_b200_ivf {
+    int device = 0;
+    int num_sms = 148;
+    uint32_t m = 0, dim = 0, cb = 0, nlist = 0;
+    std::vector<float> h_codebooks, h_coarse;
+    std::vector<uint16_t> h_perms;
+    float* d_codebooks = nullptr;
+    uint16_t* d_perms = nullptr;
+    float* d_coarse = nullptr;
+
+    // insertion-order staging
+    uint8_t* d_codes_ins = nullptr;
+    uint32_t* d_cells_ins = nullptr;
+    uint64_t n = 0, cap_ins = 0;
+    pbh::IdMap idm;
+
+    // CSR lists (rebuilt lazily after adds)
+    bool lists_dirty = true;
+    std::vector<uint64_t> h_off;
+    uint64_t* d_off = nullptr;
+    uint8_t* d_codes_list = nullptr;
+    uint32_t* d_low_list = nullptr;
+    uint64_t max_list = 0;
+
+    // search scratch
+    unsigned long long* ckeys = nullptr;  // IVF_NQB x nlist
+    uint32_t* nl_counts = nullptr;         // IVF_NQB x nlist (for K3)
+    unsigned long long* probe_keys = nullptr;
+    uint32_t* probe_counts = nullptr;
+    uint32_t* np_eff = nullptr;
+    unsigned long long* scanned = nullptr;
+    uint32_t scratch_nprobe = 0;
+    float* lutp = nullptr;
+    uint8_t* qcodes = nullptr;
+    unsigned long long* cand = nullptr;
+    uint32_t cand_cap = 0;
+    uint32_t* ctrl = nullptr;  // [ccount NQB][overflow][work x 16]
+    unsigned long long* thr = nullptr;
+    unsigned long long* keys = nullptr;
+    uint32_t keys_k = 0;
+    uint32_t* kcounts = nullptr;
+    unsigned long long* surv_total = nullptr;
+    unsigned long long* scan_total = nullptr;
+    uint32_t* sticky_overflow = nullptr;
+    float* d_q = nullptr;
+    uint64_t d_q_cap = 0;
+    int64_t* d_oid = nullptr;
+    float* d_osc = nullptr;
+    uint32_t* d_ocnt = nullptr;
+    uint64_t d_out_rows = 0;
+    uint32_t d_out_k = 0;
+
+    cudaStream_t stream = nullptr;
+    std::mutex mu;
+    uint32_t code_bits() const { return m * 8; }
+};
+
+namespace {
+
+__global__ void fill_u32(uint32_t* p, uint64_t n, uint32_t v) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+__global__ void add_u64(const unsigned long long* src, uint32_t n, unsigned long long* dst) {
+    unsigned long long s = 0;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) s += src[i];
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+    if ((threadIdx.x & 31) == 0 && s) atomicAdd(dst, s);
+}
+
+__global__ void probes_to_cells(const unsigned long long* keys, uint64_t n, uint32_t* cells) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        cells[i] = (uint32_t)keys[i];
+}
+
+void grow_ins(poly_b200_ivf* iv, uint64_t need) {
+    if (need <= iv->cap_ins) return;
+    const uint64_t cap = std::max<uint64_t>(need, iv->cap_ins * 2);
+    uint8_t* c = dalloc<uint8_t>(cap * iv->cb);
+    uint32_t* a = dalloc<uint32_t>(cap);
+    if (iv->n) {
+        CK(cudaMemcpyAsync(c, iv->d_codes_ins, iv->n * iv->cb, cudaMemcpyDeviceToDevice, iv->stream));
+        CK(cudaMemcpyAsync(a, iv->d_cells_ins, iv->n * 4, cudaMemcpyDeviceToDevice, iv->stream));
+    }
+    CK(cudaStreamSynchronize(iv->stream));
+    dfree(iv->d_codes_ins);
+    dfree(iv->d_cells_ins);
+    iv->d_codes_ins = c;
+    iv->d_cells_ins = a;
+    iv->cap_ins = cap;
+}
+
+// CSR rebuild: histogram of cells -> offsets -> scatter codes and key-low words.
+void rebuild_lists(poly_b200_ivf* iv) {
+    if (!iv->lists_dirty) return;
+    cudaStream_t s = iv->stream;
+    iv->idm.sync(iv->n);
+    dfree(iv->d_codes_list);
+    dfree(iv->d_low_list);
+    const uint64_t pad = 1024;
+    iv->d_codes_list = dalloc<uint8_t>((iv->n + pad) * iv->cb);
+    iv->d_low_list = dalloc<uint32_t>(iv->n + pad);
+    unsigned long long* hist = dalloc<unsigned long long>(iv->nlist);
+    uint32_t* low_ins = dalloc<uint32_t>(std::max<uint64_t>(iv->n, 1));
+    try {
+        CK(cudaMemsetAsync(hist, 0, iv->nlist * 8, s));
+        pb::launch_cell_hist(iv->d_cells_ins, iv->n, hist, s);
+        std::vector<unsigned long long> h(iv->nlist);
+        CK(cudaMemcpyAsync(h.data(), hist, iv->nlist * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        iv->h_off.assign(iv->nlist + 1, 0);
+        iv->max_list = 0;
+        for (uint32_t c = 0; c < iv->nlist; ++c) {
+            iv->h_off[c + 1] = iv->h_off[c] + h[c];
+            iv->max_list = std::max<uint64_t>(iv->max_list, h[c]);
+        }
+        CK(cudaMemcpyAsync(iv->d_off, iv->h_off.data(), (iv->nlist + 1) * 8, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(hist, iv->h_off.data(), iv->nlist * 8, cudaMemcpyHostToDevice, s));  // cursors
+        pb::launch_key_low(iv->n, iv->idm.mode, iv->idm.key_id0, iv->idm.d_id32, low_ins, s);
+        pb::launch_cell_scatter(iv->d_cells_ins, iv->n, iv->cb, iv->d_codes_ins, low_ins, hist, iv->d_codes_list,
+                                iv->d_low_list, s);
+        CK(cudaStreamSynchronize(s));
+        CK(cudaGetLastError());
+    } catch (...) {
+        dfree(hist);
+        dfree(low_ins);
+        throw;
+    }
+    dfree(hist);
+    dfree(low_ins);
+    iv->lists_dirty = false;
+}
+
+void ensure_ivf_scratch(poly_b200_ivf* iv, uint32_t nprobe, uint32_t k) {
+    if (!iv->ckeys) {
+        iv->ckeys = dalloc<unsigned long long>((size_t)IVF_NQB * iv->nlist);
+        iv->nl_counts = dalloc<uint32_t>(IVF_NQB);
+        fill_u32<<<1, 256, 0, iv->stream>>>(iv->nl_counts, IVF_NQB, iv->nlist);
+        pb::count_launch();
+        iv->np_eff = dalloc<uint32_t>(IVF_NQB);
+        iv->scanned = dalloc<unsigned long long>(IVF_NQB);
+        iv->ctrl = dalloc<uint32_t>(IVF_NQB + 32);
+        iv->thr = dalloc<unsigned long long>(IVF_NQB);
+        iv->kcounts = dalloc<uint32_t>(IVF_NQB);
+        iv->surv_total = dalloc<unsigned long long>(1);
+        iv->scan_total = dalloc<unsigned long long>(1);
+        iv->sticky_overflow = dalloc<uint32_t>(1);
+    }
+    if (iv->scratch_nprobe < nprobe) {
+        dfree(iv->probe_keys);
+        dfree(iv->probe_counts);
+        dfree(iv->lutp);
+        dfree(iv->qcodes);
+        iv->scratch_nprobe = nprobe;
+        iv->probe_keys = dalloc<unsigned long long>((size_t)IVF_NQB * nprobe);
+        iv->probe_counts = dalloc<uint32_t>(IVF_NQB);
+        iv->lutp = dalloc<float>((size_t)IVF_NQB * nprobe * iv->m * 256);
+        iv->qcodes = dalloc<uint8_t>((size_t)IVF_NQB * nprobe * iv->cb);
+    }
+    const uint32_t cap = (uint32_t)std::max<uint64_t>(131072, 4 * iv->max_list);
+    if (iv->cand_cap < cap) {
+        dfree(iv->cand);
+        iv->cand_cap = cap;
+        iv->cand = dalloc<unsigned long long>((size_t)IVF_NQB * cap);
+    }
+    if (iv->keys_k < k) {
+        dfree(iv->keys);
+        iv->keys_k = k;
+        iv->keys = dalloc<unsigned long long>((size_t)IVF_NQB * k);
+    }
+}
+
+void validate(const poly_b200_ivf* iv, const poly_b200_ivf_params* p) {
+    require(p != nullptr, POLY_B200_INVALID_ARGUMENT, "null search params");
+    require(p->strategy >= 0 && p->strategy <= 3, POLY_B200_INVALID_ARGUMENT, "unknown strategy");
+    require(p->tau <= iv->code_bits(), POLY_B200_INVALID_ARGUMENT, "tau exceeds code bits");
+    require(p->k <= (uint32_t)pb::KMAX, POLY_B200_INVALID_ARGUMENT, "k > 2048 is not supported on the GPU path");
+    require(p->nprobe >= 1, POLY_B200_INVALID_ARGUMENT, "nprobe must be >= 1");  // CoarseConfig: nprobe >= 1
+}
+
+// Enqueue enumerate_cells for a batch: probe_keys (nqb x np) ascending.
+void enumerate_cells(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, uint32_t np, cudaStream_t s) {
+    pb::launch_coarse_keys(d_q, nqb, iv->dim, iv->d_coarse, iv->nlist, iv->ckeys, s);
+    pb::launch_topk(iv->ckeys, iv->nl_counts, iv->nlist, 1, 0, 0, nqb, np, iv->probe_keys, iv->probe_counts, s);
+}
+
+// One batch of <= 256 queries; outputs through keys_to_ids.
+void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_b200_ivf_params* p, int64_t* d_ids,
+                  float* d_scores, uint32_t* d_counts, cudaStream_t s) {
+    const uint32_t k = p->k;
+    const uint32_t np = std::min(p->nprobe, iv->nlist);
+    int strategy = p->strategy;
+    if (strategy == pb::DUAL && p->tau >= iv->code_bits()) strategy = pb::ADC;  // SPEC.md:388 boundary
+    CK(cudaMemsetAsync(iv->ctrl, 0, (IVF_NQB + 32) * 4, s));
+    CK(cudaMemsetAsync(iv->thr, 0xFF, IVF_NQB * 8, s));
+    enumerate_cells(iv, d_q, nqb, np, s);
+    pb::launch_ivf_probe_count(iv->probe_keys, nqb, np, iv->d_off, p->cap, iv->np_eff, iv->scanned, s);
+    add_u64<<<1, 256, 0, s>>>(iv->scanned, nqb, iv->scan_total);
+    pb::count_launch();
+    pb::launch_residual_lut(d_q, nqb, iv->dim, iv->m, iv->probe_keys, np, iv->d_coarse, iv->d_codebooks,
+                            iv->d_perms, iv->lutp, iv->qcodes, s);
+    pb::IvfScanArgs a{};
+    a.codes = iv->d_codes_list;
+    a.low = iv->d_low_list;
+    a.off = iv->d_off;
+    a.probe_keys = iv->probe_keys;
+    a.np_eff = iv->np_eff;
+    a.lutp = iv->lutp;
+    a.qcodes = iv->qcodes;
+    a.nq = nqb;
+    a.nprobe = np;
+    a.tau = p->tau;
+    a.thr = iv->thr;
+    a.cand = iv->cand;
+    a.cap = iv->cand_cap;
+    a.ccount = iv->ctrl;
+    a.overflow = iv->ctrl + IVF_NQB;
+    a.surv_total = iv->surv_total;
+    // rounds of probes [0,1), [1,4), [4,16), ...: each later round scans with the
+    // exact k-th key of the candidates so far as its bound
+    uint32_t round = 0;
+    for (uint32_t pb_ = 0; pb_ < np; ++round) {
+        const uint32_t pe = std::min(np, pb_ == 0 ? 1u : pb_ * 4);
+        a.p_begin = pb_;
+        a.p_end = pe;
+        a.work = iv->ctrl + IVF_NQB + 1 + round;
+        pb::launch_ivf_scan(a, strategy, iv->m, iv->num_sms, s);
+        pb::launch_topk(iv->cand, iv->ctrl, iv->cand_cap, 1, 0, 0, nqb, k, iv->keys, iv->kcounts, s);
+        if (pe < np) pb::launch_seed_thr(iv->keys, iv->kcounts, nqb, k, iv->thr, s);
+        pb_ = pe;
+    }
+    pb::launch_or_flag(iv->sticky_overflow, iv->ctrl + IVF_NQB, s);
+    pb::launch_keys_to_ids(iv->keys, iv->kcounts, nqb, k, iv->idm.d_rank_to_id, d_ids, d_scores, d_counts, s);
+}
+
+// All batches; returns strategy survivors semantics (0 none, 1 = scanned, 2 counted).
+int device_search(poly_b200_ivf* iv, const float* d_q, uint64_t nq, const poly_b200_ivf_params* p, int64_t* d_ids,
+                  float* d_scores, uint32_t* d_counts, cudaStream_t s) {
+    validate(iv, p);
+    if (nq == 0) return 0;
+    if (p->k == 0 || iv->n == 0) {
+        if (d_counts) CK(cudaMemsetAsync(d_counts, 0, nq * 4, s));
+        if (p->k) pb::launch_keys_to_ids(nullptr, nullptr, (uint32_t)nq, p->k, nullptr, d_ids, d_scores, nullptr, s);
+        return 0;
+    }
+    rebuild_lists(iv);
+    ensure_ivf_scratch(iv, std::min(p->nprobe, iv->nlist), p->k);
+    CK(cudaMemsetAsync(iv->surv_total, 0, 8, s));
+    CK(cudaMemsetAsync(iv->scan_total, 0, 8, s));
+    CK(cudaMemsetAsync(iv->sticky_overflow, 0, 4, s));
+    for (uint64_t b0 = 0; b0 < nq; b0 += IVF_NQB) {
+        const uint32_t nqb = (uint32_t)std::min<uint64_t>(IVF_NQB, nq - b0);
+        search_batch(iv, d_q + b0 * iv->dim, nqb, p, d_ids + b0 * p->k, d_scores + b0 * p->k,
+                     d_counts ? d_counts + b0 : nullptr, s);
+        CK(cudaGetLastError());
+    }
+    if (p->strategy == pb::DUAL) return p->tau >= iv->code_bits() ? 1 : 2;
+    return 0;
+}
+
+void read_stats(poly_b200_ivf* iv, int mode, poly_b200_search_stats* st, cudaStream_t s) {
+    unsigned long long h[2] = {0, 0};
+    uint32_t ovf = 0;
+    if (iv->scan_total) {
+        CK(cudaMemcpyAsync(&h[0], iv->scan_total, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&h[1], iv->surv_total, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&ovf, iv->sticky_overflow, 4, cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    require(!ovf, POLY_B200_INTERNAL, "IVF candidate list overflow: results incomplete");
+    if (st) {
+        st->scanned = h[0];
+        st->survivors = mode == 2 ? h[1] : (mode == 1 ? h[0] : 0);
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int poly_b200_ivf_create(const poly_b200_pq_desc* pq, const float* coarse, uint32_t nlist, int device,
+                         poly_b200_ivf** out) {
+    return guard([&] {
+        require(out != nullptr, POLY_B200_INVALID_ARGUMENT, "null output handle");
+        check_pq(pq);
+        require(coarse != nullptr && nlist > 0, POLY_B200_INVALID_ARGUMENT, "empty coarse quantizer");
+        for (uint64_t i = 0; i < (uint64_t)nlist * pq->dim; ++i)
+            require(std::isfinite(coarse[i]), POLY_B200_INVALID_ARGUMENT, "non-finite coarse centroid");
+        int ndev = 0;
+        CK(cudaGetDeviceCount(&ndev));
+        require(device >= 0 && device < ndev, POLY_B200_INVALID_ARGUMENT, "no such CUDA device");
+        DeviceGuard dg(device);
+        auto* iv = new poly_b200_ivf();
+        try {
+            iv->device = device;
+            CK(cudaDeviceGetAttribute(&iv->num_sms, cudaDevAttrMultiProcessorCount, device));
+            iv->m = pq->m;
+            iv->dim = (uint32_t)pq->dim;
+            iv->cb = pq->m;
+            iv->nlist = nlist;
+            const size_t ncb = (size_t)pq->m * 256 * pb::DSUB;
+            iv->h_codebooks.assign(pq->codebooks, pq->codebooks + ncb);
+            iv->h_perms.assign(pq->perms, pq->perms + (size_t)pq->m * 256);
+            iv->h_coarse.assign(coarse, coarse + (size_t)nlist * pq->dim);
+            CK(cudaStreamCreateWithFlags(&iv->stream, cudaStreamNonBlocking));
+            iv->d_codebooks = dalloc<float>(ncb);
+            iv->d_perms = dalloc<uint16_t>(iv->h_perms.size());
+            iv->d_coarse = dalloc<float>(iv->h_coarse.size());
+            iv->d_off = dalloc<uint64_t>(nlist + 1);
+            CK(cudaMemcpy(iv->d_codebooks, iv->h_codebooks.data(), ncb * 4, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(iv->d_perms, iv->h_perms.data(), iv->h_perms.size() * 2, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(iv->d_coarse, iv->h_coarse.data(), iv->h_coarse.size() * 4, cudaMemcpyHostToDevice));
+            CK(cudaMemset(iv->d_off, 0, (nlist + 1) * 8));
+        } catch (...) {
+            poly_b200_ivf_destroy(iv);
+            throw;
+        }
+        *out = iv;
+    });
+}
+
+int poly_b200_ivf_destroy(poly_b200_ivf* iv) {
+    if (!iv) return POLY_B200_OK;
+    return guard([&] {
+        {
+            DeviceGuard dg(iv->device);
+            if (iv->stream) cudaStreamSynchronize(iv->stream);
+            for (void* p : {(void*)iv->d_codebooks, (void*)iv->d_perms, (void*)iv->d_coarse, (void*)iv->d_codes_ins,
+                            (void*)iv->d_cells_ins, (void*)iv->d_off, (void*)iv->d_codes_list, (void*)iv->d_low_list,
+                            (void*)iv->ckeys, (void*)iv->nl_counts, (void*)iv->probe_keys, (void*)iv->probe_counts,
+                            (void*)iv->np_eff, (void*)iv->scanned, (void*)iv->lutp, (void*)iv->qcodes,
+                            (void*)iv->cand, (void*)iv->ctrl, (void*)iv->thr, (void*)iv->keys, (void*)iv->kcounts,
+                            (void*)iv->surv_total, (void*)iv->scan_total, (void*)iv->sticky_overflow, (void*)iv->d_q,
+                            (void*)iv->d_oid, (void*)iv->d_osc, (void*)iv->d_ocnt})
+                dfree(p);
+            iv->idm.release();
+            if (iv->stream) cudaStreamDestroy(iv->stream);
+        }
+        delete iv;
+    });
+}
+
+uint64_t poly_b200_ivf_size(const poly_b200_ivf* iv) { return iv ? iv->n : 0; }
+
+int poly_b200_ivf_assign(poly_b200_ivf* iv, const float* x, uint64_t n, uint32_t* cells) {
+    return guard([&] {
+        require(iv && (n == 0 || (x && cells)), POLY_B200_INVALID_ARGUMENT, "null arguments");
+        std::lock_guard<std::mutex> lk(iv->mu);
+        DeviceGuard dg(iv->device);
+        if (n == 0) return;
+        float* d_x = dalloc<float>(n * iv->dim);
+        uint32_t* d_c = dalloc<uint32_t>(n);
+        cudaError_t e = cudaMemcpyAsync(d_x, x, n * iv->dim * 4, cudaMemcpyHostToDevice, iv->stream);
+        if (e == cudaSuccess) {
+            pb::launch_assign(d_x, n, iv->dim, iv->d_coarse, iv->nlist, d_c, iv->stream);
+            e = cudaMemcpyAsync(cells, d_c, n * 4, cudaMemcpyDeviceToHost, iv->stream);
+        }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(iv->stream);
+        dfree(d_x);
+        dfree(d_c);
+        CK(e);
+    });
+}
+
+int poly_b200_ivf_add_device(poly_b200_ivf* iv, const float* d_x, const uint32_t* d_cells, uint64_t n, int64_t id0,
+                             void* stream) {
+    return guard([&] {
+        require(iv && (n == 0 || (d_x && d_cells)), POLY_B200_INVALID_ARGUMENT, "null arguments");
+        std::lock_guard<std::mutex> lk(iv->mu);
+        DeviceGuard dg(iv->device);
+        if (n == 0) return;
+        cudaStream_t s = (cudaStream_t)stream;
+        CK(cudaStreamSynchronize(s));
+        grow_ins(iv, iv->n + n);
+        CK(cudaMemcpyAsync(iv->d_cells_ins + iv->n, d_cells, n * 4, cudaMemcpyDeviceToDevice, iv->stream));
+        pb::launch_residual_encode(d_x, n, iv->dim, iv->m, iv->d_coarse, d_cells, iv->d_codebooks, iv->d_perms,
+                                   iv->d_codes_ins + iv->n * iv->cb, iv->stream);
+        CK(cudaStreamSynchronize(iv->stream));
+        CK(cudaGetLastError());
+        iv->idm.append_range(id0, iv->n, n);
+        iv->n += n;
+        iv->lists_dirty = true;
+    });
+}
+
+int poly_b200_ivf_add(poly_b200_ivf* iv, const float* x, uint64_t n, const uint32_t* cells, const int64_t* ids) {
+    return guard([&] {
+        require(iv && (n == 0 || x), POLY_B200_INVALID_ARGUMENT, "null arguments");
+        std::lock_guard<std::mutex> lk(iv->mu);
+        DeviceGuard dg(iv->device);
+        if (n == 0) return;
+        for (uint64_t i = 0; i < n * iv->dim; ++i)
+            require(std::isfinite(x[i]), POLY_B200_INVALID_ARGUMENT, "non-finite entry in vector set");
+        if (cells)
+            for (uint64_t i = 0; i < n; ++i) require(cells[i] < iv->nlist, POLY_B200_INVALID_ARGUMENT, "bad cell");
+        grow_ins(iv, iv->n + n);
+        float* d_x = dalloc<float>(n * iv->dim);
+        cudaError_t e = cudaMemcpyAsync(d_x, x, n * iv->dim * 4, cudaMemcpyHostToDevice, iv->stream);
+        uint32_t* d_c = iv->d_cells_ins + iv->n;
+        if (e == cudaSuccess) {
+            if (cells) e = cudaMemcpyAsync(d_c, cells, n * 4, cudaMemcpyHostToDevice, iv->stream);
+            else pb::launch_assign(d_x, n, iv->dim, iv->d_coarse, iv->nlist, d_c, iv->stream);
+        }
+        if (e == cudaSuccess) {
+            pb::launch_residual_encode(d_x, n, iv->dim, iv->m, iv->d_coarse, d_c, iv->d_codebooks, iv->d_perms,
+                                       iv->d_codes_ins + iv->n * iv->cb, iv->stream);
+            e = cudaStreamSynchronize(iv->stream);
+        }
+        dfree(d_x);
+        CK(e);
+        CK(cudaGetLastError());
+        iv->idm.append(ids, iv->n, n);
+        iv->n += n;
+        iv->lists_dirty = true;
+    });
+}
+
+int poly_b200_ivf_add_codes(poly_b200_ivf* iv, const uint32_t* cells, const uint8_t* codes, const int64_t* ids,
+                            uint64_t n) {
+    return guard([&] {
+        require(iv && (n == 0 || (cells && codes)), POLY_B200_INVALID_ARGUMENT, "null arguments");
+        std::lock_guard<std::mutex> lk(iv->mu);
+        DeviceGuard dg(iv->device);
+        if (n == 0) return;
+        for (uint64_t i = 0; i < n; ++i) require(cells[i] < iv->nlist, POLY_B200_INVALID_ARGUMENT, "bad cell");
+        grow_ins(iv, iv->n + n);
+        CK(cudaMemcpyAsync(iv->d_cells_ins + iv->n, cells, n * 4, cudaMemcpyHostToDevice, iv->stream));
+        CK(cudaMemcpyAsync(iv->d_codes_ins + iv->n * iv->cb, codes, n * iv->cb, cudaMemcpyHostToDevice, iv->stream));
+        CK(cudaStreamSynchronize(iv->stream));
+        iv->idm.append(ids, iv->n, n);
+        iv->n += n;
+        iv->lists_dirty = true;
+    });
+}
+
+int poly_b200_ivf_get_lists(poly_b200_ivf* iv, uint64_t* off, uint8_t* codes, int64_t* ids) {
+    return guard([&] {
+        require(iv != nullptr, POLY_B200_INVALID_ARGUMENT, "null index");
+        std::lock_guard<std::mutex> lk(iv->mu);
+        DeviceGuard dg(iv->device);
+        rebuild_lists(iv);
+        if (off) std::copy(iv->h_off.begin(), iv->h_off.end(), off);
+        if (codes && iv->n) CK(cudaMemcpy(codes, iv->d_codes_list, iv->n * iv->cb, cudaMemcpyDeviceToHost));
+        if (ids && iv->n) {
+            std::vector<uint32_t> low(iv->n);
+            CK(cudaMemcpy(low.data(), iv->d_low_list, iv->n * 4, cudaMemcpyDeviceToHost));
+            std::vector<int64_t> r2id;
+            if (iv->idm.d_rank_to_id) {
+                r2id.resize(iv->n);
+                CK(cudaMemcpy(r2id.data(), iv->idm.d_rank_to_id, iv->n * 8, cudaMemcpyDeviceToHost));
+            }
+            for (uint64_t i = 0; i < iv->n; ++i) ids[i] = r2id.empty() ? (int64_t)low[i] : r2id[low[i]];
+        }
+    });
+}
+
+int poly_b200_ivf_probes(poly_b200_ivf* iv, const float* queries, uint64_t nq, uint32_t nprobe, uint32_t* cells) {
+    return guard([&] {
+        require(iv && (nq == 0 || (queries && cells)) && nprobe >= 1 && nprobe <= iv->nlist &&
+                    nprobe <= (uint32_t)pb::KMAX,
+                POLY_B200_INVALID_ARGUMENT, "bad arguments");
+        std::lock_guard<std::mutex> lk(iv->mu);
+        DeviceGuard dg(iv->device);
+        ensure_ivf_scratch(iv, nprobe, 1);
+        cudaStream_t s = iv->stream;
+        float* d_q = dalloc<float>(std::max<uint64_t>(nq, 1) * iv->dim);
+        uint32_t* d_c = dalloc<uint32_t>((size_t)IVF_NQB * nprobe);
+        cudaError_t e = cudaSuccess;
+        if (nq) e = cudaMemcpyAsync(d_q, queries, nq * iv->dim * 4, cudaMemcpyHostToDevice, s);
+        for (uint64_t b0 = 0; b0 < nq && e == cudaSuccess; b0 += IVF_NQB) {
+            const uint32_t nqb = (uint32_t)std::min<uint64_t>(IVF_NQB, nq - b0);
+            enumerate_cells(iv, d_q + b0 * iv->dim, nqb, nprobe, s);
+            probes_to_cells<<<64, 256, 0, s>>>(iv->probe_keys, (uint64_t)nqb * nprobe, d_c);
+            pb::count_launch();
+            e = cudaMemcpyAsync(cells + b0 * nprobe, d_c, (size_t)nqb * nprobe * 4, cudaMemcpyDeviceToHost, s);
+        }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        dfree(d_q);
+        dfree(d_c);
+        CK(e);
+    });
+}
+
+int poly_b200_ivf_search_device(poly_b200_ivf* iv, const float* d_q, uint64_t nq, const poly_b200_ivf_params* p,
+                                int64_t* d_ids, float* d_scores, uint32_t* d_counts, void* stream,
+                                poly_b200_search_stats* stats) {
+    return guard([&] {
+        require(iv != nullptr, POLY_B200_INVALID_ARGUMENT, "null index");
+        require(nq == 0 || (d_q && d_ids && d_scores) || (p && p->k == 0), POLY_B200_INVALID_ARGUMENT, "null buffers");
+        std::lock_guard<std::mutex> lk(iv->mu);
+        DeviceGuard dg(iv->device);
+        cudaStream_t s = (cudaStream_t)stream;
+        const int mode = device_search(iv, d_q, nq, p, d_ids, d_scores, d_counts, s);
+        if (stats) {
+            stats->scanned = stats->survivors = 0;
+            if (nq && p->k && iv->n) read_stats(iv, mode, stats, s);
+        }
+    });
+}
+
+int poly_b200_ivf_search(poly_b200_ivf* iv, const float* queries, uint64_t nq, const poly_b200_ivf_params* p,
+                         int64_t* out_ids, float* out_scores, uint32_t* out_counts, poly_b200_search_stats* stats) {
+    return guard([&] {
+        require(iv != nullptr, POLY_B200_INVALID_ARGUMENT, "null index");
+        validate(iv, p);
+        require(nq == 0 || queries, POLY_B200_INVALID_ARGUMENT, "null queries");
+        std::lock_guard<std::mutex> lk(iv->mu);
+        DeviceGuard dg(iv->device);
+        if (stats) *stats = {0, 0};
+        if (nq == 0) return;
+        const uint32_t k = std::max<uint32_t>(p->k, 1);
+        cudaStream_t s = iv->stream;
+        if (iv->d_q_cap < nq * iv->dim) {
+            dfree(iv->d_q);
+            iv->d_q_cap = nq * iv->dim;
+            iv->d_q = dalloc<float>(iv->d_q_cap);
+        }
+        if (iv->d_out_rows < nq || iv->d_out_k < k) {
+            dfree(iv->d_oid);
+            dfree(iv->d_osc);
+            dfree(iv->d_ocnt);
+            iv->d_out_rows = std::max<uint64_t>(nq, iv->d_out_rows);
+            iv->d_out_k = std::max<uint32_t>(k, iv->d_out_k);
+            iv->d_oid = dalloc<int64_t>(iv->d_out_rows * iv->d_out_k);
+            iv->d_osc = dalloc<float>(iv->d_out_rows * iv->d_out_k);
+            iv->d_ocnt = dalloc<uint32_t>(iv->d_out_rows);
+        }
+        CK(cudaMemcpyAsync(iv->d_q, queries, nq * iv->dim * 4, cudaMemcpyHostToDevice, s));
+        const int mode = device_search(iv, iv->d_q, nq, p, iv->d_oid, iv->d_osc, iv->d_ocnt, s);
+        if (p->k) {
+            CK(cudaMemcpyAsync(out_ids, iv->d_oid, nq * p->k * 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(out_scores, iv->d_osc, nq * p->k * 4, cudaMemcpyDeviceToHost, s));
+        }
+        if (out_counts) CK(cudaMemcpyAsync(out_counts, iv->d_ocnt, nq * 4, cudaMemcpyDeviceToHost, s));
+        if (p->k && iv->n) read_stats(iv, mode, stats, s);
+        else CK(cudaStreamSynchronize(s));
+    });
+}
+
+}  // extern "C"

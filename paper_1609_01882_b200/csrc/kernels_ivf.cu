@@ -1,0 +1,473 @@
+// kernels_ivf.cu -- IVF search path (coarseindex; configs 2/4).
+//
+// The reference ships no IVF code; these kernels follow the oracle restatement
+// (oracle/polyoracle.c po_ivf_*), itself pinned to golden vectors composed
+// from the reference primitives:
+//   K5  coarse_keys_kernel   sq_l2(q, c) (distances.cpp:10-17) for every cell, exact
+//                            fp32 in dim order; key = (dist bits << 32 | cell), so K3
+//                            with k = nprobe yields enumerate_cells:
+//                            ascending distance, ties -> lower cell.
+//   K1r residual_lut_kernel  per (query, probe): r = q - c_cell, then compute_lut /
+//                            permuted_lut / encode on r (pq.cpp:29-45,91-119).
+//   K6  ivf_scan_kernel      per (query, probe) item, one warp: stream the cell's
+//                            (residual code, id) list, Hamming filter against the
+//                            item's query code, ADC from the item's LUT in shared
+//                            memory, candidate keys appended to the query's list.
+//   assign_kernel            build: nearest coarse cell by sq_l2 (strict <).
+#include "poly_b200.cuh"
+#include "synth.cuh"
+
+namespace pb {
+
+// ------------------------------------------------------------------ K5
+// CTA tile: 64 queries x 64 cells, 256 threads, 4 x 4 register block per thread;
+// dims are consumed in chunks of 32 staged in shared memory.
+constexpr int K5_T = 64, K5_D = 32;
+
+__global__ void __launch_bounds__(256) coarse_keys_kernel(const float* __restrict__ q, uint32_t nq, uint32_t dim,
+                                                          const float* __restrict__ cent, uint32_t nlist,
+                                                          unsigned long long* __restrict__ keys) {
+    __shared__ float qs[K5_T][K5_D + 1];
+    __shared__ float cs[K5_T][K5_D + 1];
+    const uint32_t c0 = blockIdx.x * K5_T, q0 = blockIdx.y * K5_T;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16 x 16 threads, 4 x 4 each
+    float acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+    for (uint32_t d0 = 0; d0 < dim; d0 += K5_D) {
+        for (int e = threadIdx.x; e < K5_T * K5_D; e += 256) {
+            const int r = e / K5_D, c = e % K5_D;
+            qs[r][c] = (q0 + r < nq) ? q[(size_t)(q0 + r) * dim + d0 + c] : 0.0f;
+            cs[r][c] = (c0 + r < nlist) ? cent[(size_t)(c0 + r) * dim + d0 + c] : 0.0f;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int d = 0; d < K5_D; ++d) {
+            float a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = qs[ty + 16 * i][d];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = cs[tx + 16 * j][d];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float t = __fsub_rn(a[i], b[j]);
+                    acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(t, t));  // sq_l2 order, no FMA
+                }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t qi = q0 + ty + 16 * i;
+        if (qi >= nq) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t c = c0 + tx + 16 * j;
+            if (c < nlist) keys[(size_t)qi * nlist + c] = ((unsigned long long)__float_as_uint(acc[i][j]) << 32) | c;
+        }
+    }
+}
+
+void launch_coarse_keys(const float* q, uint32_t nq, uint32_t dim, const float* cent, uint32_t nlist,
+                        unsigned long long* keys, cudaStream_t s) {
+    if (nq == 0) return;
+    dim3 grid((nlist + K5_T - 1) / K5_T, (nq + K5_T - 1) / K5_T);
+    coarse_keys_kernel<<<grid, 256, 0, s>>>(q, nq, dim, cent, nlist, keys);
+    count_launch();
+}
+
+// ------------------------------------------------------------------ K1r
+// grid (nq * nprobe, m): item (q, p) -> residual LUT (stored-field indexed) + code.
+__global__ void __launch_bounds__(256) residual_lut_kernel(const float* __restrict__ queries, uint32_t dim, uint32_t m,
+                                                           const unsigned long long* __restrict__ probe_keys,
+                                                           uint32_t nprobe, const float* __restrict__ cent,
+                                                           const float* __restrict__ codebooks,
+                                                           const uint16_t* __restrict__ perms, float* __restrict__ lutp,
+                                                           uint8_t* __restrict__ qcodes) {
+    const uint32_t item = blockIdx.x, sq = blockIdx.y, j = threadIdx.x;
+    const uint32_t qi = item / nprobe;
+    const uint32_t cell = (uint32_t)probe_keys[item];
+    __shared__ float sub[DSUB];
+    __shared__ float wv[8];
+    __shared__ uint32_t wj[8];
+    if (j < DSUB) {
+        const uint32_t d = sq * DSUB + j;
+        sub[j] = __fsub_rn(queries[(size_t)qi * dim + d], cent[(size_t)cell * dim + d]);  // r = q - c
+    }
+    __syncthreads();
+    const float4* c = reinterpret_cast<const float4*>(codebooks + ((size_t)sq * KSUB + j) * DSUB);
+    float acc = 0.0f;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+        const float4 cc = c[v];
+        float t;
+        t = __fsub_rn(sub[4 * v + 0], cc.x); acc = __fadd_rn(acc, __fmul_rn(t, t));
+        t = __fsub_rn(sub[4 * v + 1], cc.y); acc = __fadd_rn(acc, __fmul_rn(t, t));
+        t = __fsub_rn(sub[4 * v + 2], cc.z); acc = __fadd_rn(acc, __fmul_rn(t, t));
+        t = __fsub_rn(sub[4 * v + 3], cc.w); acc = __fadd_rn(acc, __fmul_rn(t, t));
+    }
+    const uint32_t p = perms[sq * KSUB + j];
+    lutp[((size_t)item * m + sq) * KSUB + p] = acc;
+    float bv = acc;
+    uint32_t bj = j;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const float ov = __shfl_down_sync(0xffffffffu, bv, off);
+        const uint32_t oj = __shfl_down_sync(0xffffffffu, bj, off);
+        if (ov < bv || (ov == bv && oj < bj)) { bv = ov; bj = oj; }
+    }
+    if ((j & 31) == 0) { wv[j >> 5] = bv; wj[j >> 5] = bj; }
+    __syncthreads();
+    if (j == 0) {
+        for (int w = 1; w < 8; ++w)
+            if (wv[w] < bv || (wv[w] == bv && wj[w] < bj)) { bv = wv[w]; bj = wj[w]; }
+        qcodes[(size_t)item * m + sq] = static_cast<uint8_t>(perms[sq * KSUB + bj]);
+    }
+}
+
+void launch_residual_lut(const float* queries, uint32_t nq, uint32_t dim, uint32_t m,
+                         const unsigned long long* probe_keys, uint32_t nprobe, const float* cent,
+                         const float* codebooks, const uint16_t* perms, float* lutp, uint8_t* qcodes, cudaStream_t s) {
+    if (nq == 0) return;
+    residual_lut_kernel<<<dim3(nq * nprobe, m), 256, 0, s>>>(queries, dim, m, probe_keys, nprobe, cent, codebooks,
+                                                            perms, lutp, qcodes);
+    count_launch();
+}
+
+// ------------------------------------------------------------------ probes under the cap
+// np_eff[q] = number of probes visited: stop after the probe at which the
+// scanned count reaches cap (0 = no cap); scanned[q] = codes visited.
+__global__ void ivf_probe_count_kernel(const unsigned long long* __restrict__ probe_keys, uint32_t nq,
+                                       uint32_t nprobe, const uint64_t* __restrict__ off, uint64_t cap,
+                                       uint32_t* __restrict__ np_eff, unsigned long long* __restrict__ scanned) {
+    const uint32_t qi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (qi >= nq) return;
+    uint64_t ns = 0;
+    uint32_t p = 0;
+    for (; p < nprobe; ++p) {
+        if (cap && ns >= cap) break;
+        const uint32_t cell = (uint32_t)probe_keys[(size_t)qi * nprobe + p];
+        ns += off[cell + 1] - off[cell];
+    }
+    np_eff[qi] = p;
+    scanned[qi] = ns;
+}
+
+void launch_ivf_probe_count(const unsigned long long* probe_keys, uint32_t nq, uint32_t nprobe, const uint64_t* off,
+                            uint64_t cap, uint32_t* np_eff, unsigned long long* scanned, cudaStream_t s) {
+    if (nq == 0) return;
+    ivf_probe_count_kernel<<<(nq + 127) / 128, 128, 0, s>>>(probe_keys, nq, nprobe, off, cap, np_eff, scanned);
+    count_launch();
+}
+
+// ------------------------------------------------------------------ K6
+constexpr int K6_WARPS = 8;
+
+template <int M> struct IvfCode;
+template <> struct IvfCode<8> { using T = uint2; };
+template <> struct IvfCode<16> { using T = uint4; };
+
+__device__ __forceinline__ uint32_t k6_ham(const uint2& a, const uint2& b) {
+    return __popc(a.x ^ b.x) + __popc(a.y ^ b.y);
+}
+__device__ __forceinline__ uint32_t k6_ham(const uint4& a, const uint4& b) {
+    return __popc(a.x ^ b.x) + __popc(a.y ^ b.y) + __popc(a.z ^ b.z) + __popc(a.w ^ b.w);
+}
+__device__ __forceinline__ uint32_t k6_nz(uint32_t x) {
+    x |= x >> 4;
+    x |= x >> 2;
+    x |= x >> 1;
+    return __popc(x & 0x01010101u);
+}
+__device__ __forceinline__ uint32_t k6_dis(const uint2& a, const uint2& b) { return k6_nz(a.x ^ b.x) + k6_nz(a.y ^ b.y); }
+__device__ __forceinline__ uint32_t k6_dis(const uint4& a, const uint4& b) {
+    return k6_nz(a.x ^ b.x) + k6_nz(a.y ^ b.y) + k6_nz(a.z ^ b.z) + k6_nz(a.w ^ b.w);
+}
+__device__ __forceinline__ uint32_t k6_word(const uint2& c, int w) { return w == 0 ? c.x : c.y; }
+__device__ __forceinline__ uint32_t k6_word(const uint4& c, int w) {
+    return w == 0 ? c.x : (w == 1 ? c.y : (w == 2 ? c.z : c.w));
+}
+template <int M, class C>
+__device__ __forceinline__ float k6_adc(const float* L, const C& c) {
+    float acc = L[k6_word(c, 0) & 0xFFu];
+#pragma unroll
+    for (int sq = 1; sq < M; ++sq) acc = __fadd_rn(acc, L[sq * KSUB + ((k6_word(c, sq >> 2) >> (8 * (sq & 3))) & 0xFFu)]);
+    return acc;
+}
+
+// One warp per (query, probe) item of probes [p_begin, p_end) of each query.
+template <int M, int STRAT>
+__global__ void __launch_bounds__(K6_WARPS * 32) ivf_scan_kernel(const IvfScanArgs a) {
+    using C = typename IvfCode<M>::T;
+    extern __shared__ __align__(16) uint8_t k6_smem[];
+    // per warp: LUT (M x 256 floats), survivor queue (64 codes + 64 positions)
+    constexpr size_t PER_WARP = (size_t)M * KSUB * 4 + 64 * sizeof(C) + 64 * 4;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint8_t* base = k6_smem + warp * PER_WARP;
+    float* L = reinterpret_cast<float*>(base);
+    C* qcode_q = reinterpret_cast<C*>(base + (size_t)M * KSUB * 4);
+    uint32_t* qpos_q = reinterpret_cast<uint32_t*>(base + (size_t)M * KSUB * 4 + 64 * sizeof(C));
+    const uint32_t span = a.p_end - a.p_begin;
+    const uint64_t nitems = (uint64_t)a.nq * span;
+    uint32_t surv_total = 0;
+    for (;;) {
+        uint32_t it = 0;
+        if (lane == 0) it = atomicAdd(a.work, 1u);
+        it = __shfl_sync(0xffffffffu, it, 0);
+        if (it >= nitems) break;
+        const uint32_t qi = it / span, p = a.p_begin + it % span;
+        if (p >= a.np_eff[qi]) continue;
+        const size_t item = (size_t)qi * a.nprobe + p;
+        const uint32_t cell = (uint32_t)a.probe_keys[item];
+        const uint64_t beg = a.off[cell], end = a.off[cell + 1];
+        // item LUT -> shared memory (M x 256 floats), query code -> registers
+        const float4* src = reinterpret_cast<const float4*>(a.lutp + item * M * KSUB);
+        for (int i = lane; i < M * KSUB / 4; i += 32) reinterpret_cast<float4*>(L)[i] = src[i];
+        const C qc = reinterpret_cast<const C*>(a.qcodes)[item];
+        const unsigned long long thr = __ldcg(a.thr + qi);
+        __syncwarp();
+        const C* codes = reinterpret_cast<const C*>(a.codes);
+        uint32_t qn = 0;
+        auto drain = [&](uint32_t cnt) {
+            __syncwarp();
+            if ((uint32_t)lane < cnt) {
+                const float score = k6_adc<M>(L, qcode_q[lane]);
+                const uint32_t pos = qpos_q[lane];
+                const uint32_t sb = __float_as_uint(score);
+                if (sb <= (uint32_t)(thr >> 32)) {
+                    const uint32_t low = __ldg(a.low + pos);
+                    const unsigned long long key = ((unsigned long long)sb << 32) | low;
+                    if (key < thr) {
+                        const uint32_t slot = atomicAdd(&a.ccount[qi], 1u);
+                        if (slot < a.cap) a.cand[(size_t)qi * a.cap + slot] = key;
+                        else atomicOr(a.overflow, 1u);
+                    }
+                }
+            }
+            __syncwarp();
+        };
+        for (uint64_t i0 = beg; i0 < end; i0 += 128) {
+            C c[4];
+            bool in[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint64_t i = i0 + u * 32 + lane;
+                in[u] = i < end;
+                if (in[u]) c[u] = __ldcs(codes + i);  // streamed once: evict-first
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t pos = (uint32_t)(i0 + u * 32 + lane);
+                if constexpr (STRAT == DUAL) {
+                    const bool pass = in[u] && k6_ham(c[u], qc) <= a.tau;
+                    const uint32_t b = __ballot_sync(0xffffffffu, pass);
+                    if (b) {
+                        if (pass) {
+                            const uint32_t at = qn + __popc(b & ((1u << lane) - 1u));
+                            qcode_q[at] = c[u];
+                            qpos_q[at] = pos;
+                        }
+                        qn += __popc(b);
+                        surv_total += __popc(b);
+                        if (qn >= 32) {
+                            drain(32);
+                            qn -= 32;
+                            if ((uint32_t)lane < qn) {
+                                qcode_q[lane] = qcode_q[32 + lane];
+                                qpos_q[lane] = qpos_q[32 + lane];
+                            }
+                            __syncwarp();
+                        }
+                    }
+                } else if (in[u]) {
+                    float score;
+                    if constexpr (STRAT == ADC) score = k6_adc<M>(L, c[u]);
+                    else if constexpr (STRAT == BINARY) score = (float)k6_ham(c[u], qc);
+                    else score = (float)k6_dis(c[u], qc);
+                    const uint32_t sb = __float_as_uint(score);
+                    if (sb <= (uint32_t)(thr >> 32)) {
+                        const uint32_t low = __ldg(a.low + pos);
+                        const unsigned long long key = ((unsigned long long)sb << 32) | low;
+                        if (key < thr) {
+                            const uint32_t slot = atomicAdd(&a.ccount[qi], 1u);
+                            if (slot < a.cap) a.cand[(size_t)qi * a.cap + slot] = key;
+                            else atomicOr(a.overflow, 1u);
+                        }
+                    }
+                }
+            }
+        }
+        if (STRAT == DUAL && qn) drain(qn);
+        __syncwarp();
+    }
+    if (STRAT == DUAL && lane == 0 && surv_total) atomicAdd(a.surv_total, (unsigned long long)surv_total);
+}
+
+template <int M, int STRAT>
+static void launch_ivf_one(const IvfScanArgs& a, unsigned grid, cudaStream_t s) {
+    using C = typename IvfCode<M>::T;
+    const size_t smem = (size_t)K6_WARPS * ((size_t)M * KSUB * 4 + 64 * sizeof(C) + 64 * 4);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(ivf_scan_kernel<M, STRAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    ivf_scan_kernel<M, STRAT><<<grid, K6_WARPS * 32, smem, s>>>(a);
+}
+
+template <int M>
+static void launch_ivf_m(const IvfScanArgs& a, int strategy, int num_sms, cudaStream_t s) {
+    const unsigned grid = (unsigned)num_sms * (M == 8 ? 3 : 1);  // 64 KB (m=8) / 128 KB (m=16) smem per CTA
+    switch (strategy) {
+        case DUAL: launch_ivf_one<M, DUAL>(a, grid, s); break;
+        case ADC: launch_ivf_one<M, ADC>(a, grid, s); break;
+        case BINARY: launch_ivf_one<M, BINARY>(a, grid, s); break;
+        default: launch_ivf_one<M, DISIDX>(a, grid, s); break;
+    }
+    count_launch();
+}
+
+void launch_ivf_scan(const IvfScanArgs& a, int strategy, uint32_t m, int num_sms, cudaStream_t s) {
+    if (a.nq == 0 || a.p_end <= a.p_begin) return;
+    if (m == 8) launch_ivf_m<8>(a, strategy, num_sms, s);
+    else launch_ivf_m<16>(a, strategy, num_sms, s);
+}
+
+// ------------------------------------------------------------------ build
+// Nearest coarse cell of each vector (sq_l2, strict <, ties -> lowest cell);
+// cells are staged through shared memory 32 at a time.
+__global__ void __launch_bounds__(128) assign_kernel(const float* __restrict__ x, uint64_t n, uint32_t dim,
+                                                     const float* __restrict__ cent, uint32_t nlist,
+                                                     uint32_t* __restrict__ assign) {
+    extern __shared__ float cs[];  // 32 x dim
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = i < n;
+    float best = 0.0f;
+    uint32_t bi = 0;
+    for (uint32_t c0 = 0; c0 < nlist; c0 += 32) {
+        const uint32_t nc = min(32u, nlist - c0);
+        __syncthreads();
+        for (uint32_t e = threadIdx.x; e < nc * dim; e += blockDim.x) cs[e] = cent[(size_t)c0 * dim + e];
+        __syncthreads();
+        if (!live) continue;
+        for (uint32_t c = 0; c < nc; ++c) {
+            float acc = 0.0f;
+            for (uint32_t d = 0; d < dim; ++d) {
+                const float t = __fsub_rn(x[i * dim + d], cs[c * dim + d]);
+                acc = __fadd_rn(acc, __fmul_rn(t, t));
+            }
+            if ((c0 == 0 && c == 0) || acc < best) { best = acc; bi = c0 + c; }
+        }
+    }
+    if (live) assign[i] = bi;
+}
+
+void launch_assign(const float* x, uint64_t n, uint32_t dim, const float* cent, uint32_t nlist, uint32_t* assign,
+                   cudaStream_t s) {
+    if (n == 0) return;
+    assign_kernel<<<(unsigned)((n + 127) / 128), 128, 32 * dim * sizeof(float), s>>>(x, n, dim, cent, nlist, assign);
+    count_launch();
+}
+
+// Residual codes encode(x - c_assign) (pq.cpp:29-45 on residuals), one thread per vector.
+__global__ void __launch_bounds__(128) residual_encode_kernel(const float* __restrict__ x, uint64_t n, uint32_t dim,
+                                                              uint32_t m, const float* __restrict__ cent,
+                                                              const uint32_t* __restrict__ assign,
+                                                              const float* __restrict__ codebooks,
+                                                              const uint16_t* __restrict__ perms,
+                                                              uint8_t* __restrict__ codes) {
+    __shared__ float4 cb[KSUB * DSUB / 4];
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = i < n;
+    const float* cr = live ? cent + (size_t)assign[i] * dim : cent;
+    for (uint32_t sq = 0; sq < m; ++sq) {
+        __syncthreads();
+        const float4* src = reinterpret_cast<const float4*>(codebooks + (size_t)sq * KSUB * DSUB);
+        for (int e = threadIdx.x; e < KSUB * DSUB / 4; e += blockDim.x) cb[e] = src[e];
+        __syncthreads();
+        if (!live) continue;
+        float r[DSUB];
+#pragma unroll
+        for (int t = 0; t < DSUB; ++t) r[t] = __fsub_rn(x[i * dim + sq * DSUB + t], cr[sq * DSUB + t]);
+        uint32_t best = 0;
+        float best_d = 0.0f;
+        for (uint32_t j = 0; j < KSUB; ++j) {
+            float acc = 0.0f;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const float4 cc = cb[j * 4 + v];
+                float t;
+                t = __fsub_rn(r[4 * v + 0], cc.x); acc = __fadd_rn(acc, __fmul_rn(t, t));
+                t = __fsub_rn(r[4 * v + 1], cc.y); acc = __fadd_rn(acc, __fmul_rn(t, t));
+                t = __fsub_rn(r[4 * v + 2], cc.z); acc = __fadd_rn(acc, __fmul_rn(t, t));
+                t = __fsub_rn(r[4 * v + 3], cc.w); acc = __fadd_rn(acc, __fmul_rn(t, t));
+            }
+            if (j == 0 || acc < best_d) { best_d = acc; best = j; }
+        }
+        codes[i * m + sq] = static_cast<uint8_t>(perms[sq * KSUB + best]);
+    }
+}
+
+void launch_residual_encode(const float* x, uint64_t n, uint32_t dim, uint32_t m, const float* cent,
+                            const uint32_t* assign, const float* codebooks, const uint16_t* perms, uint8_t* codes,
+                            cudaStream_t s) {
+    if (n == 0) return;
+    residual_encode_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(x, n, dim, m, cent, assign, codebooks, perms,
+                                                                        codes);
+    count_launch();
+}
+
+// Synthetic rows [row0, row0 + n) of the mixture, written as floats (chunked build).
+// (launch_gen_points in kernels_encode.cu does this.)
+
+// CSR bucketing: histogram of cells, then scatter (order within a list is
+// irrelevant: results order by (score, id), never by list position).
+__global__ void cell_hist_kernel(const uint32_t* __restrict__ assign, uint64_t n, unsigned long long* __restrict__ hist) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        atomicAdd(&hist[assign[i]], 1ull);
+}
+
+__global__ void cell_scatter_kernel(const uint32_t* __restrict__ assign, uint64_t n, uint32_t cb,
+                                    const uint8_t* __restrict__ codes_in, const uint32_t* __restrict__ low_in,
+                                    unsigned long long* __restrict__ cursor, uint8_t* __restrict__ codes_out,
+                                    uint32_t* __restrict__ low_out) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t at = atomicAdd(&cursor[assign[i]], 1ull);
+        for (uint32_t b = 0; b < cb; b += 8)
+            *reinterpret_cast<uint2*>(codes_out + at * cb + b) = *reinterpret_cast<const uint2*>(codes_in + i * cb + b);
+        low_out[at] = low_in[i];
+    }
+}
+
+void launch_cell_hist(const uint32_t* assign, uint64_t n, unsigned long long* hist, cudaStream_t s) {
+    if (n == 0) return;
+    cell_hist_kernel<<<148 * 4, 256, 0, s>>>(assign, n, hist);
+    count_launch();
+}
+
+void launch_cell_scatter(const uint32_t* assign, uint64_t n, uint32_t cb, const uint8_t* codes_in,
+                         const uint32_t* low_in, unsigned long long* cursor, uint8_t* codes_out, uint32_t* low_out,
+                         cudaStream_t s) {
+    if (n == 0) return;
+    cell_scatter_kernel<<<148 * 4, 256, 0, s>>>(assign, n, cb, codes_in, low_in, cursor, codes_out, low_out);
+    count_launch();
+}
+
+// key low word of insertion position i: id0 + i (arithmetic ids) or id32[i].
+__global__ void key_low_kernel(uint64_t n, int mode, uint32_t id0, const uint32_t* __restrict__ id32,
+                               uint32_t* __restrict__ out) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = mode == ID_ARITH ? id0 + (uint32_t)i : id32[i];
+}
+
+void launch_key_low(uint64_t n, int mode, uint32_t id0, const uint32_t* id32, uint32_t* out, cudaStream_t s) {
+    if (n == 0) return;
+    key_low_kernel<<<148 * 4, 256, 0, s>>>(n, mode, id0, id32, out);
+    count_launch();
+}
+
+}  // namespace pb

@@ -43,6 +43,25 @@ struct ScanArgs {
     uint32_t bs;                 // candidate block size (>= k) for threshold selects
 };
 
+// Argument block of the IVF list scan (K6).
+struct IvfScanArgs {
+    const uint8_t* codes;                 // list-ordered residual codes
+    const uint32_t* low;                  // list-ordered key low words (id or id rank)
+    const uint64_t* off;                  // nlist + 1 list offsets
+    const unsigned long long* probe_keys; // nq x nprobe (dist bits << 32 | cell), ascending
+    const uint32_t* np_eff;               // probes visited per query (cap)
+    const float* lutp;                    // (nq x nprobe) x M x 256 residual LUTs
+    const uint8_t* qcodes;                // (nq x nprobe) x CB residual query codes
+    uint32_t nq, nprobe, p_begin, p_end, tau;
+    unsigned long long* thr;              // per-query key bound (seeded between rounds)
+    unsigned long long* cand;             // nq x cap candidate keys
+    uint32_t cap;
+    uint32_t* ccount;
+    uint32_t* overflow;
+    uint32_t* work;
+    unsigned long long* surv_total;
+};
+
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -123,6 +142,25 @@ void launch_relabel(uint8_t* codes, uint64_t n, uint32_t m, const uint8_t* maps,
 
 void launch_seed_thr(const unsigned long long* keys, const uint32_t* counts, uint32_t nq, uint32_t k,
                      unsigned long long* thr, cudaStream_t s);
+// IVF (kernels_ivf.cu)
+void launch_coarse_keys(const float* q, uint32_t nq, uint32_t dim, const float* cent, uint32_t nlist,
+                        unsigned long long* keys, cudaStream_t s);
+void launch_residual_lut(const float* queries, uint32_t nq, uint32_t dim, uint32_t m,
+                         const unsigned long long* probe_keys, uint32_t nprobe, const float* cent,
+                         const float* codebooks, const uint16_t* perms, float* lutp, uint8_t* qcodes, cudaStream_t s);
+void launch_ivf_probe_count(const unsigned long long* probe_keys, uint32_t nq, uint32_t nprobe, const uint64_t* off,
+                            uint64_t cap, uint32_t* np_eff, unsigned long long* scanned, cudaStream_t s);
+void launch_ivf_scan(const IvfScanArgs& a, int strategy, uint32_t m, int num_sms, cudaStream_t s);
+void launch_assign(const float* x, uint64_t n, uint32_t dim, const float* cent, uint32_t nlist, uint32_t* assign,
+                   cudaStream_t s);
+void launch_residual_encode(const float* x, uint64_t n, uint32_t dim, uint32_t m, const float* cent,
+                            const uint32_t* assign, const float* codebooks, const uint16_t* perms, uint8_t* codes,
+                            cudaStream_t s);
+void launch_cell_hist(const uint32_t* assign, uint64_t n, unsigned long long* hist, cudaStream_t s);
+void launch_cell_scatter(const uint32_t* assign, uint64_t n, uint32_t cb, const uint8_t* codes_in,
+                         const uint32_t* low_in, unsigned long long* cursor, uint8_t* codes_out, uint32_t* low_out,
+                         cudaStream_t s);
+void launch_key_low(uint64_t n, int mode, uint32_t id0, const uint32_t* id32, uint32_t* out, cudaStream_t s);
 void launch_or_flag(uint32_t* dst, const uint32_t* src, cudaStream_t s);
 void count_launch();
 

@@ -1,0 +1,119 @@
+"""IVF + polysemous index (SPEC.md coarseindex, :350-417) over the C ABI.
+
+Names follow the SPEC operations: ``assign`` / ``add`` (build, :370-375),
+``probes`` (enumerate_cells, :376-381) and ``search`` (search_coarse,
+:382-390, with nprobe and the pre-filter candidate cap).  The reference
+ships no code for this module; parity is against the oracle restatement
+pinned to golden vectors composed from the reference's primitives.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from ._lib import IvfParamsC, PqDesc, SearchStatsC, lib
+from .flat_index import Errc, PolyError, ProductQuantizer, SearchStats, Strategy, _check, _p
+
+
+@dataclass
+class CoarseParams:
+    """SearchParams + CoarseConfig: k, tau, strategy, nprobe, cap (0 = none)."""
+    strategy: Strategy = Strategy.dual
+    k: int = 10
+    tau: int = 0
+    nprobe: int = 1
+    cap: int = 0
+
+    def c(self):
+        return IvfParamsC(int(self.strategy), int(self.k), int(self.tau), int(self.nprobe), int(self.cap))
+
+
+class IVFIndex:
+    """Inverted file over residual polysemous codes on one B200."""
+
+    def __init__(self, pq: ProductQuantizer, coarse, device: int = 0):
+        self._pq = pq
+        self.coarse = np.ascontiguousarray(coarse, np.float32).reshape(-1, pq.dim)
+        self.nlist = self.coarse.shape[0]
+        d = PqDesc(pq.m, pq.dbits, pq.dim, _p(pq.codebooks), _p(pq.perms))
+        h = C.c_void_p()
+        _check(lib.poly_b200_ivf_create(C.byref(d), _p(self.coarse), self.nlist, device, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.poly_b200_ivf_destroy(h)
+            self._h = None
+
+    def pq(self):
+        return self._pq
+
+    def size(self) -> int:
+        return int(lib.poly_b200_ivf_size(self._h))
+
+    def assign(self, x):
+        x = np.ascontiguousarray(x, np.float32).reshape(-1, self._pq.dim)
+        out = np.empty(x.shape[0], np.uint32)
+        _check(lib.poly_b200_ivf_assign(self._h, _p(x), x.shape[0], _p(out)))
+        return out
+
+    def add(self, x, ids=None, cells=None):
+        x = np.ascontiguousarray(x, np.float32)
+        if x.ndim != 2 or x.shape[1] != self._pq.dim:
+            raise PolyError(Errc.invalid_argument, "encode dimension mismatch")
+        ids = None if ids is None else np.ascontiguousarray(ids, np.int64)
+        cells = None if cells is None else np.ascontiguousarray(cells, np.uint32)
+        _check(lib.poly_b200_ivf_add(self._h, _p(x), x.shape[0], _p(cells), _p(ids)))
+
+    def add_device(self, d_x, d_cells, id0, stream=0):
+        _check(lib.poly_b200_ivf_add_device(self._h, d_x.data_ptr(), d_cells.data_ptr(), d_x.shape[0], int(id0),
+                                            C.c_void_p(stream)))
+
+    def add_codes(self, cells, codes, ids=None):
+        cells = np.ascontiguousarray(cells, np.uint32)
+        codes = np.ascontiguousarray(codes, np.uint8)
+        ids = None if ids is None else np.ascontiguousarray(ids, np.int64)
+        _check(lib.poly_b200_ivf_add_codes(self._h, _p(cells), _p(codes), _p(ids), cells.shape[0]))
+
+    def lists(self):
+        """(off [nlist+1], codes [n, code_bytes], ids [n]) in list order."""
+        n = self.size()
+        off = np.empty(self.nlist + 1, np.uint64)
+        codes = np.empty((n, self._pq.code_bytes()), np.uint8)
+        ids = np.empty(n, np.int64)
+        _check(lib.poly_b200_ivf_get_lists(self._h, _p(off), _p(codes), _p(ids)))
+        return off, codes, ids
+
+    def probes(self, queries, nprobe):
+        q = np.ascontiguousarray(queries, np.float32).reshape(-1, self._pq.dim)
+        out = np.empty((q.shape[0], nprobe), np.uint32)
+        _check(lib.poly_b200_ivf_probes(self._h, _p(q), q.shape[0], nprobe, _p(out)))
+        return out
+
+    def search(self, queries, params: CoarseParams, stats: SearchStats | None = None):
+        q = np.ascontiguousarray(queries, np.float32).reshape(-1, self._pq.dim)
+        nq, k = q.shape[0], int(params.k)
+        ids = np.empty((nq, k), np.int64)
+        scores = np.empty((nq, k), np.float32)
+        counts = np.empty(nq, np.uint32)
+        st = SearchStatsC()
+        _check(lib.poly_b200_ivf_search(self._h, _p(q), nq, C.byref(params.c()), _p(ids), _p(scores), _p(counts),
+                                        C.byref(st)))
+        if stats is not None:
+            stats.scanned += st.scanned
+            stats.survivors += st.survivors
+        return ids, scores, counts
+
+    def search_device(self, d_queries, params: CoarseParams, d_ids, d_scores, d_counts=None, stream=0,
+                      stats: SearchStats | None = None):
+        ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731
+        st = SearchStatsC()
+        _check(lib.poly_b200_ivf_search_device(self._h, ptr(d_queries), d_queries.shape[0], C.byref(params.c()),
+                                               ptr(d_ids), ptr(d_scores), ptr(d_counts), C.c_void_p(stream),
+                                               C.byref(st) if stats is not None else None))
+        if stats is not None:
+            stats.scanned += st.scanned
+            stats.survivors += st.survivors

@@ -1,0 +1,132 @@
+"""GPU parity of the IVF path through the C ABI: build,
+enumerate_cells, search_coarse (nprobe, cap, tau, strategies) against golden
+vectors composed from the reference's primitives and against the oracle.
+Bit-exact: lists, probe order, ids, scores, counts, survivors."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_ivf.npz")
+
+
+@pytest.fixture(scope="module")
+def pb():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_1609_01882_b200 as pb
+    return pb
+
+
+@pytest.fixture(scope="module")
+def gi():
+    z = dict(np.load(GOLDEN))
+    z["pq"] = oracle.PQ(8, 8, 128, z["codebooks"], z["perms"])
+    z["lists"] = oracle.IVFLists(z["off"], z["list_codes"], z["list_ids"])
+    return z
+
+
+def _bits(x):
+    return np.ascontiguousarray(x, np.float32).view(np.uint32)
+
+
+def _ivf(pb, gi):
+    pq = pb.ProductQuantizer(8, 8, 128, gi["codebooks"], gi["perms"])
+    return pb.IVFIndex(pq, gi["coarse"])
+
+
+@pytest.fixture(scope="module")
+def built(pb, gi):
+    centers = oracle.gen_centers(int(gi["data_seed"]), 1000, 128)
+    base = oracle.gen_points(int(gi["data_seed"]), 2, 0, int(gi["n"]), centers)
+    ix = _ivf(pb, gi)
+    ix.add(base, ids=np.arange(int(gi["n"])) * 7 + 3)  # GPU assignment + residual encode
+    return ix, base
+
+
+def test_build_matches_reference(pb, gi, built):
+    ix, base = built
+    assert np.array_equal(ix.assign(base), gi["assign_exact"])
+    off, codes, ids = ix.lists()
+    assert np.array_equal(off, gi["off"])
+    for c in range(len(off) - 1):  # order inside a list is not part of the contract
+        a, b = int(off[c]), int(off[c + 1])
+        og = np.argsort(gi["list_ids"][a:b])
+        ob = np.argsort(ids[a:b])
+        assert np.array_equal(ids[a:b][ob], gi["list_ids"][a:b][og])
+        assert np.array_equal(codes[a:b][ob], gi["list_codes"][a:b][og])
+
+
+def test_probe_order_matches_oracle(pb, gi, built):
+    ix, _ = built
+    for nprobe in (1, 7, 64):
+        want = oracle.ivf_search(gi["pq"], gi["coarse"], gi["lists"], gi["queries"], 5, nprobe)[5]
+        assert np.array_equal(ix.probes(gi["queries"], nprobe), want)
+
+
+@pytest.mark.parametrize("nprobe", [1, 4, 16, 64])
+def test_search_coarse_matches_reference(pb, gi, built, nprobe):
+    ix, _ = built
+    for tau in (20, 26, 64):
+        for cap in (0, 1500):
+            key = f"p{nprobe}_t{tau}_c{cap}"
+            st = pb.SearchStats()
+            ids, sc, cnt = ix.search(gi["queries"], pb.CoarseParams(pb.Strategy.dual, 50, tau, nprobe, cap), st)
+            assert np.array_equal(ids, gi[key + "_ids"]), key
+            assert np.array_equal(_bits(sc), _bits(gi[key + "_scores"])), key
+            assert np.array_equal(cnt, gi[key + "_counts"]), key
+            assert st.survivors == int(gi[key + "_surv"].sum()), key
+            _, _, _, _, scanned, _ = oracle.ivf_search(gi["pq"], gi["coarse"], gi["lists"], gi["queries"], 50,
+                                                       nprobe, tau=tau, cap=cap)
+            assert st.scanned == int(scanned.sum()), key
+
+
+def test_strategies_edges_and_codes_path(pb, gi, built):
+    ix, _ = built
+    for strat in ("adc", "binary"):
+        ids, sc, cnt = ix.search(gi["queries"], pb.CoarseParams(pb.strategy_from_string(strat), 50, 0, 16, 0))
+        assert np.array_equal(ids, gi[f"{strat}16_ids"])
+        assert np.array_equal(_bits(sc), _bits(gi[f"{strat}16_scores"]))
+    ids, sc, cnt = ix.search(gi["queries"][:3], pb.CoarseParams(pb.Strategy.dual, 0, 26, 4, 0))
+    assert cnt.tolist() == [0, 0, 0]
+    with pytest.raises(pb.PolyError):
+        ix.search(gi["queries"][:3], pb.CoarseParams(pb.Strategy.dual, 10, 65, 4, 0))
+    empty = _ivf(pb, gi)
+    ids, sc, cnt = empty.search(gi["queries"][:3], pb.CoarseParams(pb.Strategy.dual, 10, 26, 4, 0))
+    assert (cnt == 0).all() and (ids == -1).all()
+    # serialization path: the golden lists re-added as codes give the golden answers
+    ix2 = _ivf(pb, gi)
+    cells = np.repeat(np.arange(64, dtype=np.uint32), np.diff(gi["off"]).astype(np.int64))
+    ix2.add_codes(cells, gi["list_codes"], gi["list_ids"])
+    ids, sc, cnt = ix2.search(gi["queries"], pb.CoarseParams(pb.Strategy.dual, 50, 26, 16, 1500))
+    assert np.array_equal(ids, gi["p16_t26_c1500_ids"])
+
+
+def test_larger_ivf_matches_oracle(pb, gi):
+    """256 cells, 300k codes, 300 queries (two batches), several nprobe / tau."""
+    seed = int(gi["data_seed"])
+    centers = oracle.gen_centers(seed, 1000, 128)
+    rng = np.random.default_rng(5)
+    train = oracle.gen_points(seed, 1, 0, 20000, centers)
+    coarse = train[rng.choice(20000, 256, replace=False)]
+    base = oracle.gen_points(seed, 2, 0, 300_000, centers)
+    pq = gi["pq"]
+    lists, assign = oracle.ivf_build(pq, base, coarse)
+    ix = pb.IVFIndex(pb.ProductQuantizer(8, 8, 128, gi["codebooks"], gi["perms"]), coarse)
+    ix.add(base)
+    assert np.array_equal(ix.assign(base[:5000]), assign[:5000])
+    queries = oracle.gen_points(seed, 3, 0, 300, centers)
+    for nprobe, tau, cap in ((8, 26, 0), (32, 24, 0), (32, 64, 0), (64, 28, 20000)):
+        oi, osc, oc, osv, _, _ = oracle.ivf_search(pq, coarse, lists, queries, 100, nprobe, tau=tau, cap=cap,
+                                                   threads=16)
+        st = pb.SearchStats()
+        ids, sc, cnt = ix.search(queries, pb.CoarseParams(pb.Strategy.dual, 100, tau, nprobe, cap), st)
+        assert np.array_equal(ids, oi), (nprobe, tau, cap)
+        assert np.array_equal(_bits(sc), _bits(osc))
+        assert np.array_equal(cnt, oc)
+        if tau < 64:
+            assert st.survivors == int(osv.sum())
