@@ -43,6 +43,9 @@ NQ = 10_000
 CONFIGS = {
     1: dict(dim=128, ncent=1000, m=8, n=100_000_000, ht=24, per_ht="28,32", pq="pq_d128_m8.npz"),
     3: dict(dim=256, ncent=4096, m=16, n=200_000_000, ht=56, per_ht="48,64", pq="pq_d256_m16.npz"),
+    # IVF: the per-GPU share of the 1B-code config (1e9 / 8 GPUs)
+    2: dict(dim=128, ncent=1000, m=8, n=125_000_000, ht=26, per_ht="", pq="pq_ivf65536_d128_m8.npz",
+            nlist=65536, nprobe=16, per_nprobe="64"),
 }
 NCENT = 1000
 DIM = 128
@@ -71,6 +74,8 @@ def parse():
     args.n = c["n"] if args.n is None else args.n
     args.ht = c["ht"] if args.ht is None else args.ht
     args.per_ht = c["per_ht"] if args.per_ht is None else args.per_ht
+    if args.config == 2 and args.impl == "reference":
+        raise SystemExit("--impl reference is defined for the flat configs (1, 3)")
     return args
 
 
@@ -179,6 +184,88 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------ IVF (config 2)
+def run_ivf(args, rank, world, local):
+    """search_coarse throughput: codes scanned/s over the probed lists."""
+    import torch
+    import paper_1609_01882_b200 as pb
+    from paper_1609_01882_b200 import synth
+    from paper_1609_01882_b200.distributed import shard_range
+    c = CONFIGS[2]
+    torch.cuda.set_device(local)
+    z = np.load(os.path.join(ROOT, "tests", "golden", PQFILE))
+    pq = pb.ProductQuantizer(M, 8, DIM, z["codebooks"], z["perms"])
+    centers = synth.gen_centers(SEED, NCENT, DIM)
+    coarse = synth.gen_points(SEED, 1, 0, c["nlist"], centers)  # the fixture's coarse recipe
+    ivf = pb.IVFIndex(pq, coarse, device=local)
+    row0, row1 = shard_range(args.n, world, rank)
+    # build (setup, untimed): GPU generator, TF32-GEMM nearest-cell assignment,
+    # exact residual encoding through the C ABI
+    t = time.time()
+    torch.backends.cuda.matmul.allow_tf32 = True
+    dc = torch.from_numpy(coarse).cuda()
+    cn = (dc * dc).sum(1)
+    chunk = 1 << 20
+    xbuf = torch.empty((chunk, DIM), dtype=torch.float32, device="cuda")
+    cells = torch.empty(chunk, dtype=torch.int32, device="cuda")
+    for r in range(row0, row1, chunk):
+        nb = min(chunk, row1 - r)
+        x = xbuf[:nb]
+        pb.gen_points_device(centers, SEED, 2, r, nb, x, device=local)
+        for b in range(0, nb, 8192):
+            xs = x[b:b + 8192]
+            cells[b:b + xs.shape[0]] = torch.argmin(cn[None, :] - 2.0 * (xs @ dc.T), dim=1).to(torch.int32)
+        ivf.add_device(x, cells[:nb], r)
+    torch.cuda.synchronize()
+    setup_s = time.time() - t
+    dq = torch.empty((NQ, DIM), dtype=torch.float32, device="cuda")
+    pb.gen_points_device(centers, SEED, 3, 0, NQ, dq, device=local)
+    stream = torch.cuda.current_stream()
+    k = args.k
+    o_ids = torch.empty((BATCH, k), dtype=torch.int64, device="cuda")
+    o_sc = torch.empty((BATCH, k), dtype=torch.float32, device="cuda")
+    o_cnt = torch.empty(BATCH, dtype=torch.int32, device="cuda")
+    nbatches = NQ // BATCH
+    results = {}
+    for nprobe in [c["nprobe"]] + [int(x) for x in c["per_nprobe"].split(",") if x]:
+        p = pb.CoarseParams(pb.Strategy.dual, k, args.ht, nprobe, 0)
+        steps = args.steps if nprobe == c["nprobe"] else max(3, args.steps // 2)
+        scanned = surv = 0
+        for i in range(args.warmup, args.warmup + steps):  # per-batch work (untimed)
+            st = pb.SearchStats()
+            ivf.search_device(dq[(i % nbatches) * BATCH:][:BATCH], p, o_ids, o_sc, o_cnt, stream.cuda_stream, st)
+            scanned += st.scanned
+            surv += st.survivors
+        for i in range(args.warmup):
+            ivf.search_device(dq[(i % nbatches) * BATCH:][:BATCH], p, o_ids, o_sc, o_cnt, stream.cuda_stream)
+        torch.cuda.synchronize()
+        l0 = pb.launch_count()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(args.warmup, args.warmup + steps):
+            ivf.search_device(dq[(i % nbatches) * BATCH:][:BATCH], p, o_ids, o_sc, o_cnt, stream.cuda_stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        results[nprobe] = {"value": scanned / (ms / 1e3), "ms_per_step": ms / steps,
+                           "scanned_per_query": scanned / (steps * BATCH), "survivor_frac": surv / max(scanned, 1),
+                           "gpu_launches": pb.launch_count() - l0, "steps": steps}
+    head = results[c["nprobe"]]
+    line = {"metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": world, "steps": head["steps"],
+            "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u8/f32", "data": "synthetic (seeded Gaussian mixture, BASELINE cfg2)",
+            "config": {"workload": f"cfg2 IVF+polysemous: nlist={c['nlist']}, N={args.n} codes on this GPU (the "
+                                   f"per-GPU share of 1e9 over 8), PQ m={M} on residuals, nq={NQ} in batches of "
+                                   f"{BATCH}, nprobe={c['nprobe']}, k={k}, ht={args.ht}",
+                       "nlist": c["nlist"], "n_codes": args.n, "m": M, "nprobe": c["nprobe"], "k": k, "ht": args.ht,
+                       "coarse": "training-stream rows [0, nlist) (sampled coarse quantizer; DESIGN.md)",
+                       "build_assignment": "TF32 GEMM argmin (setup only)"},
+            "gpu_launches": head["gpu_launches"], "per_nprobe": {str(kk): v for kk, v in results.items()},
+            "setup_s": round(setup_s, 1)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 # ------------------------------------------------------------------ our arm
 def cpu_baseline(args, index, dq_host):
     """Reference CPU search (oracle/_ref) on one full step of the workload:
@@ -208,6 +295,9 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", 0))
     if args.impl == "reference":
         run_reference(args, rank)
+        return
+    if args.config == 2:
+        run_ivf(args, rank, world, local)
         return
 
     import torch

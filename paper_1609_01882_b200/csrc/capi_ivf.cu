@@ -45,8 +45,8 @@ struct poly_b200_ivf {
     uint64_t max_list = 0;
 
     // search scratch
-    unsigned long long* ckeys = nullptr;  // IVF_NQB x nlist
-    uint32_t* nl_counts = nullptr;         // IVF_NQB x nlist (for K3)
+    unsigned long long* ckeys = nullptr;  // IVF_NQB x max(nlist, 64 slices x 64)
+    uint32_t* nl_counts = nullptr;         // K3 counts: nlist per query, or per (slice, query)
     unsigned long long* probe_keys = nullptr;
     uint32_t* probe_counts = nullptr;
     uint32_t* np_eff = nullptr;
@@ -156,10 +156,8 @@ void rebuild_lists(poly_b200_ivf* iv) {
 
 void ensure_ivf_scratch(poly_b200_ivf* iv, uint32_t nprobe, uint32_t k) {
     if (!iv->ckeys) {
-        iv->ckeys = dalloc<unsigned long long>((size_t)IVF_NQB * iv->nlist);
-        iv->nl_counts = dalloc<uint32_t>(IVF_NQB);
-        fill_u32<<<1, 256, 0, iv->stream>>>(iv->nl_counts, IVF_NQB, iv->nlist);
-        pb::count_launch();
+        iv->ckeys = dalloc<unsigned long long>((size_t)IVF_NQB * std::max<uint32_t>(iv->nlist, 64 * 64));
+        iv->nl_counts = dalloc<uint32_t>((size_t)IVF_NQB * 64);  // per-slice counts (K5s) or nlist (K5)
         iv->np_eff = dalloc<uint32_t>(IVF_NQB);
         iv->scanned = dalloc<unsigned long long>(IVF_NQB);
         iv->ctrl = dalloc<uint32_t>(IVF_NQB + 32);
@@ -202,9 +200,23 @@ void validate(const poly_b200_ivf* iv, const poly_b200_ivf_params* p) {
 }
 
 // Enqueue enumerate_cells for a batch: probe_keys (nqb x np) ascending.
+// np <= 64: fused distance + per-slice selection (K5s), slices merged by K3;
+// larger np: all keys (K5), then K3 over nlist keys per query.
 void enumerate_cells(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, uint32_t np, cudaStream_t s) {
-    pb::launch_coarse_keys(d_q, nqb, iv->dim, iv->d_coarse, iv->nlist, iv->ckeys, s);
-    pb::launch_topk(iv->ckeys, iv->nl_counts, iv->nlist, 1, 0, 0, nqb, np, iv->probe_keys, iv->probe_counts, s);
+    if (np <= 64) {
+        const uint32_t qtiles = (nqb + 63) / 64;
+        uint32_t slices = std::max<uint32_t>(1, std::min<uint32_t>(64, 2u * iv->num_sms / qtiles));
+        slices = std::min<uint32_t>(slices, std::max<uint32_t>(1, iv->nlist / 64));
+        pb::launch_coarse_select(d_q, nqb, iv->dim, iv->d_coarse, iv->nlist, np, slices, iv->ckeys, iv->nl_counts,
+                                 s);
+        pb::launch_topk(iv->ckeys, iv->nl_counts, np, slices, (uint64_t)nqb * np, nqb, nqb, np, iv->probe_keys,
+                        iv->probe_counts, s);
+    } else {
+        pb::launch_coarse_keys(d_q, nqb, iv->dim, iv->d_coarse, iv->nlist, iv->ckeys, s);
+        fill_u32<<<1, 256, 0, s>>>(iv->nl_counts, IVF_NQB, iv->nlist);
+        pb::count_launch();
+        pb::launch_topk(iv->ckeys, iv->nl_counts, iv->nlist, 1, 0, 0, nqb, np, iv->probe_keys, iv->probe_counts, s);
+    }
 }
 
 // One batch of <= 256 queries; outputs through keys_to_ids.
@@ -239,11 +251,11 @@ void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_
     a.ccount = iv->ctrl;
     a.overflow = iv->ctrl + IVF_NQB;
     a.surv_total = iv->surv_total;
-    // rounds of probes [0,1), [1,4), [4,16), ...: each later round scans with the
-    // exact k-th key of the candidates so far as its bound
+    // two rounds: the nearest cell of every query first, then the rest with the
+    // exact k-th key of the first round's candidates as the bound
     uint32_t round = 0;
     for (uint32_t pb_ = 0; pb_ < np; ++round) {
-        const uint32_t pe = std::min(np, pb_ == 0 ? 1u : pb_ * 4);
+        const uint32_t pe = pb_ == 0 ? 1u : np;
         a.p_begin = pb_;
         a.p_end = pe;
         a.work = iv->ctrl + IVF_NQB + 1 + round;

@@ -80,6 +80,137 @@ void launch_coarse_keys(const float* q, uint32_t nq, uint32_t dim, const float* 
     count_launch();
 }
 
+// K5s: the same exact distances, fused with a per-(query, cell-slice) top-np
+// selection: each CTA owns 64 queries x one slice of the cells, filters keys
+// against the query's running np-th key and inserts the few that pass into a
+// sorted shared-memory list (one warp per query, lane-parallel shift).  The
+// per-slice lists are merged by K3 (parts = slices).  np <= K5S_NP.
+constexpr int K5S_NP = 64;
+
+__global__ void __launch_bounds__(256) coarse_select_kernel(const float* __restrict__ q, uint32_t nq, uint32_t dim,
+                                                            const float* __restrict__ cent, uint32_t nlist,
+                                                            uint32_t np, uint32_t slices,
+                                                            unsigned long long* __restrict__ out_keys,
+                                                            uint32_t* __restrict__ out_counts) {
+    // dynamic smem: top[64][np_pad] | pend[64][64] | qs[64][dim+1] (resident) | cs[64][33]
+    extern __shared__ __align__(16) uint8_t k5s_smem[];
+    const uint32_t np_pad = np <= 32 ? 32 : 64;
+    unsigned long long* top = reinterpret_cast<unsigned long long*>(k5s_smem);
+    unsigned long long* pend = top + K5_T * np_pad;
+    float* qs = reinterpret_cast<float*>(pend + K5_T * K5_T);
+    const uint32_t qstride = dim + 1;
+    auto cs = reinterpret_cast<float(*)[K5_D + 1]>(qs + K5_T * qstride);
+    __shared__ unsigned long long thr[K5_T];
+    __shared__ uint32_t topn[K5_T], pn[K5_T];
+    const uint32_t slice = blockIdx.x, q0 = blockIdx.y * K5_T;
+    const uint32_t per = (nlist + slices - 1) / slices;
+    const uint32_t c_lo = min(nlist, slice * per), c_hi = min(nlist, c_lo + per);
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x < K5_T) {
+        thr[threadIdx.x] = ~0ull;
+        topn[threadIdx.x] = 0;
+        pn[threadIdx.x] = 0;
+    }
+    for (uint32_t e = threadIdx.x; e < K5_T * dim; e += 256) {
+        const uint32_t r = e / dim, c = e % dim;
+        qs[r * qstride + c] = (q0 + r < nq) ? q[(size_t)(q0 + r) * dim + c] : 0.0f;
+    }
+    for (uint32_t c0 = c_lo; c0 < c_hi; c0 += K5_T) {
+        float acc[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+        for (uint32_t d0 = 0; d0 < dim; d0 += K5_D) {
+            __syncthreads();
+            for (int e = threadIdx.x; e < K5_T * K5_D; e += 256) {
+                const int r = e / K5_D, c = e % K5_D;
+                cs[r][c] = (c0 + r < c_hi) ? cent[(size_t)(c0 + r) * dim + d0 + c] : 0.0f;
+            }
+            __syncthreads();
+#pragma unroll 4
+            for (int d = 0; d < K5_D; ++d) {
+                float av[4], bv[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) av[i] = qs[(ty + 16 * i) * qstride + d0 + d];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) bv[j] = cs[tx + 16 * j][d];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const float t = __fsub_rn(av[i], bv[j]);
+                        acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(t, t));
+                    }
+            }
+        }
+        // filter against the running np-th key, queue the passing keys per query
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int r = ty + 16 * i;
+            const unsigned long long tr = thr[r];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t c = c0 + tx + 16 * j;
+                const unsigned long long key = ((unsigned long long)__float_as_uint(acc[i][j]) << 32) | c;
+                if (c < c_hi && key < tr) pend[r * K5_T + atomicAdd(&pn[r], 1u)] = key;
+            }
+        }
+        __syncthreads();
+        // merge: warp per query, sorted insertion (ascending, at most np kept)
+        for (int r = warp; r < K5_T; r += 8) {
+            const uint32_t cnt = pn[r];
+            if (cnt == 0) continue;
+            unsigned long long* T = top + r * np_pad;
+            uint32_t n = topn[r];
+            for (uint32_t t = 0; t < cnt; ++t) {
+                const unsigned long long x = pend[r * K5_T + t];
+                const unsigned long long e0 = lane < (int)n ? T[lane] : ~0ull;
+                const unsigned long long e1 = lane + 32 < (int)n ? T[lane + 32] : ~0ull;
+                const uint32_t pos = __popc(__ballot_sync(0xffffffffu, e0 < x)) + __popc(__ballot_sync(0xffffffffu, e1 < x));
+                if (pos >= np) continue;
+                __syncwarp();
+                if (lane >= (int)pos && lane + 1 < (int)np && lane < (int)n) T[lane + 1] = e0;
+                if (lane + 32 >= (int)pos && lane + 33 < (int)np && lane + 32 < (int)n) T[lane + 33] = e1;
+                __syncwarp();
+                if (lane == 0) T[pos] = x;
+                n = min(n + 1, np);
+                __syncwarp();
+            }
+            if (lane == 0) {
+                topn[r] = n;
+                pn[r] = 0;
+                if (n == np) thr[r] = T[np - 1];
+            }
+        }
+    }
+    __syncthreads();
+    for (int r = warp; r < K5_T; r += 8) {
+        const uint32_t qi = q0 + r;
+        if (qi >= nq) continue;
+        const uint32_t n = topn[r];
+        unsigned long long* o = out_keys + ((size_t)slice * nq + qi) * np;
+        for (uint32_t t = lane; t < np; t += 32) o[t] = t < n ? top[r * np_pad + t] : ~0ull;
+        if (lane == 0) out_counts[(size_t)slice * nq + qi] = n;
+    }
+}
+
+void launch_coarse_select(const float* q, uint32_t nq, uint32_t dim, const float* cent, uint32_t nlist, uint32_t np,
+                          uint32_t slices, unsigned long long* out_keys, uint32_t* out_counts, cudaStream_t s) {
+    if (nq == 0) return;
+    const size_t np_pad = np <= 32 ? 32 : 64;
+    const size_t smem = (size_t)K5_T * (np_pad + K5_T) * 8 + (size_t)K5_T * (dim + 1) * 4 + (size_t)K5_T * (K5_D + 1) * 4;
+    static size_t attr = 0;
+    if (attr < smem) {
+        cudaFuncSetAttribute(coarse_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = smem;
+    }
+    coarse_select_kernel<<<dim3(slices, (nq + K5_T - 1) / K5_T), 256, smem, s>>>(q, nq, dim, cent, nlist, np, slices,
+                                                                                 out_keys, out_counts);
+    count_launch();
+}
+
 // ------------------------------------------------------------------ K1r
 // grid (nq * nprobe, m): item (q, p) -> residual LUT (stored-field indexed) + code.
 __global__ void __launch_bounds__(256) residual_lut_kernel(const float* __restrict__ queries, uint32_t dim, uint32_t m,
@@ -199,58 +330,59 @@ __device__ __forceinline__ float k6_adc(const float* L, const C& c) {
     return acc;
 }
 
-// One warp per (query, probe) item of probes [p_begin, p_end) of each query.
+// One CTA per (query, probe) item of probes [p_begin, p_end) of each query
+// (dynamic fetch): the 8 warps split the cell's list and share the item's LUT
+// in shared memory; each warp compacts its survivors with a ballot into its
+// own queue and drains 32 at a time (ADC, candidate test).
 template <int M, int STRAT>
 __global__ void __launch_bounds__(K6_WARPS * 32) ivf_scan_kernel(const IvfScanArgs a) {
     using C = typename IvfCode<M>::T;
     extern __shared__ __align__(16) uint8_t k6_smem[];
-    // per warp: LUT (M x 256 floats), survivor queue (64 codes + 64 positions)
-    constexpr size_t PER_WARP = (size_t)M * KSUB * 4 + 64 * sizeof(C) + 64 * 4;
+    float* L = reinterpret_cast<float*>(k6_smem);  // M x 256 floats
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint8_t* base = k6_smem + warp * PER_WARP;
-    float* L = reinterpret_cast<float*>(base);
-    C* qcode_q = reinterpret_cast<C*>(base + (size_t)M * KSUB * 4);
-    uint32_t* qpos_q = reinterpret_cast<uint32_t*>(base + (size_t)M * KSUB * 4 + 64 * sizeof(C));
+    uint8_t* qbase = k6_smem + (size_t)M * KSUB * 4 + warp * 64 * (sizeof(C) + 4);
+    C* qcode_q = reinterpret_cast<C*>(qbase);
+    uint32_t* qpos_q = reinterpret_cast<uint32_t*>(qbase + 64 * sizeof(C));
+    __shared__ uint32_t item_s;
     const uint32_t span = a.p_end - a.p_begin;
     const uint64_t nitems = (uint64_t)a.nq * span;
     uint32_t surv_total = 0;
     for (;;) {
-        uint32_t it = 0;
-        if (lane == 0) it = atomicAdd(a.work, 1u);
-        it = __shfl_sync(0xffffffffu, it, 0);
+        __syncthreads();
+        if (threadIdx.x == 0) item_s = atomicAdd(a.work, 1u);
+        __syncthreads();
+        const uint32_t it = item_s;
         if (it >= nitems) break;
         const uint32_t qi = it / span, p = a.p_begin + it % span;
         if (p >= a.np_eff[qi]) continue;
         const size_t item = (size_t)qi * a.nprobe + p;
         const uint32_t cell = (uint32_t)a.probe_keys[item];
         const uint64_t beg = a.off[cell], end = a.off[cell + 1];
-        // item LUT -> shared memory (M x 256 floats), query code -> registers
         const float4* src = reinterpret_cast<const float4*>(a.lutp + item * M * KSUB);
-        for (int i = lane; i < M * KSUB / 4; i += 32) reinterpret_cast<float4*>(L)[i] = src[i];
+        for (int i = threadIdx.x; i < M * KSUB / 4; i += K6_WARPS * 32) reinterpret_cast<float4*>(L)[i] = src[i];
         const C qc = reinterpret_cast<const C*>(a.qcodes)[item];
         const unsigned long long thr = __ldcg(a.thr + qi);
-        __syncwarp();
+        __syncthreads();
         const C* codes = reinterpret_cast<const C*>(a.codes);
         uint32_t qn = 0;
-        auto drain = [&](uint32_t cnt) {
-            __syncwarp();
-            if ((uint32_t)lane < cnt) {
-                const float score = k6_adc<M>(L, qcode_q[lane]);
-                const uint32_t pos = qpos_q[lane];
-                const uint32_t sb = __float_as_uint(score);
-                if (sb <= (uint32_t)(thr >> 32)) {
-                    const uint32_t low = __ldg(a.low + pos);
-                    const unsigned long long key = ((unsigned long long)sb << 32) | low;
-                    if (key < thr) {
-                        const uint32_t slot = atomicAdd(&a.ccount[qi], 1u);
-                        if (slot < a.cap) a.cand[(size_t)qi * a.cap + slot] = key;
-                        else atomicOr(a.overflow, 1u);
-                    }
+        auto candidate = [&](float score, uint32_t pos) {
+            const uint32_t sb = __float_as_uint(score);
+            if (sb <= (uint32_t)(thr >> 32)) {
+                const unsigned long long key = ((unsigned long long)sb << 32) | __ldg(a.low + pos);
+                if (key < thr) {
+                    const uint32_t slot = atomicAdd(&a.ccount[qi], 1u);
+                    if (slot < a.cap) a.cand[(size_t)qi * a.cap + slot] = key;
+                    else atomicOr(a.overflow, 1u);
                 }
             }
+        };
+        auto drain = [&](uint32_t cnt) {
+            __syncwarp();
+            if ((uint32_t)lane < cnt) candidate(k6_adc<M>(L, qcode_q[lane]), qpos_q[lane]);
             __syncwarp();
         };
-        for (uint64_t i0 = beg; i0 < end; i0 += 128) {
+        // warp w scans rows beg + 128*w + ..., stride 128 * K6_WARPS
+        for (uint64_t i0 = beg + (uint64_t)warp * 128; i0 < end; i0 += 128 * K6_WARPS) {
             C c[4];
             bool in[4];
 #pragma unroll
@@ -288,21 +420,11 @@ __global__ void __launch_bounds__(K6_WARPS * 32) ivf_scan_kernel(const IvfScanAr
                     if constexpr (STRAT == ADC) score = k6_adc<M>(L, c[u]);
                     else if constexpr (STRAT == BINARY) score = (float)k6_ham(c[u], qc);
                     else score = (float)k6_dis(c[u], qc);
-                    const uint32_t sb = __float_as_uint(score);
-                    if (sb <= (uint32_t)(thr >> 32)) {
-                        const uint32_t low = __ldg(a.low + pos);
-                        const unsigned long long key = ((unsigned long long)sb << 32) | low;
-                        if (key < thr) {
-                            const uint32_t slot = atomicAdd(&a.ccount[qi], 1u);
-                            if (slot < a.cap) a.cand[(size_t)qi * a.cap + slot] = key;
-                            else atomicOr(a.overflow, 1u);
-                        }
-                    }
+                    candidate(score, pos);
                 }
             }
         }
         if (STRAT == DUAL && qn) drain(qn);
-        __syncwarp();
     }
     if (STRAT == DUAL && lane == 0 && surv_total) atomicAdd(a.surv_total, (unsigned long long)surv_total);
 }
@@ -310,7 +432,7 @@ __global__ void __launch_bounds__(K6_WARPS * 32) ivf_scan_kernel(const IvfScanAr
 template <int M, int STRAT>
 static void launch_ivf_one(const IvfScanArgs& a, unsigned grid, cudaStream_t s) {
     using C = typename IvfCode<M>::T;
-    const size_t smem = (size_t)K6_WARPS * ((size_t)M * KSUB * 4 + 64 * sizeof(C) + 64 * 4);
+    const size_t smem = (size_t)M * KSUB * 4 + (size_t)K6_WARPS * 64 * (sizeof(C) + 4);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(ivf_scan_kernel<M, STRAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -321,7 +443,7 @@ static void launch_ivf_one(const IvfScanArgs& a, unsigned grid, cudaStream_t s) 
 
 template <int M>
 static void launch_ivf_m(const IvfScanArgs& a, int strategy, int num_sms, cudaStream_t s) {
-    const unsigned grid = (unsigned)num_sms * (M == 8 ? 3 : 1);  // 64 KB (m=8) / 128 KB (m=16) smem per CTA
+    const unsigned grid = (unsigned)num_sms * (M == 8 ? 8 : 6);  // ~14 KB (m=8) / ~24 KB (m=16) smem per CTA
     switch (strategy) {
         case DUAL: launch_ivf_one<M, DUAL>(a, grid, s); break;
         case ADC: launch_ivf_one<M, ADC>(a, grid, s); break;

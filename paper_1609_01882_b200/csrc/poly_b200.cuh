@@ -145,6 +145,8 @@ void launch_seed_thr(const unsigned long long* keys, const uint32_t* counts, uin
 // IVF (kernels_ivf.cu)
 void launch_coarse_keys(const float* q, uint32_t nq, uint32_t dim, const float* cent, uint32_t nlist,
                         unsigned long long* keys, cudaStream_t s);
+void launch_coarse_select(const float* q, uint32_t nq, uint32_t dim, const float* cent, uint32_t nlist, uint32_t np,
+                          uint32_t slices, unsigned long long* out_keys, uint32_t* out_counts, cudaStream_t s);
 void launch_residual_lut(const float* queries, uint32_t nq, uint32_t dim, uint32_t m,
                          const unsigned long long* probe_keys, uint32_t nprobe, const float* cent,
                          const float* codebooks, const uint16_t* perms, float* lutp, uint8_t* qcodes, cudaStream_t s);

@@ -1,0 +1,33 @@
+"""IVF search driver for ncu launch lists: sampled 65,536-cell coarse quantizer,
+N codes built on the GPU, one 256-query batch searched `reps` times."""
+import argparse, os, sys, time
+import numpy as np
+import torch
+sys.path.insert(0, '.')
+import paper_1609_01882_b200 as pb
+from paper_1609_01882_b200 import synth
+ap = argparse.ArgumentParser()
+ap.add_argument('--n', type=int, default=20_000_000)
+ap.add_argument('--nprobe', type=int, default=16)
+ap.add_argument('--reps', type=int, default=2)
+args = ap.parse_args()
+z = np.load('tests/golden/pq_ivf65536_d128_m8.npz')
+pq = pb.ProductQuantizer(8, 8, 128, z['codebooks'], z['perms'])
+centers = synth.gen_centers(160901882, 1000, 128)
+coarse = synth.gen_points(160901882, 1, 0, 65536, centers)
+ivf = pb.IVFIndex(pq, coarse)
+torch.backends.cuda.matmul.allow_tf32 = True
+dc = torch.from_numpy(coarse).cuda(); cn = (dc * dc).sum(1)
+x = torch.empty((1 << 20, 128), device='cuda'); cells = torch.empty(1 << 20, dtype=torch.int32, device='cuda')
+for r in range(0, args.n, 1 << 20):
+    nb = min(1 << 20, args.n - r)
+    pb.gen_points_device(centers, 160901882, 2, r, nb, x[:nb])
+    for b in range(0, nb, 8192):
+        xs = x[b:min(b + 8192, nb)]
+        cells[b:b + xs.shape[0]] = torch.argmin(cn[None, :] - 2.0 * (xs @ dc.T), dim=1).to(torch.int32)
+    ivf.add_device(x[:nb], cells[:nb], r)
+q = synth.gen_points(160901882, 3, 0, 256, centers)
+p = pb.CoarseParams(pb.Strategy.dual, 100, 26, args.nprobe, 0)
+for i in range(args.reps):
+    st = pb.SearchStats(); t = time.time(); ivf.search(q, p, st); dt = time.time() - t
+print(f"n={args.n} nprobe={args.nprobe}: {dt*1e3:.2f} ms, scanned/query {st.scanned/256:.0f}, surv {st.survivors/max(st.scanned,1):.3f}")
