@@ -215,6 +215,14 @@ int poly_b200_ivf_search_device(poly_b200_ivf* ivf, const float* d_queries, uint
                                 const poly_b200_ivf_params* params, int64_t* d_out_ids, float* d_out_scores,
                                 uint32_t* d_out_counts, void* stream, poly_b200_search_stats* stats);
 
+/* knn_graph: the k nearest neighbours of n vectors that are
+ * themselves in the index (vector i has id id0 + i), self-match removed:
+ * search_coarse with k + 1, then the row's own id is dropped (or, if absent,
+ * the (k+1)-th result).  Device buffers: d_x n x dim, outputs n x k. */
+int poly_b200_ivf_knn_graph_device(poly_b200_ivf* ivf, const float* d_x, uint64_t n, int64_t id0,
+                                   const poly_b200_ivf_params* params, int64_t* d_out_ids, float* d_out_scores,
+                                   uint32_t* d_out_counts, void* stream);
+
 /* Number of kernel launches this library has issued so far (for bench.py). */
 uint64_t poly_b200_launch_count(void);
 

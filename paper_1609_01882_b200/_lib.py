@@ -75,6 +75,7 @@ def _load():
     L.poly_b200_ivf_search.argtypes = [_P, _P, _u64, C.POINTER(IvfParamsC), _P, _P, _P, C.POINTER(SearchStatsC)]
     L.poly_b200_ivf_search_device.argtypes = [_P, _P, _u64, C.POINTER(IvfParamsC), _P, _P, _P, _P,
                                               C.POINTER(SearchStatsC)]
+    L.poly_b200_ivf_knn_graph_device.argtypes = [_P, _P, _u64, C.c_int64, C.POINTER(IvfParamsC), _P, _P, _P, _P]
     return L
 
 
@@ -89,5 +90,5 @@ EXPORTS = [
     "poly_b200_gen_points_device", "poly_b200_debug_lut", "poly_b200_debug_counts", "poly_b200_profile_enable", "poly_b200_profile_read",
     "poly_b200_launch_count", "poly_b200_ivf_create", "poly_b200_ivf_destroy", "poly_b200_ivf_size",
     "poly_b200_ivf_assign", "poly_b200_ivf_add", "poly_b200_ivf_add_device", "poly_b200_ivf_add_codes",
-    "poly_b200_ivf_get_lists", "poly_b200_ivf_probes", "poly_b200_ivf_search", "poly_b200_ivf_search_device",
+    "poly_b200_ivf_get_lists", "poly_b200_ivf_probes", "poly_b200_ivf_search", "poly_b200_ivf_search_device", "poly_b200_ivf_knn_graph_device",
 ]

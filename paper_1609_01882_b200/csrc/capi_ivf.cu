@@ -293,6 +293,31 @@ int device_search(poly_b200_ivf* iv, const float* d_q, uint64_t nq, const poly_b
     return 0;
 }
 
+// Row i (id qid0 + i) of a (k+1)-NN result: drop the row's own id if present,
+// else the last entry; keep at most k.
+__global__ void drop_self_kernel(const int64_t* __restrict__ ids, const float* __restrict__ sc,
+                                 const uint32_t* __restrict__ cnt, uint32_t nq, uint32_t k, int64_t qid0,
+                                 int64_t* __restrict__ out_ids, float* __restrict__ out_sc, uint32_t* __restrict__ out_cnt) {
+    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    const uint32_t k1 = k + 1, c = cnt[q];
+    const int64_t self = qid0 + q;
+    uint32_t w = 0;
+    bool dropped = false;
+    for (uint32_t r = 0; r < c && w < k; ++r) {
+        const int64_t id = ids[(size_t)q * k1 + r];
+        if (!dropped && id == self) { dropped = true; continue; }
+        out_ids[(size_t)q * k + w] = id;
+        out_sc[(size_t)q * k + w] = sc[(size_t)q * k1 + r];
+        ++w;
+    }
+    for (uint32_t r = w; r < k; ++r) {
+        out_ids[(size_t)q * k + r] = -1;
+        out_sc[(size_t)q * k + r] = __int_as_float(0x7f800000);
+    }
+    if (out_cnt) out_cnt[q] = w;
+}
+
 void read_stats(poly_b200_ivf* iv, int mode, poly_b200_search_stats* st, cudaStream_t s) {
     unsigned long long h[2] = {0, 0};
     uint32_t ovf = 0;
@@ -530,6 +555,45 @@ int poly_b200_ivf_search_device(poly_b200_ivf* iv, const float* d_q, uint64_t nq
             stats->scanned = stats->survivors = 0;
             if (nq && p->k && iv->n) read_stats(iv, mode, stats, s);
         }
+    });
+}
+
+int poly_b200_ivf_knn_graph_device(poly_b200_ivf* iv, const float* d_x, uint64_t n, int64_t id0,
+                                   const poly_b200_ivf_params* p, int64_t* d_ids, float* d_scores, uint32_t* d_counts,
+                                   void* stream) {
+    return guard([&] {
+        require(iv != nullptr && p != nullptr, POLY_B200_INVALID_ARGUMENT, "null arguments");
+        require(p->k >= 1 && p->k < (uint32_t)pb::KMAX, POLY_B200_INVALID_ARGUMENT, "k must be in [1, 2047]");
+        require(n == 0 || (d_x && d_ids && d_scores), POLY_B200_INVALID_ARGUMENT, "null buffers");
+        std::lock_guard<std::mutex> lk(iv->mu);
+        DeviceGuard dg(iv->device);
+        cudaStream_t s = (cudaStream_t)stream;
+        poly_b200_ivf_params p1 = *p;
+        p1.k = p->k + 1;
+        const uint64_t step = 64 * IVF_NQB;
+        int64_t* t_ids = dalloc<int64_t>(step * p1.k);
+        float* t_sc = dalloc<float>(step * p1.k);
+        uint32_t* t_cnt = dalloc<uint32_t>(step);
+        try {
+            for (uint64_t b0 = 0; b0 < n; b0 += step) {
+                const uint32_t nb = (uint32_t)std::min<uint64_t>(step, n - b0);
+                device_search(iv, d_x + b0 * iv->dim, nb, &p1, t_ids, t_sc, t_cnt, s);
+                drop_self_kernel<<<(nb + 127) / 128, 128, 0, s>>>(t_ids, t_sc, t_cnt, nb, p->k, id0 + (int64_t)b0,
+                                                                  d_ids + b0 * p->k, d_scores + b0 * p->k,
+                                                                  d_counts ? d_counts + b0 : nullptr);
+                pb::count_launch();
+                read_stats(iv, 0, nullptr, s);  // syncs; fails loudly on a candidate overflow
+            }
+        } catch (...) {
+            cudaStreamSynchronize(s);
+            dfree(t_ids);
+            dfree(t_sc);
+            dfree(t_cnt);
+            throw;
+        }
+        dfree(t_ids);
+        dfree(t_sc);
+        dfree(t_cnt);
     });
 }
 

@@ -117,3 +117,9 @@ class IVFIndex:
         if stats is not None:
             stats.scanned += st.scanned
             stats.survivors += st.survivors
+
+    def knn_graph_device(self, d_x, id0, params: CoarseParams, d_ids, d_scores, d_counts=None, stream=0):
+        """knn_graph: rows of d_x are the stored vectors id0.. ; self-match removed."""
+        ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731
+        _check(lib.poly_b200_ivf_knn_graph_device(self._h, ptr(d_x), d_x.shape[0], int(id0), C.byref(params.c()),
+                                                  ptr(d_ids), ptr(d_scores), ptr(d_counts), C.c_void_p(stream)))

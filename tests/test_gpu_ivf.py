@@ -130,3 +130,35 @@ def test_larger_ivf_matches_oracle(pb, gi):
         assert np.array_equal(cnt, oc)
         if tau < 64:
             assert st.survivors == int(osv.sum())
+
+
+def test_knn_graph_matches_oracle(pb, gi):
+    """knn_graph on unit-normalised 256-d data, m = 16 codes."""
+    import torch
+    seed = int(gi["data_seed"])
+    centers = oracle.gen_centers(seed, 4096, 256)
+    z = np.load(os.path.join(os.path.dirname(GOLDEN), "pq_d256_m16.npz"))
+    pq = oracle.PQ(16, 8, 256, z["codebooks"], z["perms"])
+    x = oracle.gen_points(seed, 2, 0, 30000, centers, normalize=True)
+    coarse = oracle.gen_points(seed, 1, 0, 128, centers, normalize=True)
+    lists, _ = oracle.ivf_build(pq, x, coarse)
+    ix = pb.IVFIndex(pb.ProductQuantizer(16, 8, 256, z["codebooks"], z["perms"]), coarse)
+    ix.add(x)
+    nq, k = 3000, 10
+    dx = torch.from_numpy(x[:nq]).cuda()
+    ids = torch.empty((nq, k), dtype=torch.int64, device="cuda")
+    sc = torch.empty((nq, k), dtype=torch.float32, device="cuda")
+    cnt = torch.empty(nq, dtype=torch.int32, device="cuda")
+    ix.knn_graph_device(dx, 0, pb.CoarseParams(pb.Strategy.dual, k, 52, 8, 0), ids, sc, cnt)
+    torch.cuda.synchronize()
+    oi, osc, oc, _, _, _ = oracle.ivf_search(pq, coarse, lists, x[:nq], k + 1, 8, tau=52, threads=16)
+    for i in range(nq):
+        row, srow = list(oi[i, :oc[i]]), list(osc[i, :oc[i]])
+        if i in row:
+            j = row.index(i)
+            del row[j], srow[j]
+        row, srow = row[:k], srow[:k]
+        got = ids[i].cpu().numpy()
+        assert got[:len(row)].tolist() == row, i
+        assert int(cnt[i]) == len(row)
+        assert (got[len(row):] == -1).all()
