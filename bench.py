@@ -46,6 +46,9 @@ CONFIGS = {
     # IVF: the per-GPU share of the 1B-code config (1e9 / 8 GPUs)
     2: dict(dim=128, ncent=1000, m=8, n=125_000_000, ht=26, per_ht="", pq="pq_ivf65536_d128_m8.npz",
             nlist=65536, nprobe=16, per_nprobe="64"),
+    # approximate k-NN graph: every database vector queries the rest
+    4: dict(dim=256, ncent=4096, m=16, n=10_000_000, ht=52, per_ht="", pq="pq_ivf16384_d256_m16.npz",
+            nlist=16384, nprobe=32, per_nprobe="", knn_k=10),
 }
 NCENT = 1000
 DIM = 128
@@ -74,7 +77,7 @@ def parse():
     args.n = c["n"] if args.n is None else args.n
     args.ht = c["ht"] if args.ht is None else args.ht
     args.per_ht = c["per_ht"] if args.per_ht is None else args.per_ht
-    if args.config == 2 and args.impl == "reference":
+    if args.config in (2, 4) and args.impl == "reference":
         raise SystemExit("--impl reference is defined for the flat configs (1, 3)")
     return args
 
@@ -184,19 +187,22 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
-# ------------------------------------------------------------------ IVF (config 2)
+# ------------------------------------------------------------------ IVF (configs 2 and 4)
 def run_ivf(args, rank, world, local):
-    """search_coarse throughput: codes scanned/s over the probed lists."""
+    """search_coarse throughput: codes scanned/s over the probed lists (config 2),
+    or the k-NN graph where every stored vector is a query (config 4)."""
     import torch
     import paper_1609_01882_b200 as pb
     from paper_1609_01882_b200 import synth
     from paper_1609_01882_b200.distributed import shard_range
-    c = CONFIGS[2]
+    c = CONFIGS[args.config]
+    knn = args.config == 4
+    norm = knn
     torch.cuda.set_device(local)
     z = np.load(os.path.join(ROOT, "tests", "golden", PQFILE))
     pq = pb.ProductQuantizer(M, 8, DIM, z["codebooks"], z["perms"])
     centers = synth.gen_centers(SEED, NCENT, DIM)
-    coarse = synth.gen_points(SEED, 1, 0, c["nlist"], centers)  # the fixture's coarse recipe
+    coarse = synth.gen_points(SEED, 1, 0, c["nlist"], centers, normalize=norm)  # the fixture's coarse recipe
     ivf = pb.IVFIndex(pq, coarse, device=local)
     row0, row1 = shard_range(args.n, world, rank)
     # build (setup, untimed): GPU generator, TF32-GEMM nearest-cell assignment,
@@ -211,13 +217,15 @@ def run_ivf(args, rank, world, local):
     for r in range(row0, row1, chunk):
         nb = min(chunk, row1 - r)
         x = xbuf[:nb]
-        pb.gen_points_device(centers, SEED, 2, r, nb, x, device=local)
+        pb.gen_points_device(centers, SEED, 2, r, nb, x, device=local, normalize=norm)
         for b in range(0, nb, 8192):
             xs = x[b:b + 8192]
             cells[b:b + xs.shape[0]] = torch.argmin(cn[None, :] - 2.0 * (xs @ dc.T), dim=1).to(torch.int32)
         ivf.add_device(x, cells[:nb], r)
     torch.cuda.synchronize()
     setup_s = time.time() - t
+    if knn:
+        return run_knn(args, c, ivf, centers, setup_s, rank, world, local, row0, row1)
     dq = torch.empty((NQ, DIM), dtype=torch.float32, device="cuda")
     pb.gen_points_device(centers, SEED, 3, 0, NQ, dq, device=local)
     stream = torch.cuda.current_stream()
@@ -266,6 +274,58 @@ def run_ivf(args, rank, world, local):
         print(json.dumps(line), flush=True)
 
 
+def run_knn(args, c, ivf, centers, setup_s, rank, world, local, row0, row1):
+    """Config 4: the k-NN graph.  A step = 256 stored vectors searched against the
+    whole index with k + 1 neighbours and the self-match removed."""
+    import torch
+    import paper_1609_01882_b200 as pb
+    k = c["knn_k"]
+    p = pb.CoarseParams(pb.Strategy.dual, k, args.ht, c["nprobe"], 0)
+    stream = torch.cuda.current_stream()
+    steps = args.steps
+    nrows = (args.warmup + steps) * BATCH
+    dx = torch.empty((nrows, DIM), dtype=torch.float32, device="cuda")
+    pb.gen_points_device(centers, SEED, 2, row0, nrows, dx, device=local, normalize=True)
+    o_ids = torch.empty((BATCH, k), dtype=torch.int64, device="cuda")
+    o_sc = torch.empty((BATCH, k), dtype=torch.float32, device="cuda")
+    o_cnt = torch.empty(BATCH, dtype=torch.int32, device="cuda")
+    scanned = 0
+    p1 = pb.CoarseParams(pb.Strategy.dual, k + 1, args.ht, c["nprobe"], 0)
+    for i in range(args.warmup, args.warmup + steps):  # per-batch work (untimed)
+        st = pb.SearchStats()
+        qb = dx[i * BATCH:(i + 1) * BATCH]
+        ob = (torch.empty((BATCH, k + 1), dtype=torch.int64, device="cuda"),
+              torch.empty((BATCH, k + 1), dtype=torch.float32, device="cuda"))
+        ivf.search_device(qb, p1, ob[0], ob[1], None, stream.cuda_stream, st)
+        scanned += st.scanned
+    for i in range(args.warmup):
+        ivf.knn_graph_device(dx[i * BATCH:(i + 1) * BATCH], row0 + i * BATCH, p, o_ids, o_sc, o_cnt,
+                             stream.cuda_stream)
+    torch.cuda.synchronize()
+    l0 = pb.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.warmup, args.warmup + steps):
+        ivf.knn_graph_device(dx[i * BATCH:(i + 1) * BATCH], row0 + i * BATCH, p, o_ids, o_sc, o_cnt,
+                             stream.cuda_stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    rows = row1 - row0
+    line = {"metric": METRIC, "value": scanned / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": steps,
+            "warmup": args.warmup, "ms_per_step": ms / steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8/f32", "data": "synthetic (unit-normalised mixture, BASELINE cfg4)",
+            "config": {"workload": f"cfg4 k-NN graph: N={args.n} d={DIM} unit-normalised, IVF {c['nlist']} + PQ "
+                                   f"m={M}, every vector queries the rest, nprobe={c['nprobe']}, ht={args.ht}, k={k}",
+                       "n_codes": args.n, "nlist": c["nlist"], "m": M, "nprobe": c["nprobe"], "k": k,
+                       "ht": args.ht, "queries_per_step": BATCH},
+            "scanned_per_query": scanned / (steps * BATCH),
+            "graph_time_est_s": rows / BATCH * ms / steps / 1e3, "gpu_launches": pb.launch_count() - l0,
+            "setup_s": round(setup_s, 1)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 # ------------------------------------------------------------------ our arm
 def cpu_baseline(args, index, dq_host):
     """Reference CPU search (oracle/_ref) on one full step of the workload:
@@ -296,7 +356,7 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank)
         return
-    if args.config == 2:
+    if args.config in (2, 4):
         run_ivf(args, rank, world, local)
         return
 
