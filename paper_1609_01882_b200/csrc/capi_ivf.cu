@@ -72,6 +72,13 @@ struct poly_b200_ivf {
     uint64_t d_out_rows = 0;
     uint32_t d_out_k = 0;
 
+    // knn_graph staging (k + 1 results per row)
+    int64_t* knn_ids = nullptr;
+    float* knn_sc = nullptr;
+    uint32_t* knn_cnt = nullptr;
+    uint64_t knn_rows = 0;
+    uint32_t knn_k1 = 0;
+
     cudaStream_t stream = nullptr;
     std::mutex mu;
     uint32_t code_bits() const { return m * 8; }
@@ -391,7 +398,8 @@ int poly_b200_ivf_destroy(poly_b200_ivf* iv) {
                             (void*)iv->np_eff, (void*)iv->scanned, (void*)iv->lutp, (void*)iv->qcodes,
                             (void*)iv->cand, (void*)iv->ctrl, (void*)iv->thr, (void*)iv->keys, (void*)iv->kcounts,
                             (void*)iv->surv_total, (void*)iv->scan_total, (void*)iv->sticky_overflow, (void*)iv->d_q,
-                            (void*)iv->d_oid, (void*)iv->d_osc, (void*)iv->d_ocnt})
+                            (void*)iv->d_oid, (void*)iv->d_osc, (void*)iv->d_ocnt,
+                            (void*)iv->knn_ids, (void*)iv->knn_sc, (void*)iv->knn_cnt})
                 dfree(p);
             iv->idm.release();
             if (iv->stream) cudaStreamDestroy(iv->stream);
@@ -571,29 +579,26 @@ int poly_b200_ivf_knn_graph_device(poly_b200_ivf* iv, const float* d_x, uint64_t
         poly_b200_ivf_params p1 = *p;
         p1.k = p->k + 1;
         const uint64_t step = 64 * IVF_NQB;
-        int64_t* t_ids = dalloc<int64_t>(step * p1.k);
-        float* t_sc = dalloc<float>(step * p1.k);
-        uint32_t* t_cnt = dalloc<uint32_t>(step);
-        try {
-            for (uint64_t b0 = 0; b0 < n; b0 += step) {
-                const uint32_t nb = (uint32_t)std::min<uint64_t>(step, n - b0);
-                device_search(iv, d_x + b0 * iv->dim, nb, &p1, t_ids, t_sc, t_cnt, s);
-                drop_self_kernel<<<(nb + 127) / 128, 128, 0, s>>>(t_ids, t_sc, t_cnt, nb, p->k, id0 + (int64_t)b0,
-                                                                  d_ids + b0 * p->k, d_scores + b0 * p->k,
-                                                                  d_counts ? d_counts + b0 : nullptr);
-                pb::count_launch();
-                read_stats(iv, 0, nullptr, s);  // syncs; fails loudly on a candidate overflow
-            }
-        } catch (...) {
+        if (iv->knn_rows < std::min(step, n) || iv->knn_k1 < p1.k) {
             cudaStreamSynchronize(s);
-            dfree(t_ids);
-            dfree(t_sc);
-            dfree(t_cnt);
-            throw;
+            dfree(iv->knn_ids);
+            dfree(iv->knn_sc);
+            dfree(iv->knn_cnt);
+            iv->knn_rows = std::max<uint64_t>(iv->knn_rows, std::min(step, n));
+            iv->knn_k1 = std::max<uint32_t>(iv->knn_k1, p1.k);
+            iv->knn_ids = dalloc<int64_t>(iv->knn_rows * iv->knn_k1);
+            iv->knn_sc = dalloc<float>(iv->knn_rows * iv->knn_k1);
+            iv->knn_cnt = dalloc<uint32_t>(iv->knn_rows);
         }
-        dfree(t_ids);
-        dfree(t_sc);
-        dfree(t_cnt);
+        for (uint64_t b0 = 0; b0 < n; b0 += step) {
+            const uint32_t nb = (uint32_t)std::min<uint64_t>(step, n - b0);
+            device_search(iv, d_x + b0 * iv->dim, nb, &p1, iv->knn_ids, iv->knn_sc, iv->knn_cnt, s);
+            drop_self_kernel<<<(nb + 127) / 128, 128, 0, s>>>(iv->knn_ids, iv->knn_sc, iv->knn_cnt, nb, p->k,
+                                                              id0 + (int64_t)b0, d_ids + b0 * p->k,
+                                                              d_scores + b0 * p->k, d_counts ? d_counts + b0 : nullptr);
+            pb::count_launch();
+            read_stats(iv, 0, nullptr, s);  // syncs; fails loudly on a candidate overflow
+        }
     });
 }
 

@@ -212,51 +212,54 @@ void launch_coarse_select(const float* q, uint32_t nq, uint32_t dim, const float
 }
 
 // ------------------------------------------------------------------ K1r
-// grid (nq * nprobe, m): item (q, p) -> residual LUT (stored-field indexed) + code.
+// grid (nq * nprobe): item (q, p) -> residual LUT (stored-field indexed) + code,
+// all m sub-quantizers per CTA; thread j owns centroid j.
 __global__ void __launch_bounds__(256) residual_lut_kernel(const float* __restrict__ queries, uint32_t dim, uint32_t m,
                                                            const unsigned long long* __restrict__ probe_keys,
                                                            uint32_t nprobe, const float* __restrict__ cent,
                                                            const float* __restrict__ codebooks,
                                                            const uint16_t* __restrict__ perms, float* __restrict__ lutp,
                                                            uint8_t* __restrict__ qcodes) {
-    const uint32_t item = blockIdx.x, sq = blockIdx.y, j = threadIdx.x;
+    const uint32_t item = blockIdx.x, j = threadIdx.x;
     const uint32_t qi = item / nprobe;
     const uint32_t cell = (uint32_t)probe_keys[item];
-    __shared__ float sub[DSUB];
-    __shared__ float wv[8];
-    __shared__ uint32_t wj[8];
-    if (j < DSUB) {
-        const uint32_t d = sq * DSUB + j;
-        sub[j] = __fsub_rn(queries[(size_t)qi * dim + d], cent[(size_t)cell * dim + d]);  // r = q - c
+    __shared__ float r[256];
+    __shared__ float wv[16][8];
+    __shared__ uint32_t wj[16][8];
+    for (uint32_t d = j; d < dim; d += 256)
+        r[d] = __fsub_rn(queries[(size_t)qi * dim + d], cent[(size_t)cell * dim + d]);  // r = q - c
+    __syncthreads();
+    for (uint32_t sq = 0; sq < m; ++sq) {
+        const float4* c = reinterpret_cast<const float4*>(codebooks + ((size_t)sq * KSUB + j) * DSUB);
+        const float* sub = r + sq * DSUB;
+        float acc = 0.0f;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const float4 cc = __ldg(c + v);
+            float t;
+            t = __fsub_rn(sub[4 * v + 0], cc.x); acc = __fadd_rn(acc, __fmul_rn(t, t));
+            t = __fsub_rn(sub[4 * v + 1], cc.y); acc = __fadd_rn(acc, __fmul_rn(t, t));
+            t = __fsub_rn(sub[4 * v + 2], cc.z); acc = __fadd_rn(acc, __fmul_rn(t, t));
+            t = __fsub_rn(sub[4 * v + 3], cc.w); acc = __fadd_rn(acc, __fmul_rn(t, t));
+        }
+        lutp[((size_t)item * m + sq) * KSUB + perms[sq * KSUB + j]] = acc;
+        float bv = acc;
+        uint32_t bj = j;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const float ov = __shfl_down_sync(0xffffffffu, bv, off);
+            const uint32_t oj = __shfl_down_sync(0xffffffffu, bj, off);
+            if (ov < bv || (ov == bv && oj < bj)) { bv = ov; bj = oj; }
+        }
+        if ((j & 31) == 0) { wv[sq][j >> 5] = bv; wj[sq][j >> 5] = bj; }
     }
     __syncthreads();
-    const float4* c = reinterpret_cast<const float4*>(codebooks + ((size_t)sq * KSUB + j) * DSUB);
-    float acc = 0.0f;
-#pragma unroll
-    for (int v = 0; v < 4; ++v) {
-        const float4 cc = c[v];
-        float t;
-        t = __fsub_rn(sub[4 * v + 0], cc.x); acc = __fadd_rn(acc, __fmul_rn(t, t));
-        t = __fsub_rn(sub[4 * v + 1], cc.y); acc = __fadd_rn(acc, __fmul_rn(t, t));
-        t = __fsub_rn(sub[4 * v + 2], cc.z); acc = __fadd_rn(acc, __fmul_rn(t, t));
-        t = __fsub_rn(sub[4 * v + 3], cc.w); acc = __fadd_rn(acc, __fmul_rn(t, t));
-    }
-    const uint32_t p = perms[sq * KSUB + j];
-    lutp[((size_t)item * m + sq) * KSUB + p] = acc;
-    float bv = acc;
-    uint32_t bj = j;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        const float ov = __shfl_down_sync(0xffffffffu, bv, off);
-        const uint32_t oj = __shfl_down_sync(0xffffffffu, bj, off);
-        if (ov < bv || (ov == bv && oj < bj)) { bv = ov; bj = oj; }
-    }
-    if ((j & 31) == 0) { wv[j >> 5] = bv; wj[j >> 5] = bj; }
-    __syncthreads();
-    if (j == 0) {
+    if (j < m) {  // argmin per sub-quantizer, ties -> lowest centroid (pq.cpp:38)
+        float bv = wv[j][0];
+        uint32_t bj = wj[j][0];
         for (int w = 1; w < 8; ++w)
-            if (wv[w] < bv || (wv[w] == bv && wj[w] < bj)) { bv = wv[w]; bj = wj[w]; }
-        qcodes[(size_t)item * m + sq] = static_cast<uint8_t>(perms[sq * KSUB + bj]);
+            if (wv[j][w] < bv || (wv[j][w] == bv && wj[j][w] < bj)) { bv = wv[j][w]; bj = wj[j][w]; }
+        qcodes[(size_t)item * m + j] = static_cast<uint8_t>(perms[j * KSUB + bj]);
     }
 }
 
@@ -264,8 +267,8 @@ void launch_residual_lut(const float* queries, uint32_t nq, uint32_t dim, uint32
                          const unsigned long long* probe_keys, uint32_t nprobe, const float* cent,
                          const float* codebooks, const uint16_t* perms, float* lutp, uint8_t* qcodes, cudaStream_t s) {
     if (nq == 0) return;
-    residual_lut_kernel<<<dim3(nq * nprobe, m), 256, 0, s>>>(queries, dim, m, probe_keys, nprobe, cent, codebooks,
-                                                            perms, lutp, qcodes);
+    residual_lut_kernel<<<nq * nprobe, 256, 0, s>>>(queries, dim, m, probe_keys, nprobe, cent, codebooks, perms, lutp,
+                                                    qcodes);
     count_launch();
 }
 
