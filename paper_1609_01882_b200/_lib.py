@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpoly_b200.so")
+LIB_PATH = os.environ.get("POLY_B200_LIB") or os.path.join(HERE, "libpoly_b200.so")  # env: experiments only
 
 _P = C.c_void_p
 _u32, _u64, _i32, _f64 = C.c_uint32, C.c_uint64, C.c_int, C.c_double

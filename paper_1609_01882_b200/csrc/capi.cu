@@ -99,7 +99,7 @@ struct poly_b200_index {
 namespace {
 
 void grow_codes(poly_b200_index* ix, uint64_t need) {
-    const uint64_t tile = 16384 / ix->cb;
+    const uint64_t tile = pb::TILE_BYTES / ix->cb;
     if (need + tile <= ix->cap_codes) return;
     uint64_t cap = std::max<uint64_t>(need, ix->cap_codes * 2) + tile;
     cap = (cap + tile - 1) / tile * tile;
@@ -149,7 +149,7 @@ void ensure_scratch(poly_b200_index* ix, uint32_t k) {
     }
     if (!ix->cand_w) {
         // warm-up samples WARM_TILES tiles: every candidate of the sample fits
-        ix->cand_w_cap = (uint32_t)(WARM_TILES * (16384 / ix->cb));
+        ix->cand_w_cap = (uint32_t)(WARM_TILES * (pb::TILE_BYTES / ix->cb));
         ix->cand_w_cap = (ix->cand_w_cap + pb::BS - 1) / pb::BS * pb::BS;
         ix->cand_w = dalloc<unsigned long long>((size_t)NQB * ix->cand_w_cap);
         ix->ctrl_w = dalloc<uint32_t>(NQB + 4 + (size_t)NQB * (ix->cand_w_cap / 256 + 1));
@@ -197,7 +197,7 @@ void run_batches(poly_b200_index* ix, const float* d_queries, uint64_t nq, const
     const bool all_pass = strategy == pb::DUAL && p->tau >= ix->code_bits();
     if (all_pass) strategy = pb::ADC;  // dual(tau = M*d) == adc
     const uint32_t Q = (uint32_t)pb::scan_queries_per_cta(ix->m);
-    const uint64_t tc = 16384 / ix->cb;
+    const uint64_t tc = pb::TILE_BYTES / ix->cb;
     const uint64_t ntiles = (ix->n + tc - 1) / tc;
     CK(cudaMemsetAsync(ix->sticky_overflow, 0, 4, s));
     CK(cudaMemsetAsync(ix->surv_total, 0, 8, s));

@@ -194,25 +194,26 @@ __device__ unsigned long long warp_select_kth(const unsigned long long* src, uin
     return prefix;
 }
 
-constexpr int RING = 768;  // per-warp survivor queue (4-byte entries, linear)
+constexpr int RING = 288;  // per-warp survivor queue (4-byte entries, linear): < 32 left + one <= 256-entry part
 
 template <int M, int Q, int W>
 struct ScanSmem {
-    static constexpr int TC = 16384 / M;                    // codes per 16 KB tile
+    static constexpr int TC = TILE_BYTES / M;               // codes per tile
     // Query q's LUT starts at q * LS floats; the +1 skew puts the same stored
     // field of up to 32 different queries in different banks (a drain holds
     // many queries' entries for the same code).
     static constexpr int LS = M * KSUB + 1;
     static constexpr size_t LUT_BYTES = (size_t)Q * LS * 4;
-    static constexpr size_t TILE_BYTES = (size_t)STAGES * 16384;
+    static constexpr size_t TILES = (size_t)STAGES * TILE_BYTES;
     static constexpr size_t RING_BYTES = (size_t)W * RING * 4;
-    static constexpr size_t TOTAL = LUT_BYTES + TILE_BYTES + RING_BYTES;
+    static constexpr size_t TOTAL = LUT_BYTES + TILES + RING_BYTES;
 };
 
 // PERQ: per-query survivor counts (ballot + popc per query) instead of the
 // free per-batch total.
 template <int M, int Q, int W, int STRAT, bool PERQ>
 __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a) {
+    static_assert(RING >= 32 + 256, "ring must hold a remainder plus one mask-byte part");
     const uint32_t bs = a.bs;
     using C = typename CodeT<M>::T;
     using SM = ScanSmem<M, Q, W>;
@@ -225,7 +226,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
     extern __shared__ __align__(128) uint8_t smem[];
     float* lut = reinterpret_cast<float*>(smem);
     C* tiles = reinterpret_cast<C*>(smem + (USE_LUT ? SM::LUT_BYTES : 0));
-    uint32_t* rings = reinterpret_cast<uint32_t*>(smem + (USE_LUT ? SM::LUT_BYTES : 0) + SM::TILE_BYTES);
+    uint32_t* rings = reinterpret_cast<uint32_t*>(smem + (USE_LUT ? SM::LUT_BYTES : 0) + SM::TILES);
 
     __shared__ __align__(8) uint64_t full_bar[STAGES];
     __shared__ __align__(8) uint64_t empty_bar[STAGES];
@@ -330,9 +331,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
                 __syncwarp();
             }
         } else {
-            C qc[Q];
-#pragma unroll
-            for (int q = 0; q < Q; ++q) qc[q] = qc_s[q];
+            const C* qc = qc_s;  // query codes read from shared memory (broadcast): frees 2Q registers
             // survivor mask layout: query q = 4g + j -> bit 8j + g (g < Q/4, j < 4)
             uint32_t vmask = 0;
             for (uint32_t q = 0; q < nqh; ++q) vmask |= 1u << (8 * (q & 3) + (q >> 2));
@@ -404,7 +403,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
             for (uint32_t j = 0; j < ntile; ++j) {
                 const uint32_t sq_ = seq + j, s = sq_ % STAGES;
                 mbar_wait(&full_bar[s], (sq_ / STAGES) & 1u);
-                const uint32_t T = tile_base + s * 16384u;
+                const uint32_t T = tile_base + s * (uint32_t)TILE_BYTES;
                 const uint64_t tfirst = (t0 + j) * a.tile_stride * TC;
                 const uint32_t tcnt = (uint32_t)min((uint64_t)TC, a.n - tfirst);
                 if constexpr (STRAT == DUAL) {
@@ -435,7 +434,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
                         if (__any_sync(0xffffffffu, m != 0)) {
                             uint32_t total;
                             const uint32_t excl = scan(__popc(m), total);
-                            if (qn + total <= RING) {
+                            if (qn + total <= (uint32_t)RING) {
                                 append(m, li, excl);
                                 qn += total;
                                 tot += total;
@@ -540,8 +539,8 @@ static void launch_m(const ScanArgs& a, int strategy, bool perq, int num_sms, cu
 
 void launch_scan(const ScanArgs& a, int strategy, uint32_t m, bool per_query_stats, int num_sms, cudaStream_t s) {
     // Q queries per CTA: Q x m x 1 KB of LUTs must fit next to the tile ring.
-    if (m == 8) launch_m<8, 16, 16>(a, strategy, per_query_stats, num_sms, s);
-    else launch_m<16, 8, 16>(a, strategy, per_query_stats, num_sms, s);
+    if (m == 8) launch_m<8, 16, SCAN_WARPS>(a, strategy, per_query_stats, num_sms, s);
+    else launch_m<16, 8, SCAN_WARPS / 2>(a, strategy, per_query_stats, num_sms, s);
 }
 
 }  // namespace pb

@@ -8,8 +8,12 @@ namespace pb {
 
 constexpr int KSUB = 256;              // dbits = 8
 constexpr int DSUB = 16;               // every configuration: 128/8 and 256/16
-constexpr int TILE = 2048;             // codes per pipeline stage
-constexpr int STAGES = 3;              // bulk-copy ring depth
+constexpr int TILE_BYTES = 12288;      // code bytes per pipeline stage (1536 codes at m = 8)
+constexpr int STAGES = 4;              // bulk-copy ring depth
+#ifndef POLY_SCAN_WARPS
+#define POLY_SCAN_WARPS 24
+#endif
+constexpr int SCAN_WARPS = POLY_SCAN_WARPS;  // K2 consumer warps (plus one TMA producer warp)
 constexpr int BS = 4096;               // candidate block size for threshold selects
 constexpr int KMAX = 2048;             // largest supported k
 constexpr int QCAP = 64;               // per-warp survivor queue entries
