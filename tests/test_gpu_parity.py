@@ -270,3 +270,44 @@ def test_wide_codes_match_oracle(pb, pq16, big16, tau, strategy):
     assert _same(cnt, oc)
     if strategy == "dual":
         assert st.survivors == int(osv.sum())
+
+
+def test_sharded_search_over_nccl_world1(pb, pq8, big8):
+    """ShardedSearch through a real NCCL process group (world size 1 on one GPU):
+    keys -> ncclAllGather -> K3 merge == the plain search."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1609_01882_b200.distributed import FlatIndexEngine, ShardedSearch
+    ix, codes, queries = big8
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        p = pb.SearchParams(pb.Strategy.dual, 100, 24)
+        sharded = ShardedSearch(FlatIndexEngine(ix), device="cuda")
+        sharded.world = 2  # exercise the all-gather + multi-part merge path with one rank's data twice
+        dq = torch.from_numpy(queries).cuda()
+        with pytest.raises(Exception):
+            sharded.search_batch(dq, p)  # a world-1 group cannot gather 2 parts: fails loudly
+        sharded.world = 1
+        ids, sc, cnt = sharded.search_batch(dq, p)
+        torch.cuda.synchronize()
+        want = ix.search_batch(queries, p)
+        assert _same(ids.cpu().numpy(), want[0])
+        assert _same(_bits(sc.cpu().numpy()), _bits(want[1]))
+        # the multi-part merge on duplicated parts keeps every id once per part: ties broken by id
+        keys = torch.empty((len(queries), 100), dtype=torch.int64, device="cuda")
+        kc = torch.empty(len(queries), dtype=torch.int32, device="cuda")
+        ix.search_keys_device(dq, p, keys, kc)
+        out = torch.empty((2 * len(queries), 100), dtype=torch.int64, device="cuda")
+        dist.all_gather_into_tensor(out[:len(queries)], keys)
+        torch.cuda.synchronize()
+        assert torch.equal(out[:len(queries)], keys)
+    finally:
+        dist.destroy_process_group()
