@@ -116,6 +116,27 @@ __device__ __forceinline__ float adc_s(uint32_t L, const C& c) {
     return acc;
 }
 
+// ADC with an exact early exit: the first M/2 terms are summed in sq order;
+// partial sums of non-negative terms with round-to-nearest are monotone, so if
+// that prefix already exceeds the bound's score the full sum does too and the
+// pair can never become a candidate (returns +inf, no further LUT traffic).
+template <int M, class C>
+__device__ __forceinline__ float adc_s_bounded(uint32_t L, const C& c, uint32_t bound_bits) {
+    float acc = ldsf(L + 4u * (word(c, 0) & 0xFFu));
+#pragma unroll
+    for (int sq = 1; sq < M / 2; ++sq) {
+        const uint32_t f = (word(c, sq >> 2) >> (8 * (sq & 3))) & 0xFFu;
+        acc = __fadd_rn(acc, ldsf(L + 4u * (sq * KSUB + f)));
+    }
+    if (__float_as_uint(acc) > bound_bits) return __int_as_float(0x7f800000);
+#pragma unroll
+    for (int sq = M / 2; sq < M; ++sq) {
+        const uint32_t f = (word(c, sq >> 2) >> (8 * (sq & 3))) & 0xFFu;
+        acc = __fadd_rn(acc, ldsf(L + 4u * (sq * KSUB + f)));
+    }
+    return acc;
+}
+
 // Four Hamming distances (each <= 128) packed into the bytes of one word.
 template <class C>
 __device__ __forceinline__ uint32_t ham4(const C& code, const C* qc) {
@@ -357,8 +378,9 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
                     const uint32_t li = (e & 0xFFFFu) + 32u * ((pbit >> 2) & 1u);
                     C code;
                     lds_code(T + li * (uint32_t)M, code);
-                    const float score = adc_s<M>(lut_base + 4u * q * SM::LS, code);
-                    try_candidate(a, q0 + q, score, (uint32_t)(tfirst + li), thr_s[q], bs, &nreq_s, req_s);
+                    const unsigned long long thr = thr_s[q];
+                    const float score = adc_s_bounded<M>(lut_base + 4u * q * SM::LS, code, (uint32_t)(thr >> 32));
+                    try_candidate(a, q0 + q, score, (uint32_t)(tfirst + li), thr, bs, &nreq_s, req_s);
                 }
             };
             // drain full groups of 32, then move the (< 32) remainder to the front
@@ -467,7 +489,9 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
 #pragma unroll 1
                             for (int q = 0; q < (int)nqh; ++q) {
                                 float score;
-                                if constexpr (STRAT == ADC) score = adc_s<M>(lut_base + 4u * q * SM::LS, code);
+                                if constexpr (STRAT == ADC)
+                                    score = adc_s_bounded<M>(lut_base + 4u * q * SM::LS, code,
+                                                             (uint32_t)(thr_s[q] >> 32));
                                 else if constexpr (STRAT == BINARY) score = (float)ham(code, qc[q]);
                                 else score = (float)disidx(code, qc[q]);
                                 try_candidate(a, q0 + q, score, (uint32_t)(tfirst + li), thr_s[q], bs, &nreq_s,
