@@ -215,7 +215,16 @@ __device__ unsigned long long warp_select_kth(const unsigned long long* src, uin
     return prefix;
 }
 
-constexpr int RING = 288;  // per-warp survivor queue (4-byte entries, linear): < 32 left + one <= 256-entry part
+#ifndef POLY_PRODUCER_POLL  // > 0: the producer polls (sleep ns) and refreshes thresholds while it waits
+#define POLY_PRODUCER_POLL 0
+#endif
+#ifndef POLY_RING
+#define POLY_RING 288
+#endif
+// per-warp survivor queue (4-byte entries, linear): < 32 left + one step part;
+// a step that does not fit is split into mask parts of PART_BITS bits (<= 32 * PART_BITS entries)
+constexpr int RING = POLY_RING;
+constexpr int PART_BITS = RING >= 32 + 256 ? 8 : 4;
 
 template <int M, int Q, int W>
 struct ScanSmem {
@@ -234,7 +243,7 @@ struct ScanSmem {
 // free per-batch total.
 template <int M, int Q, int W, int STRAT, bool PERQ>
 __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a) {
-    static_assert(RING >= 32 + 256, "ring must hold a remainder plus one mask-byte part");
+    static_assert(RING >= 32 + 32 * PART_BITS, "ring must hold a remainder plus one mask part");
     const uint32_t bs = a.bs;
     using C = typename CodeT<M>::T;
     using SM = ScanSmem<M, Q, W>;
@@ -271,6 +280,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
         req_head_s = 0;
         group_s = 0xFFFFFFFFu;
     }
+    if (threadIdx.x < MAXREQ) req_s[threadIdx.x] = 0xFFFFFFFFu;
     __syncthreads();
 
     uint32_t* ring = rings + (producer ? 0 : warp) * RING;
@@ -282,15 +292,21 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
             uint32_t req = 0xFFFFFFFFu;
             if (lane == 0) {
                 const uint32_t tail = *(volatile uint32_t*)&nreq_s;
+                if (tail - req_head_s > MAXREQ) req_head_s = tail - MAXREQ;  // dropped requests
                 if (req_head_s != tail) {
-                    if (tail - req_head_s > MAXREQ) req_head_s = tail - MAXREQ;  // dropped requests
-                    req = *(volatile uint32_t*)&req_s[req_head_s % MAXREQ];
-                    ++req_head_s;
+                    // the writer moves the tail before it fills the slot: EMPTY = not yet published
+                    volatile uint32_t* slot = &req_s[req_head_s % MAXREQ];
+                    req = *slot;
+                    if (req != 0xFFFFFFFFu) {
+                        *slot = 0xFFFFFFFFu;
+                        ++req_head_s;
+                    }
                 }
             }
             req = __shfl_sync(0xffffffffu, req, 0);
             if (req == 0xFFFFFFFFu) break;
             const uint32_t qg = req >> 16, blk = req & 0xFFFFu;
+            if (qg >= a.nqb || blk >= a.cap / bs) continue;  // (a lapped slot still holds some valid request)
             __threadfence();
             const unsigned long long kth =
                 warp_select_kth(a.cand + (size_t)qg * a.cap + (size_t)blk * bs, bs, a.k, sel_hist);
@@ -333,10 +349,31 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
         if (threadIdx.x == 0) group_s = g;
 
         if (producer) {
+            // keep the consumers' thresholds fresh (benign race: aligned 64-bit stores)
+            auto refresh = [&]() {
+                if (lane < nqh) {
+                    const unsigned long long t = __ldcg(a.thr + q0 + lane);
+                    if (t < thr_s[lane]) thr_s[lane] = t;
+                }
+                __syncwarp();
+            };
             for (uint32_t j = 0; j < ntile; ++j) {
+                const uint32_t sq_ = seq + j, s = sq_ % STAGES;
+                if (sq_ >= STAGES) {
+#if POLY_PRODUCER_POLL
+                    // while the stage is busy: serve selects, refresh thresholds
+                    for (;;) {
+                        uint32_t ok = lane == 0 ? mbar_test(&empty_bar[s], ((sq_ / STAGES) - 1) & 1u) : 0u;
+                        if (__shfl_sync(0xffffffffu, ok, 0)) break;
+                        serve_selects();
+                        refresh();
+                        __nanosleep(POLY_PRODUCER_POLL);
+                    }
+#else
+                    if (lane == 0) mbar_wait(&empty_bar[s], ((sq_ / STAGES) - 1) & 1u);
+#endif
+                }
                 if (lane == 0) {
-                    const uint32_t sq_ = seq + j, s = sq_ % STAGES;
-                    if (sq_ >= STAGES) mbar_wait(&empty_bar[s], ((sq_ / STAGES) - 1) & 1u);
                     const uint64_t first = (t0 + j) * a.tile_stride * TC;
                     const uint64_t cnt = min((uint64_t)TC, a.n - first);
                     const uint32_t bytes = (uint32_t)((cnt * M + 15) & ~15ull);
@@ -344,12 +381,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
                     bulk_g2s(tiles + s * TC, a.codes + first * M, bytes, &full_bar[s]);
                 }
                 serve_selects();
-                // keep the consumers' thresholds fresh (benign race: aligned 64-bit stores)
-                if (lane < nqh) {
-                    const unsigned long long t = __ldcg(a.thr + q0 + lane);
-                    if (t < thr_s[lane]) thr_s[lane] = t;
-                }
-                __syncwarp();
+                refresh();
             }
         } else {
             const C* qc = qc_s;  // query codes read from shared memory (broadcast): frees 2Q registers
@@ -463,10 +495,10 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
                                 __syncwarp();
                                 if (qn >= 32) drain_full(T, tfirst);
                             } else {
-                                // a step adds <= 64 * Q entries: split it by mask byte (<= 256 each)
+                                // a step adds <= 64 * Q entries: split it by mask part
 #pragma unroll 1
-                                for (int part = 0; part < 4; ++part) {
-                                    const uint32_t mm = m & (0xFFu << (8 * part));
+                                for (int part = 0; part < 32 / PART_BITS; ++part) {
+                                    const uint32_t mm = m & (((1u << PART_BITS) - 1u) << (PART_BITS * part));
                                     uint32_t ptotal;
                                     const uint32_t pex = scan(__popc(mm), ptotal);
                                     append(mm, li, pex);

@@ -8,8 +8,19 @@ namespace pb {
 
 constexpr int KSUB = 256;              // dbits = 8
 constexpr int DSUB = 16;               // every configuration: 128/8 and 256/16
-constexpr int TILE_BYTES = 12288;      // code bytes per pipeline stage (1536 codes at m = 8)
-constexpr int STAGES = 4;              // bulk-copy ring depth
+#define POLY_STR2(x) #x
+#define POLY_STR(x) POLY_STR2(x)
+#ifndef POLY_WAIT_HINT  // mbarrier try_wait suspend-time hint (ns); 0 = none
+#define POLY_WAIT_HINT 20000
+#endif
+#ifndef POLY_TILE_BYTES
+#define POLY_TILE_BYTES 12288
+#endif
+#ifndef POLY_STAGES
+#define POLY_STAGES 4
+#endif
+constexpr int TILE_BYTES = POLY_TILE_BYTES;  // code bytes per pipeline stage (1536 codes at m = 8)
+constexpr int STAGES = POLY_STAGES;          // bulk-copy ring depth
 #ifndef POLY_SCAN_WARPS
 #define POLY_SCAN_WARPS 24
 #endif
@@ -89,11 +100,29 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "{\n"
         ".reg .pred p;\n"
         "WAIT_%=:\n"
+#if POLY_WAIT_HINT > 0
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, " POLY_STR(POLY_WAIT_HINT) ";\n"
+#else
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+#endif
         "@!p bra WAIT_%=;\n"
         "}\n" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+}
+
+__device__ __forceinline__ uint32_t mbar_test(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok;
 }
 
 // 1-D TMA bulk copy global -> shared, completion counted on `bar` (bytes % 16 == 0).
