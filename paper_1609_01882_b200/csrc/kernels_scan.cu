@@ -144,6 +144,30 @@ __device__ __forceinline__ uint32_t ham4(const C& code, const C* qc) {
     return (h0 + (h1 << 8)) + ((h2 + (h3 << 8)) << 16);
 }
 
+// ---- tensor-core Hamming filter (DUAL) ----
+// h(x, q) <= tau is decided by one int8 MMA per 128 codes x 16 queries: code bit b of
+// byte t of word w becomes A element (w, plane j = b, byte t) with value 2^j (j < 7) or
+// 1 (j = 7) -- one LOP per 4 elements; the query's B element is s * 64 / value with
+// s = +1 / -1 for query bit 0 / 1, so the products sum to 64 * (|x| - 2<x,q>) =
+// 64 * (h - |q|).  A bias K-block (A = 2, B summing to 32 (|q| - tau) - 16) makes
+// D = 64 (h - tau) - 32, i.e. sign(D) = [h <= tau], exact for every tau in [0, 64 * m/8].
+__device__ __forceinline__ void expand_word(uint32_t w, uint32_t* out) {
+#pragma unroll
+    for (int j = 0; j < 7; ++j) out[j] = w & (0x01010101u << j);
+    out[7] = (w >> 7) & 0x01010101u;
+}
+// B operand: 16 rows (queries) x KB bytes, canonical K-major no-swizzle layout:
+// 8 x 16-byte core matrices, core (n8, k16) at n8 * 128 + k16 * 256 (SBO 128, LBO 256)
+__device__ __forceinline__ uint32_t bw_offset(uint32_t n, uint32_t k) {
+    return (n >> 3) * 128u + (k >> 4) * 256u + (n & 7u) * 16u + (k & 15u);
+}
+__device__ __forceinline__ uint64_t bw_desc(uint32_t saddr) {
+    return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)(256u >> 4) << 16) | ((uint64_t)(128u >> 4) << 32) |
+           (1ull << 46);
+}
+// kind::i8 instruction descriptor: D s32, A s8, B s8, K-major, N = 16, M = 128
+constexpr uint32_t IDESC_I8_M128_N16 = (2u << 4) | (1u << 7) | (1u << 10) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
+
 // Append a candidate key for batch query qg; track block completion.
 __device__ __forceinline__ void append_candidate(const ScanArgs& a, uint32_t qg, unsigned long long key, uint32_t bs,
                                                  uint32_t* nreq_s, uint32_t* req_s) {
@@ -218,6 +242,9 @@ __device__ unsigned long long warp_select_kth(const unsigned long long* src, uin
 #ifndef POLY_PRODUCER_POLL  // > 0: the producer polls (sleep ns) and refreshes thresholds while it waits
 #define POLY_PRODUCER_POLL 0
 #endif
+#ifndef POLY_TC  // 1: DUAL's Hamming filter on the tensor cores (int8 tcgen05.mma); 0: POPC
+#define POLY_TC 1
+#endif
 #ifndef POLY_RING
 #define POLY_RING 288
 #endif
@@ -267,6 +294,17 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
     __shared__ uint32_t req_s[MAXREQ];
     __shared__ uint32_t sel_hist[256];
     __shared__ uint32_t req_head_s;
+    // tensor-core filter state: B operand (query weights + bias), per-quad MMA barriers, TMEM base
+    constexpr bool TCF = POLY_TC && STRAT == DUAL && M == 8;  // m = 16: 8 queries per CTA do not amortise the expansion
+    constexpr int KB = M * 8 + 32;   // B row bytes: one per code bit + the bias block
+    constexpr int NKB = KB / 32;     // K blocks of 32 bytes
+    constexpr int AC = 2 * M;        // TMEM columns of one expanded code (M * 8 bytes)
+    constexpr int QC = 2 * AC + 32;  // columns per quad: A0, A1, D0, D1
+    static_assert(!TCF || (W % 4 == 0 && 16 + (W / 4) * QC <= 512), "TMEM budget");
+    __shared__ __align__(256) int8_t bw_s[TCF ? 16 * KB : 16];
+    __shared__ __align__(8) uint64_t qbar_s[W / 4];
+    __shared__ uint32_t qcnt_s[W / 4];  // A-row stagings per quad (the 4th of each round issues the MMA)
+    __shared__ uint32_t tmem_s;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool producer = warp == W;
@@ -276,15 +314,33 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
             mbar_init(&empty_bar[s], W);
         }
         fence_mbar_init();
+        if (TCF)
+            for (int qd = 0; qd < W / 4; ++qd) {
+                mbar_init(&qbar_s[qd], 1);
+                qcnt_s[qd] = 0;
+            }
+        fence_mbar_init();
         nreq_s = 0;
         req_head_s = 0;
         group_s = 0xFFFFFFFFu;
     }
     if (threadIdx.x < MAXREQ) req_s[threadIdx.x] = 0xFFFFFFFFu;
+    if (TCF && warp == 0) tmem_alloc(&tmem_s, 512);
+    tc_fence_before();
     __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = TCF ? tmem_s : 0u;
+    // TMEM: columns [0, 8) = the A bias block (constant 2), quad k at 16 + k * QC
+    const uint32_t tlane = (uint32_t)(32 * (warp & 3)) << 16;
+    if (TCF && warp < 4) {
+        tmem_st8(tbase + tlane, 0x02020202u);
+        tmem_wait_st();
+    }
+    tc_fence_before();
 
     uint32_t* ring = rings + (producer ? 0 : warp) * RING;
     uint32_t seq = 0;
+    uint32_t qphase = 0;  // parity of this warp's quad MMA barrier
 
     // producer warp: serve threshold selects requested by the consumers' appends
     auto serve_selects = [&]() {
@@ -340,6 +396,30 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
             }
             if (threadIdx.x < Q)
                 qc_s[threadIdx.x] = threadIdx.x < nqh ? reinterpret_cast<const C*>(a.qcodes)[q0 + threadIdx.x] : C{};
+            if (TCF) {
+                const uint32_t* qw = reinterpret_cast<const uint32_t*>(a.qcodes);
+                const uint32_t tau = min(a.tau, (uint32_t)(M * 8));
+                for (uint32_t i = threadIdx.x; i < 16u * KB; i += NT) {
+                    const uint32_t n = i / KB, k = i % KB;
+                    int v = 0;
+                    if (n < nqh) {
+                        const uint32_t* qn = qw + (size_t)(q0 + n) * (M / 4);
+                        if (k < (uint32_t)M * 8) {  // word k/32, plane j, byte t -> bit 8t + j
+                            const uint32_t j = (k & 31u) >> 2, t = k & 3u;
+                            const int mag = j < 7 ? (1 << (6 - j)) : 64;
+                            v = ((__ldg(qn + (k >> 5)) >> (8 * t + j)) & 1u) ? -mag : mag;
+                        } else {  // bias: 32 entries summing to 32 (|q| - tau) - 16
+                            int pc = 0;
+                            for (int w = 0; w < M / 4; ++w) pc += __popc(__ldg(qn + w));
+                            const int T = 32 * (pc - (int)tau) - 16, e = (int)(k - (uint32_t)M * 8);
+                            const int base = T / 32, rem = T - base * 32;
+                            v = base + (e < (rem < 0 ? -rem : rem) ? (rem < 0 ? -1 : 1) : 0);
+                        }
+                    }
+                    bw_s[bw_offset(n, k)] = (int8_t)v;
+                }
+                fence_proxy_async_smem();  // generic-proxy writes -> tensor-core reads
+            }
         }
         if (threadIdx.x < Q) {
             thr_s[threadIdx.x] = threadIdx.x < nqh ? __ldcg(a.thr + q0 + threadIdx.x) : 0ull;
@@ -406,8 +486,9 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
                     const uint32_t e = lds32v(ring_base + 4u * (off + lane));
                     // mask bit p = 8j + 4c + g -> query 4g + j of the lane's code c (tile index li + 32c)
                     const uint32_t pbit = e >> 16;
-                    const uint32_t q = 4 * (pbit & 3) + (pbit >> 3);
-                    const uint32_t li = (e & 0xFFFFu) + 32u * ((pbit >> 2) & 1u);
+                    // TCF: bit p = 16c + q; POPC: p = 8j + 4c + g for query 4g + j
+                    const uint32_t q = TCF ? (pbit & 15u) : 4 * (pbit & 3) + (pbit >> 3);
+                    const uint32_t li = (e & 0xFFFFu) + 32u * (TCF ? (pbit >> 4) : ((pbit >> 2) & 1u));
                     C code;
                     lds_code(T + li * (uint32_t)M, code);
                     const unsigned long long thr = thr_s[q];
@@ -454,9 +535,55 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
                 return incl - cnt;
             };
 
+            // TCF: tile j's A rows (expanded codes) are staged into TMEM one tile ahead;
+            // the quad's last warp to stage issues the MMA (no quad barrier)
+            const uint32_t quad = (uint32_t)warp >> 2;
+            const uint32_t A0 = tbase + tlane + 16u + quad * QC, A1 = A0 + AC;
+            const uint32_t D0 = A0 + 2 * AC, D1 = D0 + 16;
+            const uint32_t qa0 = tbase + 16u + quad * QC;   // lane 0 of the quad's columns
+            const uint64_t bdesc0 = bw_desc(smem_u32(bw_s));  // + 32 per K block (512 B >> 4)
+            auto stage_a = [&](uint32_t jj) {
+                const uint32_t sq_ = seq + jj, s = sq_ % STAGES;
+                mbar_wait(&full_bar[s], (sq_ / STAGES) & 1u);
+                const uint32_t T = tile_base + s * (uint32_t)TILE_BYTES;
+                const uint32_t li = warp * CPW + lane;
+                C c0, c1;
+                lds_code(T + li * (uint32_t)M, c0);
+                lds_code(T + (li + 32) * (uint32_t)M, c1);
+                uint32_t x[16];
+#pragma unroll
+                for (int h = 0; h < M / 8; ++h) {
+                    expand_word(word(c0, 2 * h), x);
+                    expand_word(word(c0, 2 * h + 1), x + 8);
+                    tmem_st16(A0 + 16 * h, x);
+                }
+#pragma unroll
+                for (int h = 0; h < M / 8; ++h) {
+                    expand_word(word(c1, 2 * h), x);
+                    expand_word(word(c1, 2 * h + 1), x + 8);
+                    tmem_st16(A1 + 16 * h, x);
+                }
+                tmem_wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0 && (atom_add_acq_rel(&qcnt_s[quad], 1u) & 3u) == 3u) {
+                    tc_fence_after();
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        const uint32_t ac = qa0 + c * AC, dc = qa0 + 2 * AC + 16 * c;
+#pragma unroll
+                        for (int kb = 0; kb < NKB - 1; ++kb)
+                            mma_i8_ts(dc, ac + 8 * kb, bdesc0 + (uint64_t)(32 * kb), IDESC_I8_M128_N16, kb);
+                        mma_i8_ts(dc, tbase, bdesc0 + (uint64_t)(32 * (NKB - 1)), IDESC_I8_M128_N16, 1);
+                    }
+                    tc_commit(&qbar_s[quad]);
+                }
+                __syncwarp();
+            };
+            if constexpr (TCF) stage_a(0);
             for (uint32_t j = 0; j < ntile; ++j) {
                 const uint32_t sq_ = seq + j, s = sq_ % STAGES;
-                mbar_wait(&full_bar[s], (sq_ / STAGES) & 1u);
+                if constexpr (!TCF) mbar_wait(&full_bar[s], (sq_ / STAGES) & 1u);
                 const uint32_t T = tile_base + s * (uint32_t)TILE_BYTES;
                 const uint64_t tfirst = (t0 + j) * a.tile_stride * TC;
                 const uint32_t tcnt = (uint32_t)min((uint64_t)TC, a.n - tfirst);
@@ -465,24 +592,47 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
 #pragma unroll 1
                     for (int i = 0; i < CPW / 64; ++i) {
                         const uint32_t li = warp * CPW + i * 64 + lane;
-                        C c0, c1;
-                        lds_code(T + li * (uint32_t)M, c0);
-                        lds_code(T + (li + 32) * (uint32_t)M, c1);
-                        uint32_t m0 = 0, m1 = 0;
+                        uint32_t m;
+                        if constexpr (TCF) {
+                            // this tile's MMA was issued when the quad's last warp staged it
+                            mbar_wait(&qbar_s[quad], qphase);
+                            qphase ^= 1u;
+                            tc_fence_after();
+                            // sign bits: bit q <- code li, bit 16 + q <- code li + 32
+                            uint32_t d[16];
+                            m = 0;
+                            tmem_ld16(D1, d);
+                            tmem_wait_ld();
 #pragma unroll
-                        for (int g = 0; g < Q / 4; ++g) {
-                            const uint32_t v0 = ham4(c0, qc + 4 * g) + bias;
-                            const uint32_t v1 = ham4(c1, qc + 4 * g) + bias;
-                            m0 |= (~v0 & 0x80808080u) >> (7 - g);
-                            m1 |= (~v1 & 0x80808080u) >> (3 - g);
+                            for (int q = 15; q >= 0; --q) m = __funnelshift_l(d[q], m, 1);
+                            tmem_ld16(D0, d);
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int q = 15; q >= 0; --q) m = __funnelshift_l(d[q], m, 1);
+                            const uint32_t vm = (nqh >= 16 ? 0xFFFFu : (1u << nqh) - 1u);
+                            m &= (li < tcnt ? vm : 0u) | (li + 32 < tcnt ? vm << 16 : 0u);
+                            // stage the next tile's A rows now: its MMA overlaps this tile's survivors
+                            if (j + 1 < ntile) stage_a(j + 1);
+                        } else {
+                            C c0, c1;
+                            lds_code(T + li * (uint32_t)M, c0);
+                            lds_code(T + (li + 32) * (uint32_t)M, c1);
+                            uint32_t m0 = 0, m1 = 0;
+#pragma unroll
+                            for (int g = 0; g < Q / 4; ++g) {
+                                const uint32_t v0 = ham4(c0, qc + 4 * g) + bias;
+                                const uint32_t v1 = ham4(c1, qc + 4 * g) + bias;
+                                m0 |= (~v0 & 0x80808080u) >> (7 - g);
+                                m1 |= (~v1 & 0x80808080u) >> (3 - g);
+                            }
+                            m = (li < tcnt ? m0 & vmask : 0u) | (li + 32 < tcnt ? m1 & (vmask << 4) : 0u);
                         }
-                        const uint32_t m = (li < tcnt ? m0 & vmask : 0u) | (li + 32 < tcnt ? m1 & (vmask << 4) : 0u);
                         if constexpr (PERQ) {
 #pragma unroll
                             for (int q = 0; q < Q; ++q) {
-                                const int b = 8 * (q & 3) + (q >> 2);
+                                const int b = TCF ? q : 8 * (q & 3) + (q >> 2), b2 = TCF ? q + 16 : b + 4;
                                 survq[q] += __popc(__ballot_sync(0xffffffffu, (m >> b) & 1u)) +
-                                            __popc(__ballot_sync(0xffffffffu, (m >> (b + 4)) & 1u));
+                                            __popc(__ballot_sync(0xffffffffu, (m >> b2) & 1u));
                             }
                         }
                         if (__any_sync(0xffffffffu, m != 0)) {
@@ -559,6 +709,10 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
         if (STRAT == DUAL && threadIdx.x < (PERQ ? nqh : 1u) && surv_s[threadIdx.x])
             atomicAdd(a.surv + (PERQ ? q0 + threadIdx.x : 0u), (unsigned long long)surv_s[threadIdx.x]);
         __syncthreads();
+    }
+    if (TCF) {
+        tc_fence_after();
+        if (warp == 0) tmem_dealloc(tbase, 512);
     }
 }
 
