@@ -509,17 +509,23 @@ def main():
             traffic = None
     roofline = {"bound": "hbm", "achieved": hbm_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": hbm_gbs / pk["hbm_gbs"], "traffic": traffic, "peak_kind": pk_kind,
-                "kernel": f"K2 scan_kernel<{M},{16 if M == 8 else 8},16,DUAL>", "kernel_ms_avg": avg,
+                "kernel": f"K2 scan_kernel<{M},{16 if M == 8 else 8},{24 if M == 8 else 12},DUAL>", "kernel_ms_avg": avg,
                 "kernel_launches": scan_n,
                 "kernel_share_of_step": scan_ms / ms,
                 "algorithmic_bytes_per_launch": code_bytes, "units_per_launch": f"{BATCH} queries x {nloc} codes"}
-    # issue roofline (the binding one for this integer/gather scan):
-    # POPC 16/clk/SM (2 per pair) vs random LUT gathers 13.5/clk/SM (8 per survivor), measured.
+    # secondary roofline (the binding one for this integer/gather scan), per pair:
+    #  m = 8 (tensor-core filter): TMEM read of the int32 D tile 4 B at 64 B/clk/SM, int8 MMA
+    #    (6 x 8 clk per 4096 pairs), random LUT gathers 13.5/clk/SM (M per survivor);
+    #  m = 16 (POPC filter): POPC 16/clk/SM (M/4 per pair) vs the same gathers.
     f_mhz = (clk or {}).get("sm_mhz") or pk.get("sm_max_mhz", 1965.0)
     s = per_ht[str(args.ht)]["survivor_frac"]
-    clk_per_pair = max(M / 4 / 16.0, s * M / 13.5, float(M) / BATCH / (pk["hbm_gbs"] * 1e3 / f_mhz / 148))
+    hbm_clk = float(M) / BATCH / (pk["hbm_gbs"] * 1e3 / f_mhz / 148)
+    if M == 8:
+        bound, clk_per_pair = "tmem-read/mma/lds-gather", max(4 / 64.0, 48 / 4096.0, s * M / 13.5, hbm_clk)
+    else:
+        bound, clk_per_pair = "popc/lds-gather", max(M / 4 / 16.0, s * M / 13.5, hbm_clk)
     peak_pairs = 148 * f_mhz * 1e6 / clk_per_pair
-    roofline_issue = {"bound": "popc/lds issue", "achieved": pairs / (avg / 1e3), "peak": peak_pairs,
+    roofline_issue = {"bound": bound, "achieved": pairs / (avg / 1e3), "peak": peak_pairs,
                       "unit": "pairs/s", "frac": pairs / (avg / 1e3) / peak_pairs, "sm_mhz": f_mhz,
                       "clk_per_pair_bound": clk_per_pair, "survivor_frac": s}
 

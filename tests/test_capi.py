@@ -51,3 +51,11 @@ def test_strategy_names():
         assert pb.to_string(pb.strategy_from_string(s)) == s
     with pytest.raises(pb.PolyError):
         pb.strategy_from_string("hamming")
+
+
+def test_bench_and_entry_scripts_compile():
+    """bench.py / __graft_entry__.py are driver contracts: they must at least compile."""
+    import py_compile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for f in ("bench.py", "__graft_entry__.py"):
+        py_compile.compile(os.path.join(root, f), doraise=True)
