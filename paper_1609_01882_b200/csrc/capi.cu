@@ -137,14 +137,17 @@ void ensure_scratch(poly_b200_index* ix, uint32_t k) {
         *ix->h_overflow = 0;
         CK(cudaEventCreateWithFlags(&ix->done_ev, cudaEventDisableTiming));
     }
-    const uint32_t bs = std::max<uint32_t>(pb::BS, 4 * k);
-    if (ix->cand_bs < bs) {
+    // select block: a block of bs list slots completes -> its k-th key tightens thr[q];
+    // the list holds at least 32 * BS keys per query
+    const uint32_t bs = std::max<uint32_t>(POLY_SEL_BS, POLY_SEL_KF * k);
+    const uint32_t cap = std::max<uint32_t>(32 * bs, 32 * pb::BS);
+    if (ix->cand_bs != bs || ix->cand_cap < cap) {
         dfree(ix->cand);
         dfree(ix->ctrl);
         ix->cand_bs = bs;
-        ix->cand_cap = 32 * bs;
+        ix->cand_cap = cap;
         ix->cand = dalloc<unsigned long long>((size_t)NQB * ix->cand_cap);
-        ix->ctrl_words = NQB + 4 + (size_t)NQB * 32;
+        ix->ctrl_words = NQB + 4 + (size_t)NQB * (cap / bs);
         ix->ctrl = dalloc<uint32_t>(ix->ctrl_words);
     }
     if (!ix->cand_w) {
@@ -228,7 +231,9 @@ void run_batches(poly_b200_index* ix, const float* d_queries, uint64_t nq, const
             // k * N / sample candidates in the full scan, so its in-scan selects
             // are rare.  The samples are re-scanned by the full scan (their keys
             // must be in its list); cost ~ 2% of the scan at N = 1e8.
-            for (uint64_t wt = WARM_TILES; ntiles >= 8 * wt && ix->n > ix->cand_cap / 8; wt *= 8) {
+            int level = 0;
+            for (uint64_t wt = WARM_TILES; ntiles >= 8 * wt && ix->n > ix->cand_cap / 8 && level < POLY_WARM_LEVELS;
+                 wt *= 8, ++level) {
                 pb::ScanArgs w = a;
                 const size_t nblk_w = ix->cand_w_cap / 256 + 1;
                 CK(cudaMemsetAsync(ix->ctrl_w, 0, (NQB + 4 + NQB * nblk_w) * 4, s));

@@ -16,6 +16,15 @@ constexpr int DSUB = 16;               // every configuration: 128/8 and 256/16
 #ifndef POLY_MAX_TPC  // tiles per K2 work unit (cap): fewer unit boundaries vs. tail balance
 #define POLY_MAX_TPC 128
 #endif
+#ifndef POLY_SEL_BS  // candidate-list slots per threshold select (>= 4k)
+#define POLY_SEL_BS 512
+#endif
+#ifndef POLY_SEL_KF  // select block >= KF * k slots
+#define POLY_SEL_KF 4
+#endif
+#ifndef POLY_WARM_LEVELS  // at most this many geometric warm-up samples before the full scan
+#define POLY_WARM_LEVELS 2
+#endif
 #ifndef POLY_TILE_BYTES
 #define POLY_TILE_BYTES 12288
 #endif
