@@ -232,7 +232,7 @@ void run_batches(poly_b200_index* ix, const float* d_queries, uint64_t nq, const
             // are rare.  The samples are re-scanned by the full scan (their keys
             // must be in its list); cost ~ 2% of the scan at N = 1e8.
             int level = 0;
-            for (uint64_t wt = WARM_TILES; ntiles >= 8 * wt && ix->n > ix->cand_cap / 8 && level < POLY_WARM_LEVELS;
+            for (uint64_t wt = POLY_WARM_FIRST; ntiles >= 8 * wt && ix->n > ix->cand_cap / 8 && level < POLY_WARM_LEVELS;
                  wt *= 8, ++level) {
                 pb::ScanArgs w = a;
                 const size_t nblk_w = ix->cand_w_cap / 256 + 1;
@@ -248,7 +248,9 @@ void run_batches(poly_b200_index* ix, const float* d_queries, uint64_t nq, const
                 w.tile_stride = ntiles / wt;
                 w.tiles_per_chunk = 4;  // small units: the first levels would otherwise use few SMs
                 w.units = (uint32_t)(wt / 4) * w.ngroups;
-                w.bs = ix->cand_w_cap;  // no in-scan selects: the whole sample is ranked below
+                // POLY_WARM_SEL: in-scan selects tighten thr inside the sample too (its top-k
+                // members stay in the list either way); else the whole sample is ranked below
+                w.bs = POLY_WARM_SEL ? ix->cand_bs : ix->cand_w_cap;
                 pb::launch_scan(w, strategy, ix->m, false, ix->num_sms, s);
                 // an overflowed sample list is only a weaker (still valid) bound: ranks
                 // of a subset of the sample's keys

@@ -7,10 +7,13 @@
 // (fp32 score bits << 32 | 32-bit id rank); scores are >= 0, so unsigned key
 // order == (score, id) order and ties resolve to the lower id.
 //
-// One CTA per query.  <= 8192 candidates: bitonic sort in shared memory.
-// More: 8-pass radix select of the k-th key streamed from L2, then the k keys
-// <= it are gathered and sorted.  The same kernel merges the per-GPU lists of
-// the multi-GPU path (parts > 1).
+// One CTA per query.  <= 2048 candidates: bitonic sort in shared memory.
+// More: a 3-pass bucket select -- key range (min, max), a 4096-bucket histogram
+// over the bits just below the highest bit where min and max differ, then the
+// keys of the buckets up to the k-th one are gathered (usually ~k) and sorted.
+// Fallbacks when that set exceeds TK_SEL_KEYS: bitonic sort of all keys (<= 8192,
+// in shared memory) or an 8-pass radix select of the k-th key streamed from L2.
+// The same kernel merges the per-GPU lists of the multi-GPU path (parts > 1).
 #include "poly_b200.cuh"
 
 namespace pb {
@@ -18,6 +21,9 @@ namespace pb {
 constexpr int TK_THREADS = 512;
 constexpr uint32_t TK_SMEM_KEYS = 8192;
 constexpr int TK_MAXPARTS = 64;
+constexpr uint32_t TK_DIRECT = 2048;  // at most this many: sort them all
+constexpr uint32_t TK_SEL_KEYS = 4096;
+constexpr uint32_t TK_BUCKETS = 4096;
 
 __device__ __forceinline__ void bitonic_sort(unsigned long long* s, uint32_t p) {
     for (uint32_t size = 2; size <= p; size <<= 1) {
@@ -51,15 +57,121 @@ __global__ void __launch_bounds__(TK_THREADS) topk_kernel(const unsigned long lo
     for (uint32_t p = 0; p < parts; ++p) total += pc[p];
     const uint32_t kk = min(k, total);
     unsigned long long* out = out_keys + (size_t)q * k;
-    if (total <= TK_SMEM_KEYS) {
-        uint32_t P = 1;
-        while (P < total) P <<= 1;
+    unsigned long long* sel = sk + TK_SMEM_KEYS;                       // TK_SEL_KEYS
+    uint32_t* bh = reinterpret_cast<uint32_t*>(sel + TK_SEL_KEYS);    // TK_BUCKETS
+    const bool in_smem = total <= TK_SMEM_KEYS;
+    if (in_smem) {  // stage all keys in shared memory
         uint32_t base = 0;
         for (uint32_t p = 0; p < parts; ++p) {
             const unsigned long long* src = cand + p * part_stride + (size_t)q * cap;
             for (uint32_t i = threadIdx.x; i < pc[p]; i += TK_THREADS) sk[base + i] = __ldcg(src + i);
             base += pc[p];
         }
+        __syncthreads();
+    }
+    // key i of the list (shared memory or global)
+    auto key_at = [&](uint32_t p, uint32_t i, uint32_t flat) -> unsigned long long {
+        return in_smem ? sk[flat] : __ldcg(cand + p * part_stride + (size_t)q * cap + i);
+    };
+    if (total > TK_DIRECT && kk > 0) {
+        // pass 1: key range
+        unsigned long long lo = ~0ull, hi = 0;
+        {
+            uint32_t flat = 0;
+            for (uint32_t p = 0; p < parts; ++p) {
+                for (uint32_t i = threadIdx.x; i < pc[p]; i += TK_THREADS) {
+                    const unsigned long long v = key_at(p, i, flat + i);
+                    lo = v < lo ? v : lo;
+                    hi = v > hi ? v : hi;
+                }
+                flat += pc[p];
+            }
+        }
+        for (int off = 16; off > 0; off >>= 1) {
+            const unsigned long long a = __shfl_xor_sync(0xffffffffu, lo, off), b = __shfl_xor_sync(0xffffffffu, hi, off);
+            lo = a < lo ? a : lo;
+            hi = b > hi ? b : hi;
+        }
+        __shared__ unsigned long long wlo[TK_THREADS / 32], whi[TK_THREADS / 32];
+        if ((threadIdx.x & 31) == 0) { wlo[threadIdx.x >> 5] = lo; whi[threadIdx.x >> 5] = hi; }
+        for (uint32_t i = threadIdx.x; i < TK_BUCKETS; i += TK_THREADS) bh[i] = 0;
+        __syncthreads();
+        lo = ~0ull; hi = 0;
+        for (int w = 0; w < TK_THREADS / 32; ++w) {
+            lo = wlo[w] < lo ? wlo[w] : lo;
+            hi = whi[w] > hi ? whi[w] : hi;
+        }
+        const unsigned long long span = hi - lo;
+        const int top = span ? 63 - __clzll(span) : 0;     // highest differing bit of the range
+        const int sh = top >= 12 ? top - 11 : 0;            // (span >> sh) < 4096
+        // pass 2: histogram
+        {
+            uint32_t flat = 0;
+            for (uint32_t p = 0; p < parts; ++p) {
+                for (uint32_t i = threadIdx.x; i < pc[p]; i += TK_THREADS)
+                    atomicAdd(&bh[(uint32_t)((key_at(p, i, flat + i) - lo) >> sh)], 1u);
+                flat += pc[p];
+            }
+        }
+        __syncthreads();
+        // bucket of the kk-th key: per-thread sums of 8 buckets, block scan
+        constexpr uint32_t PER = TK_BUCKETS / TK_THREADS;
+        uint32_t c = 0;
+#pragma unroll
+        for (uint32_t j = 0; j < PER; ++j) c += bh[threadIdx.x * PER + j];
+        uint32_t incl = c;
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
+            if ((threadIdx.x & 31) >= off) incl += o;
+        }
+        __shared__ uint32_t wsum[TK_THREADS / 32];
+        if ((threadIdx.x & 31) == 31) wsum[threadIdx.x >> 5] = incl;
+        __syncthreads();
+        uint32_t wbase = 0;
+        for (uint32_t w = 0; w < (threadIdx.x >> 5); ++w) wbase += wsum[w];
+        incl += wbase;
+        const uint32_t excl = incl - c;
+        if (excl < kk && kk <= incl) {
+            uint32_t cum = excl, b = threadIdx.x * PER;
+            for (uint32_t j = 0; j < PER; ++j) {
+                cum += bh[b + j];
+                if (cum >= kk) { b += j; break; }
+            }
+            k_s = b;      // bucket holding the kk-th key
+            fill_s = cum; // keys in buckets <= b
+        }
+        __syncthreads();
+        const uint32_t nsel = fill_s;
+        if (nsel <= TK_SEL_KEYS) {
+            // pass 3: gather buckets <= b, sort, emit
+            const uint32_t bsel = k_s;
+            __syncthreads();
+            if (threadIdx.x == 0) fill_s = 0;
+            __syncthreads();
+            uint32_t flat = 0;
+            for (uint32_t p = 0; p < parts; ++p) {
+                for (uint32_t i = threadIdx.x; i < pc[p]; i += TK_THREADS) {
+                    const unsigned long long v = key_at(p, i, flat + i);
+                    if (((v - lo) >> sh) <= bsel) sel[atomicAdd(&fill_s, 1u)] = v;
+                }
+                flat += pc[p];
+            }
+            __syncthreads();
+            const uint32_t n = fill_s;
+            uint32_t P = 1;
+            while (P < n) P <<= 1;
+            for (uint32_t i = n + threadIdx.x; i < P; i += TK_THREADS) sel[i] = KEY_INF;
+            __syncthreads();
+            bitonic_sort(sel, P);
+            for (uint32_t r = threadIdx.x; r < k; r += TK_THREADS) out[r] = r < kk ? sel[r] : KEY_INF;
+            if (threadIdx.x == 0) out_counts[q] = kk;
+            return;
+        }
+        __syncthreads();
+    }
+    if (in_smem) {
+        uint32_t P = 1;
+        while (P < total) P <<= 1;
         for (uint32_t i = total + threadIdx.x; i < P; i += TK_THREADS) sk[i] = KEY_INF;
         __syncthreads();
         bitonic_sort(sk, P);
@@ -132,7 +244,7 @@ void launch_topk(const unsigned long long* cand, const uint32_t* ccount, uint32_
                  uint64_t part_stride, uint64_t count_stride, uint32_t nq, uint32_t k, unsigned long long* out_keys,
                  uint32_t* out_counts, cudaStream_t s) {
     if (nq == 0 || k == 0) return;
-    const size_t smem = TK_SMEM_KEYS * sizeof(unsigned long long);
+    const size_t smem = (TK_SMEM_KEYS + TK_SEL_KEYS) * sizeof(unsigned long long) + TK_BUCKETS * sizeof(uint32_t);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

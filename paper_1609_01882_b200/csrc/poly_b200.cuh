@@ -25,6 +25,12 @@ constexpr int DSUB = 16;               // every configuration: 128/8 and 256/16
 #ifndef POLY_WARM_LEVELS  // at most this many geometric warm-up samples before the full scan
 #define POLY_WARM_LEVELS 2
 #endif
+#ifndef POLY_WARM_FIRST  // tiles in the first warm-up sample (x8 per further level)
+#define POLY_WARM_FIRST 16
+#endif
+#ifndef POLY_WARM_SEL
+#define POLY_WARM_SEL 0
+#endif
 #ifndef POLY_TILE_BYTES
 #define POLY_TILE_BYTES 12288
 #endif

@@ -311,3 +311,42 @@ def test_sharded_search_over_nccl_world1(pb, pq8, big8):
         assert torch.equal(out[:len(queries)], keys)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("parts,k,dist", [(1, 100, "spread"), (4, 1024, "narrow"), (6, 1000, "spread"),
+                                          (64, 2048, "narrow"), (40, 500, "ties"), (3, 2048, "ties")])
+def test_topk_select_paths(pb, pq8, parts, k, dist):
+    """K3 through the merge entry point: direct sort (<= 2048 keys), bucket select from
+    shared memory (<= 8192) or L2 (more), and the fallbacks when the k-th bucket is dense
+    (many equal scores). Exact (score, id) order against numpy."""
+    import torch
+    rng = np.random.default_rng(parts * 7919 + k)
+    nq = 5
+    ix = _index(pb, pq8)
+    if dist == "spread":
+        sc = rng.uniform(0.0, 1e6, (parts, nq, k)).astype(np.float32)
+    elif dist == "narrow":
+        sc = rng.uniform(1000.0, 1001.0, (parts, nq, k)).astype(np.float32)
+    else:
+        sc = np.where(rng.random((parts, nq, k)) < 0.9, np.float32(7.5),
+                      rng.uniform(7.0, 8.0, (parts, nq, k))).astype(np.float32)
+    ranks = np.stack([rng.permutation(10_000_000)[:parts * k] for _ in range(nq)], 1)  # distinct per query
+    ranks = ranks.reshape(parts, k, nq).transpose(0, 2, 1).astype(np.uint64)
+    counts = rng.integers(k // 2, k + 1, (parts, nq)).astype(np.uint32)
+    keys = (sc.view(np.uint32).astype(np.uint64) << np.uint64(32)) | ranks
+    for p in range(parts):
+        for q in range(nq):
+            keys[p, q, counts[p, q]:] = np.uint64(0xFFFFFFFFFFFFFFFF)  # beyond the count: never read
+    dk = torch.from_numpy(keys.reshape(-1).view(np.int64)).cuda()
+    dc = torch.from_numpy(counts.reshape(-1).view(np.int32)).cuda()
+    ids = torch.empty((nq, k), dtype=torch.int64, device="cuda")
+    scs = torch.empty((nq, k), dtype=torch.float32, device="cuda")
+    cnt = torch.empty(nq, dtype=torch.int32, device="cuda")
+    ix.merge_keys_device(dk, dc, parts, nq, k, ids, scs, cnt)
+    torch.cuda.synchronize()
+    for q in range(nq):
+        allk = np.concatenate([keys[p, q, :counts[p, q]] for p in range(parts)])
+        want = np.sort(allk)[:k]
+        assert int(cnt[q]) == min(k, allk.size)
+        assert np.array_equal(ids[q].cpu().numpy()[:want.size], (want & np.uint64(0xFFFFFFFF)).astype(np.int64))
+        assert np.array_equal(_bits(scs[q].cpu().numpy()[:want.size]), (want >> np.uint64(32)).astype(np.uint32))
