@@ -225,12 +225,16 @@ void run_batches(poly_b200_index* ix, const float* d_queries, uint64_t nq, const
             a.id32 = ix->idm.d_id32;
             a.thr = ix->thr;
             a.ngroups = (nqb + Q - 1) / Q;
-            // Warm-up: strided samples of 16, 128, 1024, ... tiles spread over the
-            // database, each scanned with the threshold seeded by the exact k-th
-            // key (K3) of the previous sample.  thr[] then admits about
-            // k * N / sample candidates in the full scan, so its in-scan selects
-            // are rare.  The samples are re-scanned by the full scan (their keys
-            // must be in its list); cost ~ 2% of the scan at N = 1e8.
+            // Seed: one CTA per query ranks a fixed 256-code-run sample (K2s); then
+            // the geometric warm-up levels below start from that bound.
+            if (POLY_SEED_BLOCKS > 0 && ix->n > ix->cand_cap / 8)
+                pb::launch_seed_sample(a, strategy, ix->m, nqb,
+                                       (uint32_t)std::min<uint64_t>(POLY_SEED_BLOCKS, (ix->n + 255) / 256), s);
+            // Warm-up: strided samples of POLY_WARM_FIRST tiles (x8 per further level,
+            // POLY_WARM_LEVELS levels) spread over the database, each scanned with the
+            // current bound and ranked exactly (K3) to tighten it.  With the K2s seed and
+            // 512-slot in-scan selects one 128-tile level is enough (A/B in DESIGN.md).
+            // The samples are re-scanned by the full scan (their keys must be in its list).
             int level = 0;
             for (uint64_t wt = POLY_WARM_FIRST; ntiles >= 8 * wt && ix->n > ix->cand_cap / 8 && level < POLY_WARM_LEVELS;
                  wt *= 8, ++level) {

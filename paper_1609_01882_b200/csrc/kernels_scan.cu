@@ -716,6 +716,126 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
     }
 }
 
+// K2s: threshold seed from a fixed sample, one CTA per query.  The sample is
+// SEED_BLOCKS runs of 256 consecutive codes spread evenly over the database
+// (coalesced loads; the same runs for every query, so they stay in L2).  Each
+// sampled code is scored exactly as K2 does (filter, then ADC / Hamming /
+// disidx); the k-th smallest key of the sample (8-pass radix select over the
+// keys staged in shared memory) bounds the final k-th key, so
+// thr[q] = min(thr[q], kth + 1).  A key buffer that fills up keeps the first
+// SEED_KEYS keys: the k-th of a subset is a weaker but still valid bound.
+constexpr uint32_t SEED_THREADS = 256, SEED_KEYS = 4096;
+
+template <int M, int STRAT>
+__global__ void __launch_bounds__(SEED_THREADS) seed_sample_kernel(const ScanArgs a, uint32_t seed_blocks) {
+    using C = typename CodeT<M>::T;
+    extern __shared__ __align__(16) uint8_t sm[];
+    float* lut = reinterpret_cast<float*>(sm);
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(sm + M * KSUB * 4);
+    __shared__ uint32_t cnt, hist[256];
+    __shared__ unsigned long long prefix_s;
+    __shared__ uint32_t want_s;
+    const uint32_t q = blockIdx.x;
+    constexpr bool USE_LUT = (STRAT == DUAL || STRAT == ADC);
+    if (USE_LUT)
+        for (uint32_t i = threadIdx.x; i < (uint32_t)M * KSUB; i += SEED_THREADS)
+            lut[i] = __ldg(a.lutp + (size_t)q * M * KSUB + i);
+    const C qc = reinterpret_cast<const C*>(a.qcodes)[q];
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    for (uint32_t b = 0; b < seed_blocks; ++b) {
+        const uint64_t pos = (uint64_t)b * a.n / seed_blocks + threadIdx.x;
+        if (pos >= a.n) continue;
+        const C code = __ldg(reinterpret_cast<const C*>(a.codes) + pos);
+        float score;
+        if constexpr (STRAT == DUAL) {
+            if (ham(code, qc) > a.tau) continue;
+            score = adc<M>(lut, code);
+        } else if constexpr (STRAT == ADC) {
+            score = adc<M>(lut, code);
+        } else if constexpr (STRAT == BINARY) {
+            score = (float)ham(code, qc);
+        } else {
+            score = (float)disidx(code, qc);
+        }
+        const uint32_t slot = atomicAdd(&cnt, 1u);
+        if (slot < SEED_KEYS)
+            keys[slot] = ((unsigned long long)__float_as_uint(score) << 32) | key_low(a, (uint32_t)pos);
+    }
+    __syncthreads();
+    const uint32_t n = min(cnt, SEED_KEYS);
+    if (n < a.k) return;  // too few keys in the sample: no bound
+    unsigned long long prefix = 0, mask = 0;
+    uint32_t want = a.k;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+        hist[threadIdx.x] = 0;
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < n; i += SEED_THREADS) {
+            const unsigned long long v = keys[i];
+            if ((v & mask) == prefix) atomicAdd(&hist[(v >> shift) & 0xFFu], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            const uint32_t lane = threadIdx.x;
+            uint32_t c[8], t = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) { c[j] = hist[lane * 8 + j]; t += c[j]; }
+            uint32_t incl = t;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= off) incl += o;
+            }
+            const uint32_t excl = incl - t;
+            if (excl < want && want <= incl) {
+                uint32_t r = want - excl;
+                int digit = lane * 8 + 7;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (r <= c[j]) { digit = lane * 8 + j; break; }
+                    r -= c[j];
+                }
+                prefix_s = prefix | ((unsigned long long)digit << shift);
+                want_s = r;
+            }
+        }
+        __syncthreads();
+        prefix = prefix_s;
+        want = want_s;
+        mask |= 0xFFull << shift;
+    }
+    if (threadIdx.x == 0 && prefix + 1 < a.thr[q]) a.thr[q] = prefix + 1;  // prefix = the k-th key
+}
+
+template <int M, int STRAT>
+static void launch_seed_m(const ScanArgs& a, uint32_t nq, uint32_t seed_blocks, cudaStream_t s) {
+    const size_t smem = (size_t)M * KSUB * 4 + SEED_KEYS * 8;
+    auto kfn = seed_sample_kernel<M, STRAT>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    kfn<<<nq, SEED_THREADS, smem, s>>>(a, seed_blocks);
+    count_launch();
+}
+
+void launch_seed_sample(const ScanArgs& a, int strategy, uint32_t m, uint32_t nq, uint32_t seed_blocks,
+                        cudaStream_t s) {
+    if (nq == 0 || seed_blocks == 0) return;
+    const bool w = m == 16;
+    switch (strategy) {
+        case DUAL: w ? launch_seed_m<16, DUAL>(a, nq, seed_blocks, s) : launch_seed_m<8, DUAL>(a, nq, seed_blocks, s); break;
+        case ADC: w ? launch_seed_m<16, ADC>(a, nq, seed_blocks, s) : launch_seed_m<8, ADC>(a, nq, seed_blocks, s); break;
+        case BINARY:
+            w ? launch_seed_m<16, BINARY>(a, nq, seed_blocks, s) : launch_seed_m<8, BINARY>(a, nq, seed_blocks, s);
+            break;
+        default:
+            w ? launch_seed_m<16, DISIDX>(a, nq, seed_blocks, s) : launch_seed_m<8, DISIDX>(a, nq, seed_blocks, s);
+            break;
+    }
+}
+
 template <int M, int Q, int W, int STRAT, bool PERQ>
 static void launch_one(const ScanArgs& a, int num_sms, cudaStream_t s) {
     using SM = ScanSmem<M, Q, W>;

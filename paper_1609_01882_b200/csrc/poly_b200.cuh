@@ -23,13 +23,16 @@ constexpr int DSUB = 16;               // every configuration: 128/8 and 256/16
 #define POLY_SEL_KF 4
 #endif
 #ifndef POLY_WARM_LEVELS  // at most this many geometric warm-up samples before the full scan
-#define POLY_WARM_LEVELS 2
+#define POLY_WARM_LEVELS 1
 #endif
 #ifndef POLY_WARM_FIRST  // tiles in the first warm-up sample (x8 per further level)
-#define POLY_WARM_FIRST 16
+#define POLY_WARM_FIRST 128
 #endif
 #ifndef POLY_WARM_SEL
 #define POLY_WARM_SEL 0
+#endif
+#ifndef POLY_SEED_BLOCKS  // K2s seed sample: runs of 256 codes (0 = no seed kernel)
+#define POLY_SEED_BLOCKS 64
 #endif
 #ifndef POLY_TILE_BYTES
 #define POLY_TILE_BYTES 12288
@@ -234,6 +237,8 @@ void launch_gen_points(uint64_t seed, uint32_t stream_id, uint64_t row0, uint64_
 // K2: fused filter + ADC + candidate scan.
 void launch_scan(const ScanArgs& a, int strategy, uint32_t m, bool per_query_stats, int num_sms, cudaStream_t s);
 int scan_queries_per_cta(uint32_t m);
+// K2s: thr[q] = min(thr[q], k-th key of a fixed sample + 1); one CTA per query
+void launch_seed_sample(const ScanArgs& a, int strategy, uint32_t m, uint32_t nq, uint32_t seed_blocks, cudaStream_t s);
 
 // K3: per-query exact top-k over candidate keys; K3b: key -> (id, score).
 // cand part p, query q: cand + p * part_stride + q * cap, count ccount[p * count_stride + q].
