@@ -46,7 +46,7 @@ def build(verbose: bool = False) -> str:
                 sys.stderr.write(r.stderr)
     if _stale(LIB, objs):
         subprocess.run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", LIB,
-                        "-lcudart"], check=True)
+                        "-lcudart", "-lcublas"], check=True)
     return LIB
 
 

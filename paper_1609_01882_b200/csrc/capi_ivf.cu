@@ -12,6 +12,7 @@
 
 #include "../../include/poly_b200.h"
 #include "host_common.h"
+#include <cublas_v2.h>
 #include "poly_b200.cuh"
 
 using namespace pbh;
@@ -78,6 +79,11 @@ struct poly_b200_ivf {
     uint32_t* knn_cnt = nullptr;
     uint64_t knn_rows = 0;
     uint32_t knn_k1 = 0;
+
+    // K5r (TF32 dots + exact re-rank): centroid norms, an upper bound of |c|, cuBLAS handle
+    float* d_cnorm = nullptr;
+    float cmax = 0.0f;
+    cublasHandle_t cublas = nullptr;
 
     cudaStream_t stream = nullptr;
     std::mutex mu;
@@ -210,7 +216,25 @@ void validate(const poly_b200_ivf* iv, const poly_b200_ivf_params* p) {
 // np <= 64: fused distance + per-slice selection (K5s), slices merged by K3;
 // larger np: all keys (K5), then K3 over nlist keys per query.
 void enumerate_cells(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, uint32_t np, cudaStream_t s) {
-    if (np <= 64) {
+    if (POLY_COARSE_GEMM && np <= 1024) {
+        // K5r: TF32 tensor-core dots (cuBLAS: a plain GEMM), then the exact re-rank kernel
+        if (!iv->cublas) {
+            require(cublasCreate(&iv->cublas) == CUBLAS_STATUS_SUCCESS, POLY_B200_INTERNAL, "cublasCreate failed");
+            require(cublasSetMathMode(iv->cublas, CUBLAS_TF32_TENSOR_OP_MATH) == CUBLAS_STATUS_SUCCESS,
+                    POLY_B200_INTERNAL, "cublasSetMathMode failed");
+        }
+        require(cublasSetStream(iv->cublas, s) == CUBLAS_STATUS_SUCCESS, POLY_B200_INTERNAL, "cublasSetStream failed");
+        float* dots = reinterpret_cast<float*>(iv->ckeys);                        // IVF_NQB x nlist
+        uint32_t* scratch = reinterpret_cast<uint32_t*>(iv->ckeys) + (size_t)IVF_NQB * iv->nlist;
+        const float one = 1.0f, zero = 0.0f;
+        // column-major: dots (nlist x nqb) = coarse^T (nlist x dim) . q^T (dim x nqb)
+        require(cublasSgemm(iv->cublas, CUBLAS_OP_T, CUBLAS_OP_N, (int)iv->nlist, (int)nqb, (int)iv->dim, &one,
+                            iv->d_coarse, (int)iv->dim, d_q, (int)iv->dim, &zero, dots, (int)iv->nlist) ==
+                    CUBLAS_STATUS_SUCCESS,
+                POLY_B200_INTERNAL, "cublasSgemm failed");
+        pb::launch_coarse_refine(d_q, nqb, iv->dim, dots, iv->d_cnorm, iv->cmax, iv->d_coarse, iv->nlist, np, scratch,
+                                 iv->probe_keys, iv->probe_counts, s);
+    } else if (np <= 64) {
         const uint32_t qtiles = (nqb + 63) / 64;
         uint32_t slices = std::max<uint32_t>(1, std::min<uint32_t>(64, 2u * iv->num_sms / qtiles));
         slices = std::min<uint32_t>(slices, std::max<uint32_t>(1, iv->nlist / 64));
@@ -378,6 +402,21 @@ int poly_b200_ivf_create(const poly_b200_pq_desc* pq, const float* coarse, uint3
             CK(cudaMemcpy(iv->d_perms, iv->h_perms.data(), iv->h_perms.size() * 2, cudaMemcpyHostToDevice));
             CK(cudaMemcpy(iv->d_coarse, iv->h_coarse.data(), iv->h_coarse.size() * 4, cudaMemcpyHostToDevice));
             CK(cudaMemset(iv->d_off, 0, (nlist + 1) * 8));
+            // |c|^2 per cell (approximate is fine: K5r's error bound covers it) and cmax >= max |c|
+            std::vector<float> cn(nlist);
+            double cm = 0.0;
+            for (uint32_t c = 0; c < nlist; ++c) {
+                double acc = 0.0;
+                for (size_t d = 0; d < pq->dim; ++d) {
+                    const double v = iv->h_coarse[(size_t)c * pq->dim + d];
+                    acc += v * v;
+                }
+                cn[c] = (float)acc;
+                cm = std::max(cm, acc);
+            }
+            iv->cmax = (float)(std::sqrt(cm) * (1.0 + 1e-5)) + 1e-30f;
+            iv->d_cnorm = dalloc<float>(nlist);
+            CK(cudaMemcpy(iv->d_cnorm, cn.data(), nlist * 4, cudaMemcpyHostToDevice));
         } catch (...) {
             poly_b200_ivf_destroy(iv);
             throw;
@@ -399,8 +438,9 @@ int poly_b200_ivf_destroy(poly_b200_ivf* iv) {
                             (void*)iv->cand, (void*)iv->ctrl, (void*)iv->thr, (void*)iv->keys, (void*)iv->kcounts,
                             (void*)iv->surv_total, (void*)iv->scan_total, (void*)iv->sticky_overflow, (void*)iv->d_q,
                             (void*)iv->d_oid, (void*)iv->d_osc, (void*)iv->d_ocnt,
-                            (void*)iv->knn_ids, (void*)iv->knn_sc, (void*)iv->knn_cnt})
+                            (void*)iv->knn_ids, (void*)iv->knn_sc, (void*)iv->knn_cnt, (void*)iv->d_cnorm})
                 dfree(p);
+            if (iv->cublas) cublasDestroy(iv->cublas);
             iv->idm.release();
             if (iv->stream) cudaStreamDestroy(iv->stream);
         }

@@ -211,55 +211,223 @@ void launch_coarse_select(const float* q, uint32_t nq, uint32_t dim, const float
     count_launch();
 }
 
+// ------------------------------------------------------------------ K5r
+// enumerate_cells with the tensor cores, still exact (the coarse-centroid GEMM the
+// north star allows "only if the result stays within tolerance" -- here it stays
+// exact).  A TF32 GEMM (cuBLAS, host side) gives dots[c] ~ q.c; the approximate
+// distance a(c) = |q|^2 + |c|^2 - 2 dots[c] is within E of the reference's fp32
+// sq_l2(q, c) for every cell, with
+//   E = 4.1e-3 |q| cmax + 4e-5 (|q|^2 + cmax^2 + 2 |q| cmax) + 1e-6
+// (TF32 inputs truncated to 10 mantissa bits: product error <= 2^-9; fp32
+// accumulation and the reference's own rounding add <= 2e-5 relative; x1.5 slack).
+// With T an upper bound of the np-th smallest a(c), every cell of the exact top-np
+// has a(c) <= T + 2E; those cells get the exact sq_l2 (fp32, dim order, as K5) and
+// the (dist bits << 32 | cell) keys of the np smallest are emitted in order.
+// One CTA (512 threads) per query; T from a 4096-bucket histogram over [min, max]
+// of a(c); candidates go through a global scratch list in chunks of KR_CHUNK.
+constexpr int KR_THREADS = 512, KR_BUCKETS = 4096, KR_CHUNK = 2048, KR_NPMAX = 1024, KR_BUF = 4096;  // np + chunk <= buf (pow2)
+
+__global__ void __launch_bounds__(KR_THREADS) coarse_refine_kernel(const float* __restrict__ q, uint32_t dim,
+                                                                   const float* __restrict__ dots,
+                                                                   const float* __restrict__ cnorm, float cmax,
+                                                                   const float* __restrict__ cent, uint32_t nlist,
+                                                                   uint32_t np, uint32_t* __restrict__ scratch,
+                                                                   unsigned long long* __restrict__ probe_keys,
+                                                                   uint32_t* __restrict__ probe_counts) {
+    extern __shared__ __align__(16) uint8_t kr_smem[];
+    unsigned long long* buf = reinterpret_cast<unsigned long long*>(kr_smem);  // KR_BUF keys
+    uint32_t* hist = reinterpret_cast<uint32_t*>(buf + KR_BUF);                 // KR_BUCKETS
+    float* qs = reinterpret_cast<float*>(hist + KR_BUCKETS);                    // dim
+    __shared__ float red_f[2][KR_THREADS / 32];
+    __shared__ uint32_t red_u[KR_THREADS / 32];
+    __shared__ uint32_t ncand_s, bsel_s;
+    const uint32_t qi = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const float* qrow = q + (size_t)qi * dim;
+    const float* drow = dots + (size_t)qi * nlist;
+    uint32_t* cand = scratch + (size_t)qi * nlist;
+    // |q|^2 and the range of a(c)
+    float qn = 0.0f;
+    for (uint32_t d = tid; d < dim; d += KR_THREADS) {
+        const float v = qrow[d];
+        qs[d] = v;
+        qn += v * v;
+    }
+    for (int off = 16; off; off >>= 1) qn += __shfl_xor_sync(0xffffffffu, qn, off);
+    if (lane == 0) red_f[0][warp] = qn;
+    __syncthreads();
+    qn = 0.0f;
+    for (int w = 0; w < KR_THREADS / 32; ++w) qn += red_f[0][w];
+    __syncthreads();
+    float mn = INFINITY, mx = -INFINITY;
+    for (uint32_t c = tid; c < nlist; c += KR_THREADS) {
+        const float a = qn + cnorm[c] - 2.0f * drow[c];
+        mn = fminf(mn, a);
+        mx = fmaxf(mx, a);
+    }
+    for (int off = 16; off; off >>= 1) {
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    }
+    if (lane == 0) { red_f[0][warp] = mn; red_f[1][warp] = mx; }
+    for (uint32_t i = tid; i < KR_BUCKETS; i += KR_THREADS) hist[i] = 0;
+    if (tid == 0) ncand_s = 0;
+    __syncthreads();
+    mn = INFINITY; mx = -INFINITY;
+    for (int w = 0; w < KR_THREADS / 32; ++w) { mn = fminf(mn, red_f[0][w]); mx = fmaxf(mx, red_f[1][w]); }
+    const float scale = mx > mn ? (float)(KR_BUCKETS - 1) / (mx - mn) : 0.0f;
+    for (uint32_t c = tid; c < nlist; c += KR_THREADS) {
+        const float a = qn + cnorm[c] - 2.0f * drow[c];
+        atomicAdd(&hist[min((uint32_t)((a - mn) * scale), (uint32_t)KR_BUCKETS - 1)], 1u);
+    }
+    __syncthreads();
+    // bucket holding the np-th smallest a(c): per-thread sums of 8 buckets, block scan
+    constexpr uint32_t PER = KR_BUCKETS / KR_THREADS;
+    uint32_t cs = 0;
+#pragma unroll
+    for (uint32_t j = 0; j < PER; ++j) cs += hist[tid * PER + j];
+    uint32_t incl = cs;
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= (uint32_t)off) incl += o;
+    }
+    if (lane == 31) red_u[warp] = incl;
+    __syncthreads();
+    for (uint32_t w = 0; w < warp; ++w) incl += red_u[w];
+    const uint32_t excl = incl - cs;
+    if (excl < np && np <= incl) {
+        uint32_t cum = excl, b = tid * PER;
+        for (uint32_t j = 0; j < PER; ++j) {
+            cum += hist[tid * PER + j];
+            if (cum >= np) { b = tid * PER + j; break; }
+        }
+        bsel_s = b;
+    }
+    __syncthreads();
+    // T >= the np-th smallest a(c) (bucket upper edge, rounding slack); candidate bound T + 2E
+    const float T = scale > 0.0f ? mn + (float)(bsel_s + 1) / scale * (1.0f + 1e-5f) + 1e-30f : mx;
+    const float qnorm = sqrtf(qn);
+    const float E = 4.1e-3f * qnorm * cmax + 4e-5f * (qn + cmax * cmax + 2.0f * qnorm * cmax) + 1e-6f;
+    const float bound = T + 2.0f * E;
+    for (uint32_t c = tid; c < nlist; c += KR_THREADS) {
+        const float a = qn + cnorm[c] - 2.0f * drow[c];
+        if (a <= bound) cand[atomicAdd(&ncand_s, 1u)] = c;
+    }
+    __syncthreads();
+    const uint32_t ncand = ncand_s;
+    // exact sq_l2 of the candidates, chunk by chunk, merged into the running top-np
+    uint32_t ntop = 0;
+    for (uint32_t c0 = 0; c0 < ncand; c0 += KR_CHUNK) {
+        const uint32_t cn = min((uint32_t)KR_CHUNK, ncand - c0);
+        for (uint32_t i = tid; i < cn; i += KR_THREADS) {
+            const uint32_t cell = cand[c0 + i];
+            const float* crow = cent + (size_t)cell * dim;
+            float acc = 0.0f;
+            for (uint32_t d = 0; d < dim; ++d) {
+                const float t = __fsub_rn(qs[d], __ldg(crow + d));
+                acc = __fadd_rn(acc, __fmul_rn(t, t));
+            }
+            buf[ntop + i] = ((unsigned long long)__float_as_uint(acc) << 32) | cell;
+        }
+        const uint32_t n = ntop + cn;
+        uint32_t P = 1;
+        while (P < n) P <<= 1;
+        for (uint32_t i = n + tid; i < P; i += KR_THREADS) buf[i] = ~0ull;
+        __syncthreads();
+        for (uint32_t size = 2; size <= P; size <<= 1)
+            for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+                for (uint32_t i = tid; i < P / 2; i += KR_THREADS) {
+                    const uint32_t pos = 2 * i - (i & (stride - 1));
+                    const bool asc = (pos & size) == 0;
+                    const unsigned long long x = buf[pos], y = buf[pos + stride];
+                    if ((x > y) == asc) { buf[pos] = y; buf[pos + stride] = x; }
+                }
+                __syncthreads();
+            }
+        ntop = min(n, np);
+    }
+    for (uint32_t i = tid; i < np; i += KR_THREADS) probe_keys[(size_t)qi * np + i] = i < ntop ? buf[i] : ~0ull;
+    if (tid == 0) probe_counts[qi] = ntop;
+}
+
+void launch_coarse_refine(const float* q, uint32_t nq, uint32_t dim, const float* dots, const float* cnorm, float cmax,
+                          const float* cent, uint32_t nlist, uint32_t np, uint32_t* scratch,
+                          unsigned long long* probe_keys, uint32_t* probe_counts, cudaStream_t s) {
+    if (nq == 0) return;
+    const size_t smem = (size_t)KR_BUF * 8 + KR_BUCKETS * 4 + (size_t)dim * 4;
+    static size_t attr = 0;
+    if (attr < smem) {
+        cudaFuncSetAttribute(coarse_refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = smem;
+    }
+    coarse_refine_kernel<<<nq, KR_THREADS, smem, s>>>(q, dim, dots, cnorm, cmax, cent, nlist, np, scratch, probe_keys,
+                                                      probe_counts);
+    count_launch();
+}
+
 // ------------------------------------------------------------------ K1r
-// grid (nq * nprobe): item (q, p) -> residual LUT (stored-field indexed) + code,
-// all m sub-quantizers per CTA; thread j owns centroid j.
+// items (q, p) -> residual LUT (stored-field indexed) + code, all m sub-quantizers.
+// One CTA per K1R_ITEMS consecutive items: thread j owns centroid j and loads its
+// codebook row once per sub-quantizer for all the CTA's items (the 8 KB-per-sq
+// codebook is the L2 traffic; the items share it).
+constexpr uint32_t K1R_ITEMS = 8;
+
 __global__ void __launch_bounds__(256) residual_lut_kernel(const float* __restrict__ queries, uint32_t dim, uint32_t m,
                                                            const unsigned long long* __restrict__ probe_keys,
-                                                           uint32_t nprobe, const float* __restrict__ cent,
+                                                           uint32_t nprobe, uint32_t nitems,
+                                                           const float* __restrict__ cent,
                                                            const float* __restrict__ codebooks,
                                                            const uint16_t* __restrict__ perms, float* __restrict__ lutp,
                                                            uint8_t* __restrict__ qcodes) {
-    const uint32_t item = blockIdx.x, j = threadIdx.x;
-    const uint32_t qi = item / nprobe;
-    const uint32_t cell = (uint32_t)probe_keys[item];
-    __shared__ float r[256];
-    __shared__ float wv[16][8];
-    __shared__ uint32_t wj[16][8];
-    for (uint32_t d = j; d < dim; d += 256)
-        r[d] = __fsub_rn(queries[(size_t)qi * dim + d], cent[(size_t)cell * dim + d]);  // r = q - c
+    const uint32_t item0 = blockIdx.x * K1R_ITEMS, j = threadIdx.x;
+    const uint32_t ni = min(K1R_ITEMS, nitems - item0);
+    __shared__ float r[K1R_ITEMS][256];
+    __shared__ float wv[K1R_ITEMS][16][8];
+    __shared__ uint32_t wj[K1R_ITEMS][16][8];
+    for (uint32_t e = j; e < ni * dim; e += 256) {
+        const uint32_t it = e / dim, d = e % dim, item = item0 + it;
+        const uint32_t qi = item / nprobe, cell = (uint32_t)probe_keys[item];
+        r[it][d] = __fsub_rn(queries[(size_t)qi * dim + d], cent[(size_t)cell * dim + d]);  // r = q - c
+    }
     __syncthreads();
     for (uint32_t sq = 0; sq < m; ++sq) {
         const float4* c = reinterpret_cast<const float4*>(codebooks + ((size_t)sq * KSUB + j) * DSUB);
-        const float* sub = r + sq * DSUB;
-        float acc = 0.0f;
+        float cb[DSUB];
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
             const float4 cc = __ldg(c + v);
-            float t;
-            t = __fsub_rn(sub[4 * v + 0], cc.x); acc = __fadd_rn(acc, __fmul_rn(t, t));
-            t = __fsub_rn(sub[4 * v + 1], cc.y); acc = __fadd_rn(acc, __fmul_rn(t, t));
-            t = __fsub_rn(sub[4 * v + 2], cc.z); acc = __fadd_rn(acc, __fmul_rn(t, t));
-            t = __fsub_rn(sub[4 * v + 3], cc.w); acc = __fadd_rn(acc, __fmul_rn(t, t));
+            cb[4 * v + 0] = cc.x; cb[4 * v + 1] = cc.y; cb[4 * v + 2] = cc.z; cb[4 * v + 3] = cc.w;
         }
-        lutp[((size_t)item * m + sq) * KSUB + perms[sq * KSUB + j]] = acc;
-        float bv = acc;
-        uint32_t bj = j;
+        const uint32_t dst = perms[sq * KSUB + j];
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            const float ov = __shfl_down_sync(0xffffffffu, bv, off);
-            const uint32_t oj = __shfl_down_sync(0xffffffffu, bj, off);
-            if (ov < bv || (ov == bv && oj < bj)) { bv = ov; bj = oj; }
+        for (uint32_t it = 0; it < K1R_ITEMS; ++it) {
+            if (it >= ni) break;
+            const float* sub = &r[it][sq * DSUB];
+            float acc = 0.0f;
+#pragma unroll
+            for (int d = 0; d < DSUB; ++d) {
+                const float t = __fsub_rn(sub[d], cb[d]);
+                acc = __fadd_rn(acc, __fmul_rn(t, t));
+            }
+            lutp[((size_t)(item0 + it) * m + sq) * KSUB + dst] = acc;
+            float bv = acc;
+            uint32_t bj = j;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const float ov = __shfl_down_sync(0xffffffffu, bv, off);
+                const uint32_t oj = __shfl_down_sync(0xffffffffu, bj, off);
+                if (ov < bv || (ov == bv && oj < bj)) { bv = ov; bj = oj; }
+            }
+            if ((j & 31) == 0) { wv[it][sq][j >> 5] = bv; wj[it][sq][j >> 5] = bj; }
         }
-        if ((j & 31) == 0) { wv[sq][j >> 5] = bv; wj[sq][j >> 5] = bj; }
     }
     __syncthreads();
-    if (j < m) {  // argmin per sub-quantizer, ties -> lowest centroid (pq.cpp:38)
-        float bv = wv[j][0];
-        uint32_t bj = wj[j][0];
+    if (j < ni * m) {  // argmin per (item, sub-quantizer), ties -> lowest centroid (pq.cpp:38)
+        const uint32_t it = j / m, sq = j % m;
+        float bv = wv[it][sq][0];
+        uint32_t bj = wj[it][sq][0];
         for (int w = 1; w < 8; ++w)
-            if (wv[j][w] < bv || (wv[j][w] == bv && wj[j][w] < bj)) { bv = wv[j][w]; bj = wj[j][w]; }
-        qcodes[(size_t)item * m + j] = static_cast<uint8_t>(perms[j * KSUB + bj]);
+            if (wv[it][sq][w] < bv || (wv[it][sq][w] == bv && wj[it][sq][w] < bj)) { bv = wv[it][sq][w]; bj = wj[it][sq][w]; }
+        qcodes[(size_t)(item0 + it) * m + sq] = static_cast<uint8_t>(perms[sq * KSUB + bj]);
     }
 }
 
@@ -267,8 +435,10 @@ void launch_residual_lut(const float* queries, uint32_t nq, uint32_t dim, uint32
                          const unsigned long long* probe_keys, uint32_t nprobe, const float* cent,
                          const float* codebooks, const uint16_t* perms, float* lutp, uint8_t* qcodes, cudaStream_t s) {
     if (nq == 0) return;
-    residual_lut_kernel<<<nq * nprobe, 256, 0, s>>>(queries, dim, m, probe_keys, nprobe, cent, codebooks, perms, lutp,
-                                                    qcodes);
+    const uint32_t nitems = nq * nprobe;
+    residual_lut_kernel<<<(nitems + K1R_ITEMS - 1) / K1R_ITEMS, 256, 0, s>>>(queries, dim, m, probe_keys, nprobe,
+                                                                             nitems, cent, codebooks, perms, lutp,
+                                                                             qcodes);
     count_launch();
 }
 
@@ -278,23 +448,45 @@ void launch_residual_lut(const float* queries, uint32_t nq, uint32_t dim, uint32
 __global__ void ivf_probe_count_kernel(const unsigned long long* __restrict__ probe_keys, uint32_t nq,
                                        uint32_t nprobe, const uint64_t* __restrict__ off, uint64_t cap,
                                        uint32_t* __restrict__ np_eff, unsigned long long* __restrict__ scanned) {
-    const uint32_t qi = blockIdx.x * blockDim.x + threadIdx.x;
+    // one warp per query: list sizes in parallel, running prefix over the probes in order;
+    // probe p is visited iff no cap or the codes before it are < cap
+    const uint32_t qi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (qi >= nq) return;
-    uint64_t ns = 0;
-    uint32_t p = 0;
-    for (; p < nprobe; ++p) {
-        if (cap && ns >= cap) break;
-        const uint32_t cell = (uint32_t)probe_keys[(size_t)qi * nprobe + p];
-        ns += off[cell + 1] - off[cell];
+    uint64_t base = 0;
+    uint32_t ne = nprobe;
+    for (uint32_t p0 = 0; p0 < nprobe; p0 += 32) {
+        const uint32_t p = p0 + lane;
+        uint64_t sz = 0;
+        if (p < nprobe) {
+            const uint32_t cell = (uint32_t)probe_keys[(size_t)qi * nprobe + p];
+            sz = off[cell + 1] - off[cell];
+        }
+        uint64_t incl = sz;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (uint32_t)o) incl += v;
+        }
+        const uint64_t before = base + incl - sz;  // codes of probes < p
+        const uint32_t stop = __ballot_sync(0xffffffffu, p < nprobe && cap && before >= cap);
+        if (stop) {
+            const uint32_t l = __ffs(stop) - 1;
+            ne = p0 + l;
+            base = __shfl_sync(0xffffffffu, before, l);
+            break;
+        }
+        base += __shfl_sync(0xffffffffu, incl, 31);
     }
-    np_eff[qi] = p;
-    scanned[qi] = ns;
+    if (lane == 0) {
+        np_eff[qi] = ne;
+        scanned[qi] = base;
+    }
 }
 
 void launch_ivf_probe_count(const unsigned long long* probe_keys, uint32_t nq, uint32_t nprobe, const uint64_t* off,
                             uint64_t cap, uint32_t* np_eff, unsigned long long* scanned, cudaStream_t s) {
     if (nq == 0) return;
-    ivf_probe_count_kernel<<<(nq + 127) / 128, 128, 0, s>>>(probe_keys, nq, nprobe, off, cap, np_eff, scanned);
+    ivf_probe_count_kernel<<<(nq * 32 + 127) / 128, 128, 0, s>>>(probe_keys, nq, nprobe, off, cap, np_eff, scanned);
     count_launch();
 }
 

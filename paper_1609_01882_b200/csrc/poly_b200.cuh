@@ -34,6 +34,9 @@ constexpr int DSUB = 16;               // every configuration: 128/8 and 256/16
 #ifndef POLY_SEED_BLOCKS  // K2s seed sample: runs of 256 codes (0 = no seed kernel)
 #define POLY_SEED_BLOCKS 64
 #endif
+#ifndef POLY_COARSE_GEMM  // 1: enumerate_cells via TF32 dots + exact re-rank (K5r)
+#define POLY_COARSE_GEMM 1
+#endif
 #ifndef POLY_TILE_BYTES
 #define POLY_TILE_BYTES 12288
 #endif
@@ -260,6 +263,10 @@ void launch_seed_thr(const unsigned long long* keys, const uint32_t* counts, uin
 // IVF (kernels_ivf.cu)
 void launch_coarse_keys(const float* q, uint32_t nq, uint32_t dim, const float* cent, uint32_t nlist,
                         unsigned long long* keys, cudaStream_t s);
+// K5r: exact enumerate_cells from TF32 dots (dots[q * nlist + c] ~ q.c) + exact re-rank; np <= 1024
+void launch_coarse_refine(const float* q, uint32_t nq, uint32_t dim, const float* dots, const float* cnorm, float cmax,
+                          const float* cent, uint32_t nlist, uint32_t np, uint32_t* scratch,
+                          unsigned long long* probe_keys, uint32_t* probe_counts, cudaStream_t s);
 void launch_coarse_select(const float* q, uint32_t nq, uint32_t dim, const float* cent, uint32_t nlist, uint32_t np,
                           uint32_t slices, unsigned long long* out_keys, uint32_t* out_counts, cudaStream_t s);
 void launch_residual_lut(const float* queries, uint32_t nq, uint32_t dim, uint32_t m,

@@ -10,5 +10,5 @@ for s in capi capi_ivf kernels_encode kernels_scan kernels_topk kernels_ivf; do
   /usr/local/cuda/bin/nvcc $F -c paper_1609_01882_b200/csrc/$s.cu -o $out/$s.o &
 done
 wait
-/usr/local/cuda/bin/nvcc -shared -gencode arch=compute_100a,code=sm_100a $out/*.o -o tools/lib12/$name.so -lcudart
+/usr/local/cuda/bin/nvcc -shared -gencode arch=compute_100a,code=sm_100a $out/*.o -o tools/lib12/$name.so -lcudart -lcublas
 echo tools/lib12/$name.so
