@@ -162,3 +162,25 @@ def test_knn_graph_matches_oracle(pb, gi):
         assert got[:len(row)].tolist() == row, i
         assert int(cnt[i]) == len(row)
         assert (got[len(row):] == -1).all()
+
+
+@pytest.mark.parametrize("dim,nlist", [(128, 8192), (256, 4096)])
+def test_probe_order_many_near_ties(pb, gi, dim, nlist):
+    """enumerate_cells runs TF32 tensor-core dots + an exact re-rank (K5r): probe order
+    must stay bit-exact, also with clustered cells (many near ties), exact duplicate
+    cells (ties -> lower cell) and nprobe up to 1000, against the oracle's exact
+    sq_l2 order."""
+    seed = int(gi["data_seed"])
+    centers = oracle.gen_centers(seed, 200, dim)  # 200 clusters: dozens of near-equidistant cells each
+    coarse = oracle.gen_points(seed, 1, 0, nlist, centers)
+    coarse[nlist // 2: nlist // 2 + 64] = coarse[:64]  # exact duplicates
+    queries = oracle.gen_points(seed, 3, 0, 40, centers)
+    queries[:4] = coarse[[3, 10, 70, nlist // 2 + 5]]  # queries sitting exactly on (duplicated) cells
+    m = dim // 16
+    zz = np.load(os.path.join(os.path.dirname(GOLDEN), "pq_d128_m8.npz" if dim == 128 else "pq_d256_m16.npz"))
+    opq = oracle.PQ(m, 8, dim, zz["codebooks"], zz["perms"])
+    empty = oracle.IVFLists(np.zeros(nlist + 1, np.uint64), np.zeros((0, m), np.uint8), np.zeros(0, np.int64))
+    ix = pb.IVFIndex(pb.ProductQuantizer(m, 8, dim, zz["codebooks"], zz["perms"]), coarse)
+    for nprobe in (1, 16, 100, 1000):
+        want = oracle.ivf_search(opq, coarse, empty, queries, 1, nprobe, threads=16)[5]
+        assert np.array_equal(ix.probes(queries, nprobe), want), nprobe
