@@ -544,7 +544,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
             const uint64_t bdesc0 = bw_desc(smem_u32(bw_s));  // + 32 per K block (512 B >> 4)
             auto stage_a = [&](uint32_t jj) {
                 const uint32_t sq_ = seq + jj, s = sq_ % STAGES;
-                mbar_wait(&full_bar[s], (sq_ / STAGES) & 1u);
+                mbar_wait_backoff(&full_bar[s], (sq_ / STAGES) & 1u);
                 const uint32_t T = tile_base + s * (uint32_t)TILE_BYTES;
                 const uint32_t li = warp * CPW + lane;
                 C c0, c1;
@@ -595,7 +595,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
                         uint32_t m;
                         if constexpr (TCF) {
                             // this tile's MMA was issued when the quad's last warp staged it
-                            mbar_wait(&qbar_s[quad], qphase);
+                            mbar_wait_backoff(&qbar_s[quad], qphase);
                             qphase ^= 1u;
                             tc_fence_after();
                             // sign bits: bit q <- code li, bit 16 + q <- code li + 32

@@ -37,6 +37,9 @@ constexpr int DSUB = 16;               // every configuration: 128/8 and 256/16
 #ifndef POLY_COARSE_GEMM  // 1: enumerate_cells via TF32 dots + exact re-rank (K5r)
 #define POLY_COARSE_GEMM 1
 #endif
+#ifndef POLY_SPIN_NS
+#define POLY_SPIN_NS 400
+#endif
 #ifndef POLY_TILE_BYTES
 #define POLY_TILE_BYTES 12288
 #endif
@@ -206,6 +209,16 @@ __device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v) {
 }
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Wait with a timer backoff (POLY_SPIN_NS > 0): a suspended try_wait wakes on any
+// mbarrier activity in the CTA, which a 25-warp K2 has plenty of.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+#if POLY_SPIN_NS > 0
+    while (!mbar_test(bar, parity)) __nanosleep(POLY_SPIN_NS);
+#else
+    mbar_wait(bar, parity);
+#endif
 }
 
 // 1-D TMA bulk copy global -> shared, completion counted on `bar` (bytes % 16 == 0).
