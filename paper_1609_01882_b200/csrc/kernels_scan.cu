@@ -450,7 +450,13 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
                         __nanosleep(POLY_PRODUCER_POLL);
                     }
 #else
-                    if (lane == 0) mbar_wait(&empty_bar[s], ((sq_ / STAGES) - 1) & 1u);
+                    if (lane == 0) {
+#if POLY_PROD_SPIN_NS > 0
+                        while (!mbar_test(&empty_bar[s], ((sq_ / STAGES) - 1) & 1u)) __nanosleep(POLY_PROD_SPIN_NS);
+#else
+                        mbar_wait(&empty_bar[s], ((sq_ / STAGES) - 1) & 1u);
+#endif
+                    }
 #endif
                 }
                 if (lane == 0) {
@@ -583,7 +589,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
             if constexpr (TCF) stage_a(0);
             for (uint32_t j = 0; j < ntile; ++j) {
                 const uint32_t sq_ = seq + j, s = sq_ % STAGES;
-                if constexpr (!TCF) mbar_wait(&full_bar[s], (sq_ / STAGES) & 1u);
+                if constexpr (!TCF) mbar_wait_backoff(&full_bar[s], (sq_ / STAGES) & 1u);
                 const uint32_t T = tile_base + s * (uint32_t)TILE_BYTES;
                 const uint64_t tfirst = (t0 + j) * a.tile_stride * TC;
                 const uint32_t tcnt = (uint32_t)min((uint64_t)TC, a.n - tfirst);

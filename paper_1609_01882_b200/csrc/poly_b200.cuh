@@ -37,6 +37,9 @@ constexpr int DSUB = 16;               // every configuration: 128/8 and 256/16
 #ifndef POLY_COARSE_GEMM  // 1: enumerate_cells via TF32 dots + exact re-rank (K5r)
 #define POLY_COARSE_GEMM 1
 #endif
+#ifndef POLY_PROD_SPIN_NS
+#define POLY_PROD_SPIN_NS 0
+#endif
 #ifndef POLY_SPIN_NS
 #define POLY_SPIN_NS 400
 #endif
