@@ -268,7 +268,7 @@ void run_batches(poly_b200_index* ix, const float* d_queries, uint64_t nq, const
             a.work = ix->ctrl + NQB + 1;
             a.bdone = ix->ctrl + NQB + 4;
             a.surv = perq ? ix->surv : ix->surv_total;
-            const uint64_t want = std::max<uint64_t>(1, ntiles * a.ngroups / (8ull * ix->num_sms));
+            const uint64_t want = std::max<uint64_t>(1, ntiles * a.ngroups / ((uint64_t)POLY_UNITS_PER_CTA * ix->num_sms));
             a.tiles_per_chunk = (uint32_t)std::min<uint64_t>(POLY_MAX_TPC, want);
             a.ntiles = ntiles;
             a.tile_stride = 1;
