@@ -14,7 +14,7 @@ constexpr int DSUB = 16;               // every configuration: 128/8 and 256/16
 #define POLY_WAIT_HINT 20000
 #endif
 #ifndef POLY_UNITS_PER_CTA  // K2 work units per CTA the unit size aims for (capped by POLY_MAX_TPC)
-#define POLY_UNITS_PER_CTA 8
+#define POLY_UNITS_PER_CTA 16
 #endif
 #ifndef POLY_MAX_TPC  // tiles per K2 work unit (cap): fewer unit boundaries vs. tail balance
 #define POLY_MAX_TPC 128
