@@ -199,6 +199,10 @@ def run_ivf(args, rank, world, local):
     knn = args.config == 4
     norm = knn
     torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     z = np.load(os.path.join(ROOT, "tests", "golden", PQFILE))
     pq = pb.ProductQuantizer(M, 8, DIM, z["codebooks"], z["perms"])
     centers = synth.gen_centers(SEED, NCENT, DIM)
@@ -225,7 +229,11 @@ def run_ivf(args, rank, world, local):
     torch.cuda.synchronize()
     setup_s = time.time() - t
     if knn:
-        return run_knn(args, c, ivf, centers, setup_s, rank, world, local, row0, row1)
+        try:
+            return run_knn(args, c, ivf, centers, setup_s, rank, world, local, row0, row1)
+        finally:
+            if dist is not None:
+                dist.destroy_process_group()
     dq = torch.empty((NQ, DIM), dtype=torch.float32, device="cuda")
     pb.gen_points_device(centers, SEED, 3, 0, NQ, dq, device=local)
     stream = torch.cuda.current_stream()
@@ -235,26 +243,51 @@ def run_ivf(args, rank, world, local):
     o_cnt = torch.empty(BATCH, dtype=torch.int32, device="cuda")
     nbatches = NQ // BATCH
     results = {}
+    if dist is not None:
+        # every cell's list holds this rank's id range; per-rank top-k
+        # keys are all-gathered over NCCL and merged exactly (IVFIndexEngine + ShardedSearch)
+        from paper_1609_01882_b200.distributed import IVFIndexEngine, ShardedSearch
+        engine = IVFIndexEngine(ivf, stream)
+        sharded = ShardedSearch(engine)
+
+    def step(i, p, st=None):
+        q = dq[(i % nbatches) * BATCH:][:BATCH]
+        if dist is None:
+            ivf.search_device(q, p, o_ids, o_sc, o_cnt, stream.cuda_stream, st)
+        else:
+            engine.stats = st
+            sharded.search_batch(q, p, (o_ids, o_sc, o_cnt))
+
     for nprobe in [c["nprobe"]] + [int(x) for x in c["per_nprobe"].split(",") if x]:
         p = pb.CoarseParams(pb.Strategy.dual, k, args.ht, nprobe, 0)
         steps = args.steps if nprobe == c["nprobe"] else max(3, args.steps // 2)
         scanned = surv = 0
         for i in range(args.warmup, args.warmup + steps):  # per-batch work (untimed)
             st = pb.SearchStats()
-            ivf.search_device(dq[(i % nbatches) * BATCH:][:BATCH], p, o_ids, o_sc, o_cnt, stream.cuda_stream, st)
+            step(i, p, st)
             scanned += st.scanned
             surv += st.survivors
+        if dist is not None:  # codes scanned by all ranks
+            t = torch.tensor([scanned, surv], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t)
+            scanned, surv = int(t[0].item()), int(t[1].item())
         for i in range(args.warmup):
-            ivf.search_device(dq[(i % nbatches) * BATCH:][:BATCH], p, o_ids, o_sc, o_cnt, stream.cuda_stream)
+            step(i, p)
         torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
         l0 = pb.launch_count()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for i in range(args.warmup, args.warmup + steps):
-            ivf.search_device(dq[(i % nbatches) * BATCH:][:BATCH], p, o_ids, o_sc, o_cnt, stream.cuda_stream)
+            step(i, p)
         e1.record(stream)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
+        if dist is not None:  # max over ranks
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
         results[nprobe] = {"value": scanned / (ms / 1e3), "ms_per_step": ms / steps,
                            "scanned_per_query": scanned / (steps * BATCH), "survivor_frac": surv / max(scanned, 1),
                            "gpu_launches": pb.launch_count() - l0, "steps": steps}
@@ -262,16 +295,19 @@ def run_ivf(args, rank, world, local):
     line = {"metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": world, "steps": head["steps"],
             "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u8/f32", "data": "synthetic (seeded Gaussian mixture, BASELINE cfg2)",
-            "config": {"workload": f"cfg2 IVF+polysemous: nlist={c['nlist']}, N={args.n} codes on this GPU (the "
-                                   f"per-GPU share of 1e9 over 8), PQ m={M} on residuals, nq={NQ} in batches of "
+            "config": {"workload": f"cfg2 IVF+polysemous: nlist={c['nlist']}, N={args.n} codes over {world} GPU(s) (the "
+                                   f"per-GPU share of 1e9 over 8 at N=1), PQ m={M} on residuals, nq={NQ} in batches of "
                                    f"{BATCH}, nprobe={c['nprobe']}, k={k}, ht={args.ht}",
                        "nlist": c["nlist"], "n_codes": args.n, "m": M, "nprobe": c["nprobe"], "k": k, "ht": args.ht,
+                       "parallelism": f"db-shard{world} (ids within every list) + NCCL key all-gather",
                        "coarse": "training-stream rows [0, nlist) (sampled coarse quantizer; DESIGN.md)",
                        "build_assignment": "TF32 GEMM argmin (setup only)"},
             "gpu_launches": head["gpu_launches"], "per_nprobe": {str(kk): v for kk, v in results.items()},
             "setup_s": round(setup_s, 1)}
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
 
 
 def run_knn(args, c, ivf, centers, setup_s, rank, world, local, row0, row1):

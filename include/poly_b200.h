@@ -215,6 +215,19 @@ int poly_b200_ivf_search_device(poly_b200_ivf* ivf, const float* d_queries, uint
                                 const poly_b200_ivf_params* params, int64_t* d_out_ids, float* d_out_scores,
                                 uint32_t* d_out_counts, void* stream, poly_b200_search_stats* stats);
 
+/* Multi-GPU IVF: each rank holds every cell's lists for its id
+ * range (shard by id within every list) and returns its per-query top-k as
+ * 64-bit keys (fp32 score bits << 32 | 32-bit global id); the ranks' keys are
+ * all-gathered and merged exactly by poly_b200_ivf_merge_keys_device.  Requires
+ * consecutive ids below 2^32 (POLY_B200_STATE otherwise).  Layouts as
+ * poly_b200_search_keys_device / poly_b200_merge_keys_device. */
+int poly_b200_ivf_search_keys_device(poly_b200_ivf* ivf, const float* d_queries, uint64_t nq,
+                                     const poly_b200_ivf_params* params, uint64_t* d_keys, uint32_t* d_counts,
+                                     void* stream, poly_b200_search_stats* stats);
+int poly_b200_ivf_merge_keys_device(poly_b200_ivf* ivf, const uint64_t* d_keys, const uint32_t* d_counts,
+                                    uint32_t parts, uint64_t nq, uint32_t k, int64_t* d_ids, float* d_scores,
+                                    uint32_t* d_out_counts, void* stream);
+
 /* knn_graph: the k nearest neighbours of n vectors that are
  * themselves in the index (vector i has id id0 + i), self-match removed:
  * search_coarse with k + 1, then the row's own id is dropped (or, if absent,

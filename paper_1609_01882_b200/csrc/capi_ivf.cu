@@ -252,7 +252,8 @@ void enumerate_cells(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, uint32_t
 
 // One batch of <= 256 queries; outputs through keys_to_ids.
 void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_b200_ivf_params* p, int64_t* d_ids,
-                  float* d_scores, uint32_t* d_counts, cudaStream_t s) {
+                  float* d_scores, uint32_t* d_counts, cudaStream_t s, uint64_t* d_keys_out = nullptr,
+                  uint32_t* d_kcounts_out = nullptr) {
     const uint32_t k = p->k;
     const uint32_t np = std::min(p->nprobe, iv->nlist);
     int strategy = p->strategy;
@@ -296,15 +297,26 @@ void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_
         pb_ = pe;
     }
     pb::launch_or_flag(iv->sticky_overflow, iv->ctrl + IVF_NQB, s);
+    if (d_keys_out) {  // multi-GPU: the shard's top-k keys for the cross-rank merge
+        CK(cudaMemcpyAsync(d_keys_out, iv->keys, (size_t)nqb * k * 8, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(d_kcounts_out, iv->kcounts, nqb * 4, cudaMemcpyDeviceToDevice, s));
+        return;
+    }
     pb::launch_keys_to_ids(iv->keys, iv->kcounts, nqb, k, iv->idm.d_rank_to_id, d_ids, d_scores, d_counts, s);
 }
 
 // All batches; returns strategy survivors semantics (0 none, 1 = scanned, 2 counted).
 int device_search(poly_b200_ivf* iv, const float* d_q, uint64_t nq, const poly_b200_ivf_params* p, int64_t* d_ids,
-                  float* d_scores, uint32_t* d_counts, cudaStream_t s) {
+                  float* d_scores, uint32_t* d_counts, cudaStream_t s, uint64_t* d_keys = nullptr,
+                  uint32_t* d_kcounts = nullptr) {
     validate(iv, p);
     if (nq == 0) return 0;
     if (p->k == 0 || iv->n == 0) {
+        if (d_kcounts) {
+            CK(cudaMemsetAsync(d_kcounts, 0, nq * 4, s));
+            if (p->k) CK(cudaMemsetAsync(d_keys, 0xFF, nq * p->k * 8, s));
+            return 0;
+        }
         if (d_counts) CK(cudaMemsetAsync(d_counts, 0, nq * 4, s));
         if (p->k) pb::launch_keys_to_ids(nullptr, nullptr, (uint32_t)nq, p->k, nullptr, d_ids, d_scores, nullptr, s);
         return 0;
@@ -316,8 +328,12 @@ int device_search(poly_b200_ivf* iv, const float* d_q, uint64_t nq, const poly_b
     CK(cudaMemsetAsync(iv->sticky_overflow, 0, 4, s));
     for (uint64_t b0 = 0; b0 < nq; b0 += IVF_NQB) {
         const uint32_t nqb = (uint32_t)std::min<uint64_t>(IVF_NQB, nq - b0);
-        search_batch(iv, d_q + b0 * iv->dim, nqb, p, d_ids + b0 * p->k, d_scores + b0 * p->k,
-                     d_counts ? d_counts + b0 : nullptr, s);
+        if (d_keys)
+            search_batch(iv, d_q + b0 * iv->dim, nqb, p, nullptr, nullptr, nullptr, s, d_keys + b0 * p->k,
+                         d_kcounts + b0);
+        else
+            search_batch(iv, d_q + b0 * iv->dim, nqb, p, d_ids + b0 * p->k, d_scores + b0 * p->k,
+                         d_counts ? d_counts + b0 : nullptr, s);
         CK(cudaGetLastError());
     }
     if (p->strategy == pb::DUAL) return p->tau >= iv->code_bits() ? 1 : 2;
@@ -603,6 +619,49 @@ int poly_b200_ivf_search_device(poly_b200_ivf* iv, const float* d_q, uint64_t nq
             stats->scanned = stats->survivors = 0;
             if (nq && p->k && iv->n) read_stats(iv, mode, stats, s);
         }
+    });
+}
+
+int poly_b200_ivf_search_keys_device(poly_b200_ivf* iv, const float* d_q, uint64_t nq, const poly_b200_ivf_params* p,
+                                     uint64_t* d_keys, uint32_t* d_counts, void* stream, poly_b200_search_stats* stats) {
+    return guard([&] {
+        require(iv != nullptr && p != nullptr, POLY_B200_INVALID_ARGUMENT, "null arguments");
+        require(p->k > 0, POLY_B200_INVALID_ARGUMENT, "k must be positive for key output");
+        require(nq == 0 || (d_q && d_keys && d_counts), POLY_B200_INVALID_ARGUMENT, "null buffers");
+        std::lock_guard<std::mutex> lk(iv->mu);
+        DeviceGuard dg(iv->device);
+        cudaStream_t s = (cudaStream_t)stream;
+        iv->idm.sync(iv->n);
+        require(iv->n == 0 || iv->idm.mode == pb::ID_ARITH, POLY_B200_STATE,
+                "key output needs consecutive ids below 2^32 (the key carries the id itself)");
+        const int mode = device_search(iv, d_q, nq, p, nullptr, nullptr, nullptr, s, d_keys, d_counts);
+        if (stats) {
+            stats->scanned = stats->survivors = 0;
+            if (nq && iv->n) read_stats(iv, mode, stats, s);
+        }
+    });
+}
+
+int poly_b200_ivf_merge_keys_device(poly_b200_ivf* iv, const uint64_t* d_keys, const uint32_t* d_counts,
+                                    uint32_t parts, uint64_t nq, uint32_t k, int64_t* d_ids, float* d_scores,
+                                    uint32_t* d_out_counts, void* stream) {
+    return guard([&] {
+        require(iv != nullptr, POLY_B200_INVALID_ARGUMENT, "null index");
+        require(parts >= 1 && parts <= 64, POLY_B200_INVALID_ARGUMENT, "parts must be in [1, 64]");
+        require(k >= 1 && k <= (uint32_t)pb::KMAX, POLY_B200_INVALID_ARGUMENT, "bad k");
+        std::lock_guard<std::mutex> lk(iv->mu);
+        DeviceGuard dg(iv->device);
+        cudaStream_t s = (cudaStream_t)stream;
+        ensure_ivf_scratch(iv, 1, k);
+        for (uint64_t b0 = 0; b0 < nq; b0 += IVF_NQB) {
+            const uint32_t nqb = (uint32_t)std::min<uint64_t>(IVF_NQB, nq - b0);
+            // parts x nq x k layout; keys carry the global id, so no id table is needed
+            pb::launch_topk(reinterpret_cast<const unsigned long long*>(d_keys) + b0 * k, d_counts + b0, k, parts,
+                            nq * k, nq, nqb, k, iv->keys, iv->kcounts, s);
+            pb::launch_keys_to_ids(iv->keys, iv->kcounts, nqb, k, nullptr, d_ids + b0 * k, d_scores + b0 * k,
+                                   d_out_counts ? d_out_counts + b0 : nullptr, s);
+        }
+        CK(cudaGetLastError());
     });
 }
 

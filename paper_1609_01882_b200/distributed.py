@@ -41,6 +41,19 @@ class FlatIndexEngine:
         self.index.merge_keys_device(keys_all, counts_all, parts, nq, k, ids, scores, counts, stream=self._sptr())
 
 
+class IVFIndexEngine(FlatIndexEngine):
+    """GPU engine over one rank's IVF shard: every cell's list restricted to the rank's
+    id range (shard by id within every list), coarse quantizer
+    replicated, so all ranks probe the same cells and the key merge is exact."""
+
+    def __init__(self, index, stream=None, stats=None):
+        super().__init__(index, stream)
+        self.stats = stats
+
+    def search_keys(self, queries, params, keys, counts):
+        self.index.search_keys_device(queries, params, keys, counts, stream=self._sptr(), stats=self.stats)
+
+
 class ShardedSearch:
     """search_batch over all ranks' shards: local scan, all-gather keys, merge."""
 

@@ -118,6 +118,23 @@ class IVFIndex:
             stats.scanned += st.scanned
             stats.survivors += st.survivors
 
+    def search_keys_device(self, d_queries, params: CoarseParams, d_keys, d_counts, stream=0,
+                           stats: SearchStats | None = None):
+        """Multi-GPU: this shard's top-k as int64 keys (score bits << 32 | global id)."""
+        st = SearchStatsC()
+        _check(lib.poly_b200_ivf_search_keys_device(self._h, d_queries.data_ptr(), d_queries.shape[0],
+                                                    C.byref(params.c()), d_keys.data_ptr(), d_counts.data_ptr(),
+                                                    C.c_void_p(stream), C.byref(st) if stats is not None else None))
+        if stats is not None:
+            stats.scanned += st.scanned
+            stats.survivors += st.survivors
+
+    def merge_keys_device(self, d_keys, d_counts, parts, nq, k, d_ids, d_scores, d_counts_out=None, stream=0):
+        """Exact merge of parts x nq x k keys (all ranks' search_keys_device output)."""
+        ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731
+        _check(lib.poly_b200_ivf_merge_keys_device(self._h, ptr(d_keys), ptr(d_counts), parts, nq, k, ptr(d_ids),
+                                                   ptr(d_scores), ptr(d_counts_out), C.c_void_p(stream)))
+
     def knn_graph_device(self, d_x, id0, params: CoarseParams, d_ids, d_scores, d_counts=None, stream=0):
         """knn_graph: rows of d_x are the stored vectors id0.. ; self-match removed."""
         ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731

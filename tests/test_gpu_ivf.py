@@ -184,3 +184,68 @@ def test_probe_order_many_near_ties(pb, gi, dim, nlist):
     for nprobe in (1, 16, 100, 1000):
         want = oracle.ivf_search(opq, coarse, empty, queries, 1, nprobe, threads=16)[5]
         assert np.array_equal(ix.probes(queries, nprobe), want), nprobe
+
+
+def test_sharded_ivf_merge_matches_unsharded(pb, gi):
+    """SURVEY.md sec. 8e for IVF: 4 shards (every cell's list restricted to an id range),
+    per-shard top-k keys, exact K3 merge == the unsharded search == the oracle; the
+    NCCL world-1 path of ShardedSearch with the IVF engine gives the same."""
+    import torch
+    import torch.distributed as dist
+    from paper_1609_01882_b200.distributed import IVFIndexEngine, ShardedSearch, shard_range
+    seed = int(gi["data_seed"])
+    centers = oracle.gen_centers(seed, 1000, 128)
+    rng = np.random.default_rng(9)
+    coarse = oracle.gen_points(seed, 1, 0, 20000, centers)[rng.choice(20000, 256, replace=False)]
+    n = 200_000
+    base = oracle.gen_points(seed, 2, 0, n, centers)
+    queries = oracle.gen_points(seed, 3, 0, 300, centers)
+    mk = lambda: pb.IVFIndex(pb.ProductQuantizer(8, 8, 128, gi["codebooks"], gi["perms"]), coarse)  # noqa: E731
+    full = mk()
+    full.add(base)
+    shards = []
+    for r in range(4):
+        r0, r1 = shard_range(n, 4, r)
+        ix = mk()
+        ix.add(base[r0:r1], ids=np.arange(r0, r1))
+        shards.append(ix)
+    k = 100
+    dq = torch.from_numpy(queries).cuda()
+    for nprobe, tau in ((8, 26), (32, 64)):
+        p = pb.CoarseParams(pb.Strategy.dual, k, tau, nprobe, 0)
+        want_ids, want_sc, want_cnt = full.search(queries, p)
+        keys = torch.empty((4, 300, k), dtype=torch.int64, device="cuda")
+        cnts = torch.empty((4, 300), dtype=torch.int32, device="cuda")
+        st = pb.SearchStats()
+        for r, ix in enumerate(shards):
+            ix.search_keys_device(dq, p, keys[r], cnts[r], stats=st)
+        ids = torch.empty((300, k), dtype=torch.int64, device="cuda")
+        sc = torch.empty((300, k), dtype=torch.float32, device="cuda")
+        cnt = torch.empty(300, dtype=torch.int32, device="cuda")
+        shards[0].merge_keys_device(keys, cnts, 4, 300, k, ids, sc, cnt)
+        torch.cuda.synchronize()
+        assert np.array_equal(ids.cpu().numpy(), want_ids), (nprobe, tau)
+        assert np.array_equal(_bits(sc.cpu().numpy()), _bits(want_sc))
+        assert np.array_equal(cnt.cpu().numpy(), want_cnt)
+        st_full = pb.SearchStats()
+        full.search(queries, p, st_full)
+        assert st.scanned == st_full.scanned and st.survivors == st_full.survivors
+    # the same through the rank plumbing, world = 1 over NCCL
+    if not dist.is_initialized():
+        import os as _os
+        _os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        _os.environ.setdefault("MASTER_PORT", "29631")
+        dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        p = pb.CoarseParams(pb.Strategy.dual, k, 26, 8, 0)
+        ids, sc, cnt = ShardedSearch(IVFIndexEngine(full)).search_batch(dq, p)
+        torch.cuda.synchronize()
+        want_ids, _, _ = full.search(queries, p)
+        assert np.array_equal(ids.cpu().numpy(), want_ids)
+    finally:
+        dist.destroy_process_group()
+    # non-consecutive ids cannot be carried in a key
+    odd = mk()
+    odd.add(base[:1000], ids=np.arange(1000) * 3)
+    with pytest.raises(pb.PolyError):
+        odd.search_keys_device(dq, pb.CoarseParams(pb.Strategy.dual, k, 26, 8, 0), keys[0], cnts[0])
