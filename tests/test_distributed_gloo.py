@@ -92,3 +92,65 @@ def test_sharded_search_equals_unsharded(tmp_path, pq8, g8):
     assert np.array_equal(r["ids"], oi)
     assert np.array_equal(r["scores"].view(np.uint32), osc.view(np.uint32))
     assert np.array_equal(r["counts"], oc.astype(np.int32))
+
+
+class OracleIVFEngine(OracleEngine):
+    """IVF shard (every cell's list restricted to the rank's id range, coarse quantizer
+    replicated) searched by the IVF oracle; same keys and merge as the flat engine."""
+
+    def __init__(self, pq, coarse, lists, nprobe):
+        self.pq, self.coarse, self.lists, self.nprobe = pq, coarse, lists, nprobe
+
+    def search_keys(self, queries, params, keys, counts):
+        import oracle
+        oi, osc, oc, _, _, _ = oracle.ivf_search(self.pq, self.coarse, self.lists, queries.numpy(), int(params.k),
+                                                 self.nprobe, tau=int(params.tau), threads=2)
+        key = (osc.view(np.uint32).astype(np.uint64) << np.uint64(32)) | (oi.astype(np.uint64) & np.uint64(0xFFFFFFFF))
+        key[oi < 0] = np.uint64(0xFFFFFFFFFFFFFFFF)
+        keys.copy_(torch.from_numpy(key.view(np.int64)))
+        counts.copy_(torch.from_numpy(oc.astype(np.int32)))
+
+
+def _ivf_data():
+    import oracle
+    g = np.load(os.path.join(ROOT, "tests", "golden", "golden_ivf.npz"))
+    pq = oracle.PQ(8, 8, 128, g["codebooks"], g["perms"])
+    centers = oracle.gen_centers(int(g["data_seed"]), 1000, 128)
+    base = oracle.gen_points(int(g["data_seed"]), 2, 0, 20000, centers)
+    base = np.concatenate([base, base[:500]])  # duplicates across the shard boundary: ties
+    return g, pq, base
+
+
+def _ivf_worker(rank, world, port, result_path):
+    import sys
+    sys.path.insert(0, ROOT)
+    import oracle
+    from paper_1609_01882_b200.distributed import ShardedSearch, shard_range
+
+    class P:
+        k, tau = 40, 26
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    g, pq, base = _ivf_data()
+    b, e = shard_range(len(base), world, rank)
+    lists, _ = oracle.ivf_build(pq, base[b:e], g["coarse"], ids=np.arange(b, e, dtype=np.int64))
+    eng = OracleIVFEngine(pq, g["coarse"], lists, nprobe=8)
+    ids, scores, counts = ShardedSearch(eng, device="cpu").search_batch(torch.from_numpy(g["queries"]), P())
+    if rank == 0:
+        np.savez(result_path, ids=ids.numpy(), scores=scores.numpy(), counts=counts.numpy())
+    dist.destroy_process_group()
+
+
+def test_sharded_ivf_equals_unsharded(tmp_path):
+    """SURVEY.md sec. 8e for IVF on CPU: ids sharded within every list, same probes on
+    every rank, keys all-gathered over gloo and merged == the unsharded IVF oracle."""
+    import oracle
+    out = str(tmp_path / "ivf0.npz")
+    mp.spawn(_ivf_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    r = np.load(out)
+    g, pq, base = _ivf_data()
+    lists, _ = oracle.ivf_build(pq, base, g["coarse"])
+    oi, osc, oc, _, _, _ = oracle.ivf_search(pq, g["coarse"], lists, g["queries"], 40, 8, tau=26)
+    assert np.array_equal(r["ids"], oi)
+    assert np.array_equal(r["scores"].view(np.uint32), osc.view(np.uint32))
+    assert np.array_equal(r["counts"], oc.astype(np.int32))
