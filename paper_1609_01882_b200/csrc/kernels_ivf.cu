@@ -409,15 +409,11 @@ __global__ void __launch_bounds__(256) residual_lut_kernel(const float* __restri
                 acc = __fadd_rn(acc, __fmul_rn(t, t));
             }
             lutp[((size_t)(item0 + it) * m + sq) * KSUB + dst] = acc;
-            float bv = acc;
-            uint32_t bj = j;
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                const float ov = __shfl_down_sync(0xffffffffu, bv, off);
-                const uint32_t oj = __shfl_down_sync(0xffffffffu, bj, off);
-                if (ov < bv || (ov == bv && oj < bj)) { bv = ov; bj = oj; }
-            }
-            if ((j & 31) == 0) { wv[it][sq][j >> 5] = bv; wj[it][sq][j >> 5] = bj; }
+            // warp argmin, ties -> lowest j: acc >= 0, so its bits order like the value
+            const uint32_t bits = __float_as_uint(acc);
+            const uint32_t wmin = __reduce_min_sync(0xffffffffu, bits);
+            const uint32_t first = __ffs(__ballot_sync(0xffffffffu, bits == wmin)) - 1;
+            if ((j & 31) == 0) { wv[it][sq][j >> 5] = __uint_as_float(wmin); wj[it][sq][j >> 5] = (j & ~31u) + first; }
         }
     }
     __syncthreads();

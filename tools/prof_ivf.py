@@ -28,6 +28,10 @@ for r in range(0, args.n, 1 << 20):
     ivf.add_device(x[:nb], cells[:nb], r)
 q = synth.gen_points(160901882, 3, 0, 256, centers)
 p = pb.CoarseParams(pb.Strategy.dual, 100, 26, args.nprobe, 0)
+ivf.search(q, p)  # warm (allocations)
+torch.cuda.synchronize()
+torch.cuda.profiler.start()  # ncu --profile-from-start off: only the searches below
 for i in range(args.reps):
     st = pb.SearchStats(); t = time.time(); ivf.search(q, p, st); dt = time.time() - t
+torch.cuda.profiler.stop()
 print(f"n={args.n} nprobe={args.nprobe}: {dt*1e3:.2f} ms, scanned/query {st.scanned/256:.0f}, surv {st.survivors/max(st.scanned,1):.3f}")
