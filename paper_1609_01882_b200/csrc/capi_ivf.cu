@@ -92,6 +92,8 @@ struct poly_b200_ivf {
 
 namespace {
 
+constexpr uint32_t IVF_CHUNK = 1024;  // K6 round-1 work item: 1024 list rows (8 warps x 128)
+
 __global__ void fill_u32(uint32_t* p, uint64_t n, uint32_t v) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
         p[i] = v;
@@ -290,6 +292,9 @@ void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_
         const uint32_t pe = pb_ == 0 ? 1u : np;
         a.p_begin = pb_;
         a.p_end = pe;
+        // round 1 has one item per query: split the lists into chunks so it fills the GPU
+        a.chunk_codes = IVF_CHUNK;
+        a.nchunks = pb_ == 0 ? (uint32_t)std::max<uint64_t>(1, (iv->max_list + IVF_CHUNK - 1) / IVF_CHUNK) : 1u;
         a.work = iv->ctrl + IVF_NQB + 1 + round;
         pb::launch_ivf_scan(a, strategy, iv->m, iv->num_sms, s);
         pb::launch_topk(iv->cand, iv->ctrl, iv->cand_cap, 1, 0, 0, nqb, k, iv->keys, iv->kcounts, s);

@@ -536,7 +536,7 @@ __global__ void __launch_bounds__(K6_WARPS * 32) ivf_scan_kernel(const IvfScanAr
     uint32_t* qpos_q = reinterpret_cast<uint32_t*>(qbase + 64 * sizeof(C));
     __shared__ uint32_t item_s;
     const uint32_t span = a.p_end - a.p_begin;
-    const uint64_t nitems = (uint64_t)a.nq * span;
+    const uint64_t nitems = (uint64_t)a.nq * span * a.nchunks;
     uint32_t surv_total = 0;
     for (;;) {
         __syncthreads();
@@ -544,11 +544,17 @@ __global__ void __launch_bounds__(K6_WARPS * 32) ivf_scan_kernel(const IvfScanAr
         __syncthreads();
         const uint32_t it = item_s;
         if (it >= nitems) break;
-        const uint32_t qi = it / span, p = a.p_begin + it % span;
+        const uint32_t ch = it % a.nchunks, iq = it / a.nchunks;
+        const uint32_t qi = iq / span, p = a.p_begin + iq % span;
         if (p >= a.np_eff[qi]) continue;
         const size_t item = (size_t)qi * a.nprobe + p;
         const uint32_t cell = (uint32_t)a.probe_keys[item];
-        const uint64_t beg = a.off[cell], end = a.off[cell + 1];
+        uint64_t beg = a.off[cell], end = a.off[cell + 1];
+        if (a.nchunks > 1) {  // this CTA's slice of the list
+            beg += (uint64_t)ch * a.chunk_codes;
+            if (beg >= end) continue;
+            end = min(end, beg + a.chunk_codes);
+        }
         const float4* src = reinterpret_cast<const float4*>(a.lutp + item * M * KSUB);
         for (int i = threadIdx.x; i < M * KSUB / 4; i += K6_WARPS * 32) reinterpret_cast<float4*>(L)[i] = src[i];
         const C qc = reinterpret_cast<const C*>(a.qcodes)[item];

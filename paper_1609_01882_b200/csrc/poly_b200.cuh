@@ -108,6 +108,8 @@ struct IvfScanArgs {
     uint32_t* overflow;
     uint32_t* work;
     unsigned long long* surv_total;
+    uint32_t nchunks;       // work item = (query, probe, chunk); chunk c covers list rows
+    uint32_t chunk_codes;   // [c * chunk_codes, (c + 1) * chunk_codes)  (nchunks = 1: whole list)
 };
 
 // ---------------------------------------------------------------- PTX helpers
