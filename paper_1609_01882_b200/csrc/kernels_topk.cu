@@ -8,7 +8,7 @@
 // order == (score, id) order and ties resolve to the lower id.
 //
 // One CTA per query.  <= 2048 candidates: bitonic sort in shared memory.
-// More: a 3-pass bucket select -- key range (min, max), a 4096-bucket histogram
+// More: a 3-pass bucket select -- key range (min, max), a 2048-bucket histogram
 // over the bits just below the highest bit where min and max differ, then the
 // keys of the buckets up to the k-th one are gathered (usually ~k) and sorted.
 // Fallbacks when that set exceeds TK_SEL_KEYS: bitonic sort of all keys (<= 8192,
@@ -22,8 +22,8 @@ constexpr int TK_THREADS = 512;
 constexpr uint32_t TK_SMEM_KEYS = 8192;
 constexpr int TK_MAXPARTS = 64;
 constexpr uint32_t TK_DIRECT = 2048;  // at most this many: sort them all
-constexpr uint32_t TK_SEL_KEYS = 4096;
-constexpr uint32_t TK_BUCKETS = 4096;
+constexpr uint32_t TK_SEL_KEYS = 2048;  // with 2048 buckets: 88 KB of smem, two CTAs per SM
+constexpr uint32_t TK_BUCKETS = 2048;
 
 __device__ __forceinline__ void bitonic_sort(unsigned long long* s, uint32_t p) {
     for (uint32_t size = 2; size <= p; size <<= 1) {
@@ -103,7 +103,8 @@ __global__ void __launch_bounds__(TK_THREADS) topk_kernel(const unsigned long lo
         }
         const unsigned long long span = hi - lo;
         const int top = span ? 63 - __clzll(span) : 0;     // highest differing bit of the range
-        const int sh = top >= 12 ? top - 11 : 0;            // (span >> sh) < 4096
+        constexpr int BB = 31 - __builtin_clz(TK_BUCKETS);  // log2(buckets)
+        const int sh = top >= BB ? top - (BB - 1) : 0;      // (span >> sh) < TK_BUCKETS
         // pass 2: histogram
         {
             uint32_t flat = 0;
