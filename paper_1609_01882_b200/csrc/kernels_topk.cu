@@ -8,12 +8,12 @@
 // order == (score, id) order and ties resolve to the lower id.
 //
 // One CTA per query.  <= 2048 candidates: bitonic sort in shared memory.
-// More: a 3-pass bucket select -- key range (min, max), a 2048-bucket histogram
-// over the bits just below the highest bit where min and max differ, then the
-// keys of the buckets up to the k-th one are gathered (usually ~k) and sorted.
-// Fallbacks when that set exceeds TK_SEL_KEYS: bitonic sort of all keys (<= 8192,
-// in shared memory) or an 8-pass radix select of the k-th key streamed from L2.
-// The same kernel merges the per-GPU lists of the multi-GPU path (parts > 1).
+// More: an iterative bucket select -- key range (min, max), then 2048-bucket
+// histograms that narrow to the bucket of the k-th key (11 bits per pass) until
+// the keys at or below it fit the select buffer (typically one pass; duplicate
+// scores need more), then a bitonic sort of those.  Keys come from shared memory
+// (<= 8192 candidates) or L2.  The same kernel merges the per-GPU lists of the
+// multi-GPU path (parts > 1).
 #include "poly_b200.cuh"
 
 namespace pb {
@@ -22,7 +22,7 @@ constexpr int TK_THREADS = 512;
 constexpr uint32_t TK_SMEM_KEYS = 8192;
 constexpr int TK_MAXPARTS = 64;
 constexpr uint32_t TK_DIRECT = 2048;  // at most this many: sort them all
-constexpr uint32_t TK_SEL_KEYS = 2048;  // with 2048 buckets: 88 KB of smem, two CTAs per SM
+constexpr uint32_t TK_SEL_KEYS = 4096;  // >= k + 1 (k <= 2048); with 2048 buckets: 104 KB, two CTAs per SM
 constexpr uint32_t TK_BUCKETS = 2048;
 
 __device__ __forceinline__ void bitonic_sort(unsigned long long* s, uint32_t p) {
@@ -47,198 +47,125 @@ __global__ void __launch_bounds__(TK_THREADS) topk_kernel(const unsigned long lo
                                                           uint32_t* __restrict__ out_counts) {
     extern __shared__ unsigned long long sk[];
     __shared__ uint32_t pc[TK_MAXPARTS];
-    __shared__ uint32_t hist[256];
-    __shared__ unsigned long long prefix_s;
-    __shared__ uint32_t k_s, fill_s;
-    const uint32_t q = blockIdx.x;
-    if (threadIdx.x < parts) pc[threadIdx.x] = min(ccount[(size_t)threadIdx.x * count_stride + q], cap);
+    __shared__ unsigned long long wlo[TK_THREADS / 32], whi[TK_THREADS / 32];
+    __shared__ uint32_t wsum[TK_THREADS / 32];
+    __shared__ uint32_t b_s, below_s, inb_s, fill_s;
+    const uint32_t q = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid < parts) pc[tid] = min(ccount[(size_t)tid * count_stride + q], cap);
     __syncthreads();
     uint32_t total = 0;
     for (uint32_t p = 0; p < parts; ++p) total += pc[p];
     const uint32_t kk = min(k, total);
     unsigned long long* out = out_keys + (size_t)q * k;
-    unsigned long long* sel = sk + TK_SMEM_KEYS;                       // TK_SEL_KEYS
-    uint32_t* bh = reinterpret_cast<uint32_t*>(sel + TK_SEL_KEYS);    // TK_BUCKETS
+    unsigned long long* sel = sk + TK_SMEM_KEYS;                      // TK_SEL_KEYS
+    uint32_t* bh = reinterpret_cast<uint32_t*>(sel + TK_SEL_KEYS);   // TK_BUCKETS
     const bool in_smem = total <= TK_SMEM_KEYS;
     if (in_smem) {  // stage all keys in shared memory
         uint32_t base = 0;
         for (uint32_t p = 0; p < parts; ++p) {
             const unsigned long long* src = cand + p * part_stride + (size_t)q * cap;
-            for (uint32_t i = threadIdx.x; i < pc[p]; i += TK_THREADS) sk[base + i] = __ldcg(src + i);
+            for (uint32_t i = tid; i < pc[p]; i += TK_THREADS) sk[base + i] = __ldcg(src + i);
             base += pc[p];
         }
         __syncthreads();
     }
-    // key i of the list (shared memory or global)
-    auto key_at = [&](uint32_t p, uint32_t i, uint32_t flat) -> unsigned long long {
-        return in_smem ? sk[flat] : __ldcg(cand + p * part_stride + (size_t)q * cap + i);
-    };
-    if (total > TK_DIRECT && kk > 0) {
-        // pass 1: key range
-        unsigned long long lo = ~0ull, hi = 0;
-        {
-            uint32_t flat = 0;
-            for (uint32_t p = 0; p < parts; ++p) {
-                for (uint32_t i = threadIdx.x; i < pc[p]; i += TK_THREADS) {
-                    const unsigned long long v = key_at(p, i, flat + i);
-                    lo = v < lo ? v : lo;
-                    hi = v > hi ? v : hi;
-                }
-                flat += pc[p];
-            }
+    // visit every key of the list (shared memory or L2)
+    auto for_keys = [&](auto&& f) {
+        uint32_t flat = 0;
+        for (uint32_t p = 0; p < parts; ++p) {
+            const unsigned long long* src = cand + p * part_stride + (size_t)q * cap;
+            for (uint32_t i = tid; i < pc[p]; i += TK_THREADS) f(in_smem ? sk[flat + i] : __ldcg(src + i));
+            flat += pc[p];
         }
+    };
+    unsigned long long* srt = sk;  // what gets sorted: all keys (small lists) or the selected ones
+    uint32_t n = total;
+    if (total > TK_DIRECT && kk > 0) {
+        // Iterative bucket select of the kk smallest keys (keys are distinct).  The range
+        // [rlo, rlo + (TK_BUCKETS << sh)) holds the kk-th key; keys below it are already
+        // known to be among the kk smallest and sit in sel[0, fill).  Each pass histograms
+        // the range; the buckets below the kk-th one are kept, and if the kk-th bucket fits
+        // too the select ends, else the range narrows to that bucket (11 bits finer).
+        unsigned long long lo = ~0ull, hi = 0;
+        for_keys([&](unsigned long long v) {
+            lo = v < lo ? v : lo;
+            hi = v > hi ? v : hi;
+        });
         for (int off = 16; off > 0; off >>= 1) {
             const unsigned long long a = __shfl_xor_sync(0xffffffffu, lo, off), b = __shfl_xor_sync(0xffffffffu, hi, off);
             lo = a < lo ? a : lo;
             hi = b > hi ? b : hi;
         }
-        __shared__ unsigned long long wlo[TK_THREADS / 32], whi[TK_THREADS / 32];
-        if ((threadIdx.x & 31) == 0) { wlo[threadIdx.x >> 5] = lo; whi[threadIdx.x >> 5] = hi; }
-        for (uint32_t i = threadIdx.x; i < TK_BUCKETS; i += TK_THREADS) bh[i] = 0;
+        if (lane == 0) { wlo[warp] = lo; whi[warp] = hi; }
+        if (tid == 0) fill_s = 0;
         __syncthreads();
         lo = ~0ull; hi = 0;
         for (int w = 0; w < TK_THREADS / 32; ++w) {
             lo = wlo[w] < lo ? wlo[w] : lo;
             hi = whi[w] > hi ? whi[w] : hi;
         }
-        const unsigned long long span = hi - lo;
-        const int top = span ? 63 - __clzll(span) : 0;     // highest differing bit of the range
         constexpr int BB = 31 - __builtin_clz(TK_BUCKETS);  // log2(buckets)
-        const int sh = top >= BB ? top - (BB - 1) : 0;      // (span >> sh) < TK_BUCKETS
-        // pass 2: histogram
-        {
-            uint32_t flat = 0;
-            for (uint32_t p = 0; p < parts; ++p) {
-                for (uint32_t i = threadIdx.x; i < pc[p]; i += TK_THREADS)
-                    atomicAdd(&bh[(uint32_t)((key_at(p, i, flat + i) - lo) >> sh)], 1u);
-                flat += pc[p];
-            }
-        }
-        __syncthreads();
-        // bucket of the kk-th key: per-thread sums of 8 buckets, block scan
-        constexpr uint32_t PER = TK_BUCKETS / TK_THREADS;
-        uint32_t c = 0;
-#pragma unroll
-        for (uint32_t j = 0; j < PER; ++j) c += bh[threadIdx.x * PER + j];
-        uint32_t incl = c;
-        for (int off = 1; off < 32; off <<= 1) {
-            const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
-            if ((threadIdx.x & 31) >= off) incl += o;
-        }
-        __shared__ uint32_t wsum[TK_THREADS / 32];
-        if ((threadIdx.x & 31) == 31) wsum[threadIdx.x >> 5] = incl;
-        __syncthreads();
-        uint32_t wbase = 0;
-        for (uint32_t w = 0; w < (threadIdx.x >> 5); ++w) wbase += wsum[w];
-        incl += wbase;
-        const uint32_t excl = incl - c;
-        if (excl < kk && kk <= incl) {
-            uint32_t cum = excl, b = threadIdx.x * PER;
-            for (uint32_t j = 0; j < PER; ++j) {
-                cum += bh[b + j];
-                if (cum >= kk) { b += j; break; }
-            }
-            k_s = b;      // bucket holding the kk-th key
-            fill_s = cum; // keys in buckets <= b
-        }
-        __syncthreads();
-        const uint32_t nsel = fill_s;
-        if (nsel <= TK_SEL_KEYS) {
-            // pass 3: gather buckets <= b, sort, emit
-            const uint32_t bsel = k_s;
-            __syncthreads();
-            if (threadIdx.x == 0) fill_s = 0;
-            __syncthreads();
-            uint32_t flat = 0;
-            for (uint32_t p = 0; p < parts; ++p) {
-                for (uint32_t i = threadIdx.x; i < pc[p]; i += TK_THREADS) {
-                    const unsigned long long v = key_at(p, i, flat + i);
-                    if (((v - lo) >> sh) <= bsel) sel[atomicAdd(&fill_s, 1u)] = v;
-                }
-                flat += pc[p];
-            }
-            __syncthreads();
-            const uint32_t n = fill_s;
-            uint32_t P = 1;
-            while (P < n) P <<= 1;
-            for (uint32_t i = n + threadIdx.x; i < P; i += TK_THREADS) sel[i] = KEY_INF;
-            __syncthreads();
-            bitonic_sort(sel, P);
-            for (uint32_t r = threadIdx.x; r < k; r += TK_THREADS) out[r] = r < kk ? sel[r] : KEY_INF;
-            if (threadIdx.x == 0) out_counts[q] = kk;
-            return;
-        }
-        __syncthreads();
-    }
-    if (in_smem) {
-        uint32_t P = 1;
-        while (P < total) P <<= 1;
-        for (uint32_t i = total + threadIdx.x; i < P; i += TK_THREADS) sk[i] = KEY_INF;
-        __syncthreads();
-        bitonic_sort(sk, P);
-    } else {
-        // radix select of the kk-th smallest key over all parts
-        unsigned long long prefix = 0, mask = 0;
+        const unsigned long long span = hi - lo;
+        const int top = span ? 63 - __clzll(span) : 0;      // highest differing bit of the range
+        int sh = top >= BB ? top - (BB - 1) : 0;            // (span >> sh) < TK_BUCKETS
+        unsigned long long rlo = lo;
         uint32_t want = kk;
-        for (int shift = 56; shift >= 0; shift -= 8) {
-            for (int i = threadIdx.x; i < 256; i += TK_THREADS) hist[i] = 0;
+        for (;;) {
+            for (uint32_t i = tid; i < TK_BUCKETS; i += TK_THREADS) bh[i] = 0;
             __syncthreads();
-            for (uint32_t p = 0; p < parts; ++p) {
-                const unsigned long long* src = cand + p * part_stride + (size_t)q * cap;
-                for (uint32_t i = threadIdx.x; i < pc[p]; i += TK_THREADS) {
-                    const unsigned long long v = __ldcg(src + i);
-                    if ((v & mask) == prefix) atomicAdd(&hist[(v >> shift) & 0xFFu], 1u);
+            for_keys([&](unsigned long long v) {
+                if (v >= rlo && ((v - rlo) >> sh) < TK_BUCKETS) atomicAdd(&bh[(uint32_t)((v - rlo) >> sh)], 1u);
+            });
+            __syncthreads();
+            // bucket b of the want-th key of the range: per-thread sums, block scan
+            constexpr uint32_t PER = TK_BUCKETS / TK_THREADS;
+            uint32_t c = 0;
+#pragma unroll
+            for (uint32_t j = 0; j < PER; ++j) c += bh[tid * PER + j];
+            uint32_t incl = c;
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= (uint32_t)off) incl += o;
+            }
+            if (lane == 31) wsum[warp] = incl;
+            __syncthreads();
+            for (uint32_t w = 0; w < warp; ++w) incl += wsum[w];
+            const uint32_t excl = incl - c;
+            if (excl < want && want <= incl) {
+                uint32_t cum = excl, b = tid * PER;
+                for (uint32_t j = 0; j < PER; ++j) {
+                    if (cum + bh[tid * PER + j] >= want) { b = tid * PER + j; break; }
+                    cum += bh[tid * PER + j];
                 }
+                b_s = b;
+                below_s = cum;          // keys of the range in buckets < b
+                inb_s = bh[b];          // keys in bucket b
             }
             __syncthreads();
-            if (threadIdx.x < 32) {
-                const int lane = threadIdx.x;
-                uint32_t c[8], s = 0;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) { c[j] = hist[lane * 8 + j]; s += c[j]; }
-                uint32_t incl = s;
-#pragma unroll
-                for (int off = 1; off < 32; off <<= 1) {
-                    const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
-                    if (lane >= off) incl += o;
-                }
-                const uint32_t excl = incl - s;
-                if (excl < want && want <= incl) {
-                    uint32_t r = want - excl;
-                    int digit = lane * 8 + 7;
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        if (r <= c[j]) { digit = lane * 8 + j; break; }
-                        r -= c[j];
-                    }
-                    prefix_s = prefix | ((unsigned long long)digit << shift);
-                    k_s = r;
-                }
-            }
+            const uint32_t b = b_s, below = below_s, inb = inb_s, fill = fill_s;
+            const bool done = fill + below + inb <= TK_SEL_KEYS;
+            const uint32_t last = done ? b : b - 1;  // keep buckets <= last (none when b == 0 and not done)
             __syncthreads();
-            prefix = prefix_s;
-            want = k_s;
-            mask |= 0xFFull << shift;
+            if (done || b > 0)
+                for_keys([&](unsigned long long v) {
+                    if (v >= rlo && ((v - rlo) >> sh) <= last) sel[atomicAdd(&fill_s, 1u)] = v;
+                });
+            __syncthreads();
+            if (done) break;
+            rlo += (unsigned long long)b << sh;  // narrow to bucket b
+            want -= below;
+            sh = sh > BB ? sh - BB : 0;
         }
-        // gather the kk keys <= kth (keys are distinct)
-        if (threadIdx.x == 0) fill_s = 0;
-        __syncthreads();
-        for (uint32_t p = 0; p < parts; ++p) {
-            const unsigned long long* src = cand + p * part_stride + (size_t)q * cap;
-            for (uint32_t i = threadIdx.x; i < pc[p]; i += TK_THREADS) {
-                const unsigned long long v = __ldcg(src + i);
-                if (v <= prefix) sk[atomicAdd(&fill_s, 1u)] = v;
-            }
-        }
-        uint32_t P = 1;
-        while (P < kk) P <<= 1;
-        __syncthreads();
-        for (uint32_t i = kk + threadIdx.x; i < P; i += TK_THREADS) sk[i] = KEY_INF;
-        __syncthreads();
-        bitonic_sort(sk, P);
+        srt = sel;
+        n = fill_s;
     }
-    for (uint32_t r = threadIdx.x; r < k; r += TK_THREADS) out[r] = r < kk ? sk[r] : KEY_INF;
-    if (threadIdx.x == 0) out_counts[q] = kk;
+    uint32_t P = 1;
+    while (P < n) P <<= 1;
+    for (uint32_t i = n + tid; i < P; i += TK_THREADS) srt[i] = KEY_INF;
+    __syncthreads();
+    bitonic_sort(srt, P);
+    for (uint32_t r = tid; r < k; r += TK_THREADS) out[r] = r < kk ? srt[r] : KEY_INF;
+    if (tid == 0) out_counts[q] = kk;
 }
 
 void launch_topk(const unsigned long long* cand, const uint32_t* ccount, uint32_t cap, uint32_t parts,
