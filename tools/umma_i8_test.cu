@@ -4,6 +4,9 @@
 // queries' +-2^(6-j) weights + bias row live in smem (B, K-major, no swizzle).
 // D[row][q] should equal 64 * (ham(code,q) - tau) - 32.
 // Tries descriptor variants (LBO/SBO swapped) and reports which one is right.
+// Also probes M = 64 with A rows in lanes 0-63: on B200 only rows 0-15 of each
+// 32-lane quadrant come back right, i.e. an M = 64 MMA spans 16 lanes of every
+// quadrant and still needs all four warps (no smaller MMA group for K2).
 #include <cstdio>
 #include <cstdint>
 #include <cstdlib>
@@ -17,7 +20,7 @@ __device__ __forceinline__ void expand_word(uint32_t w, uint32_t* out) {
     out[7] = (w >> 7) & 0x01010101u;
 }
 
-__global__ void k(const uint2* codes, const uint2* qcodes, int tau, int lbo, int sbo, int* dout) {
+__global__ void k(const uint2* codes, const uint2* qcodes, int tau, int lbo, int sbo, int* dout, int MM) {
     __shared__ __align__(1024) int8_t B[16 * 96];  // built in the canonical layout below
     __shared__ uint32_t tmem_base;
     __shared__ __align__(8) uint64_t bar;
@@ -82,7 +85,7 @@ __global__ void k(const uint2* codes, const uint2* qcodes, int tau, int lbo, int
         asm volatile("tcgen05.fence::after_thread_sync;");
         // instruction descriptor: D s32 (2) bits 4-5; A s8 (1) bits 7-9; B s8 (1) bits 10-12; K-major both;
         // N >> 3 at bits 17-22; M >> 4 at bits 24-28
-        const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
+        const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((16u >> 3) << 17) | (((uint32_t)MM >> 4) << 24);
         for (int kb = 0; kb < 3; ++kb) {
             const uint32_t baddr = smem_u32(B) + kb * 2 * lbo;  // K block of 32 bytes = 2 core columns
             uint64_t desc = ((uint64_t)((baddr & 0x3FFFF) >> 4)) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
@@ -128,11 +131,12 @@ int main() {
     cudaMalloc(&dd, 128 * 16 * 4);
     cudaMemcpy(dc, codes.data(), 128 * 8, cudaMemcpyHostToDevice);
     cudaMemcpy(dq, q.data(), 16 * 8, cudaMemcpyHostToDevice);
-    const int variants[2][2] = {{128, 768}, {256, 128}};  // (LBO bytes, SBO bytes)
+    const int variants[1][2] = {{256, 128}};  // (LBO bytes, SBO bytes)
+    for (int MMv : {128, 64})
     for (int tau : {24, 0, 64}) {
         for (auto& v : variants) {
             cudaMemset(dd, 0, 128 * 16 * 4);
-            k<<<1, 128>>>(dc, dq, tau, v[0], v[1], dd);
+            k<<<1, 128>>>(dc, dq, tau, v[0], v[1], dd, MMv);
             cudaError_t e = cudaDeviceSynchronize();
             if (e != cudaSuccess) {
                 printf("lbo %d sbo %d: %s\n", v[0], v[1], cudaGetErrorString(e));
@@ -141,16 +145,18 @@ int main() {
             std::vector<int> h(128 * 16);
             cudaMemcpy(h.data(), dd, h.size() * 4, cudaMemcpyDeviceToHost);
             int bad = 0, first = -1;
-            for (int r = 0; r < 128; ++r)
+            int badrows[4] = {0, 0, 0, 0};
+            for (int r = 0; r < MMv; ++r)
                 for (int n = 0; n < 16; ++n) {
                     const int ham = __builtin_popcount(codes[r].x ^ q[n].x) + __builtin_popcount(codes[r].y ^ q[n].y);
                     const int want = 64 * (ham - tau) - 32;
                     if (h[r * 16 + n] != want) {
                         if (first < 0) first = r * 16 + n;
                         ++bad;
+                        ++badrows[r / 32];
                     }
                 }
-            printf("tau %d lbo %d sbo %d: bad %d / 2048", tau, v[0], v[1], bad);
+            printf("M %d tau %d: bad %d / %d (per quadrant %d %d %d %d)", MMv, tau, bad, MMv * 16, badrows[0], badrows[1], badrows[2], badrows[3]);
             if (first >= 0) {
                 const int r = first / 16, n = first % 16;
                 const int ham = __builtin_popcount(codes[r].x ^ q[n].x) + __builtin_popcount(codes[r].y ^ q[n].y);
