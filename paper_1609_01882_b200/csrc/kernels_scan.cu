@@ -601,7 +601,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
                         uint32_t m;
                         if constexpr (TCF) {
                             // this tile's MMA was issued when the quad's last warp staged it
-                            mbar_wait_backoff(&qbar_s[quad], qphase);
+                            mbar_wait_backoff<POLY_SPIN_MMA_NS>(&qbar_s[quad], qphase);
                             qphase ^= 1u;
                             tc_fence_after();
                             // sign bits: bit q <- code li, bit 16 + q <- code li + 32

@@ -43,6 +43,9 @@ constexpr int DSUB = 16;               // every configuration: 128/8 and 256/16
 #ifndef POLY_PROD_SPIN_NS
 #define POLY_PROD_SPIN_NS 0
 #endif
+#ifndef POLY_SPIN_MMA_NS  // K2: backoff of the quad-MMA commit wait
+#define POLY_SPIN_MMA_NS 400
+#endif
 #ifndef POLY_SPIN_NS
 #define POLY_SPIN_NS 400
 #endif
@@ -221,12 +224,13 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 
 // Wait with a timer backoff (POLY_SPIN_NS > 0): a suspended try_wait wakes on any
 // mbarrier activity in the CTA, which a 25-warp K2 has plenty of.
+template <uint32_t NS = POLY_SPIN_NS>
 __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
-#if POLY_SPIN_NS > 0
-    while (!mbar_test(bar, parity)) __nanosleep(POLY_SPIN_NS);
-#else
-    mbar_wait(bar, parity);
-#endif
+    if constexpr (NS > 0) {
+        while (!mbar_test(bar, parity)) __nanosleep(NS);
+    } else {
+        mbar_wait(bar, parity);
+    }
 }
 
 // 1-D TMA bulk copy global -> shared, completion counted on `bar` (bytes % 16 == 0).
