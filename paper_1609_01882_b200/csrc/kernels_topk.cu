@@ -21,7 +21,10 @@ namespace pb {
 constexpr int TK_THREADS = 512;
 constexpr uint32_t TK_SMEM_KEYS = 8192;
 constexpr int TK_MAXPARTS = 64;
-constexpr uint32_t TK_DIRECT = 2048;  // at most this many: sort them all
+#ifndef POLY_TK_DIRECT
+#define POLY_TK_DIRECT 2048
+#endif
+constexpr uint32_t TK_DIRECT = POLY_TK_DIRECT;  // at most this many: sort them all
 constexpr uint32_t TK_SEL_KEYS = 4096;  // >= k + 1 (k <= 2048); with 2048 buckets: 104 KB, two CTAs per SM
 constexpr uint32_t TK_BUCKETS = 2048;
 
