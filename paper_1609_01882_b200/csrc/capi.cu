@@ -147,7 +147,7 @@ void ensure_scratch(poly_b200_index* ix, uint32_t k) {
         ix->cand_bs = bs;
         ix->cand_cap = cap;
         ix->cand = dalloc<unsigned long long>((size_t)NQB * ix->cand_cap);
-        ix->ctrl_words = NQB + 4 + (size_t)NQB * (cap / bs);
+        ix->ctrl_words = NQB + 4 + (size_t)NQB * (cap / bs) + 32;  // + per-group work counters (last 32)
         ix->ctrl = dalloc<uint32_t>(ix->ctrl_words);
     }
     if (!ix->cand_w) {
@@ -265,7 +265,7 @@ void run_batches(poly_b200_index* ix, const float* d_queries, uint64_t nq, const
             a.cap = ix->cand_cap;
             a.ccount = ix->ctrl;
             a.overflow = ix->ctrl + NQB;
-            a.work = ix->ctrl + NQB + 1;
+            a.work = POLY_AFFINE ? ix->ctrl + ix->ctrl_words - 32 : ix->ctrl + NQB + 1;
             a.bdone = ix->ctrl + NQB + 4;
             a.surv = perq ? ix->surv : ix->surv_total;
             const uint64_t want = std::max<uint64_t>(1, ntiles * a.ngroups / ((uint64_t)POLY_UNITS_PER_CTA * ix->num_sms));
@@ -273,7 +273,9 @@ void run_batches(poly_b200_index* ix, const float* d_queries, uint64_t nq, const
             a.ntiles = ntiles;
             a.tile_stride = 1;
             a.bs = ix->cand_bs;
-            a.units = (uint32_t)((ntiles + a.tiles_per_chunk - 1) / a.tiles_per_chunk) * a.ngroups;
+            a.nchunks = (uint32_t)((ntiles + a.tiles_per_chunk - 1) / a.tiles_per_chunk);
+            a.units = a.nchunks * a.ngroups;
+            a.affine = POLY_AFFINE;
             cudaEvent_t e0 = nullptr, e1 = nullptr;
             if (ix->profiling) {
                 if (ix->prof_used == ix->prof_events.size()) {

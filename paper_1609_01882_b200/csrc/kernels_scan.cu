@@ -370,8 +370,30 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
         }
     };  // tiles consumed so far: stage = seq % STAGES, parity = (seq / STAGES) & 1
 
+    __shared__ uint32_t cg_s;  // affine schedule: this CTA's current query group
+    if (threadIdx.x == 0) cg_s = blockIdx.x % a.ngroups;
     for (;;) {
-        if (threadIdx.x == 0) unit_s = atomicAdd(a.work, 1u);
+        if (threadIdx.x == 0) {
+            if (a.affine) {
+                // next chunk of the current group; a dry group hands over to the next
+                // one round-robin (a LUT reload); a full cycle of dry groups ends the scan
+                const uint32_t g0 = cg_s;
+                uint32_t g = g0, u = a.units;
+                for (;;) {
+                    const uint32_t c = atomicAdd(&a.work[g], 1u);
+                    if (c < a.nchunks) {
+                        u = c * a.ngroups + g;
+                        break;
+                    }
+                    g = g + 1 == a.ngroups ? 0 : g + 1;
+                    if (g == g0) break;
+                }
+                cg_s = g;
+                unit_s = u;
+            } else {
+                unit_s = atomicAdd(a.work, 1u);
+            }
+        }
         __syncthreads();
         const uint32_t unit = unit_s;
         if (unit >= a.units) break;

@@ -13,6 +13,9 @@ constexpr int DSUB = 16;               // every configuration: 128/8 and 256/16
 #ifndef POLY_WAIT_HINT  // mbarrier try_wait suspend-time hint (ns); 0 = none
 #define POLY_WAIT_HINT 20000
 #endif
+#ifndef POLY_AFFINE  // 1: group-affine K2 schedule
+#define POLY_AFFINE 1
+#endif
 #ifndef POLY_UNITS_PER_CTA  // K2 work units per CTA the unit size aims for (capped by POLY_MAX_TPC)
 #define POLY_UNITS_PER_CTA 16
 #endif
@@ -89,6 +92,9 @@ struct ScanArgs {
     uint32_t* overflow;          // set when a candidate did not fit
     uint32_t* work;              // dynamic work-unit counter
     uint32_t units, ngroups, tiles_per_chunk;
+    // group-affine schedule (affine = 1): work[g] counts the chunks handed out of
+    // query group g; a CTA stays on its group (no LUT reload) until it runs dry
+    uint32_t affine, nchunks;
     uint64_t ntiles;             // logical tiles; physical tile = logical * tile_stride
     uint64_t tile_stride;
     uint32_t bs;                 // candidate block size (>= k) for threshold selects
