@@ -227,9 +227,11 @@ void run_batches(poly_b200_index* ix, const float* d_queries, uint64_t nq, const
             a.ngroups = (nqb + Q - 1) / Q;
             // Seed: one CTA per query ranks a fixed 256-code-run sample (K2s); then
             // the geometric warm-up levels below start from that bound.
-            if (POLY_SEED_BLOCKS > 0 && ix->n > ix->cand_cap / 8)
-                pb::launch_seed_sample(a, strategy, ix->m, nqb,
-                                       (uint32_t)std::min<uint64_t>(POLY_SEED_BLOCKS, (ix->n + 255) / 256), s);
+            // at most n / 256 runs: runs never overlap, so no code is sampled twice (a repeated
+            // key would make the sample's k-th key too small and the bound invalid)
+            const uint64_t seed_blocks = std::min<uint64_t>(POLY_SEED_BLOCKS, ix->n / 256);
+            if (seed_blocks > 0 && ix->n > ix->cand_cap / 8)
+                pb::launch_seed_sample(a, strategy, ix->m, nqb, (uint32_t)seed_blocks, s);
             // Warm-up: strided samples of POLY_WARM_FIRST tiles (x8 per further level,
             // POLY_WARM_LEVELS levels) spread over the database, each scanned with the
             // current bound and ranked exactly (K3) to tighten it.  With the K2s seed and

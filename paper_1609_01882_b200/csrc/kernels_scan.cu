@@ -745,14 +745,17 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
 }
 
 // K2s: threshold seed from a fixed sample, one CTA per query.  The sample is
-// SEED_BLOCKS runs of 256 consecutive codes spread evenly over the database
+// seed_blocks <= n / 256 disjoint runs of 256 consecutive codes spread evenly over the database
 // (coalesced loads; the same runs for every query, so they stay in L2).  Each
 // sampled code is scored exactly as K2 does (filter, then ADC / Hamming /
 // disidx); the k-th smallest key of the sample (8-pass radix select over the
 // keys staged in shared memory) bounds the final k-th key, so
 // thr[q] = min(thr[q], kth + 1).  A key buffer that fills up keeps the first
 // SEED_KEYS keys: the k-th of a subset is a weaker but still valid bound.
-constexpr uint32_t SEED_THREADS = 256, SEED_KEYS = 4096;
+#ifndef POLY_SEED_KEYS
+#define POLY_SEED_KEYS 4096
+#endif
+constexpr uint32_t SEED_THREADS = 256, SEED_KEYS = POLY_SEED_KEYS;
 
 template <int M, int STRAT>
 __global__ void __launch_bounds__(SEED_THREADS) seed_sample_kernel(const ScanArgs a, uint32_t seed_blocks) {

@@ -29,7 +29,7 @@ constexpr int DSUB = 16;               // every configuration: 128/8 and 256/16
 #define POLY_SEL_KF 4
 #endif
 #ifndef POLY_WARM_LEVELS  // at most this many geometric warm-up samples before the full scan
-#define POLY_WARM_LEVELS 1
+#define POLY_WARM_LEVELS 0
 #endif
 #ifndef POLY_WARM_FIRST  // tiles in the first warm-up sample (x8 per further level)
 #define POLY_WARM_FIRST 128
@@ -38,7 +38,7 @@ constexpr int DSUB = 16;               // every configuration: 128/8 and 256/16
 #define POLY_WARM_SEL 0
 #endif
 #ifndef POLY_SEED_BLOCKS  // K2s seed sample: runs of 256 codes (0 = no seed kernel)
-#define POLY_SEED_BLOCKS 64
+#define POLY_SEED_BLOCKS 128
 #endif
 #ifndef POLY_COARSE_GEMM  // 1: enumerate_cells via TF32 dots + exact re-rank (K5r)
 #define POLY_COARSE_GEMM 1

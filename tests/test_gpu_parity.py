@@ -350,3 +350,19 @@ def test_topk_select_paths(pb, pq8, parts, k, dist):
         assert int(cnt[q]) == min(k, allk.size)
         assert np.array_equal(ids[q].cpu().numpy()[:want.size], (want & np.uint64(0xFFFFFFFF)).astype(np.int64))
         assert np.array_equal(_bits(scs[q].cpu().numpy()[:want.size]), (want >> np.uint64(32)).astype(np.uint32))
+
+
+@pytest.mark.parametrize("n", [16_400, 20_000, 25_700, 33_000, 70_000])
+def test_seed_sample_sizes_match_oracle(pb, pq8, g8, n):
+    """DB sizes around the K2s seed sample (runs of 256 codes, at most n / 256 of them):
+    the seeded bound must never drop a true top-k member (a code sampled twice would)."""
+    codes = np.concatenate([g8["codes"]] * (n // g8["codes"].shape[0] + 1))[:n]
+    ids = np.arange(n, dtype=np.int64) * 3 + 11
+    ix = _index(pb, pq8, codes, ids)
+    for tau in (20, 24, 32):
+        want_ids, want_sc, want_cnt, want_surv, _ = oracle.search(pq8, codes, g8["queries"][:64], 100, tau=tau,
+                                                                  ids=ids, threads=16)
+        got_ids, got_sc, got_cnt = ix.search_batch(g8["queries"][:64], pb.SearchParams(pb.Strategy.dual, 100, tau))
+        assert _same(got_ids, want_ids), (n, tau)
+        assert _same(_bits(got_sc), _bits(want_sc)), (n, tau)
+        assert _same(got_cnt, want_cnt), (n, tau)
