@@ -366,3 +366,40 @@ def test_seed_sample_sizes_match_oracle(pb, pq8, g8, n):
         assert _same(got_ids, want_ids), (n, tau)
         assert _same(_bits(got_sc), _bits(want_sc)), (n, tau)
         assert _same(got_cnt, want_cnt), (n, tau)
+
+
+def test_full_config1_size(pb, pq8):
+    """BASELINE config 1 at its full size: N = 1e8 codes (generated + encoded on the GPU),
+    one 256-query batch at tau = 24.  Exact against the oracle (the reference two-pass
+    dual) for 8 queries over all 1e8 codes; for all 256 queries, size-independent checks
+    of every returned neighbour: Hamming(code, qcode) <= tau, score == the fp32 ADC of its
+    code (sq order), ascending (score, id) keys, counts = min(k, survivors)."""
+    import os as _os
+    seed = 160901882
+    centers = oracle.gen_centers(seed, 1000, 128)
+    ix = _index(pb, pq8)
+    ix.add_synthetic(seed, centers, 0, 100_000_000)
+    queries = oracle.gen_points(seed, 3, 0, 256, centers)
+    tau, k = 24, 100
+    ids, sc, cnt = ix.search_batch(queries, pb.SearchParams(pb.Strategy.dual, k, tau))
+    codes = ix.codes()  # 800 MB on the host
+    sub = np.array([0, 1, 37, 101, 128, 199, 254, 255])
+    st = pb.SearchStats()
+    ids_s, sc_s, cnt_s = ix.search_batch(queries[sub], pb.SearchParams(pb.Strategy.dual, k, tau), st)
+    oi, osc, oc, osv, _ = oracle.search(pq8, codes, queries[sub], k, tau=tau, threads=_os.cpu_count() or 8)
+    assert _same(ids_s, oi) and _same(ids[sub], oi)
+    assert _same(_bits(sc_s), _bits(osc)) and _same(_bits(sc[sub]), _bits(osc))
+    assert _same(cnt_s, oc) and _same(cnt[sub], oc)
+    assert st.survivors == int(osv.sum())
+    # every returned neighbour of every query
+    lutp, qc = pb.flat_index.debug_lut(ix, queries)
+    assert (cnt == k).all()  # 1e8 codes: every query has >= k survivors
+    rows = codes[ids]                                            # [256, k, 8]
+    ham = np.unpackbits(rows ^ qc[:, None, :], axis=2).sum(2)
+    assert (ham <= tau).all()
+    acc = np.zeros(ids.shape, np.float32)
+    for s in range(8):
+        acc = (acc + np.take_along_axis(lutp[:, s, :], rows[:, :, s].astype(np.int64), axis=1)).astype(np.float32)
+    assert _same(_bits(acc), _bits(sc))
+    keys = (_bits(sc).astype(np.uint64) << np.uint64(32)) | ids.astype(np.uint64)
+    assert (keys[:, 1:] > keys[:, :-1]).all()  # strictly ascending (score, id)
