@@ -403,3 +403,30 @@ def test_full_config1_size(pb, pq8):
     assert _same(_bits(acc), _bits(sc))
     keys = (_bits(sc).astype(np.uint64) << np.uint64(32)) | ids.astype(np.uint64)
     assert (keys[:, 1:] > keys[:, :-1]).all()  # strictly ascending (score, id)
+
+
+def test_full_config3_size(pb, pq16):
+    """BASELINE config 3 at its full size: N = 2e8 128-bit codes (m = 16, POPC filter),
+    tau = 56.  Exact against the oracle for 4 queries over all 2e8 codes; every returned
+    neighbour of a 64-query batch satisfies the Hamming bound and carries the exact ADC."""
+    import os as _os
+    seed = 160901882
+    centers = oracle.gen_centers(seed, 4096, 256)
+    ix = _index(pb, pq16)
+    ix.add_synthetic(seed, centers, 0, 200_000_000)
+    queries = oracle.gen_points(seed, 3, 0, 64, centers)
+    tau, k = 56, 100
+    ids, sc, cnt = ix.search_batch(queries, pb.SearchParams(pb.Strategy.dual, k, tau))
+    codes = ix.codes()  # 3.2 GB on the host
+    sub = np.array([0, 17, 42, 63])
+    oi, osc, oc, _, _ = oracle.search(pq16, codes, queries[sub], k, tau=tau, threads=_os.cpu_count() or 8)
+    assert _same(ids[sub], oi)
+    assert _same(_bits(sc[sub]), _bits(osc))
+    assert _same(cnt[sub], oc)
+    lutp, qc = pb.flat_index.debug_lut(ix, queries)
+    rows = codes[ids]
+    assert (np.unpackbits(rows ^ qc[:, None, :], axis=2).sum(2) <= tau).all()
+    acc = np.zeros(ids.shape, np.float32)
+    for s in range(16):
+        acc = (acc + np.take_along_axis(lutp[:, s, :], rows[:, :, s].astype(np.int64), axis=1)).astype(np.float32)
+    assert _same(_bits(acc), _bits(sc))
