@@ -249,3 +249,61 @@ def test_sharded_ivf_merge_matches_unsharded(pb, gi):
     odd.add(base[:1000], ids=np.arange(1000) * 3)
     with pytest.raises(pb.PolyError):
         odd.search_keys_device(dq, pb.CoarseParams(pb.Strategy.dual, k, 26, 8, 0), keys[0], cnts[0])
+
+
+def test_full_config2_size(pb):
+    """BASELINE config 2 at its per-GPU size: 1.25e8 residual codes in 65,536 lists (the
+    bench's build: GPU generator, TF32 nearest-cell assignment, exact residual encoding).
+    The oracle searches the identical lists (read back with lists()): 4 queries exact at
+    nprobe 16; every returned neighbour of a 256-query batch lies in one of its query's
+    probed cells."""
+    import time
+    import torch
+    from paper_1609_01882_b200 import synth
+    seed = 160901882
+    z = np.load(os.path.join(os.path.dirname(GOLDEN), "pq_ivf65536_d128_m8.npz"))
+    pq = pb.ProductQuantizer(8, 8, 128, z["codebooks"], z["perms"])
+    opq = oracle.PQ(8, 8, 128, z["codebooks"], z["perms"])
+    centers = synth.gen_centers(seed, 1000, 128)
+    coarse = synth.gen_points(seed, 1, 0, 65536, centers)
+    ivf = pb.IVFIndex(pq, coarse)
+    n, chunk = 125_000_000, 1 << 22
+    t = time.time()
+    torch.backends.cuda.matmul.allow_tf32 = True
+    dc = torch.from_numpy(coarse).cuda()
+    cn = (dc * dc).sum(1)
+    x = torch.empty((chunk, 128), device="cuda")
+    cells = torch.empty(chunk, dtype=torch.int32, device="cuda")
+    for r in range(0, n, chunk):
+        nb = min(chunk, n - r)
+        pb.gen_points_device(centers, seed, 2, r, nb, x[:nb])
+        for b in range(0, nb, 16384):
+            xs = x[b:min(b + 16384, nb)]
+            cells[b:b + xs.shape[0]] = torch.argmin(cn[None, :] - 2.0 * (xs @ dc.T), dim=1).to(torch.int32)
+        ivf.add_device(x[:nb], cells[:nb], r)
+    torch.cuda.synchronize()
+    build_s = time.time() - t
+    queries = synth.gen_points(seed, 3, 0, 256, centers)
+    p = pb.CoarseParams(pb.Strategy.dual, 100, 26, 16, 0)
+    ids, sc, cnt = ivf.search(queries, p)
+    off, codes, lids = ivf.lists()
+    lists = oracle.IVFLists(off, codes, lids)
+    sub = np.array([0, 85, 170, 255])
+    oi, osc, oc, _, _, pr = oracle.ivf_search(opq, coarse, lists, queries[sub], 100, 16, tau=26,
+                                              threads=os.cpu_count() or 8)
+    assert _same(ids[sub], oi)
+    assert _same(_bits(sc[sub]), _bits(osc))
+    assert _same(cnt[sub], oc)
+    assert _same(ivf.probes(queries[sub], 16), pr)
+    # every returned neighbour sits in one of its query's probed cells
+    probes = ivf.probes(queries, 16)
+    cell_of = np.empty(n, np.int64)
+    cell_of[lids] = np.repeat(np.arange(65536), np.diff(off).astype(np.int64))
+    for qi in range(256):
+        got = ids[qi, :cnt[qi]]
+        assert np.isin(cell_of[got], probes[qi]).all(), qi
+    print(f"build {build_s:.1f} s")
+
+
+def _same(a, b):
+    return np.array_equal(np.asarray(a), np.asarray(b))
