@@ -307,3 +307,53 @@ def test_full_config2_size(pb):
 
 def _same(a, b):
     return np.array_equal(np.asarray(a), np.asarray(b))
+
+
+def test_full_config4_size(pb):
+    """BASELINE config 4 at its full size: 1e7 unit-normalised 256-d vectors, IVF 16,384
+    + PQ m=16, knn_graph with nprobe 32, ht 52, k 10 (SPEC.md:391-396) for 2,048 rows;
+    4 rows exact against the oracle on the same lists (k + 1 results, self removed)."""
+    import torch
+    from paper_1609_01882_b200 import synth
+    seed = 160901882
+    z = np.load(os.path.join(os.path.dirname(GOLDEN), "pq_ivf16384_d256_m16.npz"))
+    pq = pb.ProductQuantizer(16, 8, 256, z["codebooks"], z["perms"])
+    opq = oracle.PQ(16, 8, 256, z["codebooks"], z["perms"])
+    centers = synth.gen_centers(seed, 4096, 256)
+    coarse = synth.gen_points(seed, 1, 0, 16384, centers, normalize=True)
+    ivf = pb.IVFIndex(pq, coarse)
+    n, chunk = 10_000_000, 1 << 21
+    torch.backends.cuda.matmul.allow_tf32 = True
+    dc = torch.from_numpy(coarse).cuda()
+    cn = (dc * dc).sum(1)
+    x = torch.empty((chunk, 256), device="cuda")
+    cells = torch.empty(chunk, dtype=torch.int32, device="cuda")
+    for r in range(0, n, chunk):
+        nb = min(chunk, n - r)
+        pb.gen_points_device(centers, seed, 2, r, nb, x[:nb], normalize=True)
+        for b in range(0, nb, 16384):
+            xs = x[b:min(b + 16384, nb)]
+            cells[b:b + xs.shape[0]] = torch.argmin(cn[None, :] - 2.0 * (xs @ dc.T), dim=1).to(torch.int32)
+        ivf.add_device(x[:nb], cells[:nb], r)
+    row0, rows, k = 4_000_000, 2048, 10
+    dx = torch.empty((rows, 256), device="cuda")
+    pb.gen_points_device(centers, seed, 2, row0, rows, dx, normalize=True)
+    ids = torch.empty((rows, k), dtype=torch.int64, device="cuda")
+    sc = torch.empty((rows, k), dtype=torch.float32, device="cuda")
+    cnt = torch.empty(rows, dtype=torch.int32, device="cuda")
+    ivf.knn_graph_device(dx, row0, pb.CoarseParams(pb.Strategy.dual, k, 52, 32, 0), ids, sc, cnt)
+    torch.cuda.synchronize()
+    off, codes, lids = ivf.lists()
+    lists = oracle.IVFLists(off, codes, lids)
+    sub = np.array([0, 700, 1400, 2047])
+    xq = dx[sub].cpu().numpy()
+    oi, osc, oc, _, _, _ = oracle.ivf_search(opq, coarse, lists, xq, k + 1, 32, tau=52, threads=os.cpu_count() or 8)
+    for j, r in enumerate(sub):
+        row, srow = list(oi[j, :oc[j]]), list(osc[j, :oc[j]])
+        if row0 + r in row:
+            i = row.index(row0 + r)
+            del row[i], srow[i]
+        row, srow = row[:k], srow[:k]
+        assert ids[r].cpu().numpy()[:len(row)].tolist() == row, r
+        assert _same(_bits(sc[r].cpu().numpy()[:len(row)]), _bits(np.array(srow, np.float32)))
+        assert int(cnt[r]) == len(row)
