@@ -245,6 +245,9 @@ __device__ unsigned long long warp_select_kth(const unsigned long long* src, uin
 #ifndef POLY_TC  // 1: DUAL's Hamming filter on the tensor cores (int8 tcgen05.mma); 0: POPC
 #define POLY_TC 1
 #endif
+#ifndef POLY_TC16  // 1: the tensor-core filter also for m = 16
+#define POLY_TC16 0
+#endif
 #ifndef POLY_RING
 #define POLY_RING 288
 #endif
@@ -295,7 +298,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
     __shared__ uint32_t sel_hist[256];
     __shared__ uint32_t req_head_s;
     // tensor-core filter state: B operand (query weights + bias), per-quad MMA barriers, TMEM base
-    constexpr bool TCF = POLY_TC && STRAT == DUAL && M == 8;  // m = 16: 8 queries per CTA do not amortise the expansion
+    constexpr bool TCF = POLY_TC && STRAT == DUAL && (M == 8 || POLY_TC16);  // m = 16: 8 queries per CTA (A/B in DESIGN)
     constexpr int KB = M * 8 + 32;   // B row bytes: one per code bit + the bias block
     constexpr int NKB = KB / 32;     // K blocks of 32 bytes
     constexpr int AC = 2 * M;        // TMEM columns of one expanded code (M * 8 bytes)
