@@ -430,3 +430,42 @@ def test_full_config3_size(pb, pq16):
     for s in range(16):
         acc = (acc + np.take_along_axis(lutp[:, s, :], rows[:, :, s].astype(np.int64), axis=1)).astype(np.float32)
     assert _same(_bits(acc), _bits(sc))
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_randomized_against_oracle(pb, pq8, pq16, g8, g16, seed):
+    """Randomised sweep (sizes around tiles, seed runs, warm-up gates, batches and
+    groups; k, tau, strategy, m, id schemes) of the flat search against the oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    wide = seed % 3 == 2
+    pq, g = (pq16, g16) if wide else (pq8, g8)
+    n = int(rng.choice([1, 7, 255, 256, 1535, 1536, 1537, 16385, 20000, 33000, 70000, 150000]))
+    nq = int(rng.choice([1, 15, 16, 17, 100, 257, 300]))
+    k = int(rng.choice([1, 10, 100, 257]))
+    strategy = ["dual", "dual", "dual", "adc", "binary", "disidx"][seed % 6]
+    tau = int(rng.integers(0, pq.code_bits + 1)) if strategy == "dual" else 0
+    base = g["codes"]
+    codes = base[rng.integers(0, base.shape[0], n)]
+    id_mode = seed % 4
+    if id_mode == 0:
+        ids = None                                                   # positions
+    elif id_mode == 1:
+        ids = np.arange(n, dtype=np.int64) + 5_000_000_000          # arithmetic, above 2^32
+    elif id_mode == 2:
+        ids = rng.permutation(n).astype(np.int64) * 7 + 3           # arbitrary, not monotone
+    else:
+        ids = np.arange(n, dtype=np.int64) * 2                      # not consecutive
+    qsrc = g["queries"]
+    queries = qsrc[rng.integers(0, qsrc.shape[0], nq)] + rng.normal(0, 0.01, (nq, qsrc.shape[1])).astype(np.float32)
+    queries = np.abs(queries).astype(np.float32)
+    ix = _index(pb, pq, codes, ids)
+    oi, osc, oc, osv, _ = oracle.search(pq, codes, queries, k, tau=tau, strategy=strategy,
+                                        ids=np.arange(n, dtype=np.int64) if ids is None else ids, threads=16)
+    st = pb.SearchStats()
+    gi, gsc, gc = ix.search_batch(queries, pb.SearchParams(pb.strategy_from_string(strategy), k, tau), st)
+    ctx = (n, nq, k, strategy, tau, wide, id_mode)
+    assert _same(gi, oi), ctx
+    assert _same(_bits(gsc), _bits(osc)), ctx
+    assert _same(gc, oc), ctx
+    if strategy == "dual" and tau < pq.code_bits:
+        assert st.survivors == int(osv.sum()), ctx
