@@ -357,3 +357,43 @@ def test_full_config4_size(pb):
         assert ids[r].cpu().numpy()[:len(row)].tolist() == row, r
         assert _same(_bits(sc[r].cpu().numpy()[:len(row)]), _bits(np.array(srow, np.float32)))
         assert int(cnt[r]) == len(row)
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_randomized_ivf_against_oracle(pb, gi, seed):
+    """Randomised IVF sweep (cells, list sizes, nprobe incl. > 64, cap, tau, strategy, k,
+    ids) of search_coarse against the oracle (exact assignment + residual encoding on
+    both sides, so the lists are the same)."""
+    rng = np.random.default_rng(2000 + seed)
+    dseed = int(gi["data_seed"])
+    centers = oracle.gen_centers(dseed, 1000, 128)
+    nlist = int(rng.choice([1, 3, 64, 200, 1024]))
+    n = int(rng.choice([0, 1, 500, 5000, 40000]))
+    coarse = oracle.gen_points(dseed, 1, int(rng.integers(0, 1000)), nlist, centers)
+    base = oracle.gen_points(dseed, 2, int(rng.integers(0, 10_000)), n, centers) if n else np.zeros((0, 128), np.float32)
+    ids = (rng.permutation(n).astype(np.int64) * 5 + 1) if seed % 2 else np.arange(n, dtype=np.int64)
+    nq = int(rng.choice([1, 17, 256, 300]))
+    queries = oracle.gen_points(dseed, 3, int(rng.integers(0, 1000)), nq, centers)
+    nprobe = int(min(nlist, rng.choice([1, 4, 16, 65, 100])))
+    k = int(rng.choice([1, 10, 100]))
+    strategy = ["dual", "dual", "adc", "binary", "disidx"][seed % 5]
+    tau = int(rng.integers(0, 65)) if strategy == "dual" else 64
+    cap = int(rng.choice([0, 0, 300]))
+    pq = gi["pq"]
+    ix = pb.IVFIndex(pb.ProductQuantizer(8, 8, 128, gi["codebooks"], gi["perms"]), coarse)
+    if n:
+        ix.add(base, ids=ids)
+        lists, _ = oracle.ivf_build(pq, base, coarse, ids=ids)
+    else:
+        lists = oracle.IVFLists(np.zeros(nlist + 1, np.uint64), np.zeros((0, 8), np.uint8), np.zeros(0, np.int64))
+    oi, osc, oc, osv, oscan, opr = oracle.ivf_search(pq, coarse, lists, queries, k, nprobe, tau=tau,
+                                                     strategy=strategy, cap=cap, threads=16)
+    st = pb.SearchStats()
+    gi_, gsc, gc = ix.search(queries, pb.CoarseParams(pb.strategy_from_string(strategy), k, tau, nprobe, cap), st)
+    ctx = (nlist, n, nq, nprobe, k, strategy, tau, cap)
+    assert np.array_equal(ix.probes(queries, nprobe), opr), ctx
+    assert np.array_equal(gi_, oi), ctx
+    assert np.array_equal(_bits(gsc), _bits(osc)), ctx
+    assert np.array_equal(gc, oc), ctx
+    if n and strategy == "dual" and tau < 64:
+        assert st.survivors == int(osv.sum()), ctx
