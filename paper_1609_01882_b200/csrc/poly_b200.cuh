@@ -53,7 +53,7 @@ constexpr int DSUB = 16;               // every configuration: 128/8 and 256/16
 #define POLY_SPIN_NS 400
 #endif
 #ifndef POLY_TILE_BYTES
-#define POLY_TILE_BYTES 12288
+#define POLY_TILE_BYTES 14336
 #endif
 #ifndef POLY_STAGES
 #define POLY_STAGES 4
@@ -61,7 +61,7 @@ constexpr int DSUB = 16;               // every configuration: 128/8 and 256/16
 constexpr int TILE_BYTES = POLY_TILE_BYTES;  // code bytes per pipeline stage (1536 codes at m = 8)
 constexpr int STAGES = POLY_STAGES;          // bulk-copy ring depth
 #ifndef POLY_SCAN_WARPS
-#define POLY_SCAN_WARPS 24
+#define POLY_SCAN_WARPS 28
 #endif
 constexpr int SCAN_WARPS = POLY_SCAN_WARPS;  // K2 consumer warps (plus one TMA producer warp)
 constexpr int BS = 4096;               // candidate block size for threshold selects
