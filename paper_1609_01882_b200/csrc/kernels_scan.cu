@@ -248,6 +248,9 @@ __device__ unsigned long long warp_select_kth(const unsigned long long* src, uin
 #ifndef POLY_TC16  // 1: the tensor-core filter also for m = 16
 #define POLY_TC16 0
 #endif
+#ifndef POLY_AFFINE_LEAD  // chunks a query group may run ahead of the slowest one
+#define POLY_AFFINE_LEAD 16
+#endif
 #ifndef POLY_RING
 #define POLY_RING 288
 #endif
@@ -378,18 +381,29 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
     for (;;) {
         if (threadIdx.x == 0) {
             if (a.affine) {
-                // next chunk of the current group; a dry group hands over to the next
-                // one round-robin (a LUT reload); a full cycle of dry groups ends the scan
-                const uint32_t g0 = cg_s;
-                uint32_t g = g0, u = a.units;
-                for (;;) {
+                // next chunk of the current group.  A group may lead the slowest group
+                // still holding work by at most POLY_AFFINE_LEAD chunks: beyond that (or when
+                // its own group is dry) the CTA helps the slowest group (one LUT reload).  All
+                // groups then sweep the same window of the database, which L2 keeps, so
+                // the codes are read from HBM about once per batch.
+                uint32_t g = cg_s, u = a.units;
+                for (uint32_t tries = 0; tries < 4 * a.ngroups + 4; ++tries) {
+                    uint32_t gmin = g, cmin = 0xFFFFFFFFu;
+                    for (uint32_t h = 0; h < a.ngroups; ++h) {
+                        const uint32_t c = *(volatile uint32_t*)&a.work[h];
+                        if (c < a.nchunks && c < cmin) {
+                            cmin = c;
+                            gmin = h;
+                        }
+                    }
+                    if (cmin == 0xFFFFFFFFu) break;  // every group is dry
+                    const uint32_t cg = *(volatile uint32_t*)&a.work[g];
+                    if (cg >= a.nchunks || cg > cmin + POLY_AFFINE_LEAD) g = gmin;
                     const uint32_t c = atomicAdd(&a.work[g], 1u);
                     if (c < a.nchunks) {
                         u = c * a.ngroups + g;
                         break;
                     }
-                    g = g + 1 == a.ngroups ? 0 : g + 1;
-                    if (g == g0) break;
                 }
                 cg_s = g;
                 unit_s = u;

@@ -8,5 +8,5 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
 echo "launch-list rc=$?"
 C2="python tools/prof_scan.py --n 100000000 --ht 24"
 $C2 > gpurun_out/plain_scan.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:scan_kernel -s 1 -c 1 -o gpurun_out/prof_scan_full $C2 > gpurun_out/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:scan_kernel -s 0 -c 1 -o gpurun_out/prof_scan_full $C2 > gpurun_out/ncu_full.log 2>&1
 echo "full rc=$?"
