@@ -51,6 +51,7 @@ struct poly_b200_ivf {
     unsigned long long* probe_keys = nullptr;
     uint32_t* probe_counts = nullptr;
     uint32_t* np_eff = nullptr;
+    uint32_t* split = nullptr;  // per query: probes of round 1
     unsigned long long* scanned = nullptr;
     uint32_t scratch_nprobe = 0;
     float* lutp = nullptr;
@@ -92,6 +93,14 @@ struct poly_b200_ivf {
 
 namespace {
 
+#ifndef POLY_IVF_R1_MAX
+#define POLY_IVF_R1_MAX 2
+#endif
+#ifndef POLY_IVF_R1_CODES
+#define POLY_IVF_R1_CODES 2048
+#endif
+constexpr uint32_t IVF_R1_MAX = POLY_IVF_R1_MAX;      // round 1: at most this many leading probes
+constexpr uint64_t IVF_R1_CODES = POLY_IVF_R1_CODES;  // ... and at least this many codes
 constexpr uint32_t IVF_CHUNK = 1024;  // K6 round-1 work item: 1024 list rows (8 warps x 128)
 
 __global__ void fill_u32(uint32_t* p, uint64_t n, uint32_t v) {
@@ -174,6 +183,7 @@ void ensure_ivf_scratch(poly_b200_ivf* iv, uint32_t nprobe, uint32_t k) {
         iv->ckeys = dalloc<unsigned long long>((size_t)IVF_NQB * std::max<uint32_t>(iv->nlist, 64 * 64));
         iv->nl_counts = dalloc<uint32_t>((size_t)IVF_NQB * 64);  // per-slice counts (K5s) or nlist (K5)
         iv->np_eff = dalloc<uint32_t>(IVF_NQB);
+        iv->split = dalloc<uint32_t>(IVF_NQB);
         iv->scanned = dalloc<unsigned long long>(IVF_NQB);
         iv->ctrl = dalloc<uint32_t>(IVF_NQB + 32);
         iv->thr = dalloc<unsigned long long>(IVF_NQB);
@@ -263,7 +273,8 @@ void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_
     CK(cudaMemsetAsync(iv->ctrl, 0, (IVF_NQB + 32) * 4, s));
     CK(cudaMemsetAsync(iv->thr, 0xFF, IVF_NQB * 8, s));
     enumerate_cells(iv, d_q, nqb, np, s);
-    pb::launch_ivf_probe_count(iv->probe_keys, nqb, np, iv->d_off, p->cap, iv->np_eff, iv->scanned, s);
+    pb::launch_ivf_probe_count(iv->probe_keys, nqb, np, iv->d_off, p->cap, iv->np_eff, iv->scanned, s, iv->split,
+                               IVF_R1_CODES, IVF_R1_MAX);
     add_u64<<<1, 256, 0, s>>>(iv->scanned, nqb, iv->scan_total);
     pb::count_launch();
     pb::launch_residual_lut(d_q, nqb, iv->dim, iv->m, iv->probe_keys, np, iv->d_coarse, iv->d_codebooks,
@@ -287,19 +298,22 @@ void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_
     a.surv_total = iv->surv_total;
     // two rounds: the nearest cell of every query first, then the rest with the
     // exact k-th key of the first round's candidates as the bound
-    uint32_t round = 0;
-    for (uint32_t pb_ = 0; pb_ < np; ++round) {
-        const uint32_t pe = pb_ == 0 ? 1u : np;
-        a.p_begin = pb_;
-        a.p_end = pe;
-        // round 1 has one item per query: split the lists into chunks so it fills the GPU
+    // round 1: each query's leading probes holding >= IVF_R1_CODES codes (at most IVF_R1_MAX
+    // probes; the split is per query), in list chunks so the round fills the GPU; its exact
+    // k-th key (K3) bounds round 2, which scans the remaining probes
+    a.split = iv->split;
+    const uint32_t r1_end = std::min(np, IVF_R1_MAX);
+    for (uint32_t round = 0; round < 2; ++round) {
+        if (round == 1 && np <= 1) break;  // one probe: round 1 saw everything
+        a.round1 = round == 0;
+        a.p_begin = round == 0 ? 0 : 1;    // round 2 skips p < split (split >= 1)
+        a.p_end = round == 0 ? r1_end : np;
         a.chunk_codes = IVF_CHUNK;
-        a.nchunks = pb_ == 0 ? (uint32_t)std::max<uint64_t>(1, (iv->max_list + IVF_CHUNK - 1) / IVF_CHUNK) : 1u;
+        a.nchunks = round == 0 ? (uint32_t)std::max<uint64_t>(1, (iv->max_list + IVF_CHUNK - 1) / IVF_CHUNK) : 1u;
         a.work = iv->ctrl + IVF_NQB + 1 + round;
         pb::launch_ivf_scan(a, strategy, iv->m, iv->num_sms, s);
         pb::launch_topk(iv->cand, iv->ctrl, iv->cand_cap, 1, 0, 0, nqb, k, iv->keys, iv->kcounts, s);
-        if (pe < np) pb::launch_seed_thr(iv->keys, iv->kcounts, nqb, k, iv->thr, s);
-        pb_ = pe;
+        if (round == 0 && np > 1) pb::launch_seed_thr(iv->keys, iv->kcounts, nqb, k, iv->thr, s);
     }
     pb::launch_or_flag(iv->sticky_overflow, iv->ctrl + IVF_NQB, s);
     if (d_keys_out) {  // multi-GPU: the shard's top-k keys for the cross-rank merge
@@ -455,7 +469,7 @@ int poly_b200_ivf_destroy(poly_b200_ivf* iv) {
             for (void* p : {(void*)iv->d_codebooks, (void*)iv->d_perms, (void*)iv->d_coarse, (void*)iv->d_codes_ins,
                             (void*)iv->d_cells_ins, (void*)iv->d_off, (void*)iv->d_codes_list, (void*)iv->d_low_list,
                             (void*)iv->ckeys, (void*)iv->nl_counts, (void*)iv->probe_keys, (void*)iv->probe_counts,
-                            (void*)iv->np_eff, (void*)iv->scanned, (void*)iv->lutp, (void*)iv->qcodes,
+                            (void*)iv->np_eff, (void*)iv->split, (void*)iv->scanned, (void*)iv->lutp, (void*)iv->qcodes,
                             (void*)iv->cand, (void*)iv->ctrl, (void*)iv->thr, (void*)iv->keys, (void*)iv->kcounts,
                             (void*)iv->surv_total, (void*)iv->scan_total, (void*)iv->sticky_overflow, (void*)iv->d_q,
                             (void*)iv->d_oid, (void*)iv->d_osc, (void*)iv->d_ocnt,

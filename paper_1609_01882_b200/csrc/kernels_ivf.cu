@@ -443,7 +443,8 @@ void launch_residual_lut(const float* queries, uint32_t nq, uint32_t dim, uint32
 // scanned count reaches cap (0 = no cap); scanned[q] = codes visited.
 __global__ void ivf_probe_count_kernel(const unsigned long long* __restrict__ probe_keys, uint32_t nq,
                                        uint32_t nprobe, const uint64_t* __restrict__ off, uint64_t cap,
-                                       uint32_t* __restrict__ np_eff, unsigned long long* __restrict__ scanned) {
+                                       uint32_t* __restrict__ np_eff, unsigned long long* __restrict__ scanned,
+                                       uint32_t* __restrict__ split, uint64_t r1_codes, uint32_t r1_max) {
     // one warp per query: list sizes in parallel, running prefix over the probes in order;
     // probe p is visited iff no cap or the codes before it are < cap
     const uint32_t qi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
@@ -477,12 +478,31 @@ __global__ void ivf_probe_count_kernel(const unsigned long long* __restrict__ pr
         np_eff[qi] = ne;
         scanned[qi] = base;
     }
+    // round-1 split: the fewest leading probes (>= 1, <= r1_max, <= ne) holding >= r1_codes codes
+    if (split) {
+        const uint32_t lim = min(min(r1_max, ne), 32u);
+        uint64_t sz = 0;
+        if (lane < lim) {
+            const uint32_t cell = (uint32_t)probe_keys[(size_t)qi * nprobe + lane];
+            sz = off[cell + 1] - off[cell];
+        }
+        uint64_t incl = sz;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (uint32_t)o) incl += v;
+        }
+        const uint32_t hit = __ballot_sync(0xffffffffu, lane < lim && incl >= r1_codes);
+        if (lane == 0) split[qi] = max(1u, hit ? (uint32_t)__ffs(hit) : lim);
+    }
 }
 
 void launch_ivf_probe_count(const unsigned long long* probe_keys, uint32_t nq, uint32_t nprobe, const uint64_t* off,
-                            uint64_t cap, uint32_t* np_eff, unsigned long long* scanned, cudaStream_t s) {
+                            uint64_t cap, uint32_t* np_eff, unsigned long long* scanned, cudaStream_t s,
+                            uint32_t* split, uint64_t r1_codes, uint32_t r1_max) {
     if (nq == 0) return;
-    ivf_probe_count_kernel<<<(nq * 32 + 127) / 128, 128, 0, s>>>(probe_keys, nq, nprobe, off, cap, np_eff, scanned);
+    ivf_probe_count_kernel<<<(nq * 32 + 127) / 128, 128, 0, s>>>(probe_keys, nq, nprobe, off, cap, np_eff, scanned,
+                                                                  split, r1_codes, r1_max);
     count_launch();
 }
 
@@ -547,6 +567,7 @@ __global__ void __launch_bounds__(K6_WARPS * 32) ivf_scan_kernel(const IvfScanAr
         const uint32_t ch = it % a.nchunks, iq = it / a.nchunks;
         const uint32_t qi = iq / span, p = a.p_begin + iq % span;
         if (p >= a.np_eff[qi]) continue;
+        if (a.split && (a.round1 ? p >= a.split[qi] : p < a.split[qi])) continue;  // round 1: p < split
         const size_t item = (size_t)qi * a.nprobe + p;
         const uint32_t cell = (uint32_t)a.probe_keys[item];
         uint64_t beg = a.off[cell], end = a.off[cell + 1];

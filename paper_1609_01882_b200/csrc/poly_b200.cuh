@@ -117,6 +117,8 @@ struct IvfScanArgs {
     uint32_t* overflow;
     uint32_t* work;
     unsigned long long* surv_total;
+    const uint32_t* split;  // per query: round 1 scans probes [0, split), round 2 the rest (null: by p range)
+    uint32_t round1;
     uint32_t nchunks;       // work item = (query, probe, chunk); chunk c covers list rows
     uint32_t chunk_codes;   // [c * chunk_codes, (c + 1) * chunk_codes)  (nchunks = 1: whole list)
 };
@@ -304,7 +306,8 @@ void launch_residual_lut(const float* queries, uint32_t nq, uint32_t dim, uint32
                          const unsigned long long* probe_keys, uint32_t nprobe, const float* cent,
                          const float* codebooks, const uint16_t* perms, float* lutp, uint8_t* qcodes, cudaStream_t s);
 void launch_ivf_probe_count(const unsigned long long* probe_keys, uint32_t nq, uint32_t nprobe, const uint64_t* off,
-                            uint64_t cap, uint32_t* np_eff, unsigned long long* scanned, cudaStream_t s);
+                            uint64_t cap, uint32_t* np_eff, unsigned long long* scanned, cudaStream_t s,
+                            uint32_t* split = nullptr, uint64_t r1_codes = 0, uint32_t r1_max = 1);
 void launch_ivf_scan(const IvfScanArgs& a, int strategy, uint32_t m, int num_sms, cudaStream_t s);
 void launch_assign(const float* x, uint64_t n, uint32_t dim, const float* cent, uint32_t nlist, uint32_t* assign,
                    cudaStream_t s);
