@@ -369,7 +369,10 @@ void launch_coarse_refine(const float* q, uint32_t nq, uint32_t dim, const float
 // One CTA per K1R_ITEMS consecutive items: thread j owns centroid j and loads its
 // codebook row once per sub-quantizer for all the CTA's items (the 8 KB-per-sq
 // codebook is the L2 traffic; the items share it).
-constexpr uint32_t K1R_ITEMS = 8;
+#ifndef POLY_K1R_ITEMS
+#define POLY_K1R_ITEMS 8
+#endif
+constexpr uint32_t K1R_ITEMS = POLY_K1R_ITEMS;
 
 __global__ void __launch_bounds__(256) residual_lut_kernel(const float* __restrict__ queries, uint32_t dim, uint32_t m,
                                                            const unsigned long long* __restrict__ probe_keys,
