@@ -38,6 +38,7 @@ METRIC = "DB codes scanned/sec (filter+ADC+top-k)"
 UNIT = "codes/s"
 SEED = 160901882
 BATCH = 256
+IVF_BATCH = 1024  # configs 2/4 (BASELINE.json names no batch size there): the library's IVF batch
 NQ = 10_000
 # BASELINE.json configs: 1 = flat 64-bit codes (headline), 3 = wide 128-bit codes
 CONFIGS = {
@@ -69,6 +70,7 @@ def parse():
     ap.add_argument("--per-ht", default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-queries", type=int, default=256, help="queries in the CPU-baseline sample")
+    ap.add_argument("--ivf-batch", type=int, default=IVF_BATCH, help="queries per step for configs 2 and 4")
     ap.add_argument("--ref-n", type=int, default=8_000_000, help="codes in the --impl reference sample")
     args = ap.parse_args()
     global NCENT, DIM, M, PQFILE
@@ -238,10 +240,11 @@ def run_ivf(args, rank, world, local):
     pb.gen_points_device(centers, SEED, 3, 0, NQ, dq, device=local)
     stream = torch.cuda.current_stream()
     k = args.k
-    o_ids = torch.empty((BATCH, k), dtype=torch.int64, device="cuda")
-    o_sc = torch.empty((BATCH, k), dtype=torch.float32, device="cuda")
-    o_cnt = torch.empty(BATCH, dtype=torch.int32, device="cuda")
-    nbatches = NQ // BATCH
+    B = args.ivf_batch
+    o_ids = torch.empty((B, k), dtype=torch.int64, device="cuda")
+    o_sc = torch.empty((B, k), dtype=torch.float32, device="cuda")
+    o_cnt = torch.empty(B, dtype=torch.int32, device="cuda")
+    nbatches = NQ // B
     results = {}
     if dist is not None:
         # every cell's list holds this rank's id range; per-rank top-k
@@ -251,7 +254,7 @@ def run_ivf(args, rank, world, local):
         sharded = ShardedSearch(engine)
 
     def step(i, p, st=None):
-        q = dq[(i % nbatches) * BATCH:][:BATCH]
+        q = dq[(i % nbatches) * B:][:B]
         if dist is None:
             ivf.search_device(q, p, o_ids, o_sc, o_cnt, stream.cuda_stream, st)
         else:
@@ -289,7 +292,7 @@ def run_ivf(args, rank, world, local):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         results[nprobe] = {"value": scanned / (ms / 1e3), "ms_per_step": ms / steps,
-                           "scanned_per_query": scanned / (steps * BATCH), "survivor_frac": surv / max(scanned, 1),
+                           "scanned_per_query": scanned / (steps * B), "survivor_frac": surv / max(scanned, 1),
                            "gpu_launches": pb.launch_count() - l0, "steps": steps}
     head = results[c["nprobe"]]
     line = {"metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": world, "steps": head["steps"],
@@ -297,7 +300,7 @@ def run_ivf(args, rank, world, local):
             "vs_baseline": None, "dtype": "u8/f32", "data": "synthetic (seeded Gaussian mixture, BASELINE cfg2)",
             "config": {"workload": f"cfg2 IVF+polysemous: nlist={c['nlist']}, N={args.n} codes over {world} GPU(s) (the "
                                    f"per-GPU share of 1e9 over 8 at N=1), PQ m={M} on residuals, nq={NQ} in batches of "
-                                   f"{BATCH}, nprobe={c['nprobe']}, k={k}, ht={args.ht}",
+                                   f"{B}, nprobe={c['nprobe']}, k={k}, ht={args.ht}",
                        "nlist": c["nlist"], "n_codes": args.n, "m": M, "nprobe": c["nprobe"], "k": k, "ht": args.ht,
                        "parallelism": f"db-shard{world} (ids within every list) + NCCL key all-gather",
                        "coarse": "training-stream rows [0, nlist) (sampled coarse quantizer; DESIGN.md)",
@@ -319,30 +322,31 @@ def run_knn(args, c, ivf, centers, setup_s, rank, world, local, row0, row1):
     p = pb.CoarseParams(pb.Strategy.dual, k, args.ht, c["nprobe"], 0)
     stream = torch.cuda.current_stream()
     steps = args.steps
-    nrows = (args.warmup + steps) * BATCH
+    B = args.ivf_batch
+    nrows = (args.warmup + steps) * B
     dx = torch.empty((nrows, DIM), dtype=torch.float32, device="cuda")
     pb.gen_points_device(centers, SEED, 2, row0, nrows, dx, device=local, normalize=True)
-    o_ids = torch.empty((BATCH, k), dtype=torch.int64, device="cuda")
-    o_sc = torch.empty((BATCH, k), dtype=torch.float32, device="cuda")
-    o_cnt = torch.empty(BATCH, dtype=torch.int32, device="cuda")
+    o_ids = torch.empty((B, k), dtype=torch.int64, device="cuda")
+    o_sc = torch.empty((B, k), dtype=torch.float32, device="cuda")
+    o_cnt = torch.empty(B, dtype=torch.int32, device="cuda")
     scanned = 0
     p1 = pb.CoarseParams(pb.Strategy.dual, k + 1, args.ht, c["nprobe"], 0)
     for i in range(args.warmup, args.warmup + steps):  # per-batch work (untimed)
         st = pb.SearchStats()
-        qb = dx[i * BATCH:(i + 1) * BATCH]
-        ob = (torch.empty((BATCH, k + 1), dtype=torch.int64, device="cuda"),
-              torch.empty((BATCH, k + 1), dtype=torch.float32, device="cuda"))
+        qb = dx[i * B:(i + 1) * B]
+        ob = (torch.empty((B, k + 1), dtype=torch.int64, device="cuda"),
+              torch.empty((B, k + 1), dtype=torch.float32, device="cuda"))
         ivf.search_device(qb, p1, ob[0], ob[1], None, stream.cuda_stream, st)
         scanned += st.scanned
     for i in range(args.warmup):
-        ivf.knn_graph_device(dx[i * BATCH:(i + 1) * BATCH], row0 + i * BATCH, p, o_ids, o_sc, o_cnt,
+        ivf.knn_graph_device(dx[i * B:(i + 1) * B], row0 + i * B, p, o_ids, o_sc, o_cnt,
                              stream.cuda_stream)
     torch.cuda.synchronize()
     l0 = pb.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for i in range(args.warmup, args.warmup + steps):
-        ivf.knn_graph_device(dx[i * BATCH:(i + 1) * BATCH], row0 + i * BATCH, p, o_ids, o_sc, o_cnt,
+        ivf.knn_graph_device(dx[i * B:(i + 1) * B], row0 + i * B, p, o_ids, o_sc, o_cnt,
                              stream.cuda_stream)
     e1.record(stream)
     torch.cuda.synchronize()
@@ -354,9 +358,9 @@ def run_knn(args, c, ivf, centers, setup_s, rank, world, local, row0, row1):
             "config": {"workload": f"cfg4 k-NN graph: N={args.n} d={DIM} unit-normalised, IVF {c['nlist']} + PQ "
                                    f"m={M}, every vector queries the rest, nprobe={c['nprobe']}, ht={args.ht}, k={k}",
                        "n_codes": args.n, "nlist": c["nlist"], "m": M, "nprobe": c["nprobe"], "k": k,
-                       "ht": args.ht, "queries_per_step": BATCH},
-            "scanned_per_query": scanned / (steps * BATCH),
-            "graph_time_est_s": rows / BATCH * ms / steps / 1e3, "gpu_launches": pb.launch_count() - l0,
+                       "ht": args.ht, "queries_per_step": B},
+            "scanned_per_query": scanned / (steps * B),
+            "graph_time_est_s": rows / B * ms / steps / 1e3, "gpu_launches": pb.launch_count() - l0,
             "setup_s": round(setup_s, 1)}
     if rank == 0:
         print(json.dumps(line), flush=True)

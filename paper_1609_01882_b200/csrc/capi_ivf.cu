@@ -17,8 +17,11 @@
 
 using namespace pbh;
 
+#ifndef POLY_IVF_NQB
+#define POLY_IVF_NQB 1024
+#endif
 namespace {
-constexpr uint32_t IVF_NQB = 256;  // queries per batch
+constexpr uint32_t IVF_NQB = POLY_IVF_NQB;  // queries per batch
 }
 
 struct poly_b200_ivf {
@@ -54,6 +57,8 @@ struct poly_b200_ivf {
     uint32_t* split = nullptr;  // per query: probes of round 1
     unsigned long long* scanned = nullptr;
     uint32_t scratch_nprobe = 0;
+    uint4* items[2] = {nullptr, nullptr};  // K6 work lists of the two rounds
+    uint64_t items_cap[2] = {0, 0};
     float* lutp = nullptr;
     uint8_t* qcodes = nullptr;
     unsigned long long* cand = nullptr;
@@ -101,7 +106,15 @@ namespace {
 #endif
 constexpr uint32_t IVF_R1_MAX = POLY_IVF_R1_MAX;      // round 1: at most this many leading probes
 constexpr uint64_t IVF_R1_CODES = POLY_IVF_R1_CODES;  // ... and at least this many codes
-constexpr uint32_t IVF_CHUNK = 1024;  // K6 round-1 work item: 1024 list rows (8 warps x 128)
+#ifndef POLY_IVF_CHUNK2
+#define POLY_IVF_CHUNK2 4096
+#endif
+#ifndef POLY_K5R_SUB
+#define POLY_K5R_SUB POLY_IVF_NQB
+#endif
+constexpr uint32_t K5R_SUB = POLY_K5R_SUB;  // queries per coarse GEMM + K5r launch pair
+constexpr uint32_t IVF_CHUNK = 1024;             // K6 round-1 work item: 1024 list rows (8 warps x 128)
+constexpr uint32_t IVF_CHUNK2 = POLY_IVF_CHUNK2;  // round 2: longer items (fewer LUT loads per code)
 
 __global__ void fill_u32(uint32_t* p, uint64_t n, uint32_t v) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
@@ -203,6 +216,19 @@ void ensure_ivf_scratch(poly_b200_ivf* iv, uint32_t nprobe, uint32_t k) {
         iv->lutp = dalloc<float>((size_t)IVF_NQB * nprobe * iv->m * 256);
         iv->qcodes = dalloc<uint8_t>((size_t)IVF_NQB * nprobe * iv->cb);
     }
+    // work-list bounds per query: round 1 <= r1 probes -> <= r1 + r1 * max_list / CHUNK items;
+    // round 2 <= np + min(n, np * max_list) / CHUNK2 items
+    const uint64_t r1 = std::min<uint64_t>(nprobe, IVF_R1_MAX);
+    const uint64_t need[2] = {
+        (uint64_t)IVF_NQB * (r1 + (r1 * iv->max_list + IVF_CHUNK - 1) / IVF_CHUNK),
+        (uint64_t)IVF_NQB * (nprobe + (std::min<uint64_t>(iv->n, nprobe * iv->max_list) + IVF_CHUNK2 - 1) / IVF_CHUNK2)};
+    for (int r = 0; r < 2; ++r)
+        if (iv->items_cap[r] < need[r]) {
+            require(need[r] < (1ull << 32), POLY_B200_INVALID_ARGUMENT, "IVF work list too large");
+            dfree(iv->items[r]);
+            iv->items_cap[r] = need[r];
+            iv->items[r] = dalloc<uint4>(need[r]);
+        }
     const uint32_t cap = (uint32_t)std::max<uint64_t>(131072, 4 * iv->max_list);
     if (iv->cand_cap < cap) {
         dfree(iv->cand);
@@ -239,13 +265,20 @@ void enumerate_cells(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, uint32_t
         float* dots = reinterpret_cast<float*>(iv->ckeys);                        // IVF_NQB x nlist
         uint32_t* scratch = reinterpret_cast<uint32_t*>(iv->ckeys) + (size_t)IVF_NQB * iv->nlist;
         const float one = 1.0f, zero = 0.0f;
-        // column-major: dots (nlist x nqb) = coarse^T (nlist x dim) . q^T (dim x nqb)
-        require(cublasSgemm(iv->cublas, CUBLAS_OP_T, CUBLAS_OP_N, (int)iv->nlist, (int)nqb, (int)iv->dim, &one,
-                            iv->d_coarse, (int)iv->dim, d_q, (int)iv->dim, &zero, dots, (int)iv->nlist) ==
-                    CUBLAS_STATUS_SUCCESS,
-                POLY_B200_INTERNAL, "cublasSgemm failed");
-        pb::launch_coarse_refine(d_q, nqb, iv->dim, dots, iv->d_cnorm, iv->cmax, iv->d_coarse, iv->nlist, np, scratch,
-                                 iv->probe_keys, iv->probe_counts, s);
+        // sub-batches of K5R_SUB queries keep each dots block L2-resident between the
+        // GEMM that writes it and the two K5r passes that read it
+        for (uint32_t q0 = 0; q0 < nqb; q0 += K5R_SUB) {
+            const uint32_t nb = std::min(K5R_SUB, nqb - q0);
+            float* db = dots + (size_t)q0 * iv->nlist;
+            // column-major: dots (nlist x nb) = coarse^T (nlist x dim) . q^T (dim x nb)
+            require(cublasSgemm(iv->cublas, CUBLAS_OP_T, CUBLAS_OP_N, (int)iv->nlist, (int)nb, (int)iv->dim, &one,
+                                iv->d_coarse, (int)iv->dim, d_q + (size_t)q0 * iv->dim, (int)iv->dim, &zero, db,
+                                (int)iv->nlist) == CUBLAS_STATUS_SUCCESS,
+                    POLY_B200_INTERNAL, "cublasSgemm failed");
+            pb::launch_coarse_refine(d_q + (size_t)q0 * iv->dim, nb, iv->dim, db, iv->d_cnorm, iv->cmax, iv->d_coarse,
+                                     iv->nlist, np, scratch + (size_t)q0 * iv->nlist, iv->probe_keys + (size_t)q0 * np,
+                                     iv->probe_counts + q0, s);
+        }
     } else if (np <= 64) {
         const uint32_t qtiles = (nqb + 63) / 64;
         uint32_t slices = std::max<uint32_t>(1, std::min<uint32_t>(64, 2u * iv->num_sms / qtiles));
@@ -273,8 +306,17 @@ void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_
     CK(cudaMemsetAsync(iv->ctrl, 0, (IVF_NQB + 32) * 4, s));
     CK(cudaMemsetAsync(iv->thr, 0xFF, IVF_NQB * 8, s));
     enumerate_cells(iv, d_q, nqb, np, s);
+    pb::IvfWork w{};
+    w.items[0] = iv->items[0];
+    w.items[1] = iv->items[1];
+    w.nitems = iv->ctrl + IVF_NQB + 3;
+    w.cap[0] = (uint32_t)iv->items_cap[0];
+    w.cap[1] = (uint32_t)iv->items_cap[1];
+    w.chunk[0] = IVF_CHUNK;
+    w.chunk[1] = IVF_CHUNK2;
+    w.overflow = iv->ctrl + IVF_NQB;
     pb::launch_ivf_probe_count(iv->probe_keys, nqb, np, iv->d_off, p->cap, iv->np_eff, iv->scanned, s, iv->split,
-                               IVF_R1_CODES, IVF_R1_MAX);
+                               IVF_R1_CODES, IVF_R1_MAX, w);
     add_u64<<<1, 256, 0, s>>>(iv->scanned, nqb, iv->scan_total);
     pb::count_launch();
     pb::launch_residual_lut(d_q, nqb, iv->dim, iv->m, iv->probe_keys, np, iv->d_coarse, iv->d_codebooks,
@@ -284,7 +326,6 @@ void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_
     a.low = iv->d_low_list;
     a.off = iv->d_off;
     a.probe_keys = iv->probe_keys;
-    a.np_eff = iv->np_eff;
     a.lutp = iv->lutp;
     a.qcodes = iv->qcodes;
     a.nq = nqb;
@@ -296,24 +337,20 @@ void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_
     a.ccount = iv->ctrl;
     a.overflow = iv->ctrl + IVF_NQB;
     a.surv_total = iv->surv_total;
-    // two rounds: the nearest cell of every query first, then the rest with the
-    // exact k-th key of the first round's candidates as the bound
-    // round 1: each query's leading probes holding >= IVF_R1_CODES codes (at most IVF_R1_MAX
-    // probes; the split is per query), in list chunks so the round fills the GPU; its exact
-    // k-th key (K3) bounds round 2, which scans the remaining probes
-    a.split = iv->split;
-    const uint32_t r1_end = std::min(np, IVF_R1_MAX);
+    // two rounds over the work lists built by the probe-count kernel: round 1 scans each
+    // query's leading probes holding >= IVF_R1_CODES codes (at most IVF_R1_MAX probes) in
+    // 1024-row chunks; its exact k-th key (K3) bounds round 2, the remaining probes
     for (uint32_t round = 0; round < 2; ++round) {
         if (round == 1 && np <= 1) break;  // one probe: round 1 saw everything
-        a.round1 = round == 0;
-        a.p_begin = round == 0 ? 0 : 1;    // round 2 skips p < split (split >= 1)
-        a.p_end = round == 0 ? r1_end : np;
-        a.chunk_codes = IVF_CHUNK;
-        a.nchunks = round == 0 ? (uint32_t)std::max<uint64_t>(1, (iv->max_list + IVF_CHUNK - 1) / IVF_CHUNK) : 1u;
+        a.items = iv->items[round];
+        a.nitems = w.nitems + round;
+        a.items_cap = w.cap[round];
+        a.chunk_codes = w.chunk[round];
         a.work = iv->ctrl + IVF_NQB + 1 + round;
         pb::launch_ivf_scan(a, strategy, iv->m, iv->num_sms, s);
         pb::launch_topk(iv->cand, iv->ctrl, iv->cand_cap, 1, 0, 0, nqb, k, iv->keys, iv->kcounts, s);
-        if (round == 0 && np > 1) pb::launch_seed_thr(iv->keys, iv->kcounts, nqb, k, iv->thr, s);
+        if (round == 0 && np > 1)  // bound round 2; keep only round 1's top-k as candidates
+            pb::launch_seed_compact(iv->keys, iv->kcounts, nqb, k, iv->thr, iv->cand, iv->cand_cap, iv->ctrl, s);
     }
     pb::launch_or_flag(iv->sticky_overflow, iv->ctrl + IVF_NQB, s);
     if (d_keys_out) {  // multi-GPU: the shard's top-k keys for the cross-rank merge
@@ -473,7 +510,8 @@ int poly_b200_ivf_destroy(poly_b200_ivf* iv) {
                             (void*)iv->cand, (void*)iv->ctrl, (void*)iv->thr, (void*)iv->keys, (void*)iv->kcounts,
                             (void*)iv->surv_total, (void*)iv->scan_total, (void*)iv->sticky_overflow, (void*)iv->d_q,
                             (void*)iv->d_oid, (void*)iv->d_osc, (void*)iv->d_ocnt,
-                            (void*)iv->knn_ids, (void*)iv->knn_sc, (void*)iv->knn_cnt, (void*)iv->d_cnorm})
+                            (void*)iv->knn_ids, (void*)iv->knn_sc, (void*)iv->knn_cnt, (void*)iv->d_cnorm, (void*)iv->items[0],
+                            (void*)iv->items[1]})
                 dfree(p);
             if (iv->cublas) cublasDestroy(iv->cublas);
             iv->idm.release();

@@ -14,6 +14,8 @@
 //                            item's query code, ADC from the item's LUT in shared
 //                            memory, candidate keys appended to the query's list.
 //   assign_kernel            build: nearest coarse cell by sq_l2 (strict <).
+#include <type_traits>
+
 #include "poly_b200.cuh"
 #include "synth.cuh"
 
@@ -223,11 +225,26 @@ void launch_coarse_select(const float* q, uint32_t nq, uint32_t dim, const float
 // With T an upper bound of the np-th smallest a(c), every cell of the exact top-np
 // has a(c) <= T + 2E; those cells get the exact sq_l2 (fp32, dim order, as K5) and
 // the (dist bits << 32 | cell) keys of the np smallest are emitted in order.
-// One CTA (512 threads) per query; T from a 4096-bucket histogram over [min, max]
-// of a(c); candidates go through a global scratch list in chunks of KR_CHUNK.
-constexpr int KR_THREADS = 512, KR_BUCKETS = 4096, KR_CHUNK = 2048, KR_NPMAX = 1024, KR_BUF = 4096;  // np + chunk <= buf (pow2)
+// One CTA (512 threads) per query, one pass over the query's dots row (float4):
+// each thread keeps its two smallest a(c); those 1024 values are distinct cells,
+// so their np-th smallest (bitonic sort in shared memory) is >= the np-th
+// smallest a(c) over all cells and serves as T.  The cells with a(c) <= T + 2E
+// are a thread's kept ones, unless its second smallest is within the bound too
+// (then it revisits its cells); they go to a global scratch list and are
+// re-ranked in chunks of KR_CHUNK.
+constexpr int KR_THREADS = 512, KR_CHUNK = 2048, KR_NPMAX = 1024, KR_BUF = 4096;  // np + chunk <= buf (pow2)
+constexpr int KR_TVALS = 2 * KR_THREADS;  // per-thread two smallest
+constexpr int KR_UNROLL = 4;              // float4 loads in flight per thread
 
-__global__ void __launch_bounds__(KR_THREADS) coarse_refine_kernel(const float* __restrict__ q, uint32_t dim,
+__device__ __forceinline__ uint32_t kr_ord(float f) {  // order-preserving float -> uint32
+    const uint32_t b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float kr_unord(uint32_t u) {
+    return __uint_as_float((u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u);
+}
+
+__global__ void __launch_bounds__(KR_THREADS, 2) coarse_refine_kernel(const float* __restrict__ q, uint32_t dim,
                                                                    const float* __restrict__ dots,
                                                                    const float* __restrict__ cnorm, float cmax,
                                                                    const float* __restrict__ cent, uint32_t nlist,
@@ -236,16 +253,16 @@ __global__ void __launch_bounds__(KR_THREADS) coarse_refine_kernel(const float* 
                                                                    uint32_t* __restrict__ probe_counts) {
     extern __shared__ __align__(16) uint8_t kr_smem[];
     unsigned long long* buf = reinterpret_cast<unsigned long long*>(kr_smem);  // KR_BUF keys
-    uint32_t* hist = reinterpret_cast<uint32_t*>(buf + KR_BUF);                 // KR_BUCKETS
-    float* qs = reinterpret_cast<float*>(hist + KR_BUCKETS);                    // dim
-    __shared__ float red_f[2][KR_THREADS / 32];
-    __shared__ uint32_t red_u[KR_THREADS / 32];
-    __shared__ uint32_t ncand_s, bsel_s;
+    uint32_t* tv = reinterpret_cast<uint32_t*>(buf);                            // KR_TVALS (aliases buf)
+    float* qs = reinterpret_cast<float*>(buf + KR_BUF);                         // dim
+    __shared__ float red_f[KR_THREADS / 32];
+    __shared__ uint32_t ncand_s;
     const uint32_t qi = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const float* qrow = q + (size_t)qi * dim;
     const float* drow = dots + (size_t)qi * nlist;
     uint32_t* cand = scratch + (size_t)qi * nlist;
-    // |q|^2 and the range of a(c)
+    const bool vec = (nlist & 3u) == 0;  // rows 16-byte aligned
+    // |q|^2
     float qn = 0.0f;
     for (uint32_t d = tid; d < dim; d += KR_THREADS) {
         const float v = qrow[d];
@@ -253,64 +270,76 @@ __global__ void __launch_bounds__(KR_THREADS) coarse_refine_kernel(const float* 
         qn += v * v;
     }
     for (int off = 16; off; off >>= 1) qn += __shfl_xor_sync(0xffffffffu, qn, off);
-    if (lane == 0) red_f[0][warp] = qn;
-    __syncthreads();
-    qn = 0.0f;
-    for (int w = 0; w < KR_THREADS / 32; ++w) qn += red_f[0][w];
-    __syncthreads();
-    float mn = INFINITY, mx = -INFINITY;
-    for (uint32_t c = tid; c < nlist; c += KR_THREADS) {
-        const float a = qn + cnorm[c] - 2.0f * drow[c];
-        mn = fminf(mn, a);
-        mx = fmaxf(mx, a);
-    }
-    for (int off = 16; off; off >>= 1) {
-        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, off));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-    }
-    if (lane == 0) { red_f[0][warp] = mn; red_f[1][warp] = mx; }
-    for (uint32_t i = tid; i < KR_BUCKETS; i += KR_THREADS) hist[i] = 0;
+    if (lane == 0) red_f[warp] = qn;
     if (tid == 0) ncand_s = 0;
     __syncthreads();
-    mn = INFINITY; mx = -INFINITY;
-    for (int w = 0; w < KR_THREADS / 32; ++w) { mn = fminf(mn, red_f[0][w]); mx = fmaxf(mx, red_f[1][w]); }
-    const float scale = mx > mn ? (float)(KR_BUCKETS - 1) / (mx - mn) : 0.0f;
-    for (uint32_t c = tid; c < nlist; c += KR_THREADS) {
-        const float a = qn + cnorm[c] - 2.0f * drow[c];
-        atomicAdd(&hist[min((uint32_t)((a - mn) * scale), (uint32_t)KR_BUCKETS - 1)], 1u);
-    }
-    __syncthreads();
-    // bucket holding the np-th smallest a(c): per-thread sums of 8 buckets, block scan
-    constexpr uint32_t PER = KR_BUCKETS / KR_THREADS;
-    uint32_t cs = 0;
-#pragma unroll
-    for (uint32_t j = 0; j < PER; ++j) cs += hist[tid * PER + j];
-    uint32_t incl = cs;
-    for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
-        if (lane >= (uint32_t)off) incl += o;
-    }
-    if (lane == 31) red_u[warp] = incl;
-    __syncthreads();
-    for (uint32_t w = 0; w < warp; ++w) incl += red_u[w];
-    const uint32_t excl = incl - cs;
-    if (excl < np && np <= incl) {
-        uint32_t cum = excl, b = tid * PER;
-        for (uint32_t j = 0; j < PER; ++j) {
-            cum += hist[tid * PER + j];
-            if (cum >= np) { b = tid * PER + j; break; }
+    qn = 0.0f;
+    for (int w = 0; w < KR_THREADS / 32; ++w) qn += red_f[w];
+    // one pass over the row: the two smallest a(c) = |q|^2 + |c|^2 - 2 q.c of this
+    // thread's cells, with their indices
+    float m1 = INFINITY, m2 = INFINITY;
+    uint32_t i1 = 0xFFFFFFFFu, i2 = 0xFFFFFFFFu;
+    auto keep = [&](float a, uint32_t c) {
+        if (a < m2) {
+            if (a < m1) { m2 = m1; i2 = i1; m1 = a; i1 = c; }
+            else { m2 = a; i2 = c; }
         }
-        bsel_s = b;
-    }
+    };
+    const float4* d4 = reinterpret_cast<const float4*>(drow);
+    const float4* n4 = reinterpret_cast<const float4*>(cnorm);
+    const uint32_t n4c = nlist / 4;
+    // visit this thread's cells (float4 groups tid, tid + KR_THREADS, ...; scalar rows
+    // when unaligned), KR_UNROLL loads in flight
+    auto visit = [&](auto&& f) {
+        if (vec) {
+            for (uint32_t c0 = tid; c0 < n4c; c0 += KR_THREADS * KR_UNROLL) {
+                float4 d[KR_UNROLL], n[KR_UNROLL];
+#pragma unroll
+                for (int u = 0; u < KR_UNROLL; ++u) {
+                    const uint32_t c = c0 + u * KR_THREADS;
+                    if (c < n4c) { d[u] = __ldcg(d4 + c); n[u] = __ldg(n4 + c); }
+                }
+#pragma unroll
+                for (int u = 0; u < KR_UNROLL; ++u) {
+                    const uint32_t c = c0 + u * KR_THREADS;
+                    if (c >= n4c) continue;
+                    f(qn + n[u].x - 2.0f * d[u].x, 4 * c);
+                    f(qn + n[u].y - 2.0f * d[u].y, 4 * c + 1);
+                    f(qn + n[u].z - 2.0f * d[u].z, 4 * c + 2);
+                    f(qn + n[u].w - 2.0f * d[u].w, 4 * c + 3);
+                }
+            }
+        } else {
+            for (uint32_t c = tid; c < nlist; c += KR_THREADS) f(qn + cnorm[c] - 2.0f * drow[c], c);
+        }
+    };
+    visit(keep);
+    tv[2 * tid] = kr_ord(m1);
+    tv[2 * tid + 1] = kr_ord(m2);
     __syncthreads();
-    // T >= the np-th smallest a(c) (bucket upper edge, rounding slack); candidate bound T + 2E
-    const float T = scale > 0.0f ? mn + (float)(bsel_s + 1) / scale * (1.0f + 1e-5f) + 1e-30f : mx;
+    for (uint32_t size = 2; size <= KR_TVALS; size <<= 1)
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            const uint32_t pos = 2 * tid - (tid & (stride - 1));
+            const bool asc = (pos & size) == 0;
+            const uint32_t x = tv[pos], y = tv[pos + stride];
+            if ((x > y) == asc) { tv[pos] = y; tv[pos + stride] = x; }
+            __syncthreads();
+        }
+    // T >= the np-th smallest a(c); candidate bound T + 2E (np <= KR_NPMAX = KR_TVALS)
+    const float T = kr_unord(tv[min(np, (uint32_t)KR_TVALS) - 1]);
     const float qnorm = sqrtf(qn);
     const float E = 4.1e-3f * qnorm * cmax + 4e-5f * (qn + cmax * cmax + 2.0f * qnorm * cmax) + 1e-6f;
     const float bound = T + 2.0f * E;
-    for (uint32_t c = tid; c < nlist; c += KR_THREADS) {
-        const float a = qn + cnorm[c] - 2.0f * drow[c];
-        if (a <= bound) cand[atomicAdd(&ncand_s, 1u)] = c;
+    __syncthreads();  // tv (aliases buf) read by all before the re-rank writes buf
+    // candidates: a thread whose second smallest is within the bound may hold more
+    // (its third, ...): it revisits its cells (rare: the near cells are spread over
+    // the threads); otherwise its candidates are among its two smallest
+    if (!(m2 > bound)) {
+        visit([&](float a, uint32_t c) {
+            if (!(a > bound)) cand[atomicAdd(&ncand_s, 1u)] = c;
+        });
+    } else if (!(m1 > bound)) {
+        cand[atomicAdd(&ncand_s, 1u)] = i1;
     }
     __syncthreads();
     const uint32_t ncand = ncand_s;
@@ -322,9 +351,21 @@ __global__ void __launch_bounds__(KR_THREADS) coarse_refine_kernel(const float* 
             const uint32_t cell = cand[c0 + i];
             const float* crow = cent + (size_t)cell * dim;
             float acc = 0.0f;
-            for (uint32_t d = 0; d < dim; ++d) {
-                const float t = __fsub_rn(qs[d], __ldg(crow + d));
-                acc = __fadd_rn(acc, __fmul_rn(t, t));
+            if ((dim & 3u) == 0) {
+                for (uint32_t d = 0; d < dim; d += 4) {
+                    const float4 c4 = __ldg(reinterpret_cast<const float4*>(crow + d));
+                    const float cv[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float t = __fsub_rn(qs[d + e], cv[e]);
+                        acc = __fadd_rn(acc, __fmul_rn(t, t));
+                    }
+                }
+            } else {
+                for (uint32_t d = 0; d < dim; ++d) {
+                    const float t = __fsub_rn(qs[d], __ldg(crow + d));
+                    acc = __fadd_rn(acc, __fmul_rn(t, t));
+                }
             }
             buf[ntop + i] = ((unsigned long long)__float_as_uint(acc) << 32) | cell;
         }
@@ -353,7 +394,7 @@ void launch_coarse_refine(const float* q, uint32_t nq, uint32_t dim, const float
                           const float* cent, uint32_t nlist, uint32_t np, uint32_t* scratch,
                           unsigned long long* probe_keys, uint32_t* probe_counts, cudaStream_t s) {
     if (nq == 0) return;
-    const size_t smem = (size_t)KR_BUF * 8 + KR_BUCKETS * 4 + (size_t)dim * 4;
+    const size_t smem = (size_t)KR_BUF * 8 + (size_t)dim * 4;
     static size_t attr = 0;
     if (attr < smem) {
         cudaFuncSetAttribute(coarse_refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -372,6 +413,9 @@ void launch_coarse_refine(const float* q, uint32_t nq, uint32_t dim, const float
 #ifndef POLY_K1R_ITEMS
 #define POLY_K1R_ITEMS 8
 #endif
+#ifndef POLY_K1R_PAIR
+#define POLY_K1R_PAIR 1  // centroid-pair kernel (packed f32x2) instead of one centroid per thread
+#endif
 constexpr uint32_t K1R_ITEMS = POLY_K1R_ITEMS;
 
 __global__ void __launch_bounds__(256) residual_lut_kernel(const float* __restrict__ queries, uint32_t dim, uint32_t m,
@@ -383,7 +427,7 @@ __global__ void __launch_bounds__(256) residual_lut_kernel(const float* __restri
                                                            uint8_t* __restrict__ qcodes) {
     const uint32_t item0 = blockIdx.x * K1R_ITEMS, j = threadIdx.x;
     const uint32_t ni = min(K1R_ITEMS, nitems - item0);
-    __shared__ float r[K1R_ITEMS][256];
+    __shared__ __align__(16) float r[K1R_ITEMS][256];
     __shared__ float wv[K1R_ITEMS][16][8];
     __shared__ uint32_t wj[K1R_ITEMS][16][8];
     for (uint32_t e = j; e < ni * dim; e += 256) {
@@ -401,19 +445,29 @@ __global__ void __launch_bounds__(256) residual_lut_kernel(const float* __restri
             cb[4 * v + 0] = cc.x; cb[4 * v + 1] = cc.y; cb[4 * v + 2] = cc.z; cb[4 * v + 3] = cc.w;
         }
         const uint32_t dst = perms[sq * KSUB + j];
+        // the items' sums interleaved (independent chains), each in dim order as sq_l2
+        float acc[K1R_ITEMS];
+#pragma unroll
+        for (uint32_t it = 0; it < K1R_ITEMS; ++it) acc[it] = 0.0f;
+#pragma unroll
+        for (int v = 0; v < DSUB / 4; ++v) {
+#pragma unroll
+            for (uint32_t it = 0; it < K1R_ITEMS; ++it) {
+                const float4 x = *reinterpret_cast<const float4*>(&r[min(it, ni - 1)][sq * DSUB + 4 * v]);
+                const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float t = __fsub_rn(xs[e], cb[4 * v + e]);
+                    acc[it] = __fadd_rn(acc[it], __fmul_rn(t, t));
+                }
+            }
+        }
 #pragma unroll
         for (uint32_t it = 0; it < K1R_ITEMS; ++it) {
             if (it >= ni) break;
-            const float* sub = &r[it][sq * DSUB];
-            float acc = 0.0f;
-#pragma unroll
-            for (int d = 0; d < DSUB; ++d) {
-                const float t = __fsub_rn(sub[d], cb[d]);
-                acc = __fadd_rn(acc, __fmul_rn(t, t));
-            }
-            lutp[((size_t)(item0 + it) * m + sq) * KSUB + dst] = acc;
+            lutp[((size_t)(item0 + it) * m + sq) * KSUB + dst] = acc[it];
             // warp argmin, ties -> lowest j: acc >= 0, so its bits order like the value
-            const uint32_t bits = __float_as_uint(acc);
+            const uint32_t bits = __float_as_uint(acc[it]);
             const uint32_t wmin = __reduce_min_sync(0xffffffffu, bits);
             const uint32_t first = __ffs(__ballot_sync(0xffffffffu, bits == wmin)) - 1;
             if ((j & 31) == 0) { wv[it][sq][j >> 5] = __uint_as_float(wmin); wj[it][sq][j >> 5] = (j & ~31u) + first; }
@@ -430,14 +484,116 @@ __global__ void __launch_bounds__(256) residual_lut_kernel(const float* __restri
     }
 }
 
+// K1r, centroid pairs: thread t owns centroids t and t + 128 as one packed f32x2
+// lane pair, so each (item, dim) term is FADD2 (r - c), FFMA2 (t * t + z, z a
+// runtime +0.0: exactly mul.rn, and ptxas cannot contract it into the add), FADD2
+// (acc + s) for two centroids -- the same rounding sequence as sq_l2 per lane.
+// The residual sits in shared memory duplicated as (r, r) pairs.
+__device__ __forceinline__ unsigned long long k1_pack(float lo, float hi) {
+    unsigned long long v;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(v) : "f"(lo), "f"(hi));
+    return v;
+}
+
+__global__ void __launch_bounds__(128) residual_lut_pair_kernel(const float* __restrict__ queries, uint32_t dim,
+                                                                uint32_t m, const unsigned long long* __restrict__ probe_keys,
+                                                                uint32_t nprobe, uint32_t nitems,
+                                                                const float* __restrict__ cent,
+                                                                const float* __restrict__ codebooks,
+                                                                const uint16_t* __restrict__ perms,
+                                                                float* __restrict__ lutp, uint8_t* __restrict__ qcodes,
+                                                                float zero) {
+    const uint32_t item0 = blockIdx.x * K1R_ITEMS, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const uint32_t ni = min(K1R_ITEMS, nitems - item0);
+    __shared__ __align__(16) unsigned long long rr[K1R_ITEMS][256];  // (r, r) per dim
+    __shared__ float wv[K1R_ITEMS][16][4];
+    __shared__ uint32_t wj[K1R_ITEMS][16][4];
+    __shared__ __align__(16) float stage[K1R_ITEMS][KSUB];  // one sub-quantizer's rows, stored-field order
+    for (uint32_t e = t; e < ni * dim; e += 128) {
+        const uint32_t it = e / dim, d = e % dim, item = item0 + it;
+        const uint32_t qi = item / nprobe, cell = (uint32_t)probe_keys[item];
+        const float r = __fsub_rn(queries[(size_t)qi * dim + d], cent[(size_t)cell * dim + d]);  // r = q - c
+        rr[it][d] = k1_pack(r, r);
+    }
+    __syncthreads();
+    unsigned long long zz = k1_pack(zero, zero);
+    const uint32_t j0 = t, j1 = t + 128;
+    for (uint32_t sq = 0; sq < m; ++sq) {
+        const float4* c0 = reinterpret_cast<const float4*>(codebooks + ((size_t)sq * KSUB + j0) * DSUB);
+        const float4* c1 = reinterpret_cast<const float4*>(codebooks + ((size_t)sq * KSUB + j1) * DSUB);
+        unsigned long long cc[DSUB];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const float4 a = __ldg(c0 + v), b = __ldg(c1 + v);
+            cc[4 * v + 0] = k1_pack(a.x, b.x);
+            cc[4 * v + 1] = k1_pack(a.y, b.y);
+            cc[4 * v + 2] = k1_pack(a.z, b.z);
+            cc[4 * v + 3] = k1_pack(a.w, b.w);
+        }
+        const uint32_t dst0 = perms[sq * KSUB + j0], dst1 = perms[sq * KSUB + j1];
+        unsigned long long acc[K1R_ITEMS];
+#pragma unroll
+        for (uint32_t it = 0; it < K1R_ITEMS; ++it) acc[it] = zz;
+#pragma unroll
+        for (int d2 = 0; d2 < DSUB / 2; ++d2) {
+#pragma unroll
+            for (uint32_t it = 0; it < K1R_ITEMS; ++it) {
+                const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(&rr[min(it, ni - 1)][sq * DSUB + 2 * d2]);
+                unsigned long long tt, s2;
+                asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(tt) : "l"(x.x), "l"(cc[2 * d2]));
+                asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(s2) : "l"(tt), "l"(zz));
+                asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc[it]) : "l"(acc[it]), "l"(s2));
+                asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(tt) : "l"(x.y), "l"(cc[2 * d2 + 1]));
+                asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(s2) : "l"(tt), "l"(zz));
+                asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc[it]) : "l"(acc[it]), "l"(s2));
+            }
+        }
+        __syncthreads();  // the previous sub-quantizer's stage rows are written out
+#pragma unroll
+        for (uint32_t it = 0; it < K1R_ITEMS; ++it) {
+            if (it >= ni) break;
+            float v0, v1;
+            asm("mov.b64 {%0,%1}, %2;" : "=f"(v0), "=f"(v1) : "l"(acc[it]));
+            stage[it][dst0] = v0;  // permuted (stored-field) order; written out coalesced below
+            stage[it][dst1] = v1;
+            // argmin over the 256 centroids, ties -> lowest index (pq.cpp:38): values >= 0
+            // order like their bits; the warp minimum, then the lowest index holding it
+            const uint32_t b0 = __float_as_uint(v0), b1 = __float_as_uint(v1);
+            const uint32_t wmin = __reduce_min_sync(0xffffffffu, min(b0, b1));
+            const uint32_t jj = b0 == wmin ? j0 : (b1 == wmin ? j1 : 0xFFFFFFFFu);
+            const uint32_t jmin = __reduce_min_sync(0xffffffffu, jj);
+            if (lane == 0) { wv[it][sq][warp] = __uint_as_float(wmin); wj[it][sq][warp] = jmin; }
+        }
+        __syncthreads();
+        for (uint32_t e = t; e < ni * (KSUB / 4); e += 128) {  // float4 rows out
+            const uint32_t it = e / (KSUB / 4), o = e % (KSUB / 4);
+            reinterpret_cast<float4*>(lutp + ((size_t)(item0 + it) * m + sq) * KSUB)[o] =
+                reinterpret_cast<const float4*>(stage[it])[o];
+        }
+    }
+    __syncthreads();
+    if (t < ni * m) {  // across the 4 warps
+        const uint32_t it = t / m, sq = t % m;
+        float bv = wv[it][sq][0];
+        uint32_t bj = wj[it][sq][0];
+        for (int w = 1; w < 4; ++w)
+            if (wv[it][sq][w] < bv || (wv[it][sq][w] == bv && wj[it][sq][w] < bj)) { bv = wv[it][sq][w]; bj = wj[it][sq][w]; }
+        qcodes[(size_t)(item0 + it) * m + sq] = static_cast<uint8_t>(perms[sq * KSUB + bj]);
+    }
+}
+
 void launch_residual_lut(const float* queries, uint32_t nq, uint32_t dim, uint32_t m,
                          const unsigned long long* probe_keys, uint32_t nprobe, const float* cent,
                          const float* codebooks, const uint16_t* perms, float* lutp, uint8_t* qcodes, cudaStream_t s) {
     if (nq == 0) return;
     const uint32_t nitems = nq * nprobe;
-    residual_lut_kernel<<<(nitems + K1R_ITEMS - 1) / K1R_ITEMS, 256, 0, s>>>(queries, dim, m, probe_keys, nprobe,
-                                                                             nitems, cent, codebooks, perms, lutp,
-                                                                             qcodes);
+    const uint32_t grid = (nitems + K1R_ITEMS - 1) / K1R_ITEMS;
+    if (POLY_K1R_PAIR)
+        residual_lut_pair_kernel<<<grid, 128, 0, s>>>(queries, dim, m, probe_keys, nprobe, nitems, cent, codebooks,
+                                                      perms, lutp, qcodes, 0.0f);
+    else
+        residual_lut_kernel<<<grid, 256, 0, s>>>(queries, dim, m, probe_keys, nprobe, nitems, cent, codebooks, perms,
+                                                 lutp, qcodes);
     count_launch();
 }
 
@@ -447,7 +603,8 @@ void launch_residual_lut(const float* queries, uint32_t nq, uint32_t dim, uint32
 __global__ void ivf_probe_count_kernel(const unsigned long long* __restrict__ probe_keys, uint32_t nq,
                                        uint32_t nprobe, const uint64_t* __restrict__ off, uint64_t cap,
                                        uint32_t* __restrict__ np_eff, unsigned long long* __restrict__ scanned,
-                                       uint32_t* __restrict__ split, uint64_t r1_codes, uint32_t r1_max) {
+                                       uint32_t* __restrict__ split, uint64_t r1_codes, uint32_t r1_max,
+                                       IvfWork w) {
     // one warp per query: list sizes in parallel, running prefix over the probes in order;
     // probe p is visited iff no cap or the codes before it are < cap
     const uint32_t qi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
@@ -496,16 +653,45 @@ __global__ void ivf_probe_count_kernel(const unsigned long long* __restrict__ pr
             if (lane >= (uint32_t)o) incl += v;
         }
         const uint32_t hit = __ballot_sync(0xffffffffu, lane < lim && incl >= r1_codes);
-        if (lane == 0) split[qi] = max(1u, hit ? (uint32_t)__ffs(hit) : lim);
+        const uint32_t sp = max(1u, hit ? (uint32_t)__ffs(hit) : lim);
+        if (lane == 0) split[qi] = sp;
+        // work lists: round 1 = probes [0, sp), round 2 = [sp, ne), each list cut into
+        // chunks of w.chunk[r] rows; one item per (query, probe, chunk) that has rows
+        if (w.items[0]) {
+            for (int r = 0; r < 2; ++r) {
+                const uint32_t plo = r ? sp : 0, phi = r ? ne : min(sp, ne), ch = w.chunk[r];
+                for (uint32_t p0 = plo; p0 < phi; p0 += 32) {
+                    const uint32_t p = p0 + lane;
+                    uint32_t nch = 0;
+                    if (p < phi) {
+                        const uint32_t cell = (uint32_t)probe_keys[(size_t)qi * nprobe + p];
+                        nch = (uint32_t)((off[cell + 1] - off[cell] + ch - 1) / ch);
+                    }
+                    uint32_t incl = nch;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= (uint32_t)o) incl += v;
+                    }
+                    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+                    uint32_t at = 0;
+                    if (lane == 0 && tot) at = atomicAdd(w.nitems + r, tot);
+                    at = __shfl_sync(0xffffffffu, at, 0) + incl - nch;
+                    for (uint32_t c = 0; c < nch; ++c)
+                        if (at + c < w.cap[r]) w.items[r][at + c] = make_uint4(qi, p, c, 0u);
+                        else atomicOr(w.overflow, 1u);
+                }
+            }
+        }
     }
 }
 
 void launch_ivf_probe_count(const unsigned long long* probe_keys, uint32_t nq, uint32_t nprobe, const uint64_t* off,
                             uint64_t cap, uint32_t* np_eff, unsigned long long* scanned, cudaStream_t s,
-                            uint32_t* split, uint64_t r1_codes, uint32_t r1_max) {
+                            uint32_t* split, uint64_t r1_codes, uint32_t r1_max, const IvfWork& w) {
     if (nq == 0) return;
     ivf_probe_count_kernel<<<(nq * 32 + 127) / 128, 128, 0, s>>>(probe_keys, nq, nprobe, off, cap, np_eff, scanned,
-                                                                  split, r1_codes, r1_max);
+                                                                  split, r1_codes, r1_max, w);
     count_launch();
 }
 
@@ -536,20 +722,29 @@ __device__ __forceinline__ uint32_t k6_word(const uint2& c, int w) { return w ==
 __device__ __forceinline__ uint32_t k6_word(const uint4& c, int w) {
     return w == 0 ? c.x : (w == 1 ? c.y : (w == 2 ? c.z : c.w));
 }
+// Early-exit form (as K2's adc_s_bounded): the first M/2 terms in sq order; a
+// prefix above the bound's score can only grow (non-negative terms, round-to-
+// nearest partial sums are monotone), so the pair is no candidate: +inf.
 template <int M, class C>
-__device__ __forceinline__ float k6_adc(const float* L, const C& c) {
+__device__ __forceinline__ float k6_adc_bounded(const float* L, const C& c, uint32_t bound_bits) {
     float acc = L[k6_word(c, 0) & 0xFFu];
 #pragma unroll
-    for (int sq = 1; sq < M; ++sq) acc = __fadd_rn(acc, L[sq * KSUB + ((k6_word(c, sq >> 2) >> (8 * (sq & 3))) & 0xFFu)]);
+    for (int sq = 1; sq < M / 2; ++sq) acc = __fadd_rn(acc, L[sq * KSUB + ((k6_word(c, sq >> 2) >> (8 * (sq & 3))) & 0xFFu)]);
+    if (__float_as_uint(acc) > bound_bits) return __int_as_float(0x7f800000);
+#pragma unroll
+    for (int sq = M / 2; sq < M; ++sq) acc = __fadd_rn(acc, L[sq * KSUB + ((k6_word(c, sq >> 2) >> (8 * (sq & 3))) & 0xFFu)]);
     return acc;
 }
 
-// One CTA per (query, probe) item of probes [p_begin, p_end) of each query
-// (dynamic fetch): the 8 warps split the cell's list and share the item's LUT
-// in shared memory; each warp compacts its survivors with a ballot into its
-// own queue and drains 32 at a time (ADC, candidate test).
+// Work items (query, probe, chunk of the probed cell's list) are fetched
+// dynamically; the 8 warps of a CTA split the chunk and share the item's LUT
+// in shared memory.  Each warp compacts its filter survivors with a ballot into
+// its own queue and drains 32 at a time (ADC with early exit, candidate test).
 template <int M, int STRAT>
-__global__ void __launch_bounds__(K6_WARPS * 32) ivf_scan_kernel(const IvfScanArgs a) {
+#ifndef POLY_K6_MINB
+#define POLY_K6_MINB 8  // 8 CTAs (64 warps) per SM: <= 32 registers
+#endif
+__global__ void __launch_bounds__(K6_WARPS * 32, POLY_K6_MINB) ivf_scan_kernel(const IvfScanArgs a) {
     using C = typename IvfCode<M>::T;
     extern __shared__ __align__(16) uint8_t k6_smem[];
     float* L = reinterpret_cast<float*>(k6_smem);  // M x 256 floats
@@ -558,8 +753,7 @@ __global__ void __launch_bounds__(K6_WARPS * 32) ivf_scan_kernel(const IvfScanAr
     C* qcode_q = reinterpret_cast<C*>(qbase);
     uint32_t* qpos_q = reinterpret_cast<uint32_t*>(qbase + 64 * sizeof(C));
     __shared__ uint32_t item_s;
-    const uint32_t span = a.p_end - a.p_begin;
-    const uint64_t nitems = (uint64_t)a.nq * span * a.nchunks;
+    const uint32_t nitems = min(*a.nitems, a.items_cap);
     uint32_t surv_total = 0;
     for (;;) {
         __syncthreads();
@@ -567,24 +761,17 @@ __global__ void __launch_bounds__(K6_WARPS * 32) ivf_scan_kernel(const IvfScanAr
         __syncthreads();
         const uint32_t it = item_s;
         if (it >= nitems) break;
-        const uint32_t ch = it % a.nchunks, iq = it / a.nchunks;
-        const uint32_t qi = iq / span, p = a.p_begin + iq % span;
-        if (p >= a.np_eff[qi]) continue;
-        if (a.split && (a.round1 ? p >= a.split[qi] : p < a.split[qi])) continue;  // round 1: p < split
-        const size_t item = (size_t)qi * a.nprobe + p;
+        const uint4 w = a.items[it];  // (query, probe, chunk)
+        const uint32_t qi = w.x;
+        const size_t item = (size_t)qi * a.nprobe + w.y;
         const uint32_t cell = (uint32_t)a.probe_keys[item];
-        uint64_t beg = a.off[cell], end = a.off[cell + 1];
-        if (a.nchunks > 1) {  // this CTA's slice of the list
-            beg += (uint64_t)ch * a.chunk_codes;
-            if (beg >= end) continue;
-            end = min(end, beg + a.chunk_codes);
-        }
+        const uint64_t beg = a.off[cell] + (uint64_t)w.z * a.chunk_codes;
+        const uint64_t end = min(a.off[cell + 1], beg + a.chunk_codes);
         const float4* src = reinterpret_cast<const float4*>(a.lutp + item * M * KSUB);
         for (int i = threadIdx.x; i < M * KSUB / 4; i += K6_WARPS * 32) reinterpret_cast<float4*>(L)[i] = src[i];
         const C qc = reinterpret_cast<const C*>(a.qcodes)[item];
         const unsigned long long thr = __ldcg(a.thr + qi);
         __syncthreads();
-        const C* codes = reinterpret_cast<const C*>(a.codes);
         uint32_t qn = 0;
         auto candidate = [&](float score, uint32_t pos) {
             const uint32_t sb = __float_as_uint(score);
@@ -599,33 +786,36 @@ __global__ void __launch_bounds__(K6_WARPS * 32) ivf_scan_kernel(const IvfScanAr
         };
         auto drain = [&](uint32_t cnt) {
             __syncwarp();
-            if ((uint32_t)lane < cnt) candidate(k6_adc<M>(L, qcode_q[lane]), qpos_q[lane]);
+            if ((uint32_t)lane < cnt) candidate(k6_adc_bounded<M>(L, qcode_q[lane], (uint32_t)(thr >> 32)), qpos_q[lane]);
             __syncwarp();
         };
-        // warp w scans rows beg + 128*w + ..., stride 128 * K6_WARPS
-        for (uint64_t i0 = beg + (uint64_t)warp * 128; i0 < end; i0 += 128 * K6_WARPS) {
+        // warp w scans rows 128*w + ..., stride 128 * K6_WARPS, of the item's rows
+        // [beg, end) (32-bit offsets); whole 128-row blocks skip the bounds tests
+        const C* ci = reinterpret_cast<const C*>(a.codes) + beg;
+        const uint32_t n = (uint32_t)(end - beg), pos0 = (uint32_t)beg;
+        auto block = [&](uint32_t r0, auto full) {
             C c[4];
             bool in[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const uint64_t i = i0 + u * 32 + lane;
-                in[u] = i < end;
-                if (in[u]) c[u] = __ldcs(codes + i);  // streamed once: evict-first
+                const uint32_t r = r0 + u * 32 + lane;
+                in[u] = decltype(full)::value || r < n;
+                if (in[u]) c[u] = __ldcs(ci + r);  // streamed once: evict-first
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const uint32_t pos = (uint32_t)(i0 + u * 32 + lane);
+                const uint32_t pos = pos0 + r0 + u * 32 + lane;
                 if constexpr (STRAT == DUAL) {
                     const bool pass = in[u] && k6_ham(c[u], qc) <= a.tau;
-                    const uint32_t b = __ballot_sync(0xffffffffu, pass);
-                    if (b) {
+                    const uint32_t bal = __ballot_sync(0xffffffffu, pass);
+                    if (bal) {
                         if (pass) {
-                            const uint32_t at = qn + __popc(b & ((1u << lane) - 1u));
+                            const uint32_t at = qn + __popc(bal & ((1u << lane) - 1u));
                             qcode_q[at] = c[u];
                             qpos_q[at] = pos;
                         }
-                        qn += __popc(b);
-                        surv_total += __popc(b);
+                        qn += __popc(bal);
+                        surv_total += __popc(bal);
                         if (qn >= 32) {
                             drain(32);
                             qn -= 32;
@@ -638,13 +828,16 @@ __global__ void __launch_bounds__(K6_WARPS * 32) ivf_scan_kernel(const IvfScanAr
                     }
                 } else if (in[u]) {
                     float score;
-                    if constexpr (STRAT == ADC) score = k6_adc<M>(L, c[u]);
+                    if constexpr (STRAT == ADC) score = k6_adc_bounded<M>(L, c[u], (uint32_t)(thr >> 32));
                     else if constexpr (STRAT == BINARY) score = (float)k6_ham(c[u], qc);
                     else score = (float)k6_dis(c[u], qc);
                     candidate(score, pos);
                 }
             }
-        }
+        };
+        uint32_t r0 = warp * 128;
+        for (; r0 + 128 <= n; r0 += 128 * K6_WARPS) block(r0, std::true_type{});
+        if (r0 < n) block(r0, std::false_type{});
         if (STRAT == DUAL && qn) drain(qn);
     }
     if (STRAT == DUAL && lane == 0 && surv_total) atomicAdd(a.surv_total, (unsigned long long)surv_total);
@@ -675,7 +868,7 @@ static void launch_ivf_m(const IvfScanArgs& a, int strategy, int num_sms, cudaSt
 }
 
 void launch_ivf_scan(const IvfScanArgs& a, int strategy, uint32_t m, int num_sms, cudaStream_t s) {
-    if (a.nq == 0 || a.p_end <= a.p_begin) return;
+    if (a.nq == 0) return;
     if (m == 8) launch_ivf_m<8>(a, strategy, num_sms, s);
     else launch_ivf_m<16>(a, strategy, num_sms, s);
 }

@@ -22,7 +22,7 @@ constexpr int TK_THREADS = 512;
 constexpr uint32_t TK_SMEM_KEYS = 8192;
 constexpr int TK_MAXPARTS = 64;
 #ifndef POLY_TK_DIRECT
-#define POLY_TK_DIRECT 2048
+#define POLY_TK_DIRECT 512  // IVF A/B: 2048 -> 512 cut the K3 rounds ~6% (flat path: no effect)
 #endif
 constexpr uint32_t TK_DIRECT = POLY_TK_DIRECT;  // at most this many: sort them all
 constexpr uint32_t TK_SEL_KEYS = 4096;  // >= k + 1 (k <= 2048); with 2048 buckets: 104 KB, two CTAs per SM
@@ -242,6 +242,33 @@ __global__ void seed_thr_kernel(const unsigned long long* keys, const uint32_t* 
 void launch_seed_thr(const unsigned long long* keys, const uint32_t* counts, uint32_t nq, uint32_t k,
                      unsigned long long* thr, cudaStream_t s) {
     seed_thr_kernel<<<(nq + 127) / 128, 128, 0, s>>>(keys, counts, nq, k, thr);
+    count_launch();
+}
+}  // namespace pb
+
+namespace pb {
+// Between the IVF rounds: thr[q] = k-th key of round 1 + 1 (as seed_thr_kernel),
+// and the query's candidate list is cut down to its round-1 top-k, so the final
+// K3 ranks k + (round-2 candidates) keys: top-k(A u B) = top-k(top-k(A) u B).
+__global__ void seed_compact_kernel(const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ counts,
+                                    uint32_t k, unsigned long long* __restrict__ thr,
+                                    unsigned long long* __restrict__ cand, uint32_t cap,
+                                    uint32_t* __restrict__ ccount) {
+    const uint32_t q = blockIdx.x, c = counts[q];
+    for (uint32_t i = threadIdx.x; i < c; i += blockDim.x) cand[(size_t)q * cap + i] = keys[(size_t)q * k + i];
+    if (threadIdx.x == 0) {
+        ccount[q] = c;
+        if (c >= k) {
+            const unsigned long long t = keys[(size_t)q * k + k - 1] + 1;
+            if (t < thr[q]) thr[q] = t;
+        }
+    }
+}
+void launch_seed_compact(const unsigned long long* keys, const uint32_t* counts, uint32_t nq, uint32_t k,
+                         unsigned long long* thr, unsigned long long* cand, uint32_t cap, uint32_t* ccount,
+                         cudaStream_t s) {
+    if (nq == 0) return;
+    seed_compact_kernel<<<nq, 128, 0, s>>>(keys, counts, k, thr, cand, cap, ccount);
     count_launch();
 }
 }  // namespace pb

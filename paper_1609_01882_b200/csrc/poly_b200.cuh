@@ -106,10 +106,9 @@ struct IvfScanArgs {
     const uint32_t* low;                  // list-ordered key low words (id or id rank)
     const uint64_t* off;                  // nlist + 1 list offsets
     const unsigned long long* probe_keys; // nq x nprobe (dist bits << 32 | cell), ascending
-    const uint32_t* np_eff;               // probes visited per query (cap)
     const float* lutp;                    // (nq x nprobe) x M x 256 residual LUTs
     const uint8_t* qcodes;                // (nq x nprobe) x CB residual query codes
-    uint32_t nq, nprobe, p_begin, p_end, tau;
+    uint32_t nq, nprobe, tau;
     unsigned long long* thr;              // per-query key bound (seeded between rounds)
     unsigned long long* cand;             // nq x cap candidate keys
     uint32_t cap;
@@ -117,10 +116,18 @@ struct IvfScanArgs {
     uint32_t* overflow;
     uint32_t* work;
     unsigned long long* surv_total;
-    const uint32_t* split;  // per query: round 1 scans probes [0, split), round 2 the rest (null: by p range)
-    uint32_t round1;
-    uint32_t nchunks;       // work item = (query, probe, chunk); chunk c covers list rows
-    uint32_t chunk_codes;   // [c * chunk_codes, (c + 1) * chunk_codes)  (nchunks = 1: whole list)
+    const uint4* items;      // work items (query, probe, chunk): chunk c covers list rows
+    const uint32_t* nitems;  // [c * chunk_codes, (c + 1) * chunk_codes); built by the probe-count kernel
+    uint32_t items_cap, chunk_codes;
+};
+
+// Work lists of the two K6 rounds, written by launch_ivf_probe_count.
+struct IvfWork {
+    uint4* items[2];
+    uint32_t* nitems;   // 2 counters (zeroed before the launch)
+    uint32_t cap[2];
+    uint32_t chunk[2];
+    uint32_t* overflow;
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -293,6 +300,9 @@ void launch_relabel(uint8_t* codes, uint64_t n, uint32_t m, const uint8_t* maps,
 
 void launch_seed_thr(const unsigned long long* keys, const uint32_t* counts, uint32_t nq, uint32_t k,
                      unsigned long long* thr, cudaStream_t s);
+void launch_seed_compact(const unsigned long long* keys, const uint32_t* counts, uint32_t nq, uint32_t k,
+                         unsigned long long* thr, unsigned long long* cand, uint32_t cap, uint32_t* ccount,
+                         cudaStream_t s);
 // IVF (kernels_ivf.cu)
 void launch_coarse_keys(const float* q, uint32_t nq, uint32_t dim, const float* cent, uint32_t nlist,
                         unsigned long long* keys, cudaStream_t s);
@@ -307,7 +317,7 @@ void launch_residual_lut(const float* queries, uint32_t nq, uint32_t dim, uint32
                          const float* codebooks, const uint16_t* perms, float* lutp, uint8_t* qcodes, cudaStream_t s);
 void launch_ivf_probe_count(const unsigned long long* probe_keys, uint32_t nq, uint32_t nprobe, const uint64_t* off,
                             uint64_t cap, uint32_t* np_eff, unsigned long long* scanned, cudaStream_t s,
-                            uint32_t* split = nullptr, uint64_t r1_codes = 0, uint32_t r1_max = 1);
+                            uint32_t* split, uint64_t r1_codes, uint32_t r1_max, const IvfWork& w);
 void launch_ivf_scan(const IvfScanArgs& a, int strategy, uint32_t m, int num_sms, cudaStream_t s);
 void launch_assign(const float* x, uint64_t n, uint32_t dim, const float* cent, uint32_t nlist, uint32_t* assign,
                    cudaStream_t s);

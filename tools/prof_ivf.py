@@ -10,6 +10,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument('--n', type=int, default=20_000_000)
 ap.add_argument('--nprobe', type=int, default=16)
 ap.add_argument('--reps', type=int, default=2)
+ap.add_argument('--nq', type=int, default=256)
 args = ap.parse_args()
 z = np.load('tests/golden/pq_ivf65536_d128_m8.npz')
 pq = pb.ProductQuantizer(8, 8, 128, z['codebooks'], z['perms'])
@@ -26,7 +27,7 @@ for r in range(0, args.n, 1 << 20):
         xs = x[b:min(b + 8192, nb)]
         cells[b:b + xs.shape[0]] = torch.argmin(cn[None, :] - 2.0 * (xs @ dc.T), dim=1).to(torch.int32)
     ivf.add_device(x[:nb], cells[:nb], r)
-q = synth.gen_points(160901882, 3, 0, 256, centers)
+q = synth.gen_points(160901882, 3, 0, args.nq, centers)
 p = pb.CoarseParams(pb.Strategy.dual, 100, 26, args.nprobe, 0)
 ivf.search(q, p)  # warm (allocations)
 torch.cuda.synchronize()
@@ -34,4 +35,4 @@ torch.cuda.profiler.start()  # ncu --profile-from-start off: only the searches b
 for i in range(args.reps):
     st = pb.SearchStats(); t = time.time(); ivf.search(q, p, st); dt = time.time() - t
 torch.cuda.profiler.stop()
-print(f"n={args.n} nprobe={args.nprobe}: {dt*1e3:.2f} ms, scanned/query {st.scanned/256:.0f}, surv {st.survivors/max(st.scanned,1):.3f}")
+print(f"n={args.n} nprobe={args.nprobe}: {dt*1e3:.2f} ms, scanned/query {st.scanned/args.nq:.0f}, surv {st.survivors/max(st.scanned,1):.3f}")
