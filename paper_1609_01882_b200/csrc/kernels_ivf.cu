@@ -227,7 +227,7 @@ void launch_coarse_select(const float* q, uint32_t nq, uint32_t dim, const float
 // the (dist bits << 32 | cell) keys of the np smallest are emitted in order.
 // One CTA (512 threads) per query, one pass over the query's dots row (float4):
 // each thread keeps its two smallest a(c); those 1024 values are distinct cells,
-// so their np-th smallest (bitonic sort in shared memory) is >= the np-th
+// so their np-th smallest (radix-selected to 16 bits, rounded up) is >= the np-th
 // smallest a(c) over all cells and serves as T.  The cells with a(c) <= T + 2E
 // are a thread's kept ones, unless its second smallest is within the bound too
 // (then it revisits its cells); they go to a global scratch list and are
@@ -235,6 +235,7 @@ void launch_coarse_select(const float* q, uint32_t nq, uint32_t dim, const float
 constexpr int KR_THREADS = 512, KR_CHUNK = 2048, KR_NPMAX = 1024, KR_BUF = 4096;  // np + chunk <= buf (pow2)
 constexpr int KR_TVALS = 2 * KR_THREADS;  // per-thread two smallest
 constexpr int KR_UNROLL = 4;              // float4 loads in flight per thread
+constexpr uint32_t KR_RANKMAX = 1024;     // re-rank by counting up to this many keys (else bitonic)
 
 __device__ __forceinline__ uint32_t kr_ord(float f) {  // order-preserving float -> uint32
     const uint32_t b = __float_as_uint(f);
@@ -253,9 +254,9 @@ __global__ void __launch_bounds__(KR_THREADS, 2) coarse_refine_kernel(const floa
                                                                    uint32_t* __restrict__ probe_counts) {
     extern __shared__ __align__(16) uint8_t kr_smem[];
     unsigned long long* buf = reinterpret_cast<unsigned long long*>(kr_smem);  // KR_BUF keys
-    uint32_t* tv = reinterpret_cast<uint32_t*>(buf);                            // KR_TVALS (aliases buf)
     float* qs = reinterpret_cast<float*>(buf + KR_BUF);                         // dim
     __shared__ float red_f[KR_THREADS / 32];
+    __shared__ uint32_t red_u[2];
     __shared__ uint32_t ncand_s;
     const uint32_t qi = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const float* qrow = q + (size_t)qi * dim;
@@ -314,23 +315,49 @@ __global__ void __launch_bounds__(KR_THREADS, 2) coarse_refine_kernel(const floa
         }
     };
     visit(keep);
-    tv[2 * tid] = kr_ord(m1);
-    tv[2 * tid + 1] = kr_ord(m2);
-    __syncthreads();
-    for (uint32_t size = 2; size <= KR_TVALS; size <<= 1)
-        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-            const uint32_t pos = 2 * tid - (tid & (stride - 1));
-            const bool asc = (pos & size) == 0;
-            const uint32_t x = tv[pos], y = tv[pos + stride];
-            if ((x > y) == asc) { tv[pos] = y; tv[pos + stride] = x; }
-            __syncthreads();
+    // T: an upper bound of the np-th smallest of the 1024 kept values -- a radix select
+    // of its top 16 bits (two 8-bit passes), T = the upper edge of that 16-bit bucket
+    uint32_t* hist = reinterpret_cast<uint32_t*>(buf);  // 256 bins (aliases buf)
+    const uint32_t k1 = kr_ord(m1), k2 = kr_ord(m2);
+    uint32_t prefix = 0, want = min(np, (uint32_t)KR_TVALS);
+    for (int pass = 0; pass < 2; ++pass) {
+        const int sh = 24 - 8 * pass;
+        if (tid < 256) hist[tid] = 0;
+        __syncthreads();
+        const uint32_t pm = pass ? prefix >> (sh + 8) : 0;
+        if (!pass || (k1 >> (sh + 8)) == pm) atomicAdd(&hist[(k1 >> sh) & 255u], 1u);
+        if (!pass || (k2 >> (sh + 8)) == pm) atomicAdd(&hist[(k2 >> sh) & 255u], 1u);
+        __syncthreads();
+        if (warp == 0) {  // bin holding the want-th key: lane-sums of 8 bins, warp scan
+            uint32_t c8 = 0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) c8 += hist[lane * 8 + e];
+            uint32_t incl = c8;
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= (uint32_t)off) incl += o;
+            }
+            const uint32_t excl = incl - c8;
+            if (excl < want && want <= incl) {
+                uint32_t cum = excl, dg = lane * 8;
+                for (int e = 0; e < 8; ++e) {
+                    if (cum + hist[lane * 8 + e] >= want) { dg = lane * 8 + e; break; }
+                    cum += hist[lane * 8 + e];
+                }
+                red_u[0] = dg;
+                red_u[1] = cum;
+            }
         }
+        __syncthreads();
+        prefix |= red_u[0] << sh;
+        want -= red_u[1];
+        __syncthreads();  // red_u and hist reused
+    }
     // T >= the np-th smallest a(c); candidate bound T + 2E (np <= KR_NPMAX = KR_TVALS)
-    const float T = kr_unord(tv[min(np, (uint32_t)KR_TVALS) - 1]);
+    const float T = kr_unord(prefix | 0xFFFFu);
     const float qnorm = sqrtf(qn);
     const float E = 4.1e-3f * qnorm * cmax + 4e-5f * (qn + cmax * cmax + 2.0f * qnorm * cmax) + 1e-6f;
     const float bound = T + 2.0f * E;
-    __syncthreads();  // tv (aliases buf) read by all before the re-rank writes buf
     // candidates: a thread whose second smallest is within the bound may hold more
     // (its third, ...): it revisits its cells (rare: the near cells are spread over
     // the threads); otherwise its candidates are among its two smallest
@@ -370,6 +397,21 @@ __global__ void __launch_bounds__(KR_THREADS, 2) coarse_refine_kernel(const floa
             buf[ntop + i] = ((unsigned long long)__float_as_uint(acc) << 32) | cell;
         }
         const uint32_t n = ntop + cn;
+        __syncthreads();
+        if (n <= KR_RANKMAX) {  // rank by counting (keys distinct: the low word is the cell)
+            unsigned long long* out = buf + KR_BUF / 2;
+            for (uint32_t i = tid; i < n; i += KR_THREADS) {
+                const unsigned long long ki = buf[i];
+                uint32_t rank = 0;
+                for (uint32_t j = 0; j < n; ++j) rank += buf[j] < ki;
+                if (rank < np) out[rank] = ki;
+            }
+            __syncthreads();
+            for (uint32_t i = tid; i < min(n, np); i += KR_THREADS) buf[i] = out[i];
+            __syncthreads();
+            ntop = min(n, np);
+            continue;
+        }
         uint32_t P = 1;
         while (P < n) P <<= 1;
         for (uint32_t i = n + tid; i < P; i += KR_THREADS) buf[i] = ~0ull;
