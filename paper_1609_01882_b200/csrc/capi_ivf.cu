@@ -221,7 +221,7 @@ void ensure_ivf_scratch(poly_b200_ivf* iv, uint32_t nprobe, uint32_t k) {
     const uint64_t r1 = std::min<uint64_t>(nprobe, IVF_R1_MAX);
     const uint64_t need[2] = {
         (uint64_t)IVF_NQB * (r1 + (r1 * iv->max_list + IVF_CHUNK - 1) / IVF_CHUNK),
-        (uint64_t)IVF_NQB * (nprobe + (std::min<uint64_t>(iv->n, nprobe * iv->max_list) + IVF_CHUNK2 - 1) / IVF_CHUNK2)};
+        (uint64_t)IVF_NQB * (nprobe + r1 + (std::min<uint64_t>(iv->n, nprobe * iv->max_list) + IVF_CHUNK2 - 1) / IVF_CHUNK2)};
     for (int r = 0; r < 2; ++r)
         if (iv->items_cap[r] < need[r]) {
             require(need[r] < (1ull << 32), POLY_B200_INVALID_ARGUMENT, "IVF work list too large");
@@ -345,7 +345,6 @@ void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_
         a.items = iv->items[round];
         a.nitems = w.nitems + round;
         a.items_cap = w.cap[round];
-        a.chunk_codes = w.chunk[round];
         a.work = iv->ctrl + IVF_NQB + 1 + round;
         pb::launch_ivf_scan(a, strategy, iv->m, iv->num_sms, s);
         pb::launch_topk(iv->cand, iv->ctrl, iv->cand_cap, 1, 0, 0, nqb, k, iv->keys, iv->kcounts, s);

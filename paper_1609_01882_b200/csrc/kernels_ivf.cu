@@ -530,7 +530,8 @@ __global__ void __launch_bounds__(256) residual_lut_kernel(const float* __restri
 // lane pair, so each (item, dim) term is FADD2 (r - c), FFMA2 (t * t + z, z a
 // runtime +0.0: exactly mul.rn, and ptxas cannot contract it into the add), FADD2
 // (acc + s) for two centroids -- the same rounding sequence as sq_l2 per lane.
-// The residual sits in shared memory duplicated as (r, r) pairs.
+// The residual sits in shared memory duplicated as (r, r) pairs.  (A pre-paired
+// codebook layout that spares the register-pair MOVs measured slower: 381 -> 501 us.)
 __device__ __forceinline__ unsigned long long k1_pack(float lo, float hi) {
     unsigned long long v;
     asm("mov.b64 %0, {%1,%2};" : "=l"(v) : "f"(lo), "f"(hi));
@@ -697,18 +698,22 @@ __global__ void ivf_probe_count_kernel(const unsigned long long* __restrict__ pr
         const uint32_t hit = __ballot_sync(0xffffffffu, lane < lim && incl >= r1_codes);
         const uint32_t sp = max(1u, hit ? (uint32_t)__ffs(hit) : lim);
         if (lane == 0) split[qi] = sp;
-        // work lists: round 1 = probes [0, sp), round 2 = [sp, ne), each list cut into
-        // chunks of w.chunk[r] rows; one item per (query, probe, chunk) that has rows
+        // work lists: round 1 = probes [0, sp), round 2 = [sp, ne) (A/B: cutting round 1
+        // at 2048 / 4096 rows instead of whole probes gained nothing).  Lists are cut into
+        // chunks of w.chunk[r] rows; one item (query, probe, row0, row1) per chunk.
         if (w.items[0]) {
             for (int r = 0; r < 2; ++r) {
-                const uint32_t plo = r ? sp : 0, phi = r ? ne : min(sp, ne), ch = w.chunk[r];
-                for (uint32_t p0 = plo; p0 < phi; p0 += 32) {
+                const uint32_t phi = r ? ne : min(sp, ne), ch = w.chunk[r];
+                for (uint32_t p0 = 0; p0 < phi; p0 += 32) {
                     const uint32_t p = p0 + lane;
-                    uint32_t nch = 0;
+                    uint32_t len = 0;
                     if (p < phi) {
                         const uint32_t cell = (uint32_t)probe_keys[(size_t)qi * nprobe + p];
-                        nch = (uint32_t)((off[cell + 1] - off[cell] + ch - 1) / ch);
+                        len = (uint32_t)(off[cell + 1] - off[cell]);
                     }
+                    const uint32_t ap = p < min(sp, ne) ? len : 0;  // round-1 rows of probe p
+                    const uint32_t lo = r ? ap : 0, hi = r ? len : ap;
+                    const uint32_t nch = hi > lo ? (hi - lo + ch - 1) / ch : 0;
                     uint32_t incl = nch;
 #pragma unroll
                     for (int o = 1; o < 32; o <<= 1) {
@@ -720,8 +725,10 @@ __global__ void ivf_probe_count_kernel(const unsigned long long* __restrict__ pr
                     if (lane == 0 && tot) at = atomicAdd(w.nitems + r, tot);
                     at = __shfl_sync(0xffffffffu, at, 0) + incl - nch;
                     for (uint32_t c = 0; c < nch; ++c)
-                        if (at + c < w.cap[r]) w.items[r][at + c] = make_uint4(qi, p, c, 0u);
-                        else atomicOr(w.overflow, 1u);
+                        if (at + c < w.cap[r])
+                            w.items[r][at + c] = make_uint4(qi, p, lo + c * ch, min(hi, lo + (c + 1) * ch));
+                        else
+                            atomicOr(w.overflow, 1u);
                 }
             }
         }
@@ -803,12 +810,11 @@ __global__ void __launch_bounds__(K6_WARPS * 32, POLY_K6_MINB) ivf_scan_kernel(c
         __syncthreads();
         const uint32_t it = item_s;
         if (it >= nitems) break;
-        const uint4 w = a.items[it];  // (query, probe, chunk)
+        const uint4 w = a.items[it];  // (query, probe, row0, row1)
         const uint32_t qi = w.x;
         const size_t item = (size_t)qi * a.nprobe + w.y;
         const uint32_t cell = (uint32_t)a.probe_keys[item];
-        const uint64_t beg = a.off[cell] + (uint64_t)w.z * a.chunk_codes;
-        const uint64_t end = min(a.off[cell + 1], beg + a.chunk_codes);
+        const uint64_t beg = a.off[cell] + w.z, end = a.off[cell] + w.w;  // the item's rows
         const float4* src = reinterpret_cast<const float4*>(a.lutp + item * M * KSUB);
         for (int i = threadIdx.x; i < M * KSUB / 4; i += K6_WARPS * 32) reinterpret_cast<float4*>(L)[i] = src[i];
         const C qc = reinterpret_cast<const C*>(a.qcodes)[item];

@@ -116,9 +116,9 @@ struct IvfScanArgs {
     uint32_t* overflow;
     uint32_t* work;
     unsigned long long* surv_total;
-    const uint4* items;      // work items (query, probe, chunk): chunk c covers list rows
-    const uint32_t* nitems;  // [c * chunk_codes, (c + 1) * chunk_codes); built by the probe-count kernel
-    uint32_t items_cap, chunk_codes;
+    const uint4* items;      // work items (query, probe, row0, row1): rows [row0, row1) of the
+    const uint32_t* nitems;  // probed cell's list; built by the probe-count kernel
+    uint32_t items_cap;
 };
 
 // Work lists of the two K6 rounds, written by launch_ivf_probe_count.
