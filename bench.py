@@ -343,6 +343,9 @@ def run_knn(args, c, ivf, centers, setup_s, rank, world, local, row0, row1):
                              stream.cuda_stream)
     torch.cuda.synchronize()
     l0 = pb.launch_count()
+    prof = os.environ.get("BENCH_PROFILE") == "1"  # ncu --profile-from-start off: the timed steps only
+    if prof:
+        torch.cuda.profiler.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for i in range(args.warmup, args.warmup + steps):
@@ -350,6 +353,8 @@ def run_knn(args, c, ivf, centers, setup_s, rank, world, local, row0, row1):
                              stream.cuda_stream)
     e1.record(stream)
     torch.cuda.synchronize()
+    if prof:
+        torch.cuda.profiler.stop()
     ms = e0.elapsed_time(e1)
     rows = row1 - row0
     line = {"metric": METRIC, "value": scanned / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": steps,

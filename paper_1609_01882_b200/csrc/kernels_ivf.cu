@@ -456,7 +456,7 @@ void launch_coarse_refine(const float* q, uint32_t nq, uint32_t dim, const float
 #define POLY_K1R_ITEMS 8
 #endif
 #ifndef POLY_K1R_PAIR
-#define POLY_K1R_PAIR 1  // centroid-pair kernel (packed f32x2) instead of one centroid per thread
+#define POLY_K1R_PAIR 2  // 2: two centroid pairs per thread, 1: one pair (packed f32x2), 0: one centroid
 #endif
 constexpr uint32_t K1R_ITEMS = POLY_K1R_ITEMS;
 
@@ -625,13 +625,118 @@ __global__ void __launch_bounds__(128) residual_lut_pair_kernel(const float* __r
     }
 }
 
+// K1r, two centroid pairs per thread: the 128 threads cover two sub-quantizers at a
+// time (thread t: sq 2s + (t >> 6), pairs (u, u + 128) and (u + 64, u + 192), u = t & 63),
+// so each shared-memory load of a residual pair feeds 12 packed FP ops instead of 6
+// (the pair kernel's shared-memory pipe was 93% busy).
+__global__ void __launch_bounds__(128, 4) residual_lut_quad_kernel(const float* __restrict__ queries, uint32_t dim,
+                                                                   uint32_t m,
+                                                                   const unsigned long long* __restrict__ probe_keys,
+                                                                   uint32_t nprobe, uint32_t nitems,
+                                                                   const float* __restrict__ cent,
+                                                                   const float* __restrict__ codebooks,
+                                                                   const uint16_t* __restrict__ perms,
+                                                                   float* __restrict__ lutp,
+                                                                   uint8_t* __restrict__ qcodes, float zero) {
+    const uint32_t item0 = blockIdx.x * K1R_ITEMS, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const uint32_t h = t >> 6, u = t & 63, wh = warp & 1;  // sub-quantizer half, pair index, warp within half
+    const uint32_t ni = min(K1R_ITEMS, nitems - item0);
+    __shared__ __align__(16) unsigned long long rr[K1R_ITEMS][256];  // (r, r) per dim
+    __shared__ float wv[K1R_ITEMS][16][2];
+    __shared__ uint32_t wj[K1R_ITEMS][16][2];
+    __shared__ __align__(16) float stage[K1R_ITEMS][2][KSUB];  // two sub-quantizers' rows, stored-field order
+    for (uint32_t e = t; e < ni * dim; e += 128) {
+        const uint32_t it = e / dim, d = e % dim, item = item0 + it;
+        const uint32_t qi = item / nprobe, cell = (uint32_t)probe_keys[item];
+        const float r = __fsub_rn(queries[(size_t)qi * dim + d], cent[(size_t)cell * dim + d]);  // r = q - c
+        rr[it][d] = k1_pack(r, r);
+    }
+    __syncthreads();
+    const unsigned long long zz = k1_pack(zero, zero);
+    const uint32_t ja = u, jb = u + 128, jc = u + 64, jd = u + 192;  // pair 0 = (ja, jb), pair 1 = (jc, jd)
+    for (uint32_t s2 = 0; s2 < m / 2; ++s2) {
+        const uint32_t sq = 2 * s2 + h;
+        const float4* ca = reinterpret_cast<const float4*>(codebooks + ((size_t)sq * KSUB + ja) * DSUB);
+        const float4* cb = reinterpret_cast<const float4*>(codebooks + ((size_t)sq * KSUB + jb) * DSUB);
+        const float4* cc_ = reinterpret_cast<const float4*>(codebooks + ((size_t)sq * KSUB + jc) * DSUB);
+        const float4* cd = reinterpret_cast<const float4*>(codebooks + ((size_t)sq * KSUB + jd) * DSUB);
+        unsigned long long p0[DSUB], p1[DSUB];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const float4 a = __ldg(ca + v), b = __ldg(cb + v), c = __ldg(cc_ + v), d = __ldg(cd + v);
+            p0[4 * v + 0] = k1_pack(a.x, b.x); p1[4 * v + 0] = k1_pack(c.x, d.x);
+            p0[4 * v + 1] = k1_pack(a.y, b.y); p1[4 * v + 1] = k1_pack(c.y, d.y);
+            p0[4 * v + 2] = k1_pack(a.z, b.z); p1[4 * v + 2] = k1_pack(c.z, d.z);
+            p0[4 * v + 3] = k1_pack(a.w, b.w); p1[4 * v + 3] = k1_pack(c.w, d.w);
+        }
+        unsigned long long acc0[K1R_ITEMS], acc1[K1R_ITEMS];
+#pragma unroll
+        for (uint32_t it = 0; it < K1R_ITEMS; ++it) { acc0[it] = zz; acc1[it] = zz; }
+#pragma unroll
+        for (int d2 = 0; d2 < DSUB / 2; ++d2) {
+#pragma unroll
+            for (uint32_t it = 0; it < K1R_ITEMS; ++it) {
+                const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(&rr[min(it, ni - 1)][sq * DSUB + 2 * d2]);
+                unsigned long long tt, q2;
+#define K1Q_TERM(XV, CV, ACC)                                                         \
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(tt) : "l"(XV), "l"(CV));                    \
+    asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(q2) : "l"(tt), "l"(zz));               \
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(ACC) : "l"(ACC), "l"(q2));
+                K1Q_TERM(x.x, p0[2 * d2], acc0[it])
+                K1Q_TERM(x.x, p1[2 * d2], acc1[it])
+                K1Q_TERM(x.y, p0[2 * d2 + 1], acc0[it])
+                K1Q_TERM(x.y, p1[2 * d2 + 1], acc1[it])
+#undef K1Q_TERM
+            }
+        }
+        const uint32_t da = perms[sq * KSUB + ja], db = perms[sq * KSUB + jb];
+        const uint32_t dc = perms[sq * KSUB + jc], dd = perms[sq * KSUB + jd];
+        __syncthreads();  // the previous rows are written out
+#pragma unroll
+        for (uint32_t it = 0; it < K1R_ITEMS; ++it) {
+            if (it >= ni) break;
+            float va, vb, vc, vd;
+            asm("mov.b64 {%0,%1}, %2;" : "=f"(va), "=f"(vb) : "l"(acc0[it]));
+            asm("mov.b64 {%0,%1}, %2;" : "=f"(vc), "=f"(vd) : "l"(acc1[it]));
+            stage[it][h][da] = va;
+            stage[it][h][db] = vb;
+            stage[it][h][dc] = vc;
+            stage[it][h][dd] = vd;
+            // argmin, ties -> lowest centroid (pq.cpp:38); index order ja < jc < jb < jd
+            const uint32_t ba = __float_as_uint(va), bb = __float_as_uint(vb);
+            const uint32_t bc = __float_as_uint(vc), bd = __float_as_uint(vd);
+            const uint32_t wmin = __reduce_min_sync(0xffffffffu, min(min(ba, bb), min(bc, bd)));
+            const uint32_t jj = ba == wmin ? ja : (bc == wmin ? jc : (bb == wmin ? jb : (bd == wmin ? jd : 0xFFFFFFFFu)));
+            const uint32_t jmin = __reduce_min_sync(0xffffffffu, jj);
+            if (lane == 0) { wv[it][sq][wh] = __uint_as_float(wmin); wj[it][sq][wh] = jmin; }
+        }
+        __syncthreads();
+        for (uint32_t e = t; e < ni * 2 * (KSUB / 4); e += 128) {  // float4 rows out
+            const uint32_t it = e / (2 * (KSUB / 4)), hh = (e / (KSUB / 4)) & 1, o = e % (KSUB / 4);
+            reinterpret_cast<float4*>(lutp + ((size_t)(item0 + it) * m + 2 * s2 + hh) * KSUB)[o] =
+                reinterpret_cast<const float4*>(stage[it][hh])[o];
+        }
+    }
+    __syncthreads();
+    if (t < ni * m) {  // across the 2 warps of each sub-quantizer
+        const uint32_t it = t / m, sq = t % m;
+        float bv = wv[it][sq][0];
+        uint32_t bj = wj[it][sq][0];
+        if (wv[it][sq][1] < bv || (wv[it][sq][1] == bv && wj[it][sq][1] < bj)) bj = wj[it][sq][1];
+        qcodes[(size_t)(item0 + it) * m + sq] = static_cast<uint8_t>(perms[sq * KSUB + bj]);
+    }
+}
+
 void launch_residual_lut(const float* queries, uint32_t nq, uint32_t dim, uint32_t m,
                          const unsigned long long* probe_keys, uint32_t nprobe, const float* cent,
                          const float* codebooks, const uint16_t* perms, float* lutp, uint8_t* qcodes, cudaStream_t s) {
     if (nq == 0) return;
     const uint32_t nitems = nq * nprobe;
     const uint32_t grid = (nitems + K1R_ITEMS - 1) / K1R_ITEMS;
-    if (POLY_K1R_PAIR)
+    if (POLY_K1R_PAIR == 2)
+        residual_lut_quad_kernel<<<grid, 128, 0, s>>>(queries, dim, m, probe_keys, nprobe, nitems, cent, codebooks,
+                                                      perms, lutp, qcodes, 0.0f);
+    else if (POLY_K1R_PAIR)
         residual_lut_pair_kernel<<<grid, 128, 0, s>>>(queries, dim, m, probe_keys, nprobe, nitems, cent, codebooks,
                                                       perms, lutp, qcodes, 0.0f);
     else
