@@ -896,9 +896,9 @@ __device__ __forceinline__ float k6_adc_bounded(const float* L, const C& c, uint
 // its own queue and drains 32 at a time (ADC with early exit, candidate test).
 template <int M, int STRAT>
 #ifndef POLY_K6_MINB
-#define POLY_K6_MINB 8  // 8 CTAs (64 warps) per SM: <= 32 registers
+#define POLY_K6_MINB 8  // m = 8: 8 CTAs (64 warps) per SM, <= 32 registers (m = 16: 5 CTAs)
 #endif
-__global__ void __launch_bounds__(K6_WARPS * 32, POLY_K6_MINB) ivf_scan_kernel(const IvfScanArgs a) {
+__global__ void __launch_bounds__(K6_WARPS * 32, M == 8 ? POLY_K6_MINB : 5) ivf_scan_kernel(const IvfScanArgs a) {
     using C = typename IvfCode<M>::T;
     extern __shared__ __align__(16) uint8_t k6_smem[];
     float* L = reinterpret_cast<float*>(k6_smem);  // M x 256 floats
@@ -943,18 +943,28 @@ __global__ void __launch_bounds__(K6_WARPS * 32, POLY_K6_MINB) ivf_scan_kernel(c
             __syncwarp();
         };
         // warp w scans rows 128*w + ..., stride 128 * K6_WARPS, of the item's rows
-        // [beg, end) (32-bit offsets); whole 128-row blocks skip the bounds tests
+        // [beg, end) (32-bit offsets)
         const C* ci = reinterpret_cast<const C*>(a.codes) + beg;
         const uint32_t n = (uint32_t)(end - beg), pos0 = (uint32_t)beg;
-        auto block = [&](uint32_t r0, auto full) {
+        // software-pipelined: the warp's next 128-row block is loaded while this one is
+        // filtered and drained
+        C cn[4];
+        auto load = [&](uint32_t r0) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t r = r0 + u * 32 + lane;
+                if (r < n) cn[u] = __ldcs(ci + r);  // streamed once: evict-first
+            }
+        };
+        auto block = [&](uint32_t r0) {
             C c[4];
             bool in[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const uint32_t r = r0 + u * 32 + lane;
-                in[u] = decltype(full)::value || r < n;
-                if (in[u]) c[u] = __ldcs(ci + r);  // streamed once: evict-first
+                c[u] = cn[u];
+                in[u] = r0 + u * 32 + lane < n;
             }
+            if (r0 + 128 * K6_WARPS < n) load(r0 + 128 * K6_WARPS);
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const uint32_t pos = pos0 + r0 + u * 32 + lane;
@@ -988,9 +998,8 @@ __global__ void __launch_bounds__(K6_WARPS * 32, POLY_K6_MINB) ivf_scan_kernel(c
                 }
             }
         };
-        uint32_t r0 = warp * 128;
-        for (; r0 + 128 <= n; r0 += 128 * K6_WARPS) block(r0, std::true_type{});
-        if (r0 < n) block(r0, std::false_type{});
+        if (warp * 128u < n) load(warp * 128u);
+        for (uint32_t r0 = warp * 128; r0 < n; r0 += 128 * K6_WARPS) block(r0);
         if (STRAT == DUAL && qn) drain(qn);
     }
     if (STRAT == DUAL && lane == 0 && surv_total) atomicAdd(a.surv_total, (unsigned long long)surv_total);
@@ -1010,7 +1019,7 @@ static void launch_ivf_one(const IvfScanArgs& a, unsigned grid, cudaStream_t s) 
 
 template <int M>
 static void launch_ivf_m(const IvfScanArgs& a, int strategy, int num_sms, cudaStream_t s) {
-    const unsigned grid = (unsigned)num_sms * (M == 8 ? 8 : 6);  // ~14 KB (m=8) / ~24 KB (m=16) smem per CTA
+    const unsigned grid = (unsigned)num_sms * (M == 8 ? 8 : 5);  // ~14 KB (m=8) / ~26 KB (m=16) smem per CTA
     switch (strategy) {
         case DUAL: launch_ivf_one<M, DUAL>(a, grid, s); break;
         case ADC: launch_ivf_one<M, ADC>(a, grid, s); break;
