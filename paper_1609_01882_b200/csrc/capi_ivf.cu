@@ -92,6 +92,8 @@ struct poly_b200_ivf {
     cublasHandle_t cublas = nullptr;
 
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;  // K1r of the round-2 probes, overlapping round 1
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     std::mutex mu;
     uint32_t code_bits() const { return m * 8; }
 };
@@ -319,7 +321,19 @@ void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_
                                IVF_R1_CODES, IVF_R1_MAX, w);
     add_u64<<<1, 256, 0, s>>>(iv->scanned, nqb, iv->scan_total);
     pb::count_launch();
-    pb::launch_residual_lut(d_q, nqb, iv->dim, iv->m, iv->probe_keys, np, iv->d_coarse, iv->d_codebooks,
+    // residual LUTs: the round-1 probes on the caller's stream; the others on the side
+    // stream, overlapping round 1, its top-k and the compaction (K1r is FP / shared-
+    // memory bound, round 1 memory / latency bound); round 2 waits for them
+    const uint32_t r1p = std::min(np, IVF_R1_MAX);
+    const bool side = r1p < np;
+    if (side) {
+        CK(cudaEventRecord(iv->ev_fork, s));
+        CK(cudaStreamWaitEvent(iv->side, iv->ev_fork, 0));
+        pb::launch_residual_lut(d_q, nqb, iv->dim, iv->m, iv->probe_keys, np, r1p, np, iv->d_coarse,
+                                iv->d_codebooks, iv->d_perms, iv->lutp, iv->qcodes, iv->side);
+        CK(cudaEventRecord(iv->ev_join, iv->side));
+    }
+    pb::launch_residual_lut(d_q, nqb, iv->dim, iv->m, iv->probe_keys, np, 0, r1p, iv->d_coarse, iv->d_codebooks,
                             iv->d_perms, iv->lutp, iv->qcodes, s);
     pb::IvfScanArgs a{};
     a.codes = iv->d_codes_list;
@@ -342,6 +356,7 @@ void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_
     // 1024-row chunks; its exact k-th key (K3) bounds round 2, the remaining probes
     for (uint32_t round = 0; round < 2; ++round) {
         if (round == 1 && np <= 1) break;  // one probe: round 1 saw everything
+        if (round == 1 && side) CK(cudaStreamWaitEvent(s, iv->ev_join, 0));
         a.items = iv->items[round];
         a.nitems = w.nitems + round;
         a.items_cap = w.cap[round];
@@ -465,6 +480,9 @@ int poly_b200_ivf_create(const poly_b200_pq_desc* pq, const float* coarse, uint3
             iv->h_perms.assign(pq->perms, pq->perms + (size_t)pq->m * 256);
             iv->h_coarse.assign(coarse, coarse + (size_t)nlist * pq->dim);
             CK(cudaStreamCreateWithFlags(&iv->stream, cudaStreamNonBlocking));
+            CK(cudaStreamCreateWithFlags(&iv->side, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&iv->ev_fork, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&iv->ev_join, cudaEventDisableTiming));
             iv->d_codebooks = dalloc<float>(ncb);
             iv->d_perms = dalloc<uint16_t>(iv->h_perms.size());
             iv->d_coarse = dalloc<float>(iv->h_coarse.size());
@@ -502,6 +520,7 @@ int poly_b200_ivf_destroy(poly_b200_ivf* iv) {
         {
             DeviceGuard dg(iv->device);
             if (iv->stream) cudaStreamSynchronize(iv->stream);
+            if (iv->side) cudaStreamSynchronize(iv->side);
             for (void* p : {(void*)iv->d_codebooks, (void*)iv->d_perms, (void*)iv->d_coarse, (void*)iv->d_codes_ins,
                             (void*)iv->d_cells_ins, (void*)iv->d_off, (void*)iv->d_codes_list, (void*)iv->d_low_list,
                             (void*)iv->ckeys, (void*)iv->nl_counts, (void*)iv->probe_keys, (void*)iv->probe_counts,
@@ -515,6 +534,9 @@ int poly_b200_ivf_destroy(poly_b200_ivf* iv) {
             if (iv->cublas) cublasDestroy(iv->cublas);
             iv->idm.release();
             if (iv->stream) cudaStreamDestroy(iv->stream);
+            if (iv->side) cudaStreamDestroy(iv->side);
+            if (iv->ev_fork) cudaEventDestroy(iv->ev_fork);
+            if (iv->ev_join) cudaEventDestroy(iv->ev_join);
         }
         delete iv;
     });

@@ -7,12 +7,16 @@
 //                            fp32 in dim order; key = (dist bits << 32 | cell), so K3
 //                            with k = nprobe yields enumerate_cells:
 //                            ascending distance, ties -> lower cell.
-//   K1r residual_lut_kernel  per (query, probe): r = q - c_cell, then compute_lut /
-//                            permuted_lut / encode on r (pq.cpp:29-45,91-119).
-//   K6  ivf_scan_kernel      per (query, probe) item, one warp: stream the cell's
-//                            (residual code, id) list, Hamming filter against the
-//                            item's query code, ADC from the item's LUT in shared
-//                            memory, candidate keys appended to the query's list.
+//   K5r coarse_refine_kernel enumerate_cells from TF32 dots + an exact fp32 re-rank
+//                            of every cell within the dots' error bound.
+//   K1r residual_lut_quad_kernel  per (query, probe): r = q - c_cell, then
+//                            compute_lut / permuted_lut / encode on r
+//                            (pq.cpp:29-45,91-119), packed f32x2, bit-exact.
+//   K6  ivf_scan_kernel      per work item (query, probe, row range), one CTA: stream
+//                            the cell's (residual code, id) list, Hamming filter
+//                            against the item's query code, ADC from the item's LUT
+//                            in shared memory, candidate keys appended to the
+//                            query's list.
 //   assign_kernel            build: nearest coarse cell by sq_l2 (strict <).
 #include <type_traits>
 
@@ -455,76 +459,7 @@ void launch_coarse_refine(const float* q, uint32_t nq, uint32_t dim, const float
 #ifndef POLY_K1R_ITEMS
 #define POLY_K1R_ITEMS 8
 #endif
-#ifndef POLY_K1R_PAIR
-#define POLY_K1R_PAIR 2  // 2: two centroid pairs per thread, 1: one pair (packed f32x2), 0: one centroid
-#endif
 constexpr uint32_t K1R_ITEMS = POLY_K1R_ITEMS;
-
-__global__ void __launch_bounds__(256) residual_lut_kernel(const float* __restrict__ queries, uint32_t dim, uint32_t m,
-                                                           const unsigned long long* __restrict__ probe_keys,
-                                                           uint32_t nprobe, uint32_t nitems,
-                                                           const float* __restrict__ cent,
-                                                           const float* __restrict__ codebooks,
-                                                           const uint16_t* __restrict__ perms, float* __restrict__ lutp,
-                                                           uint8_t* __restrict__ qcodes) {
-    const uint32_t item0 = blockIdx.x * K1R_ITEMS, j = threadIdx.x;
-    const uint32_t ni = min(K1R_ITEMS, nitems - item0);
-    __shared__ __align__(16) float r[K1R_ITEMS][256];
-    __shared__ float wv[K1R_ITEMS][16][8];
-    __shared__ uint32_t wj[K1R_ITEMS][16][8];
-    for (uint32_t e = j; e < ni * dim; e += 256) {
-        const uint32_t it = e / dim, d = e % dim, item = item0 + it;
-        const uint32_t qi = item / nprobe, cell = (uint32_t)probe_keys[item];
-        r[it][d] = __fsub_rn(queries[(size_t)qi * dim + d], cent[(size_t)cell * dim + d]);  // r = q - c
-    }
-    __syncthreads();
-    for (uint32_t sq = 0; sq < m; ++sq) {
-        const float4* c = reinterpret_cast<const float4*>(codebooks + ((size_t)sq * KSUB + j) * DSUB);
-        float cb[DSUB];
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-            const float4 cc = __ldg(c + v);
-            cb[4 * v + 0] = cc.x; cb[4 * v + 1] = cc.y; cb[4 * v + 2] = cc.z; cb[4 * v + 3] = cc.w;
-        }
-        const uint32_t dst = perms[sq * KSUB + j];
-        // the items' sums interleaved (independent chains), each in dim order as sq_l2
-        float acc[K1R_ITEMS];
-#pragma unroll
-        for (uint32_t it = 0; it < K1R_ITEMS; ++it) acc[it] = 0.0f;
-#pragma unroll
-        for (int v = 0; v < DSUB / 4; ++v) {
-#pragma unroll
-            for (uint32_t it = 0; it < K1R_ITEMS; ++it) {
-                const float4 x = *reinterpret_cast<const float4*>(&r[min(it, ni - 1)][sq * DSUB + 4 * v]);
-                const float xs[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const float t = __fsub_rn(xs[e], cb[4 * v + e]);
-                    acc[it] = __fadd_rn(acc[it], __fmul_rn(t, t));
-                }
-            }
-        }
-#pragma unroll
-        for (uint32_t it = 0; it < K1R_ITEMS; ++it) {
-            if (it >= ni) break;
-            lutp[((size_t)(item0 + it) * m + sq) * KSUB + dst] = acc[it];
-            // warp argmin, ties -> lowest j: acc >= 0, so its bits order like the value
-            const uint32_t bits = __float_as_uint(acc[it]);
-            const uint32_t wmin = __reduce_min_sync(0xffffffffu, bits);
-            const uint32_t first = __ffs(__ballot_sync(0xffffffffu, bits == wmin)) - 1;
-            if ((j & 31) == 0) { wv[it][sq][j >> 5] = __uint_as_float(wmin); wj[it][sq][j >> 5] = (j & ~31u) + first; }
-        }
-    }
-    __syncthreads();
-    if (j < ni * m) {  // argmin per (item, sub-quantizer), ties -> lowest centroid (pq.cpp:38)
-        const uint32_t it = j / m, sq = j % m;
-        float bv = wv[it][sq][0];
-        uint32_t bj = wj[it][sq][0];
-        for (int w = 1; w < 8; ++w)
-            if (wv[it][sq][w] < bv || (wv[it][sq][w] == bv && wj[it][sq][w] < bj)) { bv = wv[it][sq][w]; bj = wj[it][sq][w]; }
-        qcodes[(size_t)(item0 + it) * m + sq] = static_cast<uint8_t>(perms[sq * KSUB + bj]);
-    }
-}
 
 // K1r, centroid pairs: thread t owns centroids t and t + 128 as one packed f32x2
 // lane pair, so each (item, dim) term is FADD2 (r - c), FFMA2 (t * t + z, z a
@@ -538,93 +473,6 @@ __device__ __forceinline__ unsigned long long k1_pack(float lo, float hi) {
     return v;
 }
 
-__global__ void __launch_bounds__(128) residual_lut_pair_kernel(const float* __restrict__ queries, uint32_t dim,
-                                                                uint32_t m, const unsigned long long* __restrict__ probe_keys,
-                                                                uint32_t nprobe, uint32_t nitems,
-                                                                const float* __restrict__ cent,
-                                                                const float* __restrict__ codebooks,
-                                                                const uint16_t* __restrict__ perms,
-                                                                float* __restrict__ lutp, uint8_t* __restrict__ qcodes,
-                                                                float zero) {
-    const uint32_t item0 = blockIdx.x * K1R_ITEMS, t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const uint32_t ni = min(K1R_ITEMS, nitems - item0);
-    __shared__ __align__(16) unsigned long long rr[K1R_ITEMS][256];  // (r, r) per dim
-    __shared__ float wv[K1R_ITEMS][16][4];
-    __shared__ uint32_t wj[K1R_ITEMS][16][4];
-    __shared__ __align__(16) float stage[K1R_ITEMS][KSUB];  // one sub-quantizer's rows, stored-field order
-    for (uint32_t e = t; e < ni * dim; e += 128) {
-        const uint32_t it = e / dim, d = e % dim, item = item0 + it;
-        const uint32_t qi = item / nprobe, cell = (uint32_t)probe_keys[item];
-        const float r = __fsub_rn(queries[(size_t)qi * dim + d], cent[(size_t)cell * dim + d]);  // r = q - c
-        rr[it][d] = k1_pack(r, r);
-    }
-    __syncthreads();
-    unsigned long long zz = k1_pack(zero, zero);
-    const uint32_t j0 = t, j1 = t + 128;
-    for (uint32_t sq = 0; sq < m; ++sq) {
-        const float4* c0 = reinterpret_cast<const float4*>(codebooks + ((size_t)sq * KSUB + j0) * DSUB);
-        const float4* c1 = reinterpret_cast<const float4*>(codebooks + ((size_t)sq * KSUB + j1) * DSUB);
-        unsigned long long cc[DSUB];
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-            const float4 a = __ldg(c0 + v), b = __ldg(c1 + v);
-            cc[4 * v + 0] = k1_pack(a.x, b.x);
-            cc[4 * v + 1] = k1_pack(a.y, b.y);
-            cc[4 * v + 2] = k1_pack(a.z, b.z);
-            cc[4 * v + 3] = k1_pack(a.w, b.w);
-        }
-        const uint32_t dst0 = perms[sq * KSUB + j0], dst1 = perms[sq * KSUB + j1];
-        unsigned long long acc[K1R_ITEMS];
-#pragma unroll
-        for (uint32_t it = 0; it < K1R_ITEMS; ++it) acc[it] = zz;
-#pragma unroll
-        for (int d2 = 0; d2 < DSUB / 2; ++d2) {
-#pragma unroll
-            for (uint32_t it = 0; it < K1R_ITEMS; ++it) {
-                const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(&rr[min(it, ni - 1)][sq * DSUB + 2 * d2]);
-                unsigned long long tt, s2;
-                asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(tt) : "l"(x.x), "l"(cc[2 * d2]));
-                asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(s2) : "l"(tt), "l"(zz));
-                asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc[it]) : "l"(acc[it]), "l"(s2));
-                asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(tt) : "l"(x.y), "l"(cc[2 * d2 + 1]));
-                asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(s2) : "l"(tt), "l"(zz));
-                asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc[it]) : "l"(acc[it]), "l"(s2));
-            }
-        }
-        __syncthreads();  // the previous sub-quantizer's stage rows are written out
-#pragma unroll
-        for (uint32_t it = 0; it < K1R_ITEMS; ++it) {
-            if (it >= ni) break;
-            float v0, v1;
-            asm("mov.b64 {%0,%1}, %2;" : "=f"(v0), "=f"(v1) : "l"(acc[it]));
-            stage[it][dst0] = v0;  // permuted (stored-field) order; written out coalesced below
-            stage[it][dst1] = v1;
-            // argmin over the 256 centroids, ties -> lowest index (pq.cpp:38): values >= 0
-            // order like their bits; the warp minimum, then the lowest index holding it
-            const uint32_t b0 = __float_as_uint(v0), b1 = __float_as_uint(v1);
-            const uint32_t wmin = __reduce_min_sync(0xffffffffu, min(b0, b1));
-            const uint32_t jj = b0 == wmin ? j0 : (b1 == wmin ? j1 : 0xFFFFFFFFu);
-            const uint32_t jmin = __reduce_min_sync(0xffffffffu, jj);
-            if (lane == 0) { wv[it][sq][warp] = __uint_as_float(wmin); wj[it][sq][warp] = jmin; }
-        }
-        __syncthreads();
-        for (uint32_t e = t; e < ni * (KSUB / 4); e += 128) {  // float4 rows out
-            const uint32_t it = e / (KSUB / 4), o = e % (KSUB / 4);
-            reinterpret_cast<float4*>(lutp + ((size_t)(item0 + it) * m + sq) * KSUB)[o] =
-                reinterpret_cast<const float4*>(stage[it])[o];
-        }
-    }
-    __syncthreads();
-    if (t < ni * m) {  // across the 4 warps
-        const uint32_t it = t / m, sq = t % m;
-        float bv = wv[it][sq][0];
-        uint32_t bj = wj[it][sq][0];
-        for (int w = 1; w < 4; ++w)
-            if (wv[it][sq][w] < bv || (wv[it][sq][w] == bv && wj[it][sq][w] < bj)) { bv = wv[it][sq][w]; bj = wj[it][sq][w]; }
-        qcodes[(size_t)(item0 + it) * m + sq] = static_cast<uint8_t>(perms[sq * KSUB + bj]);
-    }
-}
-
 // K1r, two centroid pairs per thread: the 128 threads cover two sub-quantizers at a
 // time (thread t: sq 2s + (t >> 6), pairs (u, u + 128) and (u + 64, u + 192), u = t & 63),
 // so each shared-memory load of a residual pair feeds 12 packed FP ops instead of 6
@@ -632,7 +480,8 @@ __global__ void __launch_bounds__(128) residual_lut_pair_kernel(const float* __r
 __global__ void __launch_bounds__(128, 4) residual_lut_quad_kernel(const float* __restrict__ queries, uint32_t dim,
                                                                    uint32_t m,
                                                                    const unsigned long long* __restrict__ probe_keys,
-                                                                   uint32_t nprobe, uint32_t nitems,
+                                                                   uint32_t nprobe, uint32_t p_lo, uint32_t span,
+                                                                   uint32_t nitems,
                                                                    const float* __restrict__ cent,
                                                                    const float* __restrict__ codebooks,
                                                                    const uint16_t* __restrict__ perms,
@@ -641,12 +490,14 @@ __global__ void __launch_bounds__(128, 4) residual_lut_quad_kernel(const float* 
     const uint32_t item0 = blockIdx.x * K1R_ITEMS, t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const uint32_t h = t >> 6, u = t & 63, wh = warp & 1;  // sub-quantizer half, pair index, warp within half
     const uint32_t ni = min(K1R_ITEMS, nitems - item0);
+    // local item i covers probe p_lo + i % span of query i / span: global item q * nprobe + p
+    auto gitem = [&](uint32_t i) { return (i / span) * nprobe + p_lo + i % span; };
     __shared__ __align__(16) unsigned long long rr[K1R_ITEMS][256];  // (r, r) per dim
     __shared__ float wv[K1R_ITEMS][16][2];
     __shared__ uint32_t wj[K1R_ITEMS][16][2];
     __shared__ __align__(16) float stage[K1R_ITEMS][2][KSUB];  // two sub-quantizers' rows, stored-field order
     for (uint32_t e = t; e < ni * dim; e += 128) {
-        const uint32_t it = e / dim, d = e % dim, item = item0 + it;
+        const uint32_t it = e / dim, d = e % dim, item = gitem(item0 + it);
         const uint32_t qi = item / nprobe, cell = (uint32_t)probe_keys[item];
         const float r = __fsub_rn(queries[(size_t)qi * dim + d], cent[(size_t)cell * dim + d]);  // r = q - c
         rr[it][d] = k1_pack(r, r);
@@ -713,7 +564,7 @@ __global__ void __launch_bounds__(128, 4) residual_lut_quad_kernel(const float* 
         __syncthreads();
         for (uint32_t e = t; e < ni * 2 * (KSUB / 4); e += 128) {  // float4 rows out
             const uint32_t it = e / (2 * (KSUB / 4)), hh = (e / (KSUB / 4)) & 1, o = e % (KSUB / 4);
-            reinterpret_cast<float4*>(lutp + ((size_t)(item0 + it) * m + 2 * s2 + hh) * KSUB)[o] =
+            reinterpret_cast<float4*>(lutp + ((size_t)gitem(item0 + it) * m + 2 * s2 + hh) * KSUB)[o] =
                 reinterpret_cast<const float4*>(stage[it][hh])[o];
         }
     }
@@ -723,25 +574,19 @@ __global__ void __launch_bounds__(128, 4) residual_lut_quad_kernel(const float* 
         float bv = wv[it][sq][0];
         uint32_t bj = wj[it][sq][0];
         if (wv[it][sq][1] < bv || (wv[it][sq][1] == bv && wj[it][sq][1] < bj)) bj = wj[it][sq][1];
-        qcodes[(size_t)(item0 + it) * m + sq] = static_cast<uint8_t>(perms[sq * KSUB + bj]);
+        qcodes[(size_t)gitem(item0 + it) * m + sq] = static_cast<uint8_t>(perms[sq * KSUB + bj]);
     }
 }
 
 void launch_residual_lut(const float* queries, uint32_t nq, uint32_t dim, uint32_t m,
-                         const unsigned long long* probe_keys, uint32_t nprobe, const float* cent,
-                         const float* codebooks, const uint16_t* perms, float* lutp, uint8_t* qcodes, cudaStream_t s) {
-    if (nq == 0) return;
-    const uint32_t nitems = nq * nprobe;
+                         const unsigned long long* probe_keys, uint32_t nprobe, uint32_t p_lo, uint32_t p_hi,
+                         const float* cent, const float* codebooks, const uint16_t* perms, float* lutp,
+                         uint8_t* qcodes, cudaStream_t s) {
+    if (nq == 0 || p_hi <= p_lo) return;
+    const uint32_t span = p_hi - p_lo, nitems = nq * span;
     const uint32_t grid = (nitems + K1R_ITEMS - 1) / K1R_ITEMS;
-    if (POLY_K1R_PAIR == 2)
-        residual_lut_quad_kernel<<<grid, 128, 0, s>>>(queries, dim, m, probe_keys, nprobe, nitems, cent, codebooks,
-                                                      perms, lutp, qcodes, 0.0f);
-    else if (POLY_K1R_PAIR)
-        residual_lut_pair_kernel<<<grid, 128, 0, s>>>(queries, dim, m, probe_keys, nprobe, nitems, cent, codebooks,
-                                                      perms, lutp, qcodes, 0.0f);
-    else
-        residual_lut_kernel<<<grid, 256, 0, s>>>(queries, dim, m, probe_keys, nprobe, nitems, cent, codebooks, perms,
-                                                 lutp, qcodes);
+    residual_lut_quad_kernel<<<grid, 128, 0, s>>>(queries, dim, m, probe_keys, nprobe, p_lo, span, nitems, cent,
+                                                  codebooks, perms, lutp, qcodes, 0.0f);
     count_launch();
 }
 

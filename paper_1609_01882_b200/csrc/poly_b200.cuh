@@ -312,9 +312,11 @@ void launch_coarse_refine(const float* q, uint32_t nq, uint32_t dim, const float
                           unsigned long long* probe_keys, uint32_t* probe_counts, cudaStream_t s);
 void launch_coarse_select(const float* q, uint32_t nq, uint32_t dim, const float* cent, uint32_t nlist, uint32_t np,
                           uint32_t slices, unsigned long long* out_keys, uint32_t* out_counts, cudaStream_t s);
+// K1r over the probes [p_lo, p_hi) of every query (items q * nprobe + p)
 void launch_residual_lut(const float* queries, uint32_t nq, uint32_t dim, uint32_t m,
-                         const unsigned long long* probe_keys, uint32_t nprobe, const float* cent,
-                         const float* codebooks, const uint16_t* perms, float* lutp, uint8_t* qcodes, cudaStream_t s);
+                         const unsigned long long* probe_keys, uint32_t nprobe, uint32_t p_lo, uint32_t p_hi,
+                         const float* cent, const float* codebooks, const uint16_t* perms, float* lutp,
+                         uint8_t* qcodes, cudaStream_t s);
 void launch_ivf_probe_count(const unsigned long long* probe_keys, uint32_t nq, uint32_t nprobe, const uint64_t* off,
                             uint64_t cap, uint32_t* np_eff, unsigned long long* scanned, cudaStream_t s,
                             uint32_t* split, uint64_t r1_codes, uint32_t r1_max, const IvfWork& w);
