@@ -230,14 +230,14 @@ void launch_coarse_select(const float* q, uint32_t nq, uint32_t dim, const float
 // has a(c) <= T + 2E; those cells get the exact sq_l2 (fp32, dim order, as K5) and
 // the (dist bits << 32 | cell) keys of the np smallest are emitted in order.
 // One CTA (512 threads) per query, one pass over the query's dots row (float4):
-// each thread keeps its two smallest a(c); those 1024 values are distinct cells,
+// each thread keeps its three smallest a(c); those 1536 values are distinct cells,
 // so their np-th smallest (radix-selected to 16 bits, rounded up) is >= the np-th
 // smallest a(c) over all cells and serves as T.  The cells with a(c) <= T + 2E
-// are a thread's kept ones, unless its second smallest is within the bound too
+// are among a thread's kept ones, unless its third smallest is within the bound too
 // (then it revisits its cells); they go to a global scratch list and are
 // re-ranked in chunks of KR_CHUNK.
 constexpr int KR_THREADS = 512, KR_CHUNK = 2048, KR_NPMAX = 1024, KR_BUF = 4096;  // np + chunk <= buf (pow2)
-constexpr int KR_TVALS = 2 * KR_THREADS;  // per-thread two smallest
+constexpr int KR_TVALS = 3 * KR_THREADS;  // per-thread three smallest
 constexpr int KR_UNROLL = 4;              // float4 loads in flight per thread
 constexpr uint32_t KR_RANKMAX = 1024;     // re-rank by counting up to this many keys (else bitonic)
 
@@ -282,12 +282,17 @@ __global__ void __launch_bounds__(KR_THREADS, 2) coarse_refine_kernel(const floa
     for (int w = 0; w < KR_THREADS / 32; ++w) qn += red_f[w];
     // one pass over the row: the two smallest a(c) = |q|^2 + |c|^2 - 2 q.c of this
     // thread's cells, with their indices
-    float m1 = INFINITY, m2 = INFINITY;
+    float m1 = INFINITY, m2 = INFINITY, m3 = INFINITY;
     uint32_t i1 = 0xFFFFFFFFu, i2 = 0xFFFFFFFFu;
     auto keep = [&](float a, uint32_t c) {
-        if (a < m2) {
-            if (a < m1) { m2 = m1; i2 = i1; m1 = a; i1 = c; }
-            else { m2 = a; i2 = c; }
+        if (a < m3) {
+            if (a < m2) {
+                m3 = m2;
+                if (a < m1) { m2 = m1; i2 = i1; m1 = a; i1 = c; }
+                else { m2 = a; i2 = c; }
+            } else {
+                m3 = a;
+            }
         }
     };
     const float4* d4 = reinterpret_cast<const float4*>(drow);
@@ -322,7 +327,7 @@ __global__ void __launch_bounds__(KR_THREADS, 2) coarse_refine_kernel(const floa
     // T: an upper bound of the np-th smallest of the 1024 kept values -- a radix select
     // of its top 16 bits (two 8-bit passes), T = the upper edge of that 16-bit bucket
     uint32_t* hist = reinterpret_cast<uint32_t*>(buf);  // 256 bins (aliases buf)
-    const uint32_t k1 = kr_ord(m1), k2 = kr_ord(m2);
+    const uint32_t k1 = kr_ord(m1), k2 = kr_ord(m2), k3 = kr_ord(m3);
     uint32_t prefix = 0, want = min(np, (uint32_t)KR_TVALS);
     for (int pass = 0; pass < 2; ++pass) {
         const int sh = 24 - 8 * pass;
@@ -331,6 +336,7 @@ __global__ void __launch_bounds__(KR_THREADS, 2) coarse_refine_kernel(const floa
         const uint32_t pm = pass ? prefix >> (sh + 8) : 0;
         if (!pass || (k1 >> (sh + 8)) == pm) atomicAdd(&hist[(k1 >> sh) & 255u], 1u);
         if (!pass || (k2 >> (sh + 8)) == pm) atomicAdd(&hist[(k2 >> sh) & 255u], 1u);
+        if (!pass || (k3 >> (sh + 8)) == pm) atomicAdd(&hist[(k3 >> sh) & 255u], 1u);
         __syncthreads();
         if (warp == 0) {  // bin holding the want-th key: lane-sums of 8 bins, warp scan
             uint32_t c8 = 0;
@@ -357,20 +363,22 @@ __global__ void __launch_bounds__(KR_THREADS, 2) coarse_refine_kernel(const floa
         want -= red_u[1];
         __syncthreads();  // red_u and hist reused
     }
-    // T >= the np-th smallest a(c); candidate bound T + 2E (np <= KR_NPMAX = KR_TVALS)
+    // T >= the np-th smallest a(c); candidate bound T + 2E (np <= KR_NPMAX <= KR_TVALS)
     const float T = kr_unord(prefix | 0xFFFFu);
     const float qnorm = sqrtf(qn);
     const float E = 4.1e-3f * qnorm * cmax + 4e-5f * (qn + cmax * cmax + 2.0f * qnorm * cmax) + 1e-6f;
     const float bound = T + 2.0f * E;
-    // candidates: a thread whose second smallest is within the bound may hold more
-    // (its third, ...): it revisits its cells (rare: the near cells are spread over
-    // the threads); otherwise its candidates are among its two smallest
-    if (!(m2 > bound)) {
+    // candidates: a thread whose third smallest is within the bound may hold more (its
+    // fourth, ...): it revisits its cells -- rare, since the near cells are spread over
+    // the threads, but the CTA waits for it (with two kept values it was the main
+    // barrier stall); otherwise its candidates are among its two smallest
+    if (!(m3 > bound)) {
         visit([&](float a, uint32_t c) {
             if (!(a > bound)) cand[atomicAdd(&ncand_s, 1u)] = c;
         });
-    } else if (!(m1 > bound)) {
-        cand[atomicAdd(&ncand_s, 1u)] = i1;
+    } else {
+        if (!(m1 > bound)) cand[atomicAdd(&ncand_s, 1u)] = i1;
+        if (!(m2 > bound)) cand[atomicAdd(&ncand_s, 1u)] = i2;
     }
     __syncthreads();
     const uint32_t ncand = ncand_s;
