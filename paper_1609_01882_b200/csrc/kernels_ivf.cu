@@ -763,9 +763,6 @@ __device__ __forceinline__ float k6_adc_bounded(const float* L, const C& c, uint
 // in shared memory.  Each warp compacts its filter survivors with a ballot into
 // its own queue and drains 32 at a time (ADC with early exit, candidate test).
 template <int M, int STRAT>
-#ifndef POLY_K6_PREFETCH
-#define POLY_K6_PREFETCH 0
-#endif
 #ifndef POLY_K6_MINB
 #define POLY_K6_MINB 8  // m = 8: 8 CTAs (64 warps) per SM, <= 32 registers (m = 16: 5 CTAs)
 #endif
@@ -774,45 +771,11 @@ __global__ void __launch_bounds__(K6_WARPS * 32, M == 8 ? POLY_K6_MINB : 5) ivf_
     extern __shared__ __align__(16) uint8_t k6_smem[];
     float* L = reinterpret_cast<float*>(k6_smem);  // M x 256 floats
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint8_t* qbase = k6_smem + (POLY_K6_PREFETCH ? 2 : 1) * (size_t)M * KSUB * 4 + warp * 64 * (sizeof(C) + 4);
+    uint8_t* qbase = k6_smem + (size_t)M * KSUB * 4 + warp * 64 * (sizeof(C) + 4);
     C* qcode_q = reinterpret_cast<C*>(qbase);
     uint32_t* qpos_q = reinterpret_cast<uint32_t*>(qbase + 64 * sizeof(C));
     const uint32_t nitems = min(*a.nitems, a.items_cap);
     uint32_t surv_total = 0;
-#if POLY_K6_PREFETCH
-    // the next item's LUT is loaded into registers before this item's scan and stored
-    // to the second shared buffer after it: the LUT load latency hides behind the scan
-    constexpr int LV = M * KSUB / 4 / (K6_WARPS * 32);  // float4 per thread (2 / 4)
-    __shared__ uint32_t item_s[2];
-    uint32_t b = 0;
-    if (threadIdx.x == 0) item_s[0] = atomicAdd(a.work, 1u);
-    __syncthreads();
-    uint32_t it = item_s[0];
-    if (it < nitems) {
-        const uint4 w0 = a.items[it];
-        const float4* src = reinterpret_cast<const float4*>(a.lutp + ((size_t)w0.x * a.nprobe + w0.y) * M * KSUB);
-        for (int i = threadIdx.x; i < M * KSUB / 4; i += K6_WARPS * 32) reinterpret_cast<float4*>(L)[i] = src[i];
-    }
-    while (it < nitems) {
-        if (threadIdx.x == 0) item_s[b ^ 1] = atomicAdd(a.work, 1u);
-        __syncthreads();  // LUT(it) in buffer b; item_s[b ^ 1] visible
-        const uint32_t itn = item_s[b ^ 1];
-        float4 nx[LV];
-        if (itn < nitems) {
-            const uint4 wn = a.items[itn];
-            const float4* src = reinterpret_cast<const float4*>(a.lutp + ((size_t)wn.x * a.nprobe + wn.y) * M * KSUB);
-#pragma unroll
-            for (int v = 0; v < LV; ++v) nx[v] = __ldcg(src + threadIdx.x + v * K6_WARPS * 32);
-        }
-        const float* Lb = L + b * M * KSUB;
-        const uint4 w = a.items[it];  // (query, probe, row0, row1)
-        const uint32_t qi = w.x;
-        const size_t item = (size_t)qi * a.nprobe + w.y;
-        const uint32_t cell = (uint32_t)a.probe_keys[item];
-        const uint64_t beg = a.off[cell] + w.z, end = a.off[cell] + w.w;  // the item's rows
-        const C qc = reinterpret_cast<const C*>(a.qcodes)[item];
-        const unsigned long long thr = __ldcg(a.thr + qi);
-#else
     __shared__ uint32_t item_s;
     for (;;) {
         __syncthreads();
@@ -830,8 +793,6 @@ __global__ void __launch_bounds__(K6_WARPS * 32, M == 8 ? POLY_K6_MINB : 5) ivf_
         const C qc = reinterpret_cast<const C*>(a.qcodes)[item];
         const unsigned long long thr = __ldcg(a.thr + qi);
         __syncthreads();
-        const float* Lb = L;
-#endif
         uint32_t qn = 0;
         auto candidate = [&](float score, uint32_t pos) {
             const uint32_t sb = __float_as_uint(score);
@@ -846,7 +807,7 @@ __global__ void __launch_bounds__(K6_WARPS * 32, M == 8 ? POLY_K6_MINB : 5) ivf_
         };
         auto drain = [&](uint32_t cnt) {
             __syncwarp();
-            if ((uint32_t)lane < cnt) candidate(k6_adc_bounded<M>(Lb, qcode_q[lane], (uint32_t)(thr >> 32)), qpos_q[lane]);
+            if ((uint32_t)lane < cnt) candidate(k6_adc_bounded<M>(L, qcode_q[lane], (uint32_t)(thr >> 32)), qpos_q[lane]);
             __syncwarp();
         };
         // warp w scans rows 128*w + ..., stride 128 * K6_WARPS, of the item's rows
@@ -898,7 +859,7 @@ __global__ void __launch_bounds__(K6_WARPS * 32, M == 8 ? POLY_K6_MINB : 5) ivf_
                     }
                 } else if (in[u]) {
                     float score;
-                    if constexpr (STRAT == ADC) score = k6_adc_bounded<M>(Lb, c[u], (uint32_t)(thr >> 32));
+                    if constexpr (STRAT == ADC) score = k6_adc_bounded<M>(L, c[u], (uint32_t)(thr >> 32));
                     else if constexpr (STRAT == BINARY) score = (float)k6_ham(c[u], qc);
                     else score = (float)k6_dis(c[u], qc);
                     candidate(score, pos);
@@ -908,16 +869,6 @@ __global__ void __launch_bounds__(K6_WARPS * 32, M == 8 ? POLY_K6_MINB : 5) ivf_
         if (warp * 128u < n) load(warp * 128u);
         for (uint32_t r0 = warp * 128; r0 < n; r0 += 128 * K6_WARPS) block(r0);
         if (STRAT == DUAL && qn) drain(qn);
-#if POLY_K6_PREFETCH
-        if (itn < nitems) {
-            float4* dst = reinterpret_cast<float4*>(L + (b ^ 1) * M * KSUB);
-#pragma unroll
-            for (int v = 0; v < LV; ++v) dst[threadIdx.x + v * K6_WARPS * 32] = nx[v];
-        }
-        __syncthreads();  // buffer b ^ 1 complete; buffer b free after everyone's scan
-        b ^= 1;
-        it = itn;
-#endif
     }
     if (STRAT == DUAL && lane == 0 && surv_total) atomicAdd(a.surv_total, (unsigned long long)surv_total);
 }
@@ -925,7 +876,7 @@ __global__ void __launch_bounds__(K6_WARPS * 32, M == 8 ? POLY_K6_MINB : 5) ivf_
 template <int M, int STRAT>
 static void launch_ivf_one(const IvfScanArgs& a, unsigned grid, cudaStream_t s) {
     using C = typename IvfCode<M>::T;
-    const size_t smem = (POLY_K6_PREFETCH ? 2 : 1) * (size_t)M * KSUB * 4 + (size_t)K6_WARPS * 64 * (sizeof(C) + 4);
+    const size_t smem = (size_t)M * KSUB * 4 + (size_t)K6_WARPS * 64 * (sizeof(C) + 4);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(ivf_scan_kernel<M, STRAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
