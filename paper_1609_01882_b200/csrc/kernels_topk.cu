@@ -27,6 +27,10 @@ constexpr int TK_MAXPARTS = 64;
 constexpr uint32_t TK_DIRECT = POLY_TK_DIRECT;  // at most this many: sort them all
 constexpr uint32_t TK_SEL_KEYS = 4096;  // >= k + 1 (k <= 2048); with 2048 buckets: 104 KB, two CTAs per SM
 constexpr uint32_t TK_BUCKETS = 2048;
+#ifndef POLY_TK_RANK
+#define POLY_TK_RANK 128
+#endif
+constexpr uint32_t TK_RANK = POLY_TK_RANK;  // at most this many keys to order: rank by counting
 
 __device__ __forceinline__ void bitonic_sort(unsigned long long* s, uint32_t p) {
     for (uint32_t size = 2; size <= p; size <<= 1) {
@@ -67,8 +71,17 @@ __global__ void __launch_bounds__(TK_THREADS) topk_kernel(const unsigned long lo
         uint32_t base = 0;
         for (uint32_t p = 0; p < parts; ++p) {
             const unsigned long long* src = cand + p * part_stride + (size_t)q * cap;
-            for (uint32_t i = tid; i < pc[p]; i += TK_THREADS) sk[base + i] = __ldcg(src + i);
-            base += pc[p];
+            const uint32_t n = pc[p];
+            for (uint32_t i0 = tid; i0 < n; i0 += 4 * TK_THREADS) {  // 4 loads in flight
+                unsigned long long v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (i0 + u * TK_THREADS < n) v[u] = __ldcg(src + i0 + u * TK_THREADS);
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (i0 + u * TK_THREADS < n) sk[base + i0 + u * TK_THREADS] = v[u];
+            }
+            base += n;
         }
         __syncthreads();
     }
@@ -162,12 +175,28 @@ __global__ void __launch_bounds__(TK_THREADS) topk_kernel(const unsigned long lo
         srt = sel;
         n = fill_s;
     }
-    uint32_t P = 1;
-    while (P < n) P <<= 1;
-    for (uint32_t i = n + tid; i < P; i += TK_THREADS) srt[i] = KEY_INF;
     __syncthreads();
-    bitonic_sort(srt, P);
-    for (uint32_t r = tid; r < k; r += TK_THREADS) out[r] = r < kk ? srt[r] : KEY_INF;
+    if (n <= TK_RANK) {
+        // rank by counting (2 barriers instead of a bitonic network); ties by position,
+        // so the ranks are a permutation even for equal keys
+        for (uint32_t i = tid; i < n; i += TK_THREADS) {
+            const unsigned long long ki = srt[i];
+            uint32_t rank = 0;
+            for (uint32_t j = 0; j < n; ++j) {
+                const unsigned long long kj = srt[j];
+                rank += kj < ki || (kj == ki && j < i);
+            }
+            if (rank < kk) out[rank] = ki;
+        }
+        for (uint32_t r = kk + tid; r < k; r += TK_THREADS) out[r] = KEY_INF;
+    } else {
+        uint32_t P = 1;
+        while (P < n) P <<= 1;
+        for (uint32_t i = n + tid; i < P; i += TK_THREADS) srt[i] = KEY_INF;
+        __syncthreads();
+        bitonic_sort(srt, P);
+        for (uint32_t r = tid; r < k; r += TK_THREADS) out[r] = r < kk ? srt[r] : KEY_INF;
+    }
     if (tid == 0) out_counts[q] = kk;
 }
 
