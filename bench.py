@@ -38,7 +38,7 @@ METRIC = "DB codes scanned/sec (filter+ADC+top-k)"
 UNIT = "codes/s"
 SEED = 160901882
 BATCH = 256
-IVF_BATCH = 1024  # configs 2/4 (BASELINE.json names no batch size there): the library's IVF batch
+IVF_BATCH = 2048  # configs 2/4 (BASELINE.json names no batch size there): the library's IVF batch
 NQ = 10_000
 # BASELINE.json configs: 1 = flat 64-bit codes (headline), 3 = wide 128-bit codes
 CONFIGS = {

@@ -18,7 +18,7 @@
 using namespace pbh;
 
 #ifndef POLY_IVF_NQB
-#define POLY_IVF_NQB 1024
+#define POLY_IVF_NQB 2048
 #endif
 namespace {
 constexpr uint32_t IVF_NQB = POLY_IVF_NQB;  // queries per batch

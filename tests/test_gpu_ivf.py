@@ -372,7 +372,7 @@ def test_randomized_ivf_against_oracle(pb, gi, seed):
     coarse = oracle.gen_points(dseed, 1, int(rng.integers(0, 1000)), nlist, centers)
     base = oracle.gen_points(dseed, 2, int(rng.integers(0, 10_000)), n, centers) if n else np.zeros((0, 128), np.float32)
     ids = (rng.permutation(n).astype(np.int64) * 5 + 1) if seed % 2 else np.arange(n, dtype=np.int64)
-    nq = int(rng.choice([1, 17, 256, 300, 1100]))  # 1100: more than one 1024-query batch
+    nq = int(rng.choice([1, 17, 256, 300, 2100]))  # 2100: more than one 2048-query batch
     queries = oracle.gen_points(dseed, 3, int(rng.integers(0, 1000)), nq, centers)
     nprobe = int(min(nlist, rng.choice([1, 4, 16, 65, 100])))
     k = int(rng.choice([1, 10, 100]))
