@@ -115,7 +115,7 @@ constexpr uint64_t IVF_R1_CODES = POLY_IVF_R1_CODES;  // ... and at least this m
 #define POLY_K5R_SUB POLY_IVF_NQB
 #endif
 constexpr uint32_t K5R_SUB = POLY_K5R_SUB;  // queries per coarse GEMM + K5r launch pair
-constexpr uint32_t IVF_CHUNK = 1024;             // K6 round-1 work item: 1024 list rows (8 warps x 128)
+constexpr uint32_t IVF_CHUNK = 1024;             // K6 round-1 work item: 1024 list rows (K6 scans it in 128-row warp blocks)
 constexpr uint32_t IVF_CHUNK2 = POLY_IVF_CHUNK2;  // round 2: longer items (fewer LUT loads per code)
 
 __global__ void fill_u32(uint32_t* p, uint64_t n, uint32_t v) {
@@ -256,7 +256,7 @@ void validate(const poly_b200_ivf* iv, const poly_b200_ivf_params* p) {
 // np <= 64: fused distance + per-slice selection (K5s), slices merged by K3;
 // larger np: all keys (K5), then K3 over nlist keys per query.
 void enumerate_cells(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, uint32_t np, cudaStream_t s) {
-    if (POLY_COARSE_GEMM && np <= 1024) {
+    if (POLY_COARSE_GEMM && np <= pb::coarse_refine_npmax()) {
         // K5r: TF32 tensor-core dots (cuBLAS: a plain GEMM), then the exact re-rank kernel
         if (!iv->cublas) {
             require(cublasCreate(&iv->cublas) == CUBLAS_STATUS_SUCCESS, POLY_B200_INTERNAL, "cublasCreate failed");

@@ -236,8 +236,13 @@ void launch_coarse_select(const float* q, uint32_t nq, uint32_t dim, const float
 // are among a thread's kept ones, unless its third smallest is within the bound too
 // (then it revisits its cells); they go to a global scratch list and are
 // re-ranked in chunks of KR_CHUNK.
-constexpr int KR_THREADS = 512, KR_CHUNK = 2048, KR_NPMAX = 1024, KR_BUF = 4096;  // np + chunk <= buf (pow2)
-constexpr int KR_TVALS = 3 * KR_THREADS;  // per-thread three smallest
+#ifndef POLY_KR_THREADS
+#define POLY_KR_THREADS 512
+#endif
+constexpr int KR_THREADS = POLY_KR_THREADS, KR_CHUNK = 2048, KR_BUF = 4096;  // np + chunk <= buf (pow2)
+constexpr int KR_TVALS = 3 * KR_THREADS;                                   // per-thread three smallest
+constexpr int KR_NPMAX = KR_TVALS < 1024 ? KR_TVALS : 1024;
+uint32_t coarse_refine_npmax() { return KR_NPMAX; }
 constexpr int KR_UNROLL = 4;              // float4 loads in flight per thread
 constexpr uint32_t KR_RANKMAX = 1024;     // re-rank by counting up to this many keys (else bitonic)
 
@@ -249,7 +254,7 @@ __device__ __forceinline__ float kr_unord(uint32_t u) {
     return __uint_as_float((u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u);
 }
 
-__global__ void __launch_bounds__(KR_THREADS, 2) coarse_refine_kernel(const float* __restrict__ q, uint32_t dim,
+__global__ void __launch_bounds__(KR_THREADS, 1024 / KR_THREADS) coarse_refine_kernel(const float* __restrict__ q, uint32_t dim,
                                                                    const float* __restrict__ dots,
                                                                    const float* __restrict__ cnorm, float cmax,
                                                                    const float* __restrict__ cent, uint32_t nlist,
@@ -718,7 +723,10 @@ void launch_ivf_probe_count(const unsigned long long* probe_keys, uint32_t nq, u
 }
 
 // ------------------------------------------------------------------ K6
-constexpr int K6_WARPS = 8;
+#ifndef POLY_K6_WARPS
+#define POLY_K6_WARPS 4  // A/B at 2048 queries: 8 -> 4 warps per CTA (16 CTAs per SM) +5% / +8% (nprobe 16 / 64), cfg4 +9%
+#endif
+constexpr int K6_WARPS = POLY_K6_WARPS;
 
 template <int M> struct IvfCode;
 template <> struct IvfCode<8> { using T = uint2; };
@@ -759,14 +767,14 @@ __device__ __forceinline__ float k6_adc_bounded(const float* L, const C& c, uint
 }
 
 // Work items (query, probe, chunk of the probed cell's list) are fetched
-// dynamically; the 8 warps of a CTA split the chunk and share the item's LUT
+// dynamically; the K6_WARPS warps of a CTA split the chunk and share the item's LUT
 // in shared memory.  Each warp compacts its filter survivors with a ballot into
 // its own queue and drains 32 at a time (ADC with early exit, candidate test).
 template <int M, int STRAT>
 #ifndef POLY_K6_MINB
 #define POLY_K6_MINB 8  // m = 8: 8 CTAs (64 warps) per SM, <= 32 registers (m = 16: 5 CTAs)
 #endif
-__global__ void __launch_bounds__(K6_WARPS * 32, M == 8 ? POLY_K6_MINB : 5) ivf_scan_kernel(const IvfScanArgs a) {
+__global__ void __launch_bounds__(K6_WARPS * 32, (M == 8 ? POLY_K6_MINB : 5) * (8 / K6_WARPS)) ivf_scan_kernel(const IvfScanArgs a) {
     using C = typename IvfCode<M>::T;
     extern __shared__ __align__(16) uint8_t k6_smem[];
     float* L = reinterpret_cast<float*>(k6_smem);  // M x 256 floats
@@ -887,7 +895,7 @@ static void launch_ivf_one(const IvfScanArgs& a, unsigned grid, cudaStream_t s) 
 
 template <int M>
 static void launch_ivf_m(const IvfScanArgs& a, int strategy, int num_sms, cudaStream_t s) {
-    const unsigned grid = (unsigned)num_sms * (M == 8 ? 8 : 5);  // ~14 KB (m=8) / ~26 KB (m=16) smem per CTA
+    const unsigned grid = (unsigned)num_sms * (M == 8 ? 8 : 5) * (8 / K6_WARPS);  // ~14 KB (m=8) / ~26 KB (m=16) smem per 8-warp CTA
     switch (strategy) {
         case DUAL: launch_ivf_one<M, DUAL>(a, grid, s); break;
         case ADC: launch_ivf_one<M, ADC>(a, grid, s); break;

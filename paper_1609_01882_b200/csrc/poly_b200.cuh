@@ -306,7 +306,8 @@ void launch_seed_compact(const unsigned long long* keys, const uint32_t* counts,
 // IVF (kernels_ivf.cu)
 void launch_coarse_keys(const float* q, uint32_t nq, uint32_t dim, const float* cent, uint32_t nlist,
                         unsigned long long* keys, cudaStream_t s);
-// K5r: exact enumerate_cells from TF32 dots (dots[q * nlist + c] ~ q.c) + exact re-rank; np <= 1024
+// K5r: exact enumerate_cells from TF32 dots (dots[q * nlist + c] ~ q.c) + exact re-rank; np <= coarse_refine_npmax()
+uint32_t coarse_refine_npmax();
 void launch_coarse_refine(const float* q, uint32_t nq, uint32_t dim, const float* dots, const float* cnorm, float cmax,
                           const float* cent, uint32_t nlist, uint32_t np, uint32_t* scratch,
                           unsigned long long* probe_keys, uint32_t* probe_counts, cudaStream_t s);
