@@ -505,7 +505,10 @@ __device__ __forceinline__ unsigned long long k1_pack(float lo, float hi) {
 // time (thread t: sq 2s + (t >> 6), pairs (u, u + 128) and (u + 64, u + 192), u = t & 63),
 // so each shared-memory load of a residual pair feeds 12 packed FP ops instead of 6
 // (the pair kernel's shared-memory pipe was 93% busy).
-__global__ void __launch_bounds__(128, 4) residual_lut_quad_kernel(const float* __restrict__ queries, uint32_t dim,
+#ifndef POLY_K1R_MINB
+#define POLY_K1R_MINB 4
+#endif
+__global__ void __launch_bounds__(128, POLY_K1R_MINB) residual_lut_quad_kernel(const float* __restrict__ queries, uint32_t dim,
                                                                    uint32_t m,
                                                                    const unsigned long long* __restrict__ probe_keys,
                                                                    uint32_t nprobe, uint32_t p_lo, uint32_t span,
