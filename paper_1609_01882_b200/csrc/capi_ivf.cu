@@ -115,7 +115,10 @@ constexpr uint64_t IVF_R1_CODES = POLY_IVF_R1_CODES;  // ... and at least this m
 #define POLY_K5R_SUB POLY_IVF_NQB
 #endif
 constexpr uint32_t K5R_SUB = POLY_K5R_SUB;  // queries per coarse GEMM + K5r launch pair
-constexpr uint32_t IVF_CHUNK = 1024;             // K6 round-1 work item: 1024 list rows (K6 scans it in 128-row warp blocks)
+#ifndef POLY_IVF_CHUNK
+#define POLY_IVF_CHUNK 1024
+#endif
+constexpr uint32_t IVF_CHUNK = POLY_IVF_CHUNK;    // K6 round-1 work item: 1024 list rows (K6 scans it in 128-row warp blocks)
 constexpr uint32_t IVF_CHUNK2 = POLY_IVF_CHUNK2;  // round 2: longer items (fewer LUT loads per code)
 
 __global__ void fill_u32(uint32_t* p, uint64_t n, uint32_t v) {

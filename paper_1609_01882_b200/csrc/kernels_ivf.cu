@@ -775,7 +775,7 @@ __device__ __forceinline__ float k6_adc_bounded(const float* L, const C& c, uint
 // its own queue and drains 32 at a time (ADC with early exit, candidate test).
 template <int M, int STRAT>
 #ifndef POLY_K6_MINB
-#define POLY_K6_MINB 8  // m = 8: 8 CTAs (64 warps) per SM, <= 32 registers (m = 16: 5 CTAs)
+#define POLY_K6_MINB 8  // m = 8: 64 warps per SM, <= 32 registers (m = 16: 40 warps)
 #endif
 __global__ void __launch_bounds__(K6_WARPS * 32, (M == 8 ? POLY_K6_MINB : 5) * (8 / K6_WARPS)) ivf_scan_kernel(const IvfScanArgs a) {
     using C = typename IvfCode<M>::T;
