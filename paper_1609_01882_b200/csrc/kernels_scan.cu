@@ -791,24 +791,35 @@ __global__ void __launch_bounds__(SEED_THREADS) seed_sample_kernel(const ScanArg
     const C qc = reinterpret_cast<const C*>(a.qcodes)[q];
     if (threadIdx.x == 0) cnt = 0;
     __syncthreads();
-    for (uint32_t b = 0; b < seed_blocks; ++b) {
-        const uint64_t pos = (uint64_t)b * a.n / seed_blocks + threadIdx.x;
-        if (pos >= a.n) continue;
-        const C code = __ldg(reinterpret_cast<const C*>(a.codes) + pos);
-        float score;
-        if constexpr (STRAT == DUAL) {
-            if (ham(code, qc) > a.tau) continue;
-            score = adc<M>(lut, code);
-        } else if constexpr (STRAT == ADC) {
-            score = adc<M>(lut, code);
-        } else if constexpr (STRAT == BINARY) {
-            score = (float)ham(code, qc);
-        } else {
-            score = (float)disidx(code, qc);
+    constexpr uint32_t SU = 8;  // runs per step: their loads are in flight together
+    for (uint32_t b0 = 0; b0 < seed_blocks; b0 += SU) {
+        C codes_u[SU];
+        uint64_t pos_u[SU];
+#pragma unroll
+        for (uint32_t u = 0; u < SU; ++u) {
+            pos_u[u] = b0 + u < seed_blocks ? (uint64_t)(b0 + u) * a.n / seed_blocks + threadIdx.x : a.n;
+            if (pos_u[u] < a.n) codes_u[u] = __ldg(reinterpret_cast<const C*>(a.codes) + pos_u[u]);
         }
-        const uint32_t slot = atomicAdd(&cnt, 1u);
-        if (slot < SEED_KEYS)
-            keys[slot] = ((unsigned long long)__float_as_uint(score) << 32) | key_low(a, (uint32_t)pos);
+#pragma unroll
+        for (uint32_t u = 0; u < SU; ++u) {
+            const uint64_t pos = pos_u[u];
+            if (pos >= a.n) continue;
+            const C code = codes_u[u];
+            float score;
+            if constexpr (STRAT == DUAL) {
+                if (ham(code, qc) > a.tau) continue;
+                score = adc<M>(lut, code);
+            } else if constexpr (STRAT == ADC) {
+                score = adc<M>(lut, code);
+            } else if constexpr (STRAT == BINARY) {
+                score = (float)ham(code, qc);
+            } else {
+                score = (float)disidx(code, qc);
+            }
+            const uint32_t slot = atomicAdd(&cnt, 1u);
+            if (slot < SEED_KEYS)
+                keys[slot] = ((unsigned long long)__float_as_uint(score) << 32) | key_low(a, (uint32_t)pos);
+        }
     }
     __syncthreads();
     const uint32_t n = min(cnt, SEED_KEYS);
