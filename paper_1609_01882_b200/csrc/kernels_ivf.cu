@@ -769,6 +769,27 @@ __device__ __forceinline__ float k6_adc_bounded(const float* L, const C& c, uint
     return acc;
 }
 
+// Survivor-queue accesses through 32-bit shared-window addresses (the generic
+// pointers made ptxas rebuild the window base per access at the 32-register cap).
+__device__ __forceinline__ void k6_sts(uint32_t a, const uint2& c) {
+    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(c.x), "r"(c.y) : "memory");
+}
+__device__ __forceinline__ void k6_sts(uint32_t a, const uint4& c) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(c.x), "r"(c.y), "r"(c.z), "r"(c.w) : "memory");
+}
+__device__ __forceinline__ void k6_sts(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void k6_lds(uint32_t a, uint2& c) {
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(c.x), "=r"(c.y) : "r"(a) : "memory");
+}
+__device__ __forceinline__ void k6_lds(uint32_t a, uint4& c) {
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(c.x), "=r"(c.y), "=r"(c.z), "=r"(c.w) : "r"(a) : "memory");
+}
+__device__ __forceinline__ void k6_lds(uint32_t a, uint32_t& v) {
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+}
+
 // Work items (query, probe, chunk of the probed cell's list) are fetched
 // dynamically; the K6_WARPS warps of a CTA split the chunk and share the item's LUT
 // in shared memory.  Each warp compacts its filter survivors with a ballot into
@@ -782,9 +803,10 @@ __global__ void __launch_bounds__(K6_WARPS * 32, (M == 8 ? POLY_K6_MINB : 5) * (
     extern __shared__ __align__(16) uint8_t k6_smem[];
     float* L = reinterpret_cast<float*>(k6_smem);  // M x 256 floats
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint8_t* qbase = k6_smem + (size_t)M * KSUB * 4 + warp * 64 * (sizeof(C) + 4);
-    C* qcode_q = reinterpret_cast<C*>(qbase);
-    uint32_t* qpos_q = reinterpret_cast<uint32_t*>(qbase + 64 * sizeof(C));
+    // this warp's survivor queue: 64 codes, then 64 positions (shared-window addresses)
+    const uint32_t qcs = smem_u32(k6_smem + (size_t)M * KSUB * 4 + warp * 64 * (sizeof(C) + 4));
+    const uint32_t qps = qcs + 64 * sizeof(C);
+    const uint32_t lt = (1u << lane) - 1u, tau = a.tau;
     const uint32_t nitems = min(*a.nitems, a.items_cap);
     uint32_t surv_total = 0;
     __shared__ uint32_t item_s;
@@ -818,52 +840,52 @@ __global__ void __launch_bounds__(K6_WARPS * 32, (M == 8 ? POLY_K6_MINB : 5) * (
         };
         auto drain = [&](uint32_t cnt) {
             __syncwarp();
-            if ((uint32_t)lane < cnt) candidate(k6_adc_bounded<M>(L, qcode_q[lane], (uint32_t)(thr >> 32)), qpos_q[lane]);
+            if ((uint32_t)lane < cnt) {
+                C cc;
+                uint32_t pp;
+                k6_lds(qcs + lane * (uint32_t)sizeof(C), cc);
+                k6_lds(qps + 4u * lane, pp);
+                candidate(k6_adc_bounded<M>(L, cc, (uint32_t)(thr >> 32)), pp);
+            }
             __syncwarp();
         };
         // warp w scans rows 128*w + ..., stride 128 * K6_WARPS, of the item's rows
         // [beg, end) (32-bit offsets)
         const C* ci = reinterpret_cast<const C*>(a.codes) + beg;
         const uint32_t n = (uint32_t)(end - beg), pos0 = (uint32_t)beg;
-        // software-pipelined: the warp's next 128-row block is loaded while this one is
-        // filtered and drained
-        C cn[4];
-        auto load = [&](uint32_t r0) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t r = r0 + u * 32 + lane;
-                if (r < n) cn[u] = __ldcs(ci + r);  // streamed once: evict-first
-            }
-        };
         auto block = [&](uint32_t r0) {
             C c[4];
             bool in[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                c[u] = cn[u];
-                in[u] = r0 + u * 32 + lane < n;
+                const uint32_t r = r0 + u * 32 + lane;
+                in[u] = r < n;
+                if (in[u]) c[u] = __ldcs(ci + r);  // streamed once: evict-first
             }
-            if (r0 + 128 * K6_WARPS < n) load(r0 + 128 * K6_WARPS);
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const uint32_t pos = pos0 + r0 + u * 32 + lane;
                 if constexpr (STRAT == DUAL) {
-                    const bool pass = in[u] && k6_ham(c[u], qc) <= a.tau;
+                    const bool pass = in[u] && k6_ham(c[u], qc) <= tau;
                     const uint32_t bal = __ballot_sync(0xffffffffu, pass);
                     if (bal) {
                         if (pass) {
-                            const uint32_t at = qn + __popc(bal & ((1u << lane) - 1u));
-                            qcode_q[at] = c[u];
-                            qpos_q[at] = pos;
+                            const uint32_t at = qn + __popc(bal & lt);
+                            k6_sts(qcs + at * (uint32_t)sizeof(C), c[u]);
+                            k6_sts(qps + 4u * at, pos);
                         }
                         qn += __popc(bal);
                         surv_total += __popc(bal);
                         if (qn >= 32) {
                             drain(32);
                             qn -= 32;
-                            if ((uint32_t)lane < qn) {
-                                qcode_q[lane] = qcode_q[32 + lane];
-                                qpos_q[lane] = qpos_q[32 + lane];
+                            if ((uint32_t)lane < qn) {  // carry the overflow to the queue head
+                                C cc;
+                                uint32_t pp;
+                                k6_lds(qcs + (32u + lane) * (uint32_t)sizeof(C), cc);
+                                k6_lds(qps + 4u * (32u + lane), pp);
+                                k6_sts(qcs + lane * (uint32_t)sizeof(C), cc);
+                                k6_sts(qps + 4u * lane, pp);
                             }
                             __syncwarp();
                         }
@@ -877,7 +899,6 @@ __global__ void __launch_bounds__(K6_WARPS * 32, (M == 8 ? POLY_K6_MINB : 5) * (
                 }
             }
         };
-        if (warp * 128u < n) load(warp * 128u);
         for (uint32_t r0 = warp * 128; r0 < n; r0 += 128 * K6_WARPS) block(r0);
         if (STRAT == DUAL && qn) drain(qn);
     }
