@@ -250,7 +250,7 @@ def run_ivf(args, rank, world, local):
         # every cell's list holds this rank's id range; per-rank top-k
         # keys are all-gathered over NCCL and merged exactly (IVFIndexEngine + ShardedSearch)
         from paper_1609_01882_b200.distributed import IVFIndexEngine, ShardedSearch
-        engine = IVFIndexEngine(ivf, stream)
+        engine = IVFIndexEngine(ivf, stream, split_coarse=True)  # coarse quantization split by query
         sharded = ShardedSearch(engine)
 
     def step(i, p, st=None):
@@ -302,7 +302,7 @@ def run_ivf(args, rank, world, local):
                                    f"per-GPU share of 1e9 over 8 at N=1), PQ m={M} on residuals, nq={NQ} in batches of "
                                    f"{B}, nprobe={c['nprobe']}, k={k}, ht={args.ht}",
                        "nlist": c["nlist"], "n_codes": args.n, "m": M, "nprobe": c["nprobe"], "k": k, "ht": args.ht,
-                       "parallelism": f"db-shard{world} (ids within every list) + NCCL key all-gather",
+                       "parallelism": f"db-shard{world} (ids within every list) + query-split coarse quantization + NCCL probe / key all-gathers",
                        "coarse": "training-stream rows [0, nlist) (sampled coarse quantizer; DESIGN.md)",
                        "build_assignment": "TF32 GEMM argmin (setup only)"},
             "gpu_launches": head["gpu_launches"], "per_nprobe": {str(kk): v for kk, v in results.items()},

@@ -227,6 +227,20 @@ int poly_b200_ivf_search_keys_device(poly_b200_ivf* ivf, const float* d_queries,
 int poly_b200_ivf_merge_keys_device(poly_b200_ivf* ivf, const uint64_t* d_keys, const uint32_t* d_counts,
                                     uint32_t parts, uint64_t nq, uint32_t k, int64_t* d_ids, float* d_scores,
                                     uint32_t* d_out_counts, void* stream);
+/* The coarse quantization split by query over the ranks (the replicated part of the
+ * sharding above): a rank computes the probes of its query slice with
+ * poly_b200_ivf_probe_keys_device -- nq x min(nprobe, nlist) keys (dist bits << 32 |
+ * cell), ascending per query, exactly enumerate_cells -- the ranks
+ * all-gather them, and each rank scans its shard with the given probes through
+ * poly_b200_ivf_search_keys_probes_device (same outputs as
+ * poly_b200_ivf_search_keys_device; d_probe_keys holds nq x min(params->nprobe, nlist)
+ * keys). */
+int poly_b200_ivf_probe_keys_device(poly_b200_ivf* ivf, const float* d_queries, uint64_t nq, uint32_t nprobe,
+                                    uint64_t* d_probe_keys, void* stream);
+int poly_b200_ivf_search_keys_probes_device(poly_b200_ivf* ivf, const float* d_queries, uint64_t nq,
+                                            const poly_b200_ivf_params* params, const uint64_t* d_probe_keys,
+                                            uint64_t* d_keys, uint32_t* d_counts, void* stream,
+                                            poly_b200_search_stats* stats);
 
 /* knn_graph: the k nearest neighbours of n vectors that are
  * themselves in the index (vector i has id id0 + i), self-match removed:

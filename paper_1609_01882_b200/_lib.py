@@ -79,6 +79,9 @@ def _load():
     L.poly_b200_ivf_search_keys_device.argtypes = [_P, _P, _u64, C.POINTER(IvfParamsC), _P, _P, _P,
                                                    C.POINTER(SearchStatsC)]
     L.poly_b200_ivf_merge_keys_device.argtypes = [_P, _P, _P, _u32, _u64, _u32, _P, _P, _P, _P]
+    L.poly_b200_ivf_probe_keys_device.argtypes = [_P, _P, _u64, _u32, _P, _P]
+    L.poly_b200_ivf_search_keys_probes_device.argtypes = [_P, _P, _u64, C.POINTER(IvfParamsC), _P, _P, _P, _P,
+                                                          C.POINTER(SearchStatsC)]
     return L
 
 
@@ -94,5 +97,6 @@ EXPORTS = [
     "poly_b200_launch_count", "poly_b200_ivf_create", "poly_b200_ivf_destroy", "poly_b200_ivf_size",
     "poly_b200_ivf_assign", "poly_b200_ivf_add", "poly_b200_ivf_add_device", "poly_b200_ivf_add_codes",
     "poly_b200_ivf_get_lists", "poly_b200_ivf_probes", "poly_b200_ivf_search", "poly_b200_ivf_search_device", "poly_b200_ivf_knn_graph_device",
-    "poly_b200_ivf_search_keys_device", "poly_b200_ivf_merge_keys_device",
+    "poly_b200_ivf_search_keys_device", "poly_b200_ivf_merge_keys_device", "poly_b200_ivf_probe_keys_device",
+    "poly_b200_ivf_search_keys_probes_device",
 ]

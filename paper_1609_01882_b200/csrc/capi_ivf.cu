@@ -303,14 +303,17 @@ void enumerate_cells(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, uint32_t
 // One batch of <= 256 queries; outputs through keys_to_ids.
 void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_b200_ivf_params* p, int64_t* d_ids,
                   float* d_scores, uint32_t* d_counts, cudaStream_t s, uint64_t* d_keys_out = nullptr,
-                  uint32_t* d_kcounts_out = nullptr) {
+                  uint32_t* d_kcounts_out = nullptr, const uint64_t* d_probes_in = nullptr) {
     const uint32_t k = p->k;
     const uint32_t np = std::min(p->nprobe, iv->nlist);
     int strategy = p->strategy;
     if (strategy == pb::DUAL && p->tau >= iv->code_bits()) strategy = pb::ADC;  // SPEC.md:388 boundary
     CK(cudaMemsetAsync(iv->ctrl, 0, (IVF_NQB + 32) * 4, s));
     CK(cudaMemsetAsync(iv->thr, 0xFF, IVF_NQB * 8, s));
-    enumerate_cells(iv, d_q, nqb, np, s);
+    if (d_probes_in)  // probes computed elsewhere (the coarse quantization split by query over ranks)
+        CK(cudaMemcpyAsync(iv->probe_keys, d_probes_in, (size_t)nqb * np * 8, cudaMemcpyDeviceToDevice, s));
+    else
+        enumerate_cells(iv, d_q, nqb, np, s);
     pb::IvfWork w{};
     w.items[0] = iv->items[0];
     w.items[1] = iv->items[1];
@@ -381,7 +384,7 @@ void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_
 // All batches; returns strategy survivors semantics (0 none, 1 = scanned, 2 counted).
 int device_search(poly_b200_ivf* iv, const float* d_q, uint64_t nq, const poly_b200_ivf_params* p, int64_t* d_ids,
                   float* d_scores, uint32_t* d_counts, cudaStream_t s, uint64_t* d_keys = nullptr,
-                  uint32_t* d_kcounts = nullptr) {
+                  uint32_t* d_kcounts = nullptr, const uint64_t* d_probes = nullptr) {
     validate(iv, p);
     if (nq == 0) return 0;
     if (p->k == 0 || iv->n == 0) {
@@ -401,12 +404,13 @@ int device_search(poly_b200_ivf* iv, const float* d_q, uint64_t nq, const poly_b
     CK(cudaMemsetAsync(iv->sticky_overflow, 0, 4, s));
     for (uint64_t b0 = 0; b0 < nq; b0 += IVF_NQB) {
         const uint32_t nqb = (uint32_t)std::min<uint64_t>(IVF_NQB, nq - b0);
+        const uint64_t* pr = d_probes ? d_probes + b0 * std::min(p->nprobe, iv->nlist) : nullptr;
         if (d_keys)
             search_batch(iv, d_q + b0 * iv->dim, nqb, p, nullptr, nullptr, nullptr, s, d_keys + b0 * p->k,
-                         d_kcounts + b0);
+                         d_kcounts + b0, pr);
         else
             search_batch(iv, d_q + b0 * iv->dim, nqb, p, d_ids + b0 * p->k, d_scores + b0 * p->k,
-                         d_counts ? d_counts + b0 : nullptr, s);
+                         d_counts ? d_counts + b0 : nullptr, s, nullptr, nullptr, pr);
         CK(cudaGetLastError());
     }
     if (p->strategy == pb::DUAL) return p->tau >= iv->code_bits() ? 1 : 2;
@@ -719,6 +723,51 @@ int poly_b200_ivf_search_keys_device(poly_b200_ivf* iv, const float* d_q, uint64
         if (stats) {
             stats->scanned = stats->survivors = 0;
             if (nq && iv->n) read_stats(iv, mode, stats, s);
+        }
+    });
+}
+
+int poly_b200_ivf_search_keys_probes_device(poly_b200_ivf* iv, const float* d_q, uint64_t nq,
+                                            const poly_b200_ivf_params* p, const uint64_t* d_probe_keys,
+                                            uint64_t* d_keys, uint32_t* d_counts, void* stream,
+                                            poly_b200_search_stats* stats) {
+    return guard([&] {
+        require(iv != nullptr && p != nullptr, POLY_B200_INVALID_ARGUMENT, "null arguments");
+        require(p->k > 0, POLY_B200_INVALID_ARGUMENT, "k must be positive for key output");
+        require(nq == 0 || (d_q && d_keys && d_counts && d_probe_keys), POLY_B200_INVALID_ARGUMENT, "null buffers");
+        std::lock_guard<std::mutex> lk(iv->mu);
+        DeviceGuard dg(iv->device);
+        cudaStream_t s = (cudaStream_t)stream;
+        iv->idm.sync(iv->n);
+        require(iv->n == 0 || iv->idm.mode == pb::ID_ARITH, POLY_B200_STATE,
+                "key output needs consecutive ids below 2^32 (the key carries the id itself)");
+        const int mode = device_search(iv, d_q, nq, p, nullptr, nullptr, nullptr, s, d_keys, d_counts, d_probe_keys);
+        if (stats) {
+            stats->scanned = stats->survivors = 0;
+            if (nq && iv->n) read_stats(iv, mode, stats, s);
+        }
+    });
+}
+
+int poly_b200_ivf_probe_keys_device(poly_b200_ivf* iv, const float* d_q, uint64_t nq, uint32_t nprobe,
+                                    uint64_t* d_probe_keys, void* stream) {
+    return guard([&] {
+        require(iv != nullptr, POLY_B200_INVALID_ARGUMENT, "null index");
+        require(nprobe >= 1, POLY_B200_INVALID_ARGUMENT, "nprobe must be >= 1");
+        require(nq == 0 || (d_q && d_probe_keys), POLY_B200_INVALID_ARGUMENT, "null buffers");
+        std::lock_guard<std::mutex> lk(iv->mu);
+        DeviceGuard dg(iv->device);
+        cudaStream_t s = (cudaStream_t)stream;
+        const uint32_t np = std::min(nprobe, iv->nlist);
+        if (nq == 0) return;
+        rebuild_lists(iv);
+        ensure_ivf_scratch(iv, np, 1);
+        for (uint64_t b0 = 0; b0 < nq; b0 += IVF_NQB) {
+            const uint32_t nqb = (uint32_t)std::min<uint64_t>(IVF_NQB, nq - b0);
+            enumerate_cells(iv, d_q + b0 * iv->dim, nqb, np, s);
+            CK(cudaMemcpyAsync(d_probe_keys + b0 * np, iv->probe_keys, (size_t)nqb * np * 8, cudaMemcpyDeviceToDevice,
+                               s));
+            CK(cudaGetLastError());
         }
     });
 }

@@ -41,17 +41,57 @@ class FlatIndexEngine:
         self.index.merge_keys_device(keys_all, counts_all, parts, nq, k, ids, scores, counts, stream=self._sptr())
 
 
+def gather_query_slices(compute, queries, group=None):
+    """Split the rows of ``queries`` over the ranks (``shard_range``), run
+    ``compute(rows) -> tensor [len(rows), ...]`` on this rank's slice and all-gather
+    the slices back into one [nq, ...] tensor, in query order, on every rank.  Slices
+    are padded to the ceil size for the equal-size all-gather."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    nq = queries.shape[0]
+    if world == 1:
+        return compute(queries)
+    per = (nq + world - 1) // world
+    b, e = shard_range(nq, world, rank)
+    part = compute(queries[b:e]) if e > b else None
+    shape = (per,) + tuple(part.shape[1:] if part is not None else compute(queries[:1]).shape[1:])
+    buf = torch.zeros(shape, dtype=part.dtype if part is not None else torch.int64, device=queries.device)
+    if part is not None:
+        buf[:e - b] = part
+    out = torch.empty((world * per,) + shape[1:], dtype=buf.dtype, device=queries.device)
+    dist.all_gather_into_tensor(out, buf, group=group)
+    return out[:nq]
+
+
 class IVFIndexEngine(FlatIndexEngine):
     """GPU engine over one rank's IVF shard: every cell's list restricted to the rank's
-    id range (shard by id within every list), coarse quantizer
-    replicated, so all ranks probe the same cells and the key merge is exact."""
+    id range (shard by id within every list), so all ranks probe the
+    same cells and the key merge is exact.  With ``split_coarse`` the coarse
+    quantization (TF32 GEMM + exact re-rank) is split by query: each rank enumerates
+    the probes of its query slice and the probe keys are all-gathered, instead of
+    every rank enumerating every query."""
 
-    def __init__(self, index, stream=None, stats=None):
+    def __init__(self, index, stream=None, stats=None, split_coarse=False, group=None):
         super().__init__(index, stream)
         self.stats = stats
+        self.split_coarse = split_coarse
+        self.group = group
+
+    def probe_keys(self, queries, nprobe):
+        npr = min(int(nprobe), self.index.nlist)
+
+        def compute(rows):
+            out = torch.empty((rows.shape[0], npr), dtype=torch.int64, device=rows.device)
+            if rows.shape[0]:
+                self.index.probe_keys_device(rows, npr, out, stream=self._sptr())
+            return out
+
+        return gather_query_slices(compute, queries, self.group)
 
     def search_keys(self, queries, params, keys, counts):
-        self.index.search_keys_device(queries, params, keys, counts, stream=self._sptr(), stats=self.stats)
+        probes = self.probe_keys(queries, params.nprobe) if self.split_coarse else None
+        self.index.search_keys_device(queries, params, keys, counts, stream=self._sptr(), stats=self.stats,
+                                      probes=probes)
 
 
 class ShardedSearch:

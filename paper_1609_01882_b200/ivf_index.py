@@ -119,15 +119,28 @@ class IVFIndex:
             stats.survivors += st.survivors
 
     def search_keys_device(self, d_queries, params: CoarseParams, d_keys, d_counts, stream=0,
-                           stats: SearchStats | None = None):
-        """Multi-GPU: this shard's top-k as int64 keys (score bits << 32 | global id)."""
+                           stats: SearchStats | None = None, probes=None):
+        """Multi-GPU: this shard's top-k as int64 keys (score bits << 32 | global id).
+        probes: optional nq x min(nprobe, nlist) int64 probe keys (probe_keys_device),
+        e.g. all-gathered from the ranks that each enumerated a query slice."""
         st = SearchStatsC()
-        _check(lib.poly_b200_ivf_search_keys_device(self._h, d_queries.data_ptr(), d_queries.shape[0],
-                                                    C.byref(params.c()), d_keys.data_ptr(), d_counts.data_ptr(),
-                                                    C.c_void_p(stream), C.byref(st) if stats is not None else None))
+        stp = C.byref(st) if stats is not None else None
+        if probes is None:
+            _check(lib.poly_b200_ivf_search_keys_device(self._h, d_queries.data_ptr(), d_queries.shape[0],
+                                                        C.byref(params.c()), d_keys.data_ptr(), d_counts.data_ptr(),
+                                                        C.c_void_p(stream), stp))
+        else:
+            _check(lib.poly_b200_ivf_search_keys_probes_device(
+                self._h, d_queries.data_ptr(), d_queries.shape[0], C.byref(params.c()), probes.data_ptr(),
+                d_keys.data_ptr(), d_counts.data_ptr(), C.c_void_p(stream), stp))
         if stats is not None:
             stats.scanned += st.scanned
             stats.survivors += st.survivors
+
+    def probe_keys_device(self, d_queries, nprobe, d_out, stream=0):
+        """enumerate_cells on the GPU: nq x min(nprobe, nlist) int64 keys (dist bits << 32 | cell)."""
+        _check(lib.poly_b200_ivf_probe_keys_device(self._h, d_queries.data_ptr(), d_queries.shape[0], int(nprobe),
+                                                   d_out.data_ptr(), C.c_void_p(stream)))
 
     def merge_keys_device(self, d_keys, d_counts, parts, nq, k, d_ids, d_scores, d_counts_out=None, stream=0):
         """Exact merge of parts x nq x k keys (all ranks' search_keys_device output)."""

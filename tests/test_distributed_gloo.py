@@ -154,3 +154,36 @@ def test_sharded_ivf_equals_unsharded(tmp_path):
     assert np.array_equal(r["ids"], oi)
     assert np.array_equal(r["scores"].view(np.uint32), osc.view(np.uint32))
     assert np.array_equal(r["counts"], oc.astype(np.int32))
+
+
+def _gather_worker(rank, world, port, result_path):
+    import torch
+    import torch.distributed as dist
+    from paper_1609_01882_b200.distributed import gather_query_slices
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        q = torch.arange(7 * 3, dtype=torch.float32).reshape(7, 3)
+        seen = []
+
+        def compute(rows):  # order-sensitive: row sums as int64 probe-like keys, 2 columns
+            seen.append(rows.shape[0])
+            s = rows.sum(1).to(torch.int64)
+            return torch.stack([s, s * 10], 1)
+
+        out = gather_query_slices(compute, q)
+        want = torch.stack([q.sum(1).to(torch.int64), q.sum(1).to(torch.int64) * 10], 1)
+        if rank == 0:
+            torch.save({"ok": bool(torch.equal(out, want)), "rows": seen}, result_path)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gather_query_slices(tmp_path):
+    """The query-split coarse quantization's gather: each rank computes its slice of
+    the queries (shard_range), the all-gather returns every row in query order."""
+    import torch
+    import torch.multiprocessing as mp
+    out = str(tmp_path / "gather.pt")
+    mp.spawn(_gather_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    r = torch.load(out)
+    assert r["ok"] and r["rows"] == [4]

@@ -238,12 +238,30 @@ def test_sharded_ivf_merge_matches_unsharded(pb, gi):
         dist.init_process_group("nccl", rank=0, world_size=1)
     try:
         p = pb.CoarseParams(pb.Strategy.dual, k, 26, 8, 0)
-        ids, sc, cnt = ShardedSearch(IVFIndexEngine(full)).search_batch(dq, p)
-        torch.cuda.synchronize()
         want_ids, _, _ = full.search(queries, p)
-        assert np.array_equal(ids.cpu().numpy(), want_ids)
+        for split in (False, True):  # split: coarse quantization by query slice + all-gather of probes
+            ids, sc, cnt = ShardedSearch(IVFIndexEngine(full, split_coarse=split)).search_batch(dq, p)
+            torch.cuda.synchronize()
+            assert np.array_equal(ids.cpu().numpy(), want_ids), split
     finally:
         dist.destroy_process_group()
+    # probes enumerated in query slices (as two ranks would) and passed in == enumerated inside
+    p = pb.CoarseParams(pb.Strategy.dual, k, 26, 8, 0)
+    pr = torch.empty((300, 8), dtype=torch.int64, device="cuda")
+    shards[1].probe_keys_device(dq[:170], 8, pr[:170])
+    shards[1].probe_keys_device(dq[170:], 8, pr[170:])
+    ref = torch.empty((300, 8), dtype=torch.int64, device="cuda")
+    shards[1].probe_keys_device(dq, 8, ref)
+    torch.cuda.synchronize()
+    assert torch.equal(pr, ref)
+    assert np.array_equal((ref.cpu().numpy() & 0xFFFFFFFF).astype(np.uint32), full.probes(queries, 8))
+    for r, ix in enumerate(shards):
+        k_in = torch.empty((300, k), dtype=torch.int64, device="cuda")
+        c_in = torch.empty(300, dtype=torch.int32, device="cuda")
+        ix.search_keys_device(dq, p, keys[r], cnts[r])
+        ix.search_keys_device(dq, p, k_in, c_in, probes=pr)
+        torch.cuda.synchronize()
+        assert torch.equal(k_in, keys[r]) and torch.equal(c_in, cnts[r]), r
     # non-consecutive ids cannot be carried in a key
     odd = mk()
     odd.add(base[:1000], ids=np.arange(1000) * 3)
