@@ -19,13 +19,11 @@
 namespace pb {
 
 constexpr int TK_THREADS = 512;
-constexpr uint32_t TK_SMEM_KEYS = 8192;
 constexpr int TK_MAXPARTS = 64;
 #ifndef POLY_TK_DIRECT
 #define POLY_TK_DIRECT 512  // IVF A/B: 2048 -> 512 cut the K3 rounds ~6% (flat path: no effect)
 #endif
 constexpr uint32_t TK_DIRECT = POLY_TK_DIRECT;  // at most this many: sort them all
-constexpr uint32_t TK_SEL_KEYS = 4096;  // >= k + 1 (k <= 2048); with 2048 buckets: 104 KB, two CTAs per SM
 constexpr uint32_t TK_BUCKETS = 2048;
 #ifndef POLY_TK_RANK
 #define POLY_TK_RANK 128
@@ -46,6 +44,10 @@ __device__ __forceinline__ void bitonic_sort(unsigned long long* s, uint32_t p) 
     }
 }
 
+// SMEM_KEYS: keys staged in shared memory (more come from L2); SEL_KEYS: the select
+// buffer (>= k + 1).  Two configurations: 8192 / 4096 (104 KB, two CTAs per SM) for
+// any k <= 2048, and 4096 / 1024 (49 KB, four CTAs per SM) for k <= 512.
+template <uint32_t TK_SMEM_KEYS, uint32_t TK_SEL_KEYS>
 __global__ void __launch_bounds__(TK_THREADS) topk_kernel(const unsigned long long* __restrict__ cand,
                                                           const uint32_t* __restrict__ ccount, uint32_t cap,
                                                           uint32_t parts, uint64_t part_stride, uint64_t count_stride,
@@ -200,18 +202,28 @@ __global__ void __launch_bounds__(TK_THREADS) topk_kernel(const unsigned long lo
     if (tid == 0) out_counts[q] = kk;
 }
 
+template <uint32_t SK, uint32_t SEL>
+static void launch_topk_cfg(const unsigned long long* cand, const uint32_t* ccount, uint32_t cap, uint32_t parts,
+                            uint64_t part_stride, uint64_t count_stride, uint32_t nq, uint32_t k,
+                            unsigned long long* out_keys, uint32_t* out_counts, cudaStream_t s) {
+    const size_t smem = (SK + SEL) * sizeof(unsigned long long) + TK_BUCKETS * sizeof(uint32_t);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(topk_kernel<SK, SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    topk_kernel<SK, SEL><<<nq, TK_THREADS, smem, s>>>(cand, ccount, cap, parts, part_stride, count_stride, nq, k,
+                                                      out_keys, out_counts);
+}
+
 void launch_topk(const unsigned long long* cand, const uint32_t* ccount, uint32_t cap, uint32_t parts,
                  uint64_t part_stride, uint64_t count_stride, uint32_t nq, uint32_t k, unsigned long long* out_keys,
                  uint32_t* out_counts, cudaStream_t s) {
     if (nq == 0 || k == 0) return;
-    const size_t smem = (TK_SMEM_KEYS + TK_SEL_KEYS) * sizeof(unsigned long long) + TK_BUCKETS * sizeof(uint32_t);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
-    topk_kernel<<<nq, TK_THREADS, smem, s>>>(cand, ccount, cap, parts, part_stride, count_stride, nq, k, out_keys,
-                                              out_counts);
+    if (k <= 512)
+        launch_topk_cfg<4096, 1024>(cand, ccount, cap, parts, part_stride, count_stride, nq, k, out_keys, out_counts, s);
+    else
+        launch_topk_cfg<8192, 4096>(cand, ccount, cap, parts, part_stride, count_stride, nq, k, out_keys, out_counts, s);
     count_launch();
 }
 
