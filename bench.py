@@ -250,7 +250,7 @@ def run_ivf(args, rank, world, local):
         # every cell's list holds this rank's id range; per-rank top-k
         # keys are all-gathered over NCCL and merged exactly (IVFIndexEngine + ShardedSearch)
         from paper_1609_01882_b200.distributed import IVFIndexEngine, ShardedSearch
-        engine = IVFIndexEngine(ivf, stream, split_coarse=True)  # coarse quantization split by query
+        engine = IVFIndexEngine(ivf, split_coarse=True)  # coarse quantization split by query
         sharded = ShardedSearch(engine)
 
     def step(i, p, st=None):
@@ -440,7 +440,7 @@ def main():
     o_surv = torch.empty(BATCH, dtype=torch.int64, device="cuda")
     if world > 1:
         from paper_1609_01882_b200.distributed import FlatIndexEngine, ShardedSearch
-        sharded = ShardedSearch(FlatIndexEngine(index, stream), device="cuda")
+        sharded = ShardedSearch(FlatIndexEngine(index), device="cuda")
 
     def step(i, ht, q=None):
         qb = dq[(i % nbatches) * BATCH:][:BATCH] if q is None else q

@@ -100,6 +100,15 @@ int poly_b200_search_batch_device(poly_b200_index* index, const float* d_queries
                                   uint32_t* d_out_counts, uint64_t* d_out_survivors, void* stream,
                                   poly_b200_search_stats* stats);
 
+/* Same, plus the per-query survivor-set hash: out_survivor_hash[q] = sum over the
+ * codes that pass the dual filter of mix64(id) mod 2^64 (splitmix64 finaliser,
+ * order-independent; the parity suite compares it with the oracle's).  Either
+ * per-query output may be NULL; strategies other than dual report 0. */
+int poly_b200_search_batch_device_ex(poly_b200_index* index, const float* d_queries, uint64_t nq,
+                                     const poly_b200_search_params* params, int64_t* d_out_ids, float* d_out_scores,
+                                     uint32_t* d_out_counts, uint64_t* d_out_survivors,
+                                     uint64_t* d_out_survivor_hash, void* stream, poly_b200_search_stats* stats);
+
 /* FlatIndex::calibrate_threshold (flat_index.hpp:128-132):
  * max { tau : mean survivor fraction over the train queries <= 1 - rate };
  * returns 0 in *tau with *warning = 1 when even tau = 0 keeps too many. */
@@ -151,6 +160,13 @@ int poly_b200_debug_lut(poly_b200_index* index, const float* queries, uint64_t n
 /* Test hook: per-query candidate counts and final thresholds of the last
  * scanned batch (nq <= 256 entries each). */
 int poly_b200_debug_counts(poly_b200_index* index, uint32_t* ccount, uint64_t* thr, uint32_t nq);
+
+/* Test hooks for the candidate-list overflow path: force the per-query candidate
+ * list capacity (rounded to the select block; 0 = default), and count the queries
+ * of the last batch whose list overflowed and were re-ranked by the exact rescue
+ * scan (kernels_rescue.cu).  IVF twins below. */
+int poly_b200_debug_set_list_capacity(poly_b200_index* index, uint32_t cap);
+int poly_b200_debug_rescued(poly_b200_index* index, uint32_t* n_rescued);
 
 /* Timing hook for bench.py: while enabled, CUDA events bracket every K2 scan
  * launch on its stream; poly_b200_profile_read waits for them and returns the
@@ -215,6 +231,13 @@ int poly_b200_ivf_search_device(poly_b200_ivf* ivf, const float* d_queries, uint
                                 const poly_b200_ivf_params* params, int64_t* d_out_ids, float* d_out_scores,
                                 uint32_t* d_out_counts, void* stream, poly_b200_search_stats* stats);
 
+/* Same with per-query survivor counts and survivor-set hashes (device, nq each,
+ * either may be NULL; as poly_b200_search_batch_device_ex). */
+int poly_b200_ivf_search_device_ex(poly_b200_ivf* ivf, const float* d_queries, uint64_t nq,
+                                   const poly_b200_ivf_params* params, int64_t* d_out_ids, float* d_out_scores,
+                                   uint32_t* d_out_counts, uint64_t* d_out_survivors, uint64_t* d_out_survivor_hash,
+                                   void* stream, poly_b200_search_stats* stats);
+
 /* Multi-GPU IVF: each rank holds every cell's lists for its id
  * range (shard by id within every list) and returns its per-query top-k as
  * 64-bit keys (fp32 score bits << 32 | 32-bit global id); the ranks' keys are
@@ -241,6 +264,9 @@ int poly_b200_ivf_search_keys_probes_device(poly_b200_ivf* ivf, const float* d_q
                                             const poly_b200_ivf_params* params, const uint64_t* d_probe_keys,
                                             uint64_t* d_keys, uint32_t* d_counts, void* stream,
                                             poly_b200_search_stats* stats);
+
+int poly_b200_ivf_debug_set_list_capacity(poly_b200_ivf* ivf, uint32_t cap);
+int poly_b200_ivf_debug_rescued(poly_b200_ivf* ivf, uint32_t* n_rescued);
 
 /* knn_graph: the k nearest neighbours of n vectors that are
  * themselves in the index (vector i has id id0 + i), self-match removed:

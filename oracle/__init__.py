@@ -74,7 +74,7 @@ def lib():
         L.po_relabel_codes.argtypes = [_u32, _u32, _P, _P, _P, _u64]
         L.po_ivf_assign.argtypes = [_P, _u64, _u32, _P, _u32, C.c_uint, _P]
         L.po_ivf_search.argtypes = [_u32, _u32, _u32, _P, _P, _P, _P, _u32, _P, _P, _P, _P, _u64, _u32, _u64, _i32,
-                                    _u32, _u32, C.c_uint, _P, _P, _P, _P, _P, _P]
+                                    _u32, _u32, C.c_uint, _P, _P, _P, _P, _P, _P, _P]
         L.po_ivf_search.restype = _i32
         L.po_ivf_encode_residuals.argtypes = [_u32, _u32, _u32, _P, _P, _P, _u64, _P, _P, _P]
         _lib = L
@@ -351,8 +351,10 @@ def ivf_build(pq: PQ, x, centroids, ids=None, assign=None):
     return IVFLists(off, codes[order], ids[order]), assign
 
 
-def ivf_search(pq: PQ, centroids, lists: IVFLists, queries, k, nprobe, tau=None, strategy="dual", cap=0, threads=8):
-    """search_coarse.  Returns ids, scores, counts, survivors, scanned, probes."""
+def ivf_search(pq: PQ, centroids, lists: IVFLists, queries, k, nprobe, tau=None, strategy="dual", cap=0, threads=8,
+               return_hash=False):
+    """search_coarse.  Returns ids, scores, counts, survivors, scanned, probes
+    (+ the per-query survivor hash, sum of mix64(id), with return_hash)."""
     centroids = np.ascontiguousarray(centroids, np.float32)
     queries = np.ascontiguousarray(queries, np.float32)
     nq = queries.shape[0]
@@ -363,11 +365,14 @@ def ivf_search(pq: PQ, centroids, lists: IVFLists, queries, k, nprobe, tau=None,
     sv = np.empty(nq, np.uint64)
     sc = np.empty(nq, np.uint64)
     pr = np.empty((nq, nprobe), np.uint32)
+    sh = np.empty(nq, np.uint64)
     rc = lib().po_ivf_search(*pq.args(), _ptr(pq.inv_perms), _ptr(centroids), centroids.shape[0], _ptr(lists.off),
                              _ptr(lists.codes), _ptr(lists.ids), _ptr(queries), nq, nprobe, cap, STRATEGIES[strategy],
-                             k, tau, threads, _ptr(oi), _ptr(osc), _ptr(oc), _ptr(sv), _ptr(sc), _ptr(pr))
+                             k, tau, threads, _ptr(oi), _ptr(osc), _ptr(oc), _ptr(sv), _ptr(sc), _ptr(pr), _ptr(sh))
     if rc != 0:
         raise ValueError(f"oracle ivf search rejected arguments (rc={rc})")
+    if return_hash:
+        return oi, osc, oc, sv, sc, pr, sh
     return oi, osc, oc, sv, sc, pr
 
 

@@ -330,7 +330,7 @@ static void po_search_chunk(void* p, size_t qb, size_t qe) {
                 /* pass 2: ADC rerank of survivors, top-k by (score, id) */
                 for (uint64_t s = 0; s < nsurv; ++s) {
                     const uint64_t i = surv[s];
-                    hsurv += po_mix64(i);
+                    hsurv += po_mix64((uint64_t)c->ids[i]);  /* survivor-set hash: sum of mix64(id) */
                     po_topk_offer(&t, po_adc_permuted(pq, lutp, c->codes + i * cb), c->ids[i]);
                 }
             } else {
@@ -503,7 +503,7 @@ typedef struct {
     const po_pq* pq; const float* cent; uint32_t nlist; const uint64_t* off; const uint8_t* codes; const int64_t* ids;
     const float* queries; uint32_t nprobe; uint64_t cap; int strategy; uint32_t k, tau;
     int64_t* out_ids; float* out_scores; uint32_t* out_counts; uint64_t* out_surv; uint64_t* out_scanned;
-    uint32_t* out_probes;
+    uint32_t* out_probes; uint64_t* out_surv_hash;
 } po_ivf_ctx;
 
 static void po_ivf_chunk(void* p, size_t qb, size_t qe) {
@@ -519,7 +519,7 @@ static void po_ivf_chunk(void* p, size_t qb, size_t qe) {
     for (size_t qi = qb; qi < qe; ++qi) {
         const float* q = c->queries + qi * dim;
         t.n = 0;
-        uint64_t nsurv = 0, nscan = 0;
+        uint64_t nsurv = 0, nscan = 0, hsurv = 0;
         uint32_t visited = 0;
         if (c->k > 0) {
             for (uint32_t j = 0; j < c->nlist; ++j) { cd[j].d = po_sq_l2(q, c->cent + (size_t)j * dim, dim); cd[j].c = j; }
@@ -539,6 +539,7 @@ static void po_ivf_chunk(void* p, size_t qb, size_t qe) {
                     if (c->strategy == 3) {
                         if (po_hamming_bytes(qcode, code, cb) > c->tau) continue;
                         ++nsurv;
+                        hsurv += po_mix64((uint64_t)c->ids[i]);
                         s = po_adc_permuted(pq, lutp, code);
                     } else if (c->strategy == 0) s = po_adc_permuted(pq, lutp, code);
                     else if (c->strategy == 1) s = (float)po_hamming_bytes(qcode, code, cb);
@@ -556,6 +557,7 @@ static void po_ivf_chunk(void* p, size_t qb, size_t qe) {
         }
         c->out_counts[qi] = (uint32_t)t.n;
         if (c->out_surv) c->out_surv[qi] = nsurv;
+        if (c->out_surv_hash) c->out_surv_hash[qi] = hsurv;
         if (c->out_scanned) c->out_scanned[qi] = nscan;
         if (c->out_probes) {
             const uint32_t np = c->nprobe < c->nlist ? c->nprobe : c->nlist;
@@ -570,12 +572,12 @@ int po_ivf_search(uint32_t m, uint32_t dbits, uint32_t dim, const float* codeboo
                   const uint8_t* list_codes, const int64_t* list_ids, const float* queries, uint64_t nq, uint32_t nprobe,
                   uint64_t cap, int strategy, uint32_t k, uint32_t tau, unsigned threads, int64_t* out_ids,
                   float* out_scores, uint32_t* out_counts, uint64_t* out_survivors, uint64_t* out_scanned,
-                  uint32_t* out_probes) {
+                  uint32_t* out_probes, uint64_t* out_survivor_hash) {
     po_pq pq = {m, dbits, dim, codebooks, perms, inv_perms};
     if (m == 0 || dbits < 1 || dbits > 8 || dim % m != 0 || strategy < 0 || strategy > 3 || nlist == 0) return PO_EINVAL;
     if (tau > m * dbits || nprobe == 0) return PO_EINVAL;
     po_ivf_ctx c = {&pq, centroids, nlist, list_off, list_codes, list_ids, queries, nprobe, cap, strategy, k, tau,
-                    out_ids, out_scores, out_counts, out_survivors, out_scanned, out_probes};
+                    out_ids, out_scores, out_counts, out_survivors, out_scanned, out_probes, out_survivor_hash};
     po_parallel_chunks(nq, threads, po_ivf_chunk, &c);
     return PO_OK;
 }

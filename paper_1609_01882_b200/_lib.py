@@ -50,6 +50,8 @@ def _load():
                                          C.POINTER(SearchStatsC)]
     L.poly_b200_search_batch_device.argtypes = [_P, _P, _u64, C.POINTER(SearchParamsC), _P, _P, _P, _P, _P,
                                                 C.POINTER(SearchStatsC)]
+    L.poly_b200_search_batch_device_ex.argtypes = [_P, _P, _u64, C.POINTER(SearchParamsC), _P, _P, _P, _P, _P, _P,
+                                                   C.POINTER(SearchStatsC)]
     L.poly_b200_calibrate_threshold.argtypes = [_P, _P, _u64, _f64, C.POINTER(_u32), C.POINTER(_i32)]
     L.poly_b200_with_assignments.argtypes = [_P, _P, C.POINTER(_P)]
     L.poly_b200_get_codes.argtypes = [_P, _P, _P]
@@ -59,6 +61,10 @@ def _load():
     L.poly_b200_gen_points_device.argtypes = [_i32, _u64, _P, _u32, _u32, _u32, _u64, _u64, _i32, _P, _P]
     L.poly_b200_debug_lut.argtypes = [_P, _P, _u64, _P, _P]
     L.poly_b200_debug_counts.argtypes = [_P, _P, _P, _u32]
+    L.poly_b200_debug_set_list_capacity.argtypes = [_P, _u32]
+    L.poly_b200_debug_rescued.argtypes = [_P, C.POINTER(_u32)]
+    L.poly_b200_ivf_debug_set_list_capacity.argtypes = [_P, _u32]
+    L.poly_b200_ivf_debug_rescued.argtypes = [_P, C.POINTER(_u32)]
     L.poly_b200_profile_enable.argtypes = [_P, _i32]
     L.poly_b200_profile_read.argtypes = [_P, C.POINTER(_f64), C.POINTER(_u64)]
     L.poly_b200_launch_count.restype = _u64
@@ -75,6 +81,8 @@ def _load():
     L.poly_b200_ivf_search.argtypes = [_P, _P, _u64, C.POINTER(IvfParamsC), _P, _P, _P, C.POINTER(SearchStatsC)]
     L.poly_b200_ivf_search_device.argtypes = [_P, _P, _u64, C.POINTER(IvfParamsC), _P, _P, _P, _P,
                                               C.POINTER(SearchStatsC)]
+    L.poly_b200_ivf_search_device_ex.argtypes = [_P, _P, _u64, C.POINTER(IvfParamsC), _P, _P, _P, _P, _P, _P,
+                                                 C.POINTER(SearchStatsC)]
     L.poly_b200_ivf_knn_graph_device.argtypes = [_P, _P, _u64, C.c_int64, C.POINTER(IvfParamsC), _P, _P, _P, _P]
     L.poly_b200_ivf_search_keys_device.argtypes = [_P, _P, _u64, C.POINTER(IvfParamsC), _P, _P, _P,
                                                    C.POINTER(SearchStatsC)]
@@ -91,6 +99,8 @@ lib = _load()
 EXPORTS = [
     "poly_b200_last_error", "poly_b200_create", "poly_b200_destroy", "poly_b200_size", "poly_b200_code_bytes",
     "poly_b200_add", "poly_b200_add_codes", "poly_b200_search_batch", "poly_b200_search_batch_device",
+    "poly_b200_search_batch_device_ex", "poly_b200_ivf_search_device_ex", "poly_b200_debug_set_list_capacity",
+    "poly_b200_debug_rescued", "poly_b200_ivf_debug_set_list_capacity", "poly_b200_ivf_debug_rescued",
     "poly_b200_calibrate_threshold", "poly_b200_with_assignments", "poly_b200_get_codes",
     "poly_b200_search_keys_device", "poly_b200_merge_keys_device", "poly_b200_add_synthetic",
     "poly_b200_gen_points_device", "poly_b200_debug_lut", "poly_b200_debug_counts", "poly_b200_profile_enable", "poly_b200_profile_read",

@@ -9,6 +9,7 @@
 #include <atomic>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <numeric>
 #include <stdexcept>
@@ -22,6 +23,17 @@
 namespace pb {
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+void set_max_smem(const void* fn, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& have = done[{fn, dev}];
+    if (have >= bytes) return;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess) have = bytes;
+}
 }  // namespace pb
 
 namespace pbh {
@@ -32,7 +44,6 @@ using namespace pbh;
 namespace {
 
 constexpr uint32_t NQB = 256;  // queries per batch (BASELINE.json config 1: "batches of 256")
-constexpr uint64_t WARM_TILES = 16;  // strided sample that seeds the thresholds
 
 }  // namespace
 
@@ -57,23 +68,17 @@ struct poly_b200_index {
     uint8_t* qcodes = nullptr;
     unsigned long long* cand = nullptr;
     uint32_t cand_cap = 0, cand_bs = 0;
-    uint32_t* ctrl = nullptr;   // [ccount NQB][overflow][work][pad2][bdone NQB*nblk]
+    uint32_t cap_override = 0;  // test hook: candidate-list capacity (0 = the default)
+    // [ccount NQB][ovq NQB][rcount NQB][work][pad3][bdone NQB*nblk]...[group work counters (last 32)]
+    uint32_t* ctrl = nullptr;
     size_t ctrl_words = 0;
-    // warm-up (threshold seeding) scratch: its own candidate list and control block
-    unsigned long long* cand_w = nullptr;
-    uint32_t* ctrl_w = nullptr;
-    uint32_t cand_w_cap = 0;
     unsigned long long* thr = nullptr;
     unsigned long long* surv = nullptr;      // per-query survivors of a batch (per-query mode)
-    unsigned long long* surv_w = nullptr;    // warm-up sink
+    unsigned long long* surv_hash = nullptr; // per-query survivor hashes of a batch (per-query mode)
     unsigned long long* surv_total = nullptr;  // survivors summed over the whole call
     unsigned long long* keys = nullptr;
     uint32_t keys_k = 0;
     uint32_t* kcounts = nullptr;
-    uint32_t* sticky_overflow = nullptr;  // device, per call
-    uint32_t* h_overflow = nullptr;       // pinned
-    cudaEvent_t done_ev = nullptr;
-    bool pending_check = false;
 
     // host-API staging
     float* d_q = nullptr;
@@ -81,7 +86,6 @@ struct poly_b200_index {
     int64_t* d_oid = nullptr;
     float* d_osc = nullptr;
     uint32_t* d_ocnt = nullptr;
-    uint64_t* d_osurv = nullptr;
     uint64_t d_out_rows = 0;
     uint32_t d_out_k = 0;
 
@@ -130,32 +134,22 @@ void ensure_scratch(poly_b200_index* ix, uint32_t k) {
         ix->qcodes = dalloc<uint8_t>((size_t)NQB * ix->cb);
         ix->thr = dalloc<unsigned long long>(NQB);
         ix->surv = dalloc<unsigned long long>(NQB);
-        ix->surv_w = dalloc<unsigned long long>(NQB);
+        ix->surv_hash = dalloc<unsigned long long>(NQB);
         ix->surv_total = dalloc<unsigned long long>(1);
-        ix->sticky_overflow = dalloc<uint32_t>(1);
-        CK(cudaMallocHost(&ix->h_overflow, sizeof(uint32_t)));
-        *ix->h_overflow = 0;
-        CK(cudaEventCreateWithFlags(&ix->done_ev, cudaEventDisableTiming));
     }
     // select block: a block of bs list slots completes -> its k-th key tightens thr[q];
     // the list holds at least 32 * BS keys per query
     const uint32_t bs = std::max<uint32_t>(POLY_SEL_BS, POLY_SEL_KF * k);
-    const uint32_t cap = std::max<uint32_t>(32 * bs, 32 * pb::BS);
-    if (ix->cand_bs != bs || ix->cand_cap < cap) {
+    uint32_t cap = std::max<uint32_t>(32 * bs, 32 * pb::BS);
+    if (ix->cap_override) cap = std::max<uint32_t>(2, (ix->cap_override + bs - 1) / bs) * bs;
+    if (ix->cand_bs != bs || ix->cand_cap != cap) {
         dfree(ix->cand);
         dfree(ix->ctrl);
         ix->cand_bs = bs;
         ix->cand_cap = cap;
         ix->cand = dalloc<unsigned long long>((size_t)NQB * ix->cand_cap);
-        ix->ctrl_words = NQB + 4 + (size_t)NQB * (cap / bs) + 32;  // + per-group work counters (last 32)
+        ix->ctrl_words = 3 * NQB + 4 + (size_t)NQB * (cap / bs) + 32;  // + per-group work counters (last 32)
         ix->ctrl = dalloc<uint32_t>(ix->ctrl_words);
-    }
-    if (!ix->cand_w) {
-        // warm-up samples WARM_TILES tiles: every candidate of the sample fits
-        ix->cand_w_cap = (uint32_t)(WARM_TILES * (pb::TILE_BYTES / ix->cb));
-        ix->cand_w_cap = (ix->cand_w_cap + pb::BS - 1) / pb::BS * pb::BS;
-        ix->cand_w = dalloc<unsigned long long>((size_t)NQB * ix->cand_w_cap);
-        ix->ctrl_w = dalloc<uint32_t>(NQB + 4 + (size_t)NQB * (ix->cand_w_cap / 256 + 1));
     }
     if (ix->keys_k < k) {
         dfree(ix->keys);
@@ -166,19 +160,6 @@ void ensure_scratch(poly_b200_index* ix, uint32_t k) {
     }
 }
 
-void check_pending(poly_b200_index* ix, bool wait) {
-    if (!ix->pending_check) return;
-    if (wait) CK(cudaEventSynchronize(ix->done_ev));
-    else if (cudaEventQuery(ix->done_ev) != cudaSuccess) return;
-    ix->pending_check = false;
-    if (*ix->h_overflow) {
-        *ix->h_overflow = 0;
-        throw Error(POLY_B200_INTERNAL,
-                    "candidate list overflow in a previous search: its results are incomplete (raise k's block "
-                    "size or split the database)");
-    }
-}
-
 void validate_params(const poly_b200_index* ix, const poly_b200_search_params* p) {
     require(p != nullptr, POLY_B200_INVALID_ARGUMENT, "null search params");
     require(p->strategy >= 0 && p->strategy <= 3, POLY_B200_INVALID_ARGUMENT, "unknown strategy");
@@ -186,10 +167,10 @@ void validate_params(const poly_b200_index* ix, const poly_b200_search_params* p
     require(p->k <= (uint32_t)pb::KMAX, POLY_B200_INVALID_ARGUMENT, "k > 2048 is not supported on the GPU path");
 }
 
-// Core batched search: per batch of <= 256 queries K1 -> K2 -> K3 into keys.
-// emit(b, nqb) consumes ix->keys / ix->kcounts / ix->surv for that batch.
-// perq: per-query survivor counts in ix->surv (else the exact call total
-// accumulates in ix->surv_total at no cost in the scan).
+// Core batched search: per batch of <= 256 queries K1 -> K2s -> K2 (-> K2x) -> K3 into keys.
+// emit(b, nqb) consumes ix->keys / ix->kcounts / ix->surv / ix->surv_hash for that batch.
+// perq: per-query survivor counts and hashes in ix->surv / ix->surv_hash (else the
+// exact call total accumulates in ix->surv_total at no cost in the scan).
 template <class Emit>
 void run_batches(poly_b200_index* ix, const float* d_queries, uint64_t nq, const poly_b200_search_params* p,
                  bool perq, cudaStream_t s, Emit&& emit) {
@@ -202,13 +183,15 @@ void run_batches(poly_b200_index* ix, const float* d_queries, uint64_t nq, const
     const uint32_t Q = (uint32_t)pb::scan_queries_per_cta(ix->m);
     const uint64_t tc = pb::TILE_BYTES / ix->cb;
     const uint64_t ntiles = (ix->n + tc - 1) / tc;
-    CK(cudaMemsetAsync(ix->sticky_overflow, 0, 4, s));
     CK(cudaMemsetAsync(ix->surv_total, 0, 8, s));
     for (uint64_t b0 = 0; b0 < nq; b0 += NQB) {
         const uint32_t nqb = (uint32_t)std::min<uint64_t>(NQB, nq - b0);
         CK(cudaMemsetAsync(ix->ctrl, 0, ix->ctrl_words * 4, s));
         CK(cudaMemsetAsync(ix->thr, 0xFF, NQB * 8, s));
-        if (perq) CK(cudaMemsetAsync(ix->surv, 0, NQB * 8, s));
+        if (perq) {
+            CK(cudaMemsetAsync(ix->surv, 0, NQB * 8, s));
+            CK(cudaMemsetAsync(ix->surv_hash, 0, NQB * 8, s));
+        }
         if (k > 0 && ix->n > 0) {
             pb::launch_lut(d_queries + b0 * ix->dim, nqb, ix->dim, ix->m, ix->d_codebooks, ix->d_perms, ix->lutp,
                            ix->qcodes, s);
@@ -225,51 +208,21 @@ void run_batches(poly_b200_index* ix, const float* d_queries, uint64_t nq, const
             a.id32 = ix->idm.d_id32;
             a.thr = ix->thr;
             a.ngroups = (nqb + Q - 1) / Q;
-            // Seed: one CTA per query ranks a fixed 256-code-run sample (K2s); then
-            // the geometric warm-up levels below start from that bound.
-            // at most n / 256 runs: runs never overlap, so no code is sampled twice (a repeated
-            // key would make the sample's k-th key too small and the bound invalid)
+            // Seed: one CTA per query ranks a fixed 256-code-run sample (K2s).  At most
+            // n / 256 runs: runs never overlap, so no code is sampled twice (a repeated
+            // key would make the sample's k-th key too small and the bound invalid).
             const uint64_t seed_blocks = std::min<uint64_t>(POLY_SEED_BLOCKS, ix->n / 256);
             if (seed_blocks > 0 && ix->n > ix->cand_cap / 8)
                 pb::launch_seed_sample(a, strategy, ix->m, nqb, (uint32_t)seed_blocks, s);
-            // Warm-up: strided samples of POLY_WARM_FIRST tiles (x8 per further level,
-            // POLY_WARM_LEVELS levels) spread over the database, each scanned with the
-            // current bound and ranked exactly (K3) to tighten it.  With the K2s seed and
-            // 512-slot in-scan selects one 128-tile level is enough (A/B in DESIGN.md).
-            // The samples are re-scanned by the full scan (their keys must be in its list).
-            int level = 0;
-            for (uint64_t wt = POLY_WARM_FIRST; ntiles >= 8 * wt && ix->n > ix->cand_cap / 8 && level < POLY_WARM_LEVELS;
-                 wt *= 8, ++level) {
-                pb::ScanArgs w = a;
-                const size_t nblk_w = ix->cand_w_cap / 256 + 1;
-                CK(cudaMemsetAsync(ix->ctrl_w, 0, (NQB + 4 + NQB * nblk_w) * 4, s));
-                w.cand = ix->cand_w;
-                w.cap = ix->cand_w_cap;
-                w.ccount = ix->ctrl_w;
-                w.overflow = ix->ctrl_w + NQB;
-                w.work = ix->ctrl_w + NQB + 1;
-                w.bdone = ix->ctrl_w + NQB + 4;
-                w.surv = ix->surv_w;
-                w.ntiles = wt;
-                w.tile_stride = ntiles / wt;
-                w.tiles_per_chunk = 4;  // small units: the first levels would otherwise use few SMs
-                w.units = (uint32_t)(wt / 4) * w.ngroups;
-                // POLY_WARM_SEL: in-scan selects tighten thr inside the sample too (its top-k
-                // members stay in the list either way); else the whole sample is ranked below
-                w.bs = POLY_WARM_SEL ? ix->cand_bs : ix->cand_w_cap;
-                pb::launch_scan(w, strategy, ix->m, false, ix->num_sms, s);
-                // an overflowed sample list is only a weaker (still valid) bound: ranks
-                // of a subset of the sample's keys
-                pb::launch_topk(ix->cand_w, ix->ctrl_w, ix->cand_w_cap, 1, 0, 0, nqb, k, ix->keys, ix->kcounts, s);
-                pb::launch_seed_thr(ix->keys, ix->kcounts, nqb, k, ix->thr, s);
-            }
             a.cand = ix->cand;
             a.cap = ix->cand_cap;
             a.ccount = ix->ctrl;
-            a.overflow = ix->ctrl + NQB;
-            a.work = POLY_AFFINE ? ix->ctrl + ix->ctrl_words - 32 : ix->ctrl + NQB + 1;
-            a.bdone = ix->ctrl + NQB + 4;
+            a.ovq = ix->ctrl + NQB;
+            uint32_t* rcount = ix->ctrl + 2 * NQB;
+            a.work = POLY_AFFINE ? ix->ctrl + ix->ctrl_words - 32 : ix->ctrl + 3 * NQB;
+            a.bdone = ix->ctrl + 3 * NQB + 4;
             a.surv = perq ? ix->surv : ix->surv_total;
+            a.surv_hash = perq ? ix->surv_hash : nullptr;
             const uint64_t want = std::max<uint64_t>(1, ntiles * a.ngroups / ((uint64_t)POLY_UNITS_PER_CTA * ix->num_sms));
             a.tiles_per_chunk = (uint32_t)std::min<uint64_t>(POLY_MAX_TPC, want);
             a.ntiles = ntiles;
@@ -294,49 +247,79 @@ void run_batches(poly_b200_index* ix, const float* d_queries, uint64_t nq, const
             pb::launch_scan(a, strategy, ix->m, perq, ix->num_sms, s);
             if (e1) CK(cudaEventRecord(e1, s));
             CK(cudaGetLastError());
+            // queries whose candidate list overflowed are re-ranked exactly (no-op otherwise)
+            pb::launch_rescue(a, strategy, ix->m, rcount, ix->num_sms, s);
             pb::launch_topk(ix->cand, ix->ctrl, ix->cand_cap, 1, 0, 0, nqb, k, ix->keys, ix->kcounts, s);
-            pb::launch_or_flag(ix->sticky_overflow, ix->ctrl + NQB, s);  // sticky |= batch overflow
         } else {
             CK(cudaMemsetAsync(ix->kcounts, 0, NQB * 4, s));
         }
         CK(cudaGetLastError());
         emit(b0, nqb, strategy == pb::DUAL, all_pass);
     }
-    CK(cudaMemcpyAsync(ix->h_overflow, ix->sticky_overflow, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaEventRecord(ix->done_ev, s));
-    ix->pending_check = true;
 }
 
 __global__ void surv_out_kernel(const unsigned long long* surv, uint32_t nqb, uint64_t fill, int mode,
                                 uint64_t* out) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < nqb) out[i] = mode == 0 ? 0 : (mode == 1 ? fill : surv[i]);
+    if (i < nqb) out[i] = mode == 0 ? 0 : (mode == 1 ? fill : (mode == 3 ? surv[0] : surv[i]));
+}
+
+// sum over every stored code of mix64(key low word): the survivor hash when every code
+// survives (dual at tau = code_bits)
+__global__ void id_hash_kernel(uint64_t n, int mode, uint32_t id0, const uint32_t* __restrict__ id32,
+                               unsigned long long* out) {
+    unsigned long long h = 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        h += pb::mix64(mode == pb::ID_ARITH ? id0 + (uint32_t)i : id32[i]);
+    for (int off = 16; off; off >>= 1) h += __shfl_down_sync(0xffffffffu, h, off);
+    if ((threadIdx.x & 31) == 0 && h) atomicAdd(out, h);
+}
+
+// Returns the strategy-level survivor semantics: 0 none (adc/binary/disidx),
+// 1 all codes survive (dual at tau = code_bits), 2 counted by the scan.
+// Per-query survivor outputs of one batch (either pointer may be null).
+void emit_survivors(poly_b200_index* ix, int mode, uint32_t nqb, uint64_t* d_surv, uint64_t* d_hash, cudaStream_t s) {
+    if (d_surv) {
+        surv_out_kernel<<<(nqb + 127) / 128, 128, 0, s>>>(ix->surv, nqb, ix->n, mode, d_surv);
+        pb::count_launch();
+    }
+    if (d_hash) {
+        if (mode == 1) {  // every code survives: the hash of all stored ids
+            CK(cudaMemsetAsync(ix->surv_hash, 0, 8, s));
+            id_hash_kernel<<<4 * ix->num_sms, 256, 0, s>>>(ix->n, ix->idm.mode, ix->idm.key_id0, ix->idm.d_id32,
+                                                           ix->surv_hash);
+            pb::count_launch();
+            surv_out_kernel<<<(nqb + 127) / 128, 128, 0, s>>>(ix->surv_hash, nqb, 0, 3, d_hash);
+        } else {
+            surv_out_kernel<<<(nqb + 127) / 128, 128, 0, s>>>(ix->surv_hash, nqb, 0, mode, d_hash);
+        }
+        pb::count_launch();
+    }
 }
 
 // Returns the strategy-level survivor semantics: 0 none (adc/binary/disidx),
 // 1 all codes survive (dual at tau = code_bits), 2 counted by the scan.
 int device_search(poly_b200_index* ix, const float* d_queries, uint64_t nq, const poly_b200_search_params* p,
-                  int64_t* d_ids, float* d_scores, uint32_t* d_counts, uint64_t* d_surv, cudaStream_t s) {
+                  int64_t* d_ids, float* d_scores, uint32_t* d_counts, uint64_t* d_surv, cudaStream_t s,
+                  uint64_t* d_hash = nullptr) {
     validate_params(ix, p);
     require(nq == 0 || d_queries, POLY_B200_INVALID_ARGUMENT, "null queries");
     require(p->k == 0 || (d_ids && d_scores), POLY_B200_INVALID_ARGUMENT, "null outputs");
-    check_pending(ix, false);
     if (nq == 0) return 0;
     if (p->k == 0) {  // k = 0 -> empty lists
         if (d_counts) CK(cudaMemsetAsync(d_counts, 0, nq * 4, s));
         if (d_surv) CK(cudaMemsetAsync(d_surv, 0, nq * 8, s));
+        if (d_hash) CK(cudaMemsetAsync(d_hash, 0, nq * 8, s));
         return 0;
     }
     const uint32_t k = p->k;
     int mode = 0;
-    run_batches(ix, d_queries, nq, p, d_surv != nullptr, s, [&](uint64_t b0, uint32_t nqb, bool dual, bool all_pass) {
+    const bool perq = d_surv != nullptr || d_hash != nullptr;
+    run_batches(ix, d_queries, nq, p, perq, s, [&](uint64_t b0, uint32_t nqb, bool dual, bool all_pass) {
         mode = dual ? 2 : (all_pass ? 1 : 0);
         pb::launch_keys_to_ids(ix->keys, ix->kcounts, nqb, k, ix->idm.d_rank_to_id, d_ids + b0 * k, d_scores + b0 * k,
                                d_counts ? d_counts + b0 : nullptr, s);
-        if (d_surv) {
-            surv_out_kernel<<<(nqb + 127) / 128, 128, 0, s>>>(ix->surv, nqb, ix->n, mode, d_surv + b0);
-            pb::count_launch();
-        }
+        emit_survivors(ix, mode, nqb, d_surv ? d_surv + b0 : nullptr, d_hash ? d_hash + b0 : nullptr, s);
     });
     return mode;
 }
@@ -367,13 +350,12 @@ void ensure_host_staging(poly_b200_index* ix, uint64_t nq, uint32_t k) {
         ix->d_q = dalloc<float>(ix->d_q_cap);
     }
     if (ix->d_out_rows < nq || ix->d_out_k < k) {
-        for (void* p : {(void*)ix->d_oid, (void*)ix->d_osc, (void*)ix->d_ocnt, (void*)ix->d_osurv}) dfree(p);
+        for (void* p : {(void*)ix->d_oid, (void*)ix->d_osc, (void*)ix->d_ocnt}) dfree(p);
         ix->d_out_rows = std::max<uint64_t>(nq, ix->d_out_rows);
         ix->d_out_k = std::max<uint32_t>(k, ix->d_out_k);
         ix->d_oid = dalloc<int64_t>(ix->d_out_rows * ix->d_out_k);
         ix->d_osc = dalloc<float>(ix->d_out_rows * ix->d_out_k);
         ix->d_ocnt = dalloc<uint32_t>(ix->d_out_rows);
-        ix->d_osurv = dalloc<uint64_t>(ix->d_out_rows);
     }
 }
 
@@ -424,19 +406,16 @@ int poly_b200_destroy(poly_b200_index* ix) {
         {
             DeviceGuard dg(ix->device);
             if (ix->stream) cudaStreamSynchronize(ix->stream);
-            for (void* p : {(void*)ix->d_codebooks, (void*)ix->d_perms, (void*)ix->d_codes, (void*)ix->lutp, (void*)ix->qcodes, (void*)ix->cand,
-                            (void*)ix->ctrl, (void*)ix->thr, (void*)ix->surv,
-                            (void*)ix->surv_w, (void*)ix->surv_total, (void*)ix->cand_w, (void*)ix->ctrl_w, (void*)ix->keys, (void*)ix->kcounts,
-                            (void*)ix->sticky_overflow, (void*)ix->d_q, (void*)ix->d_oid, (void*)ix->d_osc,
-                            (void*)ix->d_ocnt, (void*)ix->d_osurv})
+            for (void* p : {(void*)ix->d_codebooks, (void*)ix->d_perms, (void*)ix->d_codes, (void*)ix->lutp,
+                            (void*)ix->qcodes, (void*)ix->cand, (void*)ix->ctrl, (void*)ix->thr, (void*)ix->surv,
+                            (void*)ix->surv_hash, (void*)ix->surv_total, (void*)ix->keys, (void*)ix->kcounts,
+                            (void*)ix->d_q, (void*)ix->d_oid, (void*)ix->d_osc, (void*)ix->d_ocnt})
                 dfree(p);
             ix->idm.release();
-            if (ix->h_overflow) cudaFreeHost(ix->h_overflow);
             for (auto& pe : ix->prof_events) {
                 cudaEventDestroy(pe.first);
                 cudaEventDestroy(pe.second);
             }
-            if (ix->done_ev) cudaEventDestroy(ix->done_ev);
             if (ix->stream) cudaStreamDestroy(ix->stream);
         }
         delete ix;
@@ -528,21 +507,28 @@ int poly_b200_gen_points_device(int device, uint64_t seed, const float* centers,
     });
 }
 
-int poly_b200_search_batch_device(poly_b200_index* ix, const float* d_queries, uint64_t nq,
-                                  const poly_b200_search_params* p, int64_t* d_ids, float* d_scores,
-                                  uint32_t* d_counts, uint64_t* d_surv, void* stream, poly_b200_search_stats* stats) {
+int poly_b200_search_batch_device_ex(poly_b200_index* ix, const float* d_queries, uint64_t nq,
+                                     const poly_b200_search_params* p, int64_t* d_ids, float* d_scores,
+                                     uint32_t* d_counts, uint64_t* d_surv, uint64_t* d_surv_hash, void* stream,
+                                     poly_b200_search_stats* stats) {
     return guard([&] {
         require(ix != nullptr, POLY_B200_INVALID_ARGUMENT, "null index");
         std::lock_guard<std::mutex> lk(ix->mu);
         DeviceGuard dg(ix->device);
         cudaStream_t s = (cudaStream_t)stream;
-        const int mode = device_search(ix, d_queries, nq, p, d_ids, d_scores, d_counts, d_surv, s);
+        const int mode = device_search(ix, d_queries, nq, p, d_ids, d_scores, d_counts, d_surv, s, d_surv_hash);
         if (stats) {
             stats->scanned = ix->n * nq;
             stats->survivors = survivor_total(ix, mode, nq, d_surv, s);
-            check_pending(ix, true);
         }
     });
+}
+
+int poly_b200_search_batch_device(poly_b200_index* ix, const float* d_queries, uint64_t nq,
+                                  const poly_b200_search_params* p, int64_t* d_ids, float* d_scores,
+                                  uint32_t* d_counts, uint64_t* d_surv, void* stream, poly_b200_search_stats* stats) {
+    return poly_b200_search_batch_device_ex(ix, d_queries, nq, p, d_ids, d_scores, d_counts, d_surv, nullptr, stream,
+                                            stats);
 }
 
 int poly_b200_search_batch(poly_b200_index* ix, const float* queries, uint64_t nq, const poly_b200_search_params* p,
@@ -567,7 +553,6 @@ int poly_b200_search_batch(poly_b200_index* ix, const float* queries, uint64_t n
         if (out_counts) CK(cudaMemcpyAsync(out_counts, ix->d_ocnt, nq * 4, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         if (stats) stats->survivors = survivor_total(ix, mode, nq, nullptr, s);
-        check_pending(ix, true);
     });
 }
 
@@ -581,16 +566,16 @@ int poly_b200_search_keys_device(poly_b200_index* ix, const float* d_queries, ui
         std::lock_guard<std::mutex> lk(ix->mu);
         DeviceGuard dg(ix->device);
         cudaStream_t s = (cudaStream_t)stream;
-        check_pending(ix, false);
+        sync_idmap(ix);
+        // a key carries the 32-bit low word: the id itself unless ids needed a rank table,
+        // whose ranks are local to this shard and would be mis-merged across ranks
+        require(ix->n == 0 || ix->idm.d_rank_to_id == nullptr, POLY_B200_STATE,
+                "key output needs ids in [0, 2^32) (the key carries the id itself)");
         const uint32_t k = p->k;
         run_batches(ix, d_queries, nq, p, d_surv != nullptr, s, [&](uint64_t b0, uint32_t nqb, bool dual, bool all_pass) {
             CK(cudaMemcpyAsync(d_keys + b0 * k, ix->keys, (size_t)nqb * k * 8, cudaMemcpyDeviceToDevice, s));
             CK(cudaMemcpyAsync(d_counts + b0, ix->kcounts, nqb * 4, cudaMemcpyDeviceToDevice, s));
-            if (d_surv) {
-                const int mode = dual ? 2 : (all_pass ? 1 : 0);
-                surv_out_kernel<<<(nqb + 127) / 128, 128, 0, s>>>(ix->surv, nqb, ix->n, mode, d_surv + b0);
-                pb::count_launch();
-            }
+            emit_survivors(ix, dual ? 2 : (all_pass ? 1 : 0), nqb, d_surv ? d_surv + b0 : nullptr, nullptr, s);
         });
     });
 }
@@ -724,6 +709,28 @@ int poly_b200_debug_lut(poly_b200_index* ix, const float* queries, uint64_t nq, 
             CK(cudaMemcpyAsync(qcodes + b0 * ix->cb, ix->qcodes, (size_t)nqb * ix->cb, cudaMemcpyDeviceToHost, s));
         }
         CK(cudaStreamSynchronize(s));
+    });
+}
+
+int poly_b200_debug_set_list_capacity(poly_b200_index* ix, uint32_t cap) {
+    return guard([&] {
+        require(ix != nullptr, POLY_B200_INVALID_ARGUMENT, "null index");
+        std::lock_guard<std::mutex> lk(ix->mu);
+        ix->cap_override = cap;
+    });
+}
+
+int poly_b200_debug_rescued(poly_b200_index* ix, uint32_t* n) {
+    return guard([&] {
+        require(ix && n, POLY_B200_INVALID_ARGUMENT, "null arguments");
+        std::lock_guard<std::mutex> lk(ix->mu);
+        DeviceGuard dg(ix->device);
+        require(ix->ctrl != nullptr, POLY_B200_STATE, "no search has run");
+        CK(cudaDeviceSynchronize());
+        std::vector<uint32_t> ovq(NQB);
+        CK(cudaMemcpy(ovq.data(), ix->ctrl + NQB, NQB * 4, cudaMemcpyDeviceToHost));
+        *n = 0;
+        for (uint32_t v : ovq) *n += v != 0;
     });
 }
 

@@ -63,6 +63,7 @@ struct poly_b200_ivf {
     uint8_t* qcodes = nullptr;
     unsigned long long* cand = nullptr;
     uint32_t cand_cap = 0;
+    uint32_t cap_override = 0;  // test hook: candidate-list capacity (0 = the default)
     uint32_t* ctrl = nullptr;  // [ccount NQB][overflow][work x 16]
     unsigned long long* thr = nullptr;
     unsigned long long* keys = nullptr;
@@ -70,7 +71,13 @@ struct poly_b200_ivf {
     uint32_t* kcounts = nullptr;
     unsigned long long* surv_total = nullptr;
     unsigned long long* scan_total = nullptr;
-    uint32_t* sticky_overflow = nullptr;
+    uint32_t* ovq = nullptr;                 // per query: candidate list overflowed (rescued)
+    unsigned long long* surv_q = nullptr;    // per-query survivor counts / hashes (stats mode)
+    unsigned long long* hash_q = nullptr;
+    uint32_t* sticky_overflow = nullptr;     // work-list overflow (an internal invariant)
+    uint32_t* h_overflow = nullptr;          // pinned copy, checked at the next call
+    cudaEvent_t done_ev = nullptr;
+    bool pending_check = false;
     float* d_q = nullptr;
     uint64_t d_q_cap = 0;
     int64_t* d_oid = nullptr;
@@ -208,7 +215,13 @@ void ensure_ivf_scratch(poly_b200_ivf* iv, uint32_t nprobe, uint32_t k) {
         iv->kcounts = dalloc<uint32_t>(IVF_NQB);
         iv->surv_total = dalloc<unsigned long long>(1);
         iv->scan_total = dalloc<unsigned long long>(1);
+        iv->ovq = dalloc<uint32_t>(IVF_NQB);
+        iv->surv_q = dalloc<unsigned long long>(IVF_NQB);
+        iv->hash_q = dalloc<unsigned long long>(IVF_NQB);
         iv->sticky_overflow = dalloc<uint32_t>(1);
+        CK(cudaMallocHost(&iv->h_overflow, sizeof(uint32_t)));
+        *iv->h_overflow = 0;
+        CK(cudaEventCreateWithFlags(&iv->done_ev, cudaEventDisableTiming));
     }
     if (iv->scratch_nprobe < nprobe) {
         dfree(iv->probe_keys);
@@ -234,8 +247,9 @@ void ensure_ivf_scratch(poly_b200_ivf* iv, uint32_t nprobe, uint32_t k) {
             iv->items_cap[r] = need[r];
             iv->items[r] = dalloc<uint4>(need[r]);
         }
-    const uint32_t cap = (uint32_t)std::max<uint64_t>(131072, 4 * iv->max_list);
-    if (iv->cand_cap < cap) {
+    uint32_t cap = (uint32_t)std::max<uint64_t>(131072, 4 * iv->max_list);
+    if (iv->cap_override) cap = std::max<uint32_t>(iv->cap_override, k);
+    if (iv->cand_cap != cap) {
         dfree(iv->cand);
         iv->cand_cap = cap;
         iv->cand = dalloc<unsigned long long>((size_t)IVF_NQB * cap);
@@ -253,6 +267,22 @@ void validate(const poly_b200_ivf* iv, const poly_b200_ivf_params* p) {
     require(p->tau <= iv->code_bits(), POLY_B200_INVALID_ARGUMENT, "tau exceeds code bits");
     require(p->k <= (uint32_t)pb::KMAX, POLY_B200_INVALID_ARGUMENT, "k > 2048 is not supported on the GPU path");
     require(p->nprobe >= 1, POLY_B200_INVALID_ARGUMENT, "nprobe must be >= 1");  // CoarseConfig: nprobe >= 1
+    // enumerate_cells ranks min(nprobe, nlist) cells per query with K3 (k <= KMAX)
+    require(std::min(p->nprobe, iv->nlist) <= (uint32_t)pb::KMAX, POLY_B200_INVALID_ARGUMENT,
+            "min(nprobe, nlist) > 2048 is not supported on the GPU path");
+}
+
+// The work-list overflow flag of an earlier call (an internal invariant: the lists are
+// sized to their bound); raised at the next call on this index.
+void check_pending(poly_b200_ivf* iv, bool wait) {
+    if (!iv->pending_check) return;
+    if (wait) CK(cudaEventSynchronize(iv->done_ev));
+    else if (cudaEventQuery(iv->done_ev) != cudaSuccess) return;
+    iv->pending_check = false;
+    if (*iv->h_overflow) {
+        *iv->h_overflow = 0;
+        throw Error(POLY_B200_INTERNAL, "IVF work list overflow in a previous search: its results are incomplete");
+    }
 }
 
 // Enqueue enumerate_cells for a batch: probe_keys (nqb x np) ascending.
@@ -303,13 +333,20 @@ void enumerate_cells(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, uint32_t
 // One batch of <= 256 queries; outputs through keys_to_ids.
 void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_b200_ivf_params* p, int64_t* d_ids,
                   float* d_scores, uint32_t* d_counts, cudaStream_t s, uint64_t* d_keys_out = nullptr,
-                  uint32_t* d_kcounts_out = nullptr, const uint64_t* d_probes_in = nullptr) {
+                  uint32_t* d_kcounts_out = nullptr, const uint64_t* d_probes_in = nullptr, uint64_t* d_surv = nullptr,
+                  uint64_t* d_hash = nullptr) {
     const uint32_t k = p->k;
     const uint32_t np = std::min(p->nprobe, iv->nlist);
     int strategy = p->strategy;
     if (strategy == pb::DUAL && p->tau >= iv->code_bits()) strategy = pb::ADC;  // SPEC.md:388 boundary
     CK(cudaMemsetAsync(iv->ctrl, 0, (IVF_NQB + 32) * 4, s));
+    CK(cudaMemsetAsync(iv->ovq, 0, IVF_NQB * 4, s));
     CK(cudaMemsetAsync(iv->thr, 0xFF, IVF_NQB * 8, s));
+    const bool perq = d_surv || d_hash;
+    if (perq) {
+        CK(cudaMemsetAsync(iv->surv_q, 0, IVF_NQB * 8, s));
+        CK(cudaMemsetAsync(iv->hash_q, 0, IVF_NQB * 8, s));
+    }
     if (d_probes_in)  // probes computed elsewhere (the coarse quantization split by query over ranks)
         CK(cudaMemcpyAsync(iv->probe_keys, d_probes_in, (size_t)nqb * np * 8, cudaMemcpyDeviceToDevice, s));
     else
@@ -355,24 +392,34 @@ void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_
     a.cand = iv->cand;
     a.cap = iv->cand_cap;
     a.ccount = iv->ctrl;
-    a.overflow = iv->ctrl + IVF_NQB;
+    a.ovq = iv->ovq;
     a.surv_total = iv->surv_total;
+    // survivors are defined for the dual strategy (other strategies report 0)
+    a.surv_q = perq && p->strategy == pb::DUAL ? iv->surv_q : nullptr;
+    a.hash_q = perq && p->strategy == pb::DUAL ? iv->hash_q : nullptr;
     // two rounds over the work lists built by the probe-count kernel: round 1 scans each
     // query's leading probes holding >= IVF_R1_CODES codes (at most IVF_R1_MAX probes) in
     // 1024-row chunks; its exact k-th key (K3) bounds round 2, the remaining probes
-    for (uint32_t round = 0; round < 2; ++round) {
-        if (round == 1 && np <= 1) break;  // one probe: round 1 saw everything
+    const uint32_t rounds = np <= 1 ? 1 : 2;  // one probe: round 1 sees everything
+    for (uint32_t round = 0; round < rounds; ++round) {
         if (round == 1 && side) CK(cudaStreamWaitEvent(s, iv->ev_join, 0));
         a.items = iv->items[round];
         a.nitems = w.nitems + round;
         a.items_cap = w.cap[round];
         a.work = iv->ctrl + IVF_NQB + 1 + round;
         pb::launch_ivf_scan(a, strategy, iv->m, iv->num_sms, s);
+        // a query whose list overflowed (in either round) is re-ranked exactly over all its
+        // visited probes (no-op for the others)
+        if (round + 1 == rounds) pb::launch_ivf_rescue(a, strategy, iv->m, iv->np_eff, k, s);
         pb::launch_topk(iv->cand, iv->ctrl, iv->cand_cap, 1, 0, 0, nqb, k, iv->keys, iv->kcounts, s);
         if (round == 0 && np > 1)  // bound round 2; keep only round 1's top-k as candidates
             pb::launch_seed_compact(iv->keys, iv->kcounts, nqb, k, iv->thr, iv->cand, iv->cand_cap, iv->ctrl, s);
     }
     pb::launch_or_flag(iv->sticky_overflow, iv->ctrl + IVF_NQB, s);
+    if (perq) {
+        if (d_surv) CK(cudaMemcpyAsync(d_surv, iv->surv_q, (size_t)nqb * 8, cudaMemcpyDeviceToDevice, s));
+        if (d_hash) CK(cudaMemcpyAsync(d_hash, iv->hash_q, (size_t)nqb * 8, cudaMemcpyDeviceToDevice, s));
+    }
     if (d_keys_out) {  // multi-GPU: the shard's top-k keys for the cross-rank merge
         CK(cudaMemcpyAsync(d_keys_out, iv->keys, (size_t)nqb * k * 8, cudaMemcpyDeviceToDevice, s));
         CK(cudaMemcpyAsync(d_kcounts_out, iv->kcounts, nqb * 4, cudaMemcpyDeviceToDevice, s));
@@ -384,10 +431,14 @@ void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_
 // All batches; returns strategy survivors semantics (0 none, 1 = scanned, 2 counted).
 int device_search(poly_b200_ivf* iv, const float* d_q, uint64_t nq, const poly_b200_ivf_params* p, int64_t* d_ids,
                   float* d_scores, uint32_t* d_counts, cudaStream_t s, uint64_t* d_keys = nullptr,
-                  uint32_t* d_kcounts = nullptr, const uint64_t* d_probes = nullptr) {
+                  uint32_t* d_kcounts = nullptr, const uint64_t* d_probes = nullptr, uint64_t* d_surv = nullptr,
+                  uint64_t* d_hash = nullptr) {
     validate(iv, p);
+    check_pending(iv, false);
     if (nq == 0) return 0;
     if (p->k == 0 || iv->n == 0) {
+        if (d_surv) CK(cudaMemsetAsync(d_surv, 0, nq * 8, s));
+        if (d_hash) CK(cudaMemsetAsync(d_hash, 0, nq * 8, s));
         if (d_kcounts) {
             CK(cudaMemsetAsync(d_kcounts, 0, nq * 4, s));
             if (p->k) CK(cudaMemsetAsync(d_keys, 0xFF, nq * p->k * 8, s));
@@ -405,14 +456,19 @@ int device_search(poly_b200_ivf* iv, const float* d_q, uint64_t nq, const poly_b
     for (uint64_t b0 = 0; b0 < nq; b0 += IVF_NQB) {
         const uint32_t nqb = (uint32_t)std::min<uint64_t>(IVF_NQB, nq - b0);
         const uint64_t* pr = d_probes ? d_probes + b0 * std::min(p->nprobe, iv->nlist) : nullptr;
+        uint64_t* sv = d_surv ? d_surv + b0 : nullptr;
+        uint64_t* hv = d_hash ? d_hash + b0 : nullptr;
         if (d_keys)
             search_batch(iv, d_q + b0 * iv->dim, nqb, p, nullptr, nullptr, nullptr, s, d_keys + b0 * p->k,
-                         d_kcounts + b0, pr);
+                         d_kcounts + b0, pr, sv, hv);
         else
             search_batch(iv, d_q + b0 * iv->dim, nqb, p, d_ids + b0 * p->k, d_scores + b0 * p->k,
-                         d_counts ? d_counts + b0 : nullptr, s, nullptr, nullptr, pr);
+                         d_counts ? d_counts + b0 : nullptr, s, nullptr, nullptr, pr, sv, hv);
         CK(cudaGetLastError());
     }
+    CK(cudaMemcpyAsync(iv->h_overflow, iv->sticky_overflow, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(iv->done_ev, s));
+    iv->pending_check = true;
     if (p->strategy == pb::DUAL) return p->tau >= iv->code_bits() ? 1 : 2;
     return 0;
 }
@@ -451,7 +507,9 @@ void read_stats(poly_b200_ivf* iv, int mode, poly_b200_search_stats* st, cudaStr
         CK(cudaMemcpyAsync(&ovf, iv->sticky_overflow, 4, cudaMemcpyDeviceToHost, s));
     }
     CK(cudaStreamSynchronize(s));
-    require(!ovf, POLY_B200_INTERNAL, "IVF candidate list overflow: results incomplete");
+    iv->pending_check = false;
+    *iv->h_overflow = 0;
+    require(!ovf, POLY_B200_INTERNAL, "IVF work list overflow: results incomplete");
     if (st) {
         st->scanned = h[0];
         st->survivors = mode == 2 ? h[1] : (mode == 1 ? h[0] : 0);
@@ -534,11 +592,14 @@ int poly_b200_ivf_destroy(poly_b200_ivf* iv) {
                             (void*)iv->np_eff, (void*)iv->split, (void*)iv->scanned, (void*)iv->lutp, (void*)iv->qcodes,
                             (void*)iv->cand, (void*)iv->ctrl, (void*)iv->thr, (void*)iv->keys, (void*)iv->kcounts,
                             (void*)iv->surv_total, (void*)iv->scan_total, (void*)iv->sticky_overflow, (void*)iv->d_q,
+                            (void*)iv->ovq, (void*)iv->surv_q, (void*)iv->hash_q,
                             (void*)iv->d_oid, (void*)iv->d_osc, (void*)iv->d_ocnt,
                             (void*)iv->knn_ids, (void*)iv->knn_sc, (void*)iv->knn_cnt, (void*)iv->d_cnorm, (void*)iv->items[0],
                             (void*)iv->items[1]})
                 dfree(p);
             if (iv->cublas) cublasDestroy(iv->cublas);
+            if (iv->h_overflow) cudaFreeHost(iv->h_overflow);
+            if (iv->done_ev) cudaEventDestroy(iv->done_ev);
             iv->idm.release();
             if (iv->stream) cudaStreamDestroy(iv->stream);
             if (iv->side) cudaStreamDestroy(iv->side);
@@ -663,6 +724,28 @@ int poly_b200_ivf_get_lists(poly_b200_ivf* iv, uint64_t* off, uint8_t* codes, in
     });
 }
 
+int poly_b200_ivf_debug_set_list_capacity(poly_b200_ivf* iv, uint32_t cap) {
+    return guard([&] {
+        require(iv != nullptr, POLY_B200_INVALID_ARGUMENT, "null index");
+        std::lock_guard<std::mutex> lk(iv->mu);
+        iv->cap_override = cap;
+    });
+}
+
+int poly_b200_ivf_debug_rescued(poly_b200_ivf* iv, uint32_t* n) {
+    return guard([&] {
+        require(iv && n, POLY_B200_INVALID_ARGUMENT, "null arguments");
+        std::lock_guard<std::mutex> lk(iv->mu);
+        DeviceGuard dg(iv->device);
+        require(iv->ovq != nullptr, POLY_B200_STATE, "no search has run");
+        CK(cudaDeviceSynchronize());
+        std::vector<uint32_t> ovq(IVF_NQB);
+        CK(cudaMemcpy(ovq.data(), iv->ovq, IVF_NQB * 4, cudaMemcpyDeviceToHost));
+        *n = 0;
+        for (uint32_t v : ovq) *n += v != 0;
+    });
+}
+
 int poly_b200_ivf_probes(poly_b200_ivf* iv, const float* queries, uint64_t nq, uint32_t nprobe, uint32_t* cells) {
     return guard([&] {
         require(iv && (nq == 0 || (queries && cells)) && nprobe >= 1 && nprobe <= iv->nlist &&
@@ -690,21 +773,28 @@ int poly_b200_ivf_probes(poly_b200_ivf* iv, const float* queries, uint64_t nq, u
     });
 }
 
-int poly_b200_ivf_search_device(poly_b200_ivf* iv, const float* d_q, uint64_t nq, const poly_b200_ivf_params* p,
-                                int64_t* d_ids, float* d_scores, uint32_t* d_counts, void* stream,
-                                poly_b200_search_stats* stats) {
+int poly_b200_ivf_search_device_ex(poly_b200_ivf* iv, const float* d_q, uint64_t nq, const poly_b200_ivf_params* p,
+                                   int64_t* d_ids, float* d_scores, uint32_t* d_counts, uint64_t* d_surv,
+                                   uint64_t* d_surv_hash, void* stream, poly_b200_search_stats* stats) {
     return guard([&] {
         require(iv != nullptr, POLY_B200_INVALID_ARGUMENT, "null index");
         require(nq == 0 || (d_q && d_ids && d_scores) || (p && p->k == 0), POLY_B200_INVALID_ARGUMENT, "null buffers");
         std::lock_guard<std::mutex> lk(iv->mu);
         DeviceGuard dg(iv->device);
         cudaStream_t s = (cudaStream_t)stream;
-        const int mode = device_search(iv, d_q, nq, p, d_ids, d_scores, d_counts, s);
+        const int mode =
+            device_search(iv, d_q, nq, p, d_ids, d_scores, d_counts, s, nullptr, nullptr, nullptr, d_surv, d_surv_hash);
         if (stats) {
             stats->scanned = stats->survivors = 0;
             if (nq && p->k && iv->n) read_stats(iv, mode, stats, s);
         }
     });
+}
+
+int poly_b200_ivf_search_device(poly_b200_ivf* iv, const float* d_q, uint64_t nq, const poly_b200_ivf_params* p,
+                                int64_t* d_ids, float* d_scores, uint32_t* d_counts, void* stream,
+                                poly_b200_search_stats* stats) {
+    return poly_b200_ivf_search_device_ex(iv, d_q, nq, p, d_ids, d_scores, d_counts, nullptr, nullptr, stream, stats);
 }
 
 int poly_b200_ivf_search_keys_device(poly_b200_ivf* iv, const float* d_q, uint64_t nq, const poly_b200_ivf_params* p,
@@ -754,6 +844,8 @@ int poly_b200_ivf_probe_keys_device(poly_b200_ivf* iv, const float* d_q, uint64_
     return guard([&] {
         require(iv != nullptr, POLY_B200_INVALID_ARGUMENT, "null index");
         require(nprobe >= 1, POLY_B200_INVALID_ARGUMENT, "nprobe must be >= 1");
+        require(std::min(nprobe, iv->nlist) <= (uint32_t)pb::KMAX, POLY_B200_INVALID_ARGUMENT,
+                "min(nprobe, nlist) > 2048 is not supported on the GPU path");
         require(nq == 0 || (d_q && d_probe_keys), POLY_B200_INVALID_ARGUMENT, "null buffers");
         std::lock_guard<std::mutex> lk(iv->mu);
         DeviceGuard dg(iv->device);

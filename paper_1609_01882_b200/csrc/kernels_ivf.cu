@@ -20,7 +20,7 @@
 //   assign_kernel            build: nearest coarse cell by sq_l2 (strict <).
 #include <type_traits>
 
-#include "poly_b200.cuh"
+#include "code_ops.cuh"
 #include "synth.cuh"
 
 namespace pb {
@@ -207,11 +207,7 @@ void launch_coarse_select(const float* q, uint32_t nq, uint32_t dim, const float
     if (nq == 0) return;
     const size_t np_pad = np <= 32 ? 32 : 64;
     const size_t smem = (size_t)K5_T * (np_pad + K5_T) * 8 + (size_t)K5_T * (dim + 1) * 4 + (size_t)K5_T * (K5_D + 1) * 4;
-    static size_t attr = 0;
-    if (attr < smem) {
-        cudaFuncSetAttribute(coarse_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = smem;
-    }
+    set_max_smem((const void*)coarse_select_kernel, smem);
     coarse_select_kernel<<<dim3(slices, (nq + K5_T - 1) / K5_T), 256, smem, s>>>(q, nq, dim, cent, nlist, np, slices,
                                                                                  out_keys, out_counts);
     count_launch();
@@ -469,11 +465,7 @@ void launch_coarse_refine(const float* q, uint32_t nq, uint32_t dim, const float
                           unsigned long long* probe_keys, uint32_t* probe_counts, cudaStream_t s) {
     if (nq == 0) return;
     const size_t smem = (size_t)KR_BUF * 8 + (size_t)dim * 4;
-    static size_t attr = 0;
-    if (attr < smem) {
-        cudaFuncSetAttribute(coarse_refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = smem;
-    }
+    set_max_smem((const void*)coarse_refine_kernel, smem);
     coarse_refine_kernel<<<nq, KR_THREADS, smem, s>>>(q, dim, dots, cnorm, cmax, cent, nlist, np, scratch, probe_keys,
                                                       probe_counts);
     count_launch();
@@ -731,44 +723,6 @@ void launch_ivf_probe_count(const unsigned long long* probe_keys, uint32_t nq, u
 #endif
 constexpr int K6_WARPS = POLY_K6_WARPS;
 
-template <int M> struct IvfCode;
-template <> struct IvfCode<8> { using T = uint2; };
-template <> struct IvfCode<16> { using T = uint4; };
-
-__device__ __forceinline__ uint32_t k6_ham(const uint2& a, const uint2& b) {
-    return __popc(a.x ^ b.x) + __popc(a.y ^ b.y);
-}
-__device__ __forceinline__ uint32_t k6_ham(const uint4& a, const uint4& b) {
-    return __popc(a.x ^ b.x) + __popc(a.y ^ b.y) + __popc(a.z ^ b.z) + __popc(a.w ^ b.w);
-}
-__device__ __forceinline__ uint32_t k6_nz(uint32_t x) {
-    x |= x >> 4;
-    x |= x >> 2;
-    x |= x >> 1;
-    return __popc(x & 0x01010101u);
-}
-__device__ __forceinline__ uint32_t k6_dis(const uint2& a, const uint2& b) { return k6_nz(a.x ^ b.x) + k6_nz(a.y ^ b.y); }
-__device__ __forceinline__ uint32_t k6_dis(const uint4& a, const uint4& b) {
-    return k6_nz(a.x ^ b.x) + k6_nz(a.y ^ b.y) + k6_nz(a.z ^ b.z) + k6_nz(a.w ^ b.w);
-}
-__device__ __forceinline__ uint32_t k6_word(const uint2& c, int w) { return w == 0 ? c.x : c.y; }
-__device__ __forceinline__ uint32_t k6_word(const uint4& c, int w) {
-    return w == 0 ? c.x : (w == 1 ? c.y : (w == 2 ? c.z : c.w));
-}
-// Early-exit form (as K2's adc_s_bounded): the first M/2 terms in sq order; a
-// prefix above the bound's score can only grow (non-negative terms, round-to-
-// nearest partial sums are monotone), so the pair is no candidate: +inf.
-template <int M, class C>
-__device__ __forceinline__ float k6_adc_bounded(const float* L, const C& c, uint32_t bound_bits) {
-    float acc = L[k6_word(c, 0) & 0xFFu];
-#pragma unroll
-    for (int sq = 1; sq < M / 2; ++sq) acc = __fadd_rn(acc, L[sq * KSUB + ((k6_word(c, sq >> 2) >> (8 * (sq & 3))) & 0xFFu)]);
-    if (__float_as_uint(acc) > bound_bits) return __int_as_float(0x7f800000);
-#pragma unroll
-    for (int sq = M / 2; sq < M; ++sq) acc = __fadd_rn(acc, L[sq * KSUB + ((k6_word(c, sq >> 2) >> (8 * (sq & 3))) & 0xFFu)]);
-    return acc;
-}
-
 // Survivor-queue accesses through 32-bit shared-window addresses (the generic
 // pointers made ptxas rebuild the window base per access at the 32-register cap).
 __device__ __forceinline__ void k6_sts(uint32_t a, const uint2& c) {
@@ -794,12 +748,12 @@ __device__ __forceinline__ void k6_lds(uint32_t a, uint32_t& v) {
 // dynamically; the K6_WARPS warps of a CTA split the chunk and share the item's LUT
 // in shared memory.  Each warp compacts its filter survivors with a ballot into
 // its own queue and drains 32 at a time (ADC with early exit, candidate test).
-template <int M, int STRAT>
+template <int M, int STRAT, bool PERQ>
 #ifndef POLY_K6_MINB
 #define POLY_K6_MINB 8  // m = 8: 64 warps per SM, <= 32 registers (m = 16: 40 warps)
 #endif
 __global__ void __launch_bounds__(K6_WARPS * 32, (M == 8 ? POLY_K6_MINB : 5) * (8 / K6_WARPS)) ivf_scan_kernel(const IvfScanArgs a) {
-    using C = typename IvfCode<M>::T;
+    using C = typename CodeT<M>::T;
     extern __shared__ __align__(16) uint8_t k6_smem[];
     float* L = reinterpret_cast<float*>(k6_smem);  // M x 256 floats
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -834,7 +788,7 @@ __global__ void __launch_bounds__(K6_WARPS * 32, (M == 8 ? POLY_K6_MINB : 5) * (
                 if (key < thr) {
                     const uint32_t slot = atomicAdd(&a.ccount[qi], 1u);
                     if (slot < a.cap) a.cand[(size_t)qi * a.cap + slot] = key;
-                    else atomicOr(a.overflow, 1u);
+                    else a.ovq[qi] = 1u;  // list full: the rescue scan re-ranks this query exactly
                 }
             }
         };
@@ -845,7 +799,7 @@ __global__ void __launch_bounds__(K6_WARPS * 32, (M == 8 ? POLY_K6_MINB : 5) * (
                 uint32_t pp;
                 k6_lds(qcs + lane * (uint32_t)sizeof(C), cc);
                 k6_lds(qps + 4u * lane, pp);
-                candidate(k6_adc_bounded<M>(L, cc, (uint32_t)(thr >> 32)), pp);
+                candidate(adc_bounded<M>(L, cc, (uint32_t)(thr >> 32)), pp);
             }
             __syncwarp();
         };
@@ -866,7 +820,13 @@ __global__ void __launch_bounds__(K6_WARPS * 32, (M == 8 ? POLY_K6_MINB : 5) * (
             for (int u = 0; u < 4; ++u) {
                 const uint32_t pos = pos0 + r0 + u * 32 + lane;
                 if constexpr (STRAT == DUAL) {
-                    const bool pass = in[u] && k6_ham(c[u], qc) <= tau;
+                    const bool pass = in[u] && ham(c[u], qc) <= tau;
+                    if constexpr (PERQ) {  // stats mode: per-query survivor count and id hash
+                        if (pass) {
+                            atomicAdd(a.surv_q + qi, 1ull);
+                            atomicAdd(a.hash_q + qi, (unsigned long long)mix64(__ldg(a.low + pos)));
+                        }
+                    }
                     const uint32_t bal = __ballot_sync(0xffffffffu, pass);
                     if (bal) {
                         if (pass) {
@@ -891,10 +851,14 @@ __global__ void __launch_bounds__(K6_WARPS * 32, (M == 8 ? POLY_K6_MINB : 5) * (
                         }
                     }
                 } else if (in[u]) {
+                    if constexpr (PERQ && STRAT == ADC) {  // dual at tau = code_bits: every code survives
+                        atomicAdd(a.surv_q + qi, 1ull);
+                        atomicAdd(a.hash_q + qi, (unsigned long long)mix64(__ldg(a.low + pos)));
+                    }
                     float score;
-                    if constexpr (STRAT == ADC) score = k6_adc_bounded<M>(L, c[u], (uint32_t)(thr >> 32));
-                    else if constexpr (STRAT == BINARY) score = (float)k6_ham(c[u], qc);
-                    else score = (float)k6_dis(c[u], qc);
+                    if constexpr (STRAT == ADC) score = adc_bounded<M>(L, c[u], (uint32_t)(thr >> 32));
+                    else if constexpr (STRAT == BINARY) score = (float)ham(c[u], qc);
+                    else score = (float)disidx(c[u], qc);
                     candidate(score, pos);
                 }
             }
@@ -907,14 +871,15 @@ __global__ void __launch_bounds__(K6_WARPS * 32, (M == 8 ? POLY_K6_MINB : 5) * (
 
 template <int M, int STRAT>
 static void launch_ivf_one(const IvfScanArgs& a, unsigned grid, cudaStream_t s) {
-    using C = typename IvfCode<M>::T;
+    using C = typename CodeT<M>::T;
     const size_t smem = (size_t)M * KSUB * 4 + (size_t)K6_WARPS * 64 * (sizeof(C) + 4);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(ivf_scan_kernel<M, STRAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
+    if (a.surv_q) {
+        set_max_smem((const void*)ivf_scan_kernel<M, STRAT, true>, smem);
+        ivf_scan_kernel<M, STRAT, true><<<grid, K6_WARPS * 32, smem, s>>>(a);
+    } else {
+        set_max_smem((const void*)ivf_scan_kernel<M, STRAT, false>, smem);
+        ivf_scan_kernel<M, STRAT, false><<<grid, K6_WARPS * 32, smem, s>>>(a);
     }
-    ivf_scan_kernel<M, STRAT><<<grid, K6_WARPS * 32, smem, s>>>(a);
 }
 
 template <int M>

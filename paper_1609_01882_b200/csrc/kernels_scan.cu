@@ -30,49 +30,9 @@
 // and atomicMin's it into thr[q].  thr[] starts from the exact k-th key of
 // strided warm-up samples (capi.cu), so these selects are rare.  Every final
 // top-k member is in the list; K3 takes the exact top-k.
-#include "poly_b200.cuh"
+#include "code_ops.cuh"
 
 namespace pb {
-
-template <int M> struct CodeT;
-template <> struct CodeT<8> { using T = uint2; };
-template <> struct CodeT<16> { using T = uint4; };
-
-__device__ __forceinline__ uint32_t ham(const uint2& a, const uint2& b) {
-    return __popc(a.x ^ b.x) + __popc(a.y ^ b.y);
-}
-__device__ __forceinline__ uint32_t ham(const uint4& a, const uint4& b) {
-    return __popc(a.x ^ b.x) + __popc(a.y ^ b.y) + __popc(a.z ^ b.z) + __popc(a.w ^ b.w);
-}
-// number of differing bytes (disidx_fields, flat_index.hpp:30-37, dbits = 8)
-__device__ __forceinline__ uint32_t nz_bytes(uint32_t x) {
-    x |= x >> 4;
-    x |= x >> 2;
-    x |= x >> 1;
-    return __popc(x & 0x01010101u);
-}
-__device__ __forceinline__ uint32_t disidx(const uint2& a, const uint2& b) {
-    return nz_bytes(a.x ^ b.x) + nz_bytes(a.y ^ b.y);
-}
-__device__ __forceinline__ uint32_t disidx(const uint4& a, const uint4& b) {
-    return nz_bytes(a.x ^ b.x) + nz_bytes(a.y ^ b.y) + nz_bytes(a.z ^ b.z) + nz_bytes(a.w ^ b.w);
-}
-__device__ __forceinline__ uint32_t word(const uint2& c, int w) { return w == 0 ? c.x : c.y; }
-__device__ __forceinline__ uint32_t word(const uint4& c, int w) {
-    return w == 0 ? c.x : (w == 1 ? c.y : (w == 2 ? c.z : c.w));
-}
-
-// ADC through the stored-field LUT of one query (M rows of 256 floats), in sq order.
-template <int M, class C>
-__device__ __forceinline__ float adc(const float* __restrict__ L, const C& c) {
-    float acc = L[word(c, 0) & 0xFFu];  // 0.0f + x == x for x >= +0
-#pragma unroll
-    for (int sq = 1; sq < M; ++sq) {
-        const uint32_t f = (word(c, sq >> 2) >> (8 * (sq & 3))) & 0xFFu;
-        acc = __fadd_rn(acc, L[sq * KSUB + f]);
-    }
-    return acc;
-}
 
 __device__ __forceinline__ uint32_t key_low(const ScanArgs& a, uint32_t pos) {
     return a.id_mode == ID_ARITH ? a.id0 + pos : __ldg(a.id32 + pos);
@@ -172,8 +132,8 @@ constexpr uint32_t IDESC_I8_M128_N16 = (2u << 4) | (1u << 7) | (1u << 10) | ((16
 __device__ __forceinline__ void append_candidate(const ScanArgs& a, uint32_t qg, unsigned long long key, uint32_t bs,
                                                  uint32_t* nreq_s, uint32_t* req_s) {
     const uint32_t slot = atomicAdd(&a.ccount[qg], 1u);
-    if (slot >= a.cap) {
-        atomicOr(a.overflow, 1u);
+    if (slot >= a.cap) {  // list full: the rescue scan (kernels_rescue.cu) re-ranks this query exactly
+        a.ovq[qg] = 1u;
         return;
     }
     a.cand[(size_t)qg * a.cap + slot] = key;
@@ -296,6 +256,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
     __shared__ unsigned long long thr_s[Q];
     __shared__ C qc_s[Q];
     __shared__ uint32_t surv_s[Q];
+    __shared__ unsigned long long hash_s[PERQ ? Q : 1];
     __shared__ uint32_t unit_s, nreq_s, group_s;
     __shared__ uint32_t req_s[MAXREQ];
     __shared__ uint32_t sel_hist[256];
@@ -463,6 +424,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
         if (threadIdx.x < Q) {
             thr_s[threadIdx.x] = threadIdx.x < nqh ? __ldcg(a.thr + q0 + threadIdx.x) : 0ull;
             surv_s[threadIdx.x] = 0;
+            if (PERQ) hash_s[threadIdx.x] = 0;
         }
         __syncthreads();
         if (threadIdx.x == 0) group_s = g;
@@ -537,6 +499,8 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
                     C code;
                     lds_code(T + li * (uint32_t)M, code);
                     const unsigned long long thr = thr_s[q];
+                    if constexpr (PERQ)  // every queued entry is a filter survivor
+                        atomicAdd(&hash_s[q], (unsigned long long)mix64(key_low(a, (uint32_t)(tfirst + li))));
                     const float score = adc_s_bounded<M>(lut_base + 4u * q * SM::LS, code, (uint32_t)(thr >> 32));
                     try_candidate(a, q0 + q, score, (uint32_t)(tfirst + li), thr, bs, &nreq_s, req_s);
                 }
@@ -751,8 +715,10 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
         if (producer) serve_selects();  // blocks completed during the unit's last tiles
         // unit boundary: survivor stats flush
         // per-query counts -> surv[q]; totals -> surv[0] (the batch total)
-        if (STRAT == DUAL && threadIdx.x < (PERQ ? nqh : 1u) && surv_s[threadIdx.x])
+        if (STRAT == DUAL && threadIdx.x < (PERQ ? nqh : 1u) && surv_s[threadIdx.x]) {
             atomicAdd(a.surv + (PERQ ? q0 + threadIdx.x : 0u), (unsigned long long)surv_s[threadIdx.x]);
+            if (PERQ) atomicAdd(a.surv_hash + q0 + threadIdx.x, hash_s[threadIdx.x]);
+        }
         __syncthreads();
     }
     if (TCF) {
@@ -870,11 +836,7 @@ template <int M, int STRAT>
 static void launch_seed_m(const ScanArgs& a, uint32_t nq, uint32_t seed_blocks, cudaStream_t s) {
     const size_t smem = (size_t)M * KSUB * 4 + SEED_KEYS * 8;
     auto kfn = seed_sample_kernel<M, STRAT>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+    set_max_smem((const void*)kfn, smem);
     kfn<<<nq, SEED_THREADS, smem, s>>>(a, seed_blocks);
     count_launch();
 }
@@ -901,11 +863,7 @@ static void launch_one(const ScanArgs& a, int num_sms, cudaStream_t s) {
     constexpr bool USE_LUT = (STRAT == DUAL || STRAT == ADC);
     const size_t smem = USE_LUT ? SM::TOTAL : SM::TOTAL - SM::LUT_BYTES;
     auto kfn = scan_kernel<M, Q, W, STRAT, PERQ>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+    set_max_smem((const void*)kfn, smem);
     const unsigned grid = (unsigned)((uint64_t)num_sms < (uint64_t)a.units ? (uint64_t)num_sms : (uint64_t)a.units);
     kfn<<<grid, (W + 1) * 32, smem, s>>>(a);
     count_launch();

@@ -207,11 +207,7 @@ static void launch_topk_cfg(const unsigned long long* cand, const uint32_t* ccou
                             uint64_t part_stride, uint64_t count_stride, uint32_t nq, uint32_t k,
                             unsigned long long* out_keys, uint32_t* out_counts, cudaStream_t s) {
     const size_t smem = (SK + SEL) * sizeof(unsigned long long) + TK_BUCKETS * sizeof(uint32_t);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(topk_kernel<SK, SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+    set_max_smem((const void*)topk_kernel<SK, SEL>, smem);
     topk_kernel<SK, SEL><<<nq, TK_THREADS, smem, s>>>(cand, ccount, cap, parts, part_stride, count_stride, nq, k,
                                                       out_keys, out_counts);
 }
@@ -264,25 +260,6 @@ namespace pb {
 __global__ void or_flag_kernel(uint32_t* dst, const uint32_t* src) { *dst |= *src; }
 void launch_or_flag(uint32_t* dst, const uint32_t* src, cudaStream_t s) {
     or_flag_kernel<<<1, 1, 0, s>>>(dst, src);
-    count_launch();
-}
-}  // namespace pb
-
-namespace pb {
-// thr[q] = min(thr[q], k-th key of the warm-up sample + 1) -- +1 so that key
-// itself is appended again by the full scan; unchanged when the sample held
-// fewer than k candidates.
-__global__ void seed_thr_kernel(const unsigned long long* keys, const uint32_t* counts, uint32_t nq, uint32_t k,
-                                unsigned long long* thr) {
-    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q < nq && counts[q] >= k) {
-        const unsigned long long t = keys[(size_t)q * k + k - 1] + 1;
-        if (t < thr[q]) thr[q] = t;
-    }
-}
-void launch_seed_thr(const unsigned long long* keys, const uint32_t* counts, uint32_t nq, uint32_t k,
-                     unsigned long long* thr, cudaStream_t s) {
-    seed_thr_kernel<<<(nq + 127) / 128, 128, 0, s>>>(keys, counts, nq, k, thr);
     count_launch();
 }
 }  // namespace pb

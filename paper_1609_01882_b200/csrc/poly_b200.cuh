@@ -28,15 +28,6 @@ constexpr int DSUB = 16;               // every configuration: 128/8 and 256/16
 #ifndef POLY_SEL_KF  // select block >= KF * k slots
 #define POLY_SEL_KF 4
 #endif
-#ifndef POLY_WARM_LEVELS  // at most this many geometric warm-up samples before the full scan
-#define POLY_WARM_LEVELS 0
-#endif
-#ifndef POLY_WARM_FIRST  // tiles in the first warm-up sample (x8 per further level)
-#define POLY_WARM_FIRST 128
-#endif
-#ifndef POLY_WARM_SEL
-#define POLY_WARM_SEL 0
-#endif
 #ifndef POLY_SEED_BLOCKS  // K2s seed sample: runs of 256 codes (0 = no seed kernel)
 #define POLY_SEED_BLOCKS 128
 #endif
@@ -89,7 +80,8 @@ struct ScanArgs {
     uint32_t* bdone;             // nqb x (cap / BS) completion counters
     unsigned long long* thr;     // nqb running upper bounds of the k-th key
     unsigned long long* surv;    // per-query survivor counts (per_query_stats) or [0] = batch total
-    uint32_t* overflow;          // set when a candidate did not fit
+    unsigned long long* surv_hash;  // per_query_stats: per-query sum of mix64(key low word) over survivors
+    uint32_t* ovq;               // per query: set when a candidate did not fit (the rescue scan re-ranks it)
     uint32_t* work;              // dynamic work-unit counter
     uint32_t units, ngroups, tiles_per_chunk;
     // group-affine schedule (affine = 1): work[g] counts the chunks handed out of
@@ -113,9 +105,11 @@ struct IvfScanArgs {
     unsigned long long* cand;             // nq x cap candidate keys
     uint32_t cap;
     uint32_t* ccount;
-    uint32_t* overflow;
+    uint32_t* ovq;                        // per query: a candidate did not fit (rescued before the final K3)
     uint32_t* work;
     unsigned long long* surv_total;
+    unsigned long long* surv_q;           // per-query survivor counts and hashes (stats mode; else null)
+    unsigned long long* hash_q;
     const uint4* items;      // work items (query, probe, row0, row1): rows [row0, row1) of the
     const uint32_t* nitems;  // probed cell's list; built by the probe-count kernel
     uint32_t items_cap;
@@ -257,6 +251,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// splitmix64 finaliser: survivor-set hash sum_i mix64(id_i) (order-independent;
+// the oracle computes the same, oracle/polyoracle.c po_mix64)
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -298,8 +301,6 @@ void launch_hamming_hist(const uint8_t* codes, uint64_t n, uint32_t cb, const ui
 // with_assignments: relabel fields through a per-sub-quantizer byte map.
 void launch_relabel(uint8_t* codes, uint64_t n, uint32_t m, const uint8_t* maps, cudaStream_t s);
 
-void launch_seed_thr(const unsigned long long* keys, const uint32_t* counts, uint32_t nq, uint32_t k,
-                     unsigned long long* thr, cudaStream_t s);
 void launch_seed_compact(const unsigned long long* keys, const uint32_t* counts, uint32_t nq, uint32_t k,
                          unsigned long long* thr, unsigned long long* cand, uint32_t cap, uint32_t* ccount,
                          cudaStream_t s);
@@ -334,5 +335,13 @@ void launch_cell_scatter(const uint32_t* assign, uint64_t n, uint32_t cb, const 
 void launch_key_low(uint64_t n, int mode, uint32_t id0, const uint32_t* id32, uint32_t* out, cudaStream_t s);
 void launch_or_flag(uint32_t* dst, const uint32_t* src, cudaStream_t s);
 void count_launch();
+// cudaFuncAttributeMaxDynamicSharedMemorySize for `fn` on the current device (the
+// attribute is per device context: tracked per (kernel, device), thread-safe)
+void set_max_smem(const void* fn, size_t bytes);
+// K2x / K6x: exact re-rank of the queries whose candidate list overflowed (ovq[q]):
+// streaming top-k over the query's codes, written back as its candidate list
+void launch_rescue(const ScanArgs& a, int strategy, uint32_t m, uint32_t* rcount, int num_sms, cudaStream_t s);
+void launch_ivf_rescue(const IvfScanArgs& a, int strategy, uint32_t m, const uint32_t* np_eff, uint32_t k,
+                       cudaStream_t s);
 
 }  // namespace pb

@@ -8,14 +8,9 @@
 #pragma once
 #include <cstdint>
 
-namespace pb {
+#include "poly_b200.cuh"  // mix64
 
-__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
-    z += 0x9E3779B97F4A7C15ull;
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-    return z ^ (z >> 31);
-}
+namespace pb {
 
 __host__ __device__ __forceinline__ uint64_t row_key(uint64_t seed, uint32_t stream, uint64_t row) {
     const uint64_t base = mix64(seed + 0x632BE59BD9B4E019ull * (uint64_t)(stream + 1));

@@ -24,15 +24,17 @@ def shard_range(n_total: int, world: int, rank: int):
 
 
 class FlatIndexEngine:
-    """GPU engine over one rank's FlatIndex shard (device tensors, caller's stream)."""
+    """GPU engine over one rank's FlatIndex shard.  Every call is enqueued on torch's
+    current stream, the stream the all-gathers and the caching allocator use too, so
+    the engine's kernels, the collectives and buffer reuse are ordered without extra
+    events."""
 
-    def __init__(self, index, stream=None):
+    def __init__(self, index):
         self.index = index
-        self.stream = stream
 
-    def _sptr(self):
-        s = self.stream if self.stream is not None else torch.cuda.current_stream()
-        return s.cuda_stream
+    @staticmethod
+    def _sptr():
+        return torch.cuda.current_stream().cuda_stream
 
     def search_keys(self, queries, params, keys, counts):
         self.index.search_keys_device(queries, params, keys, counts, None, stream=self._sptr())
@@ -71,8 +73,8 @@ class IVFIndexEngine(FlatIndexEngine):
     the probes of its query slice and the probe keys are all-gathered, instead of
     every rank enumerating every query."""
 
-    def __init__(self, index, stream=None, stats=None, split_coarse=False, group=None):
-        super().__init__(index, stream)
+    def __init__(self, index, stats=None, split_coarse=False, group=None):
+        super().__init__(index)
         self.stats = stats
         self.split_coarse = split_coarse
         self.group = group
@@ -89,6 +91,12 @@ class IVFIndexEngine(FlatIndexEngine):
         return gather_query_slices(compute, queries, self.group)
 
     def search_keys(self, queries, params, keys, counts):
+        world = dist.get_world_size(self.group) if dist.is_initialized() else 1
+        if int(getattr(params, "cap", 0)) and world > 1:
+            # the cap cuts a query's probe list where the codes scanned reach it; each rank
+            # only sees its own slice of every list, so the cut would differ per rank
+            from .flat_index import Errc, PolyError
+            raise PolyError(Errc.invalid_argument, "CoarseParams.cap > 0 is not supported with sharded lists")
         probes = self.probe_keys(queries, params.nprobe) if self.split_coarse else None
         self.index.search_keys_device(queries, params, keys, counts, stream=self._sptr(), stats=self.stats,
                                       probes=probes)

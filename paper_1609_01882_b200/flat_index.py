@@ -209,16 +209,18 @@ class FlatIndex:
         return [Neighbor(int(ids[0, i]), float(scores[0, i])) for i in range(int(counts[0]))]
 
     def search_batch_device(self, d_queries, params: SearchParams, d_ids, d_scores, d_counts=None, d_survivors=None,
-                            stream=0, stats: SearchStats | None = None):
+                            stream=0, stats: SearchStats | None = None, d_survivor_hash=None):
         """Device-resident variant: arguments are torch CUDA tensors (or raw pointers).
-        ``d_survivors`` (per-query counts) selects the per-query-stats scan variant;
+        ``d_survivors`` (per-query counts) / ``d_survivor_hash`` (per-query sum of
+        mix64(id) over the filter survivors) select the per-query-stats scan variant;
         ``stats`` (totals) synchronises the stream."""
         ptr = lambda t: None if t is None else (t if isinstance(t, int) else t.data_ptr())  # noqa: E731
         nq = d_queries.shape[0]
         st = SearchStatsC()
-        _check(lib.poly_b200_search_batch_device(self._h, ptr(d_queries), nq, C.byref(params.c()), ptr(d_ids),
-                                                 ptr(d_scores), ptr(d_counts), ptr(d_survivors), C.c_void_p(stream),
-                                                 C.byref(st) if stats is not None else None))
+        _check(lib.poly_b200_search_batch_device_ex(self._h, ptr(d_queries), nq, C.byref(params.c()), ptr(d_ids),
+                                                    ptr(d_scores), ptr(d_counts), ptr(d_survivors),
+                                                    ptr(d_survivor_hash), C.c_void_p(stream),
+                                                    C.byref(st) if stats is not None else None))
         if stats is not None:
             stats.scanned += st.scanned
             stats.survivors += st.survivors
@@ -232,6 +234,15 @@ class FlatIndex:
         ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731
         _check(lib.poly_b200_merge_keys_device(self._h, ptr(d_keys), ptr(d_counts), parts, nq, k, ptr(d_ids),
                                                ptr(d_scores), ptr(d_counts_out), C.c_void_p(stream)))
+
+    # ---- test hooks: candidate-list overflow and its exact rescue (kernels_rescue.cu)
+    def debug_set_list_capacity(self, cap: int):
+        _check(lib.poly_b200_debug_set_list_capacity(self._h, int(cap)))
+
+    def debug_rescued(self) -> int:
+        n = C.c_uint32(0)
+        _check(lib.poly_b200_debug_rescued(self._h, C.byref(n)))
+        return int(n.value)
 
     # ---- K2 timing hook (bench.py)
     def profile_enable(self, on: bool = True):

@@ -108,15 +108,26 @@ class IVFIndex:
         return ids, scores, counts
 
     def search_device(self, d_queries, params: CoarseParams, d_ids, d_scores, d_counts=None, stream=0,
-                      stats: SearchStats | None = None):
+                      stats: SearchStats | None = None, d_survivors=None, d_survivor_hash=None):
+        """Device buffers (torch CUDA tensors).  ``d_survivors`` / ``d_survivor_hash``:
+        per-query survivor counts and sum of mix64(id) over the survivors (stats mode)."""
         ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731
         st = SearchStatsC()
-        _check(lib.poly_b200_ivf_search_device(self._h, ptr(d_queries), d_queries.shape[0], C.byref(params.c()),
-                                               ptr(d_ids), ptr(d_scores), ptr(d_counts), C.c_void_p(stream),
-                                               C.byref(st) if stats is not None else None))
+        _check(lib.poly_b200_ivf_search_device_ex(self._h, ptr(d_queries), d_queries.shape[0], C.byref(params.c()),
+                                                  ptr(d_ids), ptr(d_scores), ptr(d_counts), ptr(d_survivors),
+                                                  ptr(d_survivor_hash), C.c_void_p(stream),
+                                                  C.byref(st) if stats is not None else None))
         if stats is not None:
             stats.scanned += st.scanned
             stats.survivors += st.survivors
+
+    def debug_set_list_capacity(self, cap: int):
+        _check(lib.poly_b200_ivf_debug_set_list_capacity(self._h, int(cap)))
+
+    def debug_rescued(self) -> int:
+        n = C.c_uint32(0)
+        _check(lib.poly_b200_ivf_debug_rescued(self._h, C.byref(n)))
+        return int(n.value)
 
     def search_keys_device(self, d_queries, params: CoarseParams, d_keys, d_counts, stream=0,
                            stats: SearchStats | None = None, probes=None):

@@ -404,10 +404,23 @@ def test_randomized_ivf_against_oracle(pb, gi, seed):
         lists, _ = oracle.ivf_build(pq, base, coarse, ids=ids)
     else:
         lists = oracle.IVFLists(np.zeros(nlist + 1, np.uint64), np.zeros((0, 8), np.uint8), np.zeros(0, np.int64))
-    oi, osc, oc, osv, oscan, opr = oracle.ivf_search(pq, coarse, lists, queries, k, nprobe, tau=tau,
-                                                     strategy=strategy, cap=cap, threads=16)
+    oi, osc, oc, osv, oscan, opr, osh = oracle.ivf_search(pq, coarse, lists, queries, k, nprobe, tau=tau,
+                                                          strategy=strategy, cap=cap, threads=16, return_hash=True)
     st = pb.SearchStats()
     gi_, gsc, gc = ix.search(queries, pb.CoarseParams(pb.strategy_from_string(strategy), k, tau, nprobe, cap), st)
+    if n and strategy == "dual":  # per-query survivor sets (count + id hash) through the device API
+        import torch
+        dq = torch.from_numpy(queries).cuda()
+        d = [torch.empty((nq, k), dtype=torch.int64, device="cuda"), torch.empty((nq, k), dtype=torch.float32,
+                                                                                 device="cuda")]
+        sv = torch.empty(nq, dtype=torch.int64, device="cuda")
+        sh = torch.empty(nq, dtype=torch.int64, device="cuda")
+        ix.search_device(dq, pb.CoarseParams(pb.Strategy.dual, k, tau, nprobe, cap), d[0], d[1],
+                         stream=torch.cuda.current_stream().cuda_stream, d_survivors=sv, d_survivor_hash=sh)
+        torch.cuda.synchronize()
+        assert np.array_equal(sv.cpu().numpy().view(np.uint64), osv), (nlist, n, nq, nprobe, k, tau, cap)
+        assert np.array_equal(sh.cpu().numpy().view(np.uint64), osh), (nlist, n, nq, nprobe, k, tau, cap)
+        assert np.array_equal(d[0].cpu().numpy(), oi)
     ctx = (nlist, n, nq, nprobe, k, strategy, tau, cap)
     assert np.array_equal(ix.probes(queries, nprobe), opr), ctx
     assert np.array_equal(gi_, oi), ctx

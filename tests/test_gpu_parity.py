@@ -386,11 +386,23 @@ def test_full_config1_size(pb, pq8):
     sub = np.array([0, 1, 37, 101, 128, 199, 254, 255])
     st = pb.SearchStats()
     ids_s, sc_s, cnt_s = ix.search_batch(queries[sub], pb.SearchParams(pb.Strategy.dual, k, tau), st)
-    oi, osc, oc, osv, _ = oracle.search(pq8, codes, queries[sub], k, tau=tau, threads=_os.cpu_count() or 8)
+    oi, osc, oc, osv, osh = oracle.search(pq8, codes, queries[sub], k, tau=tau, threads=_os.cpu_count() or 8)
     assert _same(ids_s, oi) and _same(ids[sub], oi)
     assert _same(_bits(sc_s), _bits(osc)) and _same(_bits(sc[sub]), _bits(osc))
     assert _same(cnt_s, oc) and _same(cnt[sub], oc)
     assert st.survivors == int(osv.sum())
+    # survivor sets of the 8 queries over all 1e8 codes: per-query count and id hash
+    import torch
+    dq = torch.from_numpy(queries[sub]).cuda()
+    did = torch.empty((len(sub), k), dtype=torch.int64, device="cuda")
+    dsc = torch.empty((len(sub), k), dtype=torch.float32, device="cuda")
+    sv = torch.empty(len(sub), dtype=torch.int64, device="cuda")
+    sh = torch.empty(len(sub), dtype=torch.int64, device="cuda")
+    ix.search_batch_device(dq, pb.SearchParams(pb.Strategy.dual, k, tau), did, dsc, None, sv,
+                           stream=torch.cuda.current_stream().cuda_stream, d_survivor_hash=sh)
+    torch.cuda.synchronize()
+    assert _same(sv.cpu().numpy().view(np.uint64), osv)
+    assert _same(sh.cpu().numpy().view(np.uint64), osh)
     # every returned neighbour of every query
     lutp, qc = pb.flat_index.debug_lut(ix, queries)
     assert (cnt == k).all()  # 1e8 codes: every query has >= k survivors
