@@ -265,6 +265,16 @@ int poly_b200_ivf_search_keys_probes_device(poly_b200_ivf* ivf, const float* d_q
                                             uint64_t* d_keys, uint32_t* d_counts, void* stream,
                                             poly_b200_search_stats* stats);
 
+/* The lists of selected cells only, CSR in the order of `cells`: off (ncells + 1),
+ * codes (off[ncells] x code_bytes), ids; codes / ids may be NULL. */
+int poly_b200_ivf_get_cells(poly_b200_ivf* ivf, const uint32_t* cells, uint32_t ncells, uint64_t* off, uint8_t* codes,
+                            int64_t* ids);
+
+/* Timing hook for bench.py (as poly_b200_profile_*): CUDA events around every K6
+ * list-scan launch while enabled; read returns the summed ms and the launch count. */
+int poly_b200_ivf_profile_enable(poly_b200_ivf* ivf, int enable);
+int poly_b200_ivf_profile_read(poly_b200_ivf* ivf, double* scan_ms, uint64_t* scan_launches);
+
 int poly_b200_ivf_debug_set_list_capacity(poly_b200_ivf* ivf, uint32_t cap);
 int poly_b200_ivf_debug_rescued(poly_b200_ivf* ivf, uint32_t* n_rescued);
 

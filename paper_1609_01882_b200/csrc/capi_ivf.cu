@@ -12,7 +12,6 @@
 
 #include "../../include/poly_b200.h"
 #include "host_common.h"
-#include <cublas_v2.h>
 #include "poly_b200.cuh"
 
 using namespace pbh;
@@ -49,8 +48,10 @@ struct poly_b200_ivf {
     uint64_t max_list = 0;
 
     // search scratch
-    unsigned long long* ckeys = nullptr;  // IVF_NQB x max(nlist, 64 slices x 64)
-    uint32_t* nl_counts = nullptr;         // K3 counts: nlist per query, or per (slice, query)
+    unsigned long long* ckeys = nullptr;  // K5 (nprobe > 1024): IVF_NQB x nlist exact keys (lazy)
+    uint32_t* nl_counts = nullptr;         // K3 counts of K5: nlist per query
+    float4* grp = nullptr;                 // K5t: per (group of 128 cells, query) kept values
+    uint32_t* rank_scratch = nullptr;      // K5q: per-query candidate cells (IVF_NQB x nlist)
     unsigned long long* probe_keys = nullptr;
     uint32_t* probe_counts = nullptr;
     uint32_t* np_eff = nullptr;
@@ -93,10 +94,16 @@ struct poly_b200_ivf {
     uint64_t knn_rows = 0;
     uint32_t knn_k1 = 0;
 
-    // K5r (TF32 dots + exact re-rank): centroid norms, an upper bound of |c|, cuBLAS handle
+    // K5t/K5q (tensor-core coarse quantization): the centroids packed into 32 KB stage
+    // images, |c|^2 per cell (+inf past nlist), an upper bound of |c|
+    float* d_cpacked = nullptr;
     float* d_cnorm = nullptr;
     float cmax = 0.0f;
-    cublasHandle_t cublas = nullptr;
+
+    // K6 timing (bench.py): CUDA events around every list-scan launch on its stream
+    bool profiling = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
+    size_t prof_used = 0;
 
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;  // K1r of the round-2 probes, overlapping round 1
@@ -118,10 +125,6 @@ constexpr uint64_t IVF_R1_CODES = POLY_IVF_R1_CODES;  // ... and at least this m
 #ifndef POLY_IVF_CHUNK2
 #define POLY_IVF_CHUNK2 4096
 #endif
-#ifndef POLY_K5R_SUB
-#define POLY_K5R_SUB POLY_IVF_NQB
-#endif
-constexpr uint32_t K5R_SUB = POLY_K5R_SUB;  // queries per coarse GEMM + K5r launch pair
 #ifndef POLY_IVF_CHUNK
 #define POLY_IVF_CHUNK 1024
 #endif
@@ -204,9 +207,9 @@ void rebuild_lists(poly_b200_ivf* iv) {
 }
 
 void ensure_ivf_scratch(poly_b200_ivf* iv, uint32_t nprobe, uint32_t k) {
-    if (!iv->ckeys) {
-        iv->ckeys = dalloc<unsigned long long>((size_t)IVF_NQB * std::max<uint32_t>(iv->nlist, 64 * 64));
-        iv->nl_counts = dalloc<uint32_t>((size_t)IVF_NQB * 64);  // per-slice counts (K5s) or nlist (K5)
+    if (!iv->np_eff) {
+        iv->grp = dalloc<float4>((size_t)IVF_NQB * 2 * pb::coarse_tc_tiles(iv->nlist));
+        iv->rank_scratch = dalloc<uint32_t>((size_t)IVF_NQB * iv->nlist);
         iv->np_eff = dalloc<uint32_t>(IVF_NQB);
         iv->split = dalloc<uint32_t>(IVF_NQB);
         iv->scanned = dalloc<unsigned long long>(IVF_NQB);
@@ -285,49 +288,24 @@ void check_pending(poly_b200_ivf* iv, bool wait) {
     }
 }
 
-// Enqueue enumerate_cells for a batch: probe_keys (nqb x np) ascending.
-// np <= 64: fused distance + per-slice selection (K5s), slices merged by K3;
-// larger np: all keys (K5), then K3 over nlist keys per query.
+// Enqueue enumerate_cells (SPEC.md:376-381) for a batch: probe_keys (nqb x np) ascending.
+// np <= 1024: tensor-core dots with the per-group kept values (K5t) and the exact re-rank
+// of the cells within the error bound (K5q); larger np: every exact key (K5), then K3.
 void enumerate_cells(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, uint32_t np, cudaStream_t s) {
-    if (POLY_COARSE_GEMM && np <= pb::coarse_refine_npmax()) {
-        // K5r: TF32 tensor-core dots (cuBLAS: a plain GEMM), then the exact re-rank kernel
-        if (!iv->cublas) {
-            require(cublasCreate(&iv->cublas) == CUBLAS_STATUS_SUCCESS, POLY_B200_INTERNAL, "cublasCreate failed");
-            require(cublasSetMathMode(iv->cublas, CUBLAS_TF32_TENSOR_OP_MATH) == CUBLAS_STATUS_SUCCESS,
-                    POLY_B200_INTERNAL, "cublasSetMathMode failed");
-        }
-        require(cublasSetStream(iv->cublas, s) == CUBLAS_STATUS_SUCCESS, POLY_B200_INTERNAL, "cublasSetStream failed");
-        float* dots = reinterpret_cast<float*>(iv->ckeys);                        // IVF_NQB x nlist
-        uint32_t* scratch = reinterpret_cast<uint32_t*>(iv->ckeys) + (size_t)IVF_NQB * iv->nlist;
-        const float one = 1.0f, zero = 0.0f;
-        // sub-batches of K5R_SUB queries keep each dots block L2-resident between the
-        // GEMM that writes it and the two K5r passes that read it
-        for (uint32_t q0 = 0; q0 < nqb; q0 += K5R_SUB) {
-            const uint32_t nb = std::min(K5R_SUB, nqb - q0);
-            float* db = dots + (size_t)q0 * iv->nlist;
-            // column-major: dots (nlist x nb) = coarse^T (nlist x dim) . q^T (dim x nb)
-            require(cublasSgemm(iv->cublas, CUBLAS_OP_T, CUBLAS_OP_N, (int)iv->nlist, (int)nb, (int)iv->dim, &one,
-                                iv->d_coarse, (int)iv->dim, d_q + (size_t)q0 * iv->dim, (int)iv->dim, &zero, db,
-                                (int)iv->nlist) == CUBLAS_STATUS_SUCCESS,
-                    POLY_B200_INTERNAL, "cublasSgemm failed");
-            pb::launch_coarse_refine(d_q + (size_t)q0 * iv->dim, nb, iv->dim, db, iv->d_cnorm, iv->cmax, iv->d_coarse,
-                                     iv->nlist, np, scratch + (size_t)q0 * iv->nlist, iv->probe_keys + (size_t)q0 * np,
-                                     iv->probe_counts + q0, s);
-        }
-    } else if (np <= 64) {
-        const uint32_t qtiles = (nqb + 63) / 64;
-        uint32_t slices = std::max<uint32_t>(1, std::min<uint32_t>(64, 2u * iv->num_sms / qtiles));
-        slices = std::min<uint32_t>(slices, std::max<uint32_t>(1, iv->nlist / 64));
-        pb::launch_coarse_select(d_q, nqb, iv->dim, iv->d_coarse, iv->nlist, np, slices, iv->ckeys, iv->nl_counts,
-                                 s);
-        pb::launch_topk(iv->ckeys, iv->nl_counts, np, slices, (uint64_t)nqb * np, nqb, nqb, np, iv->probe_keys,
-                        iv->probe_counts, s);
-    } else {
-        pb::launch_coarse_keys(d_q, nqb, iv->dim, iv->d_coarse, iv->nlist, iv->ckeys, s);
+    if (np <= pb::coarse_rank_npmax()) {
+        pb::launch_coarse_tc(d_q, nqb, iv->dim, iv->d_cpacked, iv->d_cnorm, iv->nlist, iv->num_sms, iv->grp, s);
+        pb::launch_coarse_rank(d_q, nqb, iv->dim, iv->grp, iv->nlist, iv->cmax, iv->d_coarse, np, iv->rank_scratch,
+                               iv->probe_keys, iv->probe_counts, s);
+        return;
+    }
+    if (!iv->ckeys) {
+        iv->ckeys = dalloc<unsigned long long>((size_t)IVF_NQB * iv->nlist);
+        iv->nl_counts = dalloc<uint32_t>(IVF_NQB);
         fill_u32<<<1, 256, 0, s>>>(iv->nl_counts, IVF_NQB, iv->nlist);
         pb::count_launch();
-        pb::launch_topk(iv->ckeys, iv->nl_counts, iv->nlist, 1, 0, 0, nqb, np, iv->probe_keys, iv->probe_counts, s);
     }
+    pb::launch_coarse_keys(d_q, nqb, iv->dim, iv->d_coarse, iv->nlist, iv->ckeys, s);
+    pb::launch_topk(iv->ckeys, iv->nl_counts, iv->nlist, 1, 0, 0, nqb, np, iv->probe_keys, iv->probe_counts, s);
 }
 
 // One batch of <= 256 queries; outputs through keys_to_ids.
@@ -407,7 +385,19 @@ void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_
         a.nitems = w.nitems + round;
         a.items_cap = w.cap[round];
         a.work = iv->ctrl + IVF_NQB + 1 + round;
+        cudaEvent_t e1 = nullptr;
+        if (iv->profiling) {
+            if (iv->prof_used == iv->prof_events.size()) {
+                cudaEvent_t x, y;
+                CK(cudaEventCreate(&x));
+                CK(cudaEventCreate(&y));
+                iv->prof_events.push_back({x, y});
+            }
+            CK(cudaEventRecord(iv->prof_events[iv->prof_used].first, s));
+            e1 = iv->prof_events[iv->prof_used++].second;
+        }
         pb::launch_ivf_scan(a, strategy, iv->m, iv->num_sms, s);
+        if (e1) CK(cudaEventRecord(e1, s));
         // a query whose list overflowed (in either round) is re-ranked exactly over all its
         // visited probes (no-op for the others)
         if (round + 1 == rounds) pb::launch_ivf_rescue(a, strategy, iv->m, iv->np_eff, k, s);
@@ -556,8 +546,8 @@ int poly_b200_ivf_create(const poly_b200_pq_desc* pq, const float* coarse, uint3
             CK(cudaMemcpy(iv->d_perms, iv->h_perms.data(), iv->h_perms.size() * 2, cudaMemcpyHostToDevice));
             CK(cudaMemcpy(iv->d_coarse, iv->h_coarse.data(), iv->h_coarse.size() * 4, cudaMemcpyHostToDevice));
             CK(cudaMemset(iv->d_off, 0, (nlist + 1) * 8));
-            // |c|^2 per cell (approximate is fine: K5r's error bound covers it) and cmax >= max |c|
-            std::vector<float> cn(nlist);
+            // cmax >= max |c| for K5q's error bound; |c|^2 per cell comes from the pack kernel
+            // (any rounding: the bound covers it)
             double cm = 0.0;
             for (uint32_t c = 0; c < nlist; ++c) {
                 double acc = 0.0;
@@ -565,12 +555,15 @@ int poly_b200_ivf_create(const poly_b200_pq_desc* pq, const float* coarse, uint3
                     const double v = iv->h_coarse[(size_t)c * pq->dim + d];
                     acc += v * v;
                 }
-                cn[c] = (float)acc;
                 cm = std::max(cm, acc);
             }
             iv->cmax = (float)(std::sqrt(cm) * (1.0 + 1e-5)) + 1e-30f;
-            iv->d_cnorm = dalloc<float>(nlist);
-            CK(cudaMemcpy(iv->d_cnorm, cn.data(), nlist * 4, cudaMemcpyHostToDevice));
+            const size_t npad = (size_t)pb::coarse_tc_tiles(nlist) * 256;
+            iv->d_cnorm = dalloc<float>(npad);
+            iv->d_cpacked = dalloc<float>(npad * pq->dim);
+            pb::launch_coarse_pack(iv->d_coarse, nlist, (uint32_t)pq->dim, iv->d_cpacked, iv->d_cnorm, iv->stream);
+            CK(cudaStreamSynchronize(iv->stream));
+            CK(cudaGetLastError());
         } catch (...) {
             poly_b200_ivf_destroy(iv);
             throw;
@@ -595,10 +588,14 @@ int poly_b200_ivf_destroy(poly_b200_ivf* iv) {
                             (void*)iv->ovq, (void*)iv->surv_q, (void*)iv->hash_q,
                             (void*)iv->d_oid, (void*)iv->d_osc, (void*)iv->d_ocnt,
                             (void*)iv->knn_ids, (void*)iv->knn_sc, (void*)iv->knn_cnt, (void*)iv->d_cnorm, (void*)iv->items[0],
+                            (void*)iv->d_cpacked, (void*)iv->grp, (void*)iv->rank_scratch,
                             (void*)iv->items[1]})
                 dfree(p);
-            if (iv->cublas) cublasDestroy(iv->cublas);
             if (iv->h_overflow) cudaFreeHost(iv->h_overflow);
+            for (auto& pe : iv->prof_events) {
+                cudaEventDestroy(pe.first);
+                cudaEventDestroy(pe.second);
+            }
             if (iv->done_ev) cudaEventDestroy(iv->done_ev);
             iv->idm.release();
             if (iv->stream) cudaStreamDestroy(iv->stream);
@@ -720,6 +717,65 @@ int poly_b200_ivf_get_lists(poly_b200_ivf* iv, uint64_t* off, uint8_t* codes, in
                 CK(cudaMemcpy(r2id.data(), iv->idm.d_rank_to_id, iv->n * 8, cudaMemcpyDeviceToHost));
             }
             for (uint64_t i = 0; i < iv->n; ++i) ids[i] = r2id.empty() ? (int64_t)low[i] : r2id[low[i]];
+        }
+    });
+}
+
+int poly_b200_ivf_profile_enable(poly_b200_ivf* iv, int enable) {
+    return guard([&] {
+        require(iv != nullptr, POLY_B200_INVALID_ARGUMENT, "null index");
+        std::lock_guard<std::mutex> lk(iv->mu);
+        iv->profiling = enable != 0;
+        iv->prof_used = 0;
+    });
+}
+
+int poly_b200_ivf_profile_read(poly_b200_ivf* iv, double* scan_ms, uint64_t* scan_launches) {
+    return guard([&] {
+        require(iv && scan_ms && scan_launches, POLY_B200_INVALID_ARGUMENT, "null arguments");
+        std::lock_guard<std::mutex> lk(iv->mu);
+        DeviceGuard dg(iv->device);
+        double total = 0.0;
+        for (size_t i = 0; i < iv->prof_used; ++i) {
+            CK(cudaEventSynchronize(iv->prof_events[i].second));
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, iv->prof_events[i].first, iv->prof_events[i].second));
+            total += ms;
+        }
+        *scan_ms = total;
+        *scan_launches = iv->prof_used;
+        iv->prof_used = 0;
+    });
+}
+
+// CSR of selected cells only (the CPU baseline's probed lists): off (ncells + 1),
+// codes / ids in the order of `cells`.
+int poly_b200_ivf_get_cells(poly_b200_ivf* iv, const uint32_t* cells, uint32_t ncells, uint64_t* off, uint8_t* codes,
+                            int64_t* ids) {
+    return guard([&] {
+        require(iv && (ncells == 0 || (cells && off)), POLY_B200_INVALID_ARGUMENT, "null arguments");
+        std::lock_guard<std::mutex> lk(iv->mu);
+        DeviceGuard dg(iv->device);
+        rebuild_lists(iv);
+        std::vector<int64_t> r2id;
+        if (ids && iv->idm.d_rank_to_id) {
+            r2id.resize(iv->n);
+            CK(cudaMemcpy(r2id.data(), iv->idm.d_rank_to_id, iv->n * 8, cudaMemcpyDeviceToHost));
+        }
+        off[0] = 0;
+        std::vector<uint32_t> low;
+        for (uint32_t i = 0; i < ncells; ++i) {
+            require(cells[i] < iv->nlist, POLY_B200_INVALID_ARGUMENT, "bad cell");
+            const uint64_t b = iv->h_off[cells[i]], e = iv->h_off[cells[i] + 1], len = e - b;
+            off[i + 1] = off[i] + len;
+            if (!len) continue;
+            if (codes) CK(cudaMemcpy(codes + off[i] * iv->cb, iv->d_codes_list + b * iv->cb, len * iv->cb,
+                                     cudaMemcpyDeviceToHost));
+            if (ids) {
+                low.resize(len);
+                CK(cudaMemcpy(low.data(), iv->d_low_list + b, len * 4, cudaMemcpyDeviceToHost));
+                for (uint64_t j = 0; j < len; ++j) ids[off[i] + j] = r2id.empty() ? (int64_t)low[j] : r2id[low[j]];
+            }
         }
     });
 }

@@ -7,8 +7,7 @@
 //                            fp32 in dim order; key = (dist bits << 32 | cell), so K3
 //                            with k = nprobe yields enumerate_cells:
 //                            ascending distance, ties -> lower cell.
-//   K5r coarse_refine_kernel enumerate_cells from TF32 dots + an exact fp32 re-rank
-//                            of every cell within the dots' error bound.
+//   (the tensor-core form of enumerate_cells, K5t + K5q, is in kernels_coarse.cu)
 //   K1r residual_lut_quad_kernel  per (query, probe): r = q - c_cell, then
 //                            compute_lut / permuted_lut / encode on r
 //                            (pq.cpp:29-45,91-119), packed f32x2, bit-exact.
@@ -83,391 +82,6 @@ void launch_coarse_keys(const float* q, uint32_t nq, uint32_t dim, const float* 
     if (nq == 0) return;
     dim3 grid((nlist + K5_T - 1) / K5_T, (nq + K5_T - 1) / K5_T);
     coarse_keys_kernel<<<grid, 256, 0, s>>>(q, nq, dim, cent, nlist, keys);
-    count_launch();
-}
-
-// K5s: the same exact distances, fused with a per-(query, cell-slice) top-np
-// selection: each CTA owns 64 queries x one slice of the cells, filters keys
-// against the query's running np-th key and inserts the few that pass into a
-// sorted shared-memory list (one warp per query, lane-parallel shift).  The
-// per-slice lists are merged by K3 (parts = slices).  np <= K5S_NP.
-constexpr int K5S_NP = 64;
-
-__global__ void __launch_bounds__(256) coarse_select_kernel(const float* __restrict__ q, uint32_t nq, uint32_t dim,
-                                                            const float* __restrict__ cent, uint32_t nlist,
-                                                            uint32_t np, uint32_t slices,
-                                                            unsigned long long* __restrict__ out_keys,
-                                                            uint32_t* __restrict__ out_counts) {
-    // dynamic smem: top[64][np_pad] | pend[64][64] | qs[64][dim+1] (resident) | cs[64][33]
-    extern __shared__ __align__(16) uint8_t k5s_smem[];
-    const uint32_t np_pad = np <= 32 ? 32 : 64;
-    unsigned long long* top = reinterpret_cast<unsigned long long*>(k5s_smem);
-    unsigned long long* pend = top + K5_T * np_pad;
-    float* qs = reinterpret_cast<float*>(pend + K5_T * K5_T);
-    const uint32_t qstride = dim + 1;
-    auto cs = reinterpret_cast<float(*)[K5_D + 1]>(qs + K5_T * qstride);
-    __shared__ unsigned long long thr[K5_T];
-    __shared__ uint32_t topn[K5_T], pn[K5_T];
-    const uint32_t slice = blockIdx.x, q0 = blockIdx.y * K5_T;
-    const uint32_t per = (nlist + slices - 1) / slices;
-    const uint32_t c_lo = min(nlist, slice * per), c_hi = min(nlist, c_lo + per);
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x < K5_T) {
-        thr[threadIdx.x] = ~0ull;
-        topn[threadIdx.x] = 0;
-        pn[threadIdx.x] = 0;
-    }
-    for (uint32_t e = threadIdx.x; e < K5_T * dim; e += 256) {
-        const uint32_t r = e / dim, c = e % dim;
-        qs[r * qstride + c] = (q0 + r < nq) ? q[(size_t)(q0 + r) * dim + c] : 0.0f;
-    }
-    for (uint32_t c0 = c_lo; c0 < c_hi; c0 += K5_T) {
-        float acc[4][4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
-        for (uint32_t d0 = 0; d0 < dim; d0 += K5_D) {
-            __syncthreads();
-            for (int e = threadIdx.x; e < K5_T * K5_D; e += 256) {
-                const int r = e / K5_D, c = e % K5_D;
-                cs[r][c] = (c0 + r < c_hi) ? cent[(size_t)(c0 + r) * dim + d0 + c] : 0.0f;
-            }
-            __syncthreads();
-#pragma unroll 4
-            for (int d = 0; d < K5_D; ++d) {
-                float av[4], bv[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) av[i] = qs[(ty + 16 * i) * qstride + d0 + d];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) bv[j] = cs[tx + 16 * j][d];
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const float t = __fsub_rn(av[i], bv[j]);
-                        acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(t, t));
-                    }
-            }
-        }
-        // filter against the running np-th key, queue the passing keys per query
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int r = ty + 16 * i;
-            const unsigned long long tr = thr[r];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const uint32_t c = c0 + tx + 16 * j;
-                const unsigned long long key = ((unsigned long long)__float_as_uint(acc[i][j]) << 32) | c;
-                if (c < c_hi && key < tr) pend[r * K5_T + atomicAdd(&pn[r], 1u)] = key;
-            }
-        }
-        __syncthreads();
-        // merge: warp per query, sorted insertion (ascending, at most np kept)
-        for (int r = warp; r < K5_T; r += 8) {
-            const uint32_t cnt = pn[r];
-            if (cnt == 0) continue;
-            unsigned long long* T = top + r * np_pad;
-            uint32_t n = topn[r];
-            for (uint32_t t = 0; t < cnt; ++t) {
-                const unsigned long long x = pend[r * K5_T + t];
-                const unsigned long long e0 = lane < (int)n ? T[lane] : ~0ull;
-                const unsigned long long e1 = lane + 32 < (int)n ? T[lane + 32] : ~0ull;
-                const uint32_t pos = __popc(__ballot_sync(0xffffffffu, e0 < x)) + __popc(__ballot_sync(0xffffffffu, e1 < x));
-                if (pos >= np) continue;
-                __syncwarp();
-                if (lane >= (int)pos && lane + 1 < (int)np && lane < (int)n) T[lane + 1] = e0;
-                if (lane + 32 >= (int)pos && lane + 33 < (int)np && lane + 32 < (int)n) T[lane + 33] = e1;
-                __syncwarp();
-                if (lane == 0) T[pos] = x;
-                n = min(n + 1, np);
-                __syncwarp();
-            }
-            if (lane == 0) {
-                topn[r] = n;
-                pn[r] = 0;
-                if (n == np) thr[r] = T[np - 1];
-            }
-        }
-    }
-    __syncthreads();
-    for (int r = warp; r < K5_T; r += 8) {
-        const uint32_t qi = q0 + r;
-        if (qi >= nq) continue;
-        const uint32_t n = topn[r];
-        unsigned long long* o = out_keys + ((size_t)slice * nq + qi) * np;
-        for (uint32_t t = lane; t < np; t += 32) o[t] = t < n ? top[r * np_pad + t] : ~0ull;
-        if (lane == 0) out_counts[(size_t)slice * nq + qi] = n;
-    }
-}
-
-void launch_coarse_select(const float* q, uint32_t nq, uint32_t dim, const float* cent, uint32_t nlist, uint32_t np,
-                          uint32_t slices, unsigned long long* out_keys, uint32_t* out_counts, cudaStream_t s) {
-    if (nq == 0) return;
-    const size_t np_pad = np <= 32 ? 32 : 64;
-    const size_t smem = (size_t)K5_T * (np_pad + K5_T) * 8 + (size_t)K5_T * (dim + 1) * 4 + (size_t)K5_T * (K5_D + 1) * 4;
-    set_max_smem((const void*)coarse_select_kernel, smem);
-    coarse_select_kernel<<<dim3(slices, (nq + K5_T - 1) / K5_T), 256, smem, s>>>(q, nq, dim, cent, nlist, np, slices,
-                                                                                 out_keys, out_counts);
-    count_launch();
-}
-
-// ------------------------------------------------------------------ K5r
-// enumerate_cells with the tensor cores, still exact (the coarse-centroid GEMM the
-// north star allows "only if the result stays within tolerance" -- here it stays
-// exact).  A TF32 GEMM (cuBLAS, host side) gives dots[c] ~ q.c; the approximate
-// distance a(c) = |q|^2 + |c|^2 - 2 dots[c] is within E of the reference's fp32
-// sq_l2(q, c) for every cell, with
-//   E = 4.1e-3 |q| cmax + 4e-5 (|q|^2 + cmax^2 + 2 |q| cmax) + 1e-6
-// (TF32 inputs truncated to 10 mantissa bits: product error <= 2^-9; fp32
-// accumulation and the reference's own rounding add <= 2e-5 relative; x1.5 slack).
-// With T an upper bound of the np-th smallest a(c), every cell of the exact top-np
-// has a(c) <= T + 2E; those cells get the exact sq_l2 (fp32, dim order, as K5) and
-// the (dist bits << 32 | cell) keys of the np smallest are emitted in order.
-// One CTA (512 threads) per query, one pass over the query's dots row (float4):
-// each thread keeps its three smallest a(c); those 1536 values are distinct cells,
-// so their np-th smallest (radix-selected to 16 bits, rounded up) is >= the np-th
-// smallest a(c) over all cells and serves as T.  The cells with a(c) <= T + 2E
-// are among a thread's kept ones, unless its third smallest is within the bound too
-// (then it revisits its cells); they go to a global scratch list and are
-// re-ranked in chunks of KR_CHUNK.
-#ifndef POLY_KR_THREADS
-#define POLY_KR_THREADS 512
-#endif
-constexpr int KR_THREADS = POLY_KR_THREADS, KR_CHUNK = 2048, KR_BUF = 4096;  // np + chunk <= buf (pow2)
-constexpr int KR_TVALS = 3 * KR_THREADS;                                   // per-thread three smallest
-constexpr int KR_NPMAX = KR_TVALS < 1024 ? KR_TVALS : 1024;
-uint32_t coarse_refine_npmax() { return KR_NPMAX; }
-constexpr int KR_UNROLL = 4;              // float4 loads in flight per thread
-constexpr uint32_t KR_RANKMAX = 1024;     // re-rank by counting up to this many keys (else bitonic)
-
-__device__ __forceinline__ uint32_t kr_ord(float f) {  // order-preserving float -> uint32
-    const uint32_t b = __float_as_uint(f);
-    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
-}
-__device__ __forceinline__ float kr_unord(uint32_t u) {
-    return __uint_as_float((u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u);
-}
-
-__global__ void __launch_bounds__(KR_THREADS, 1024 / KR_THREADS) coarse_refine_kernel(const float* __restrict__ q, uint32_t dim,
-                                                                   const float* __restrict__ dots,
-                                                                   const float* __restrict__ cnorm, float cmax,
-                                                                   const float* __restrict__ cent, uint32_t nlist,
-                                                                   uint32_t np, uint32_t* __restrict__ scratch,
-                                                                   unsigned long long* __restrict__ probe_keys,
-                                                                   uint32_t* __restrict__ probe_counts) {
-    extern __shared__ __align__(16) uint8_t kr_smem[];
-    unsigned long long* buf = reinterpret_cast<unsigned long long*>(kr_smem);  // KR_BUF keys
-    float* qs = reinterpret_cast<float*>(buf + KR_BUF);                         // dim
-    __shared__ float red_f[KR_THREADS / 32];
-    __shared__ uint32_t red_u[2];
-    __shared__ uint32_t ncand_s;
-    const uint32_t qi = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const float* qrow = q + (size_t)qi * dim;
-    const float* drow = dots + (size_t)qi * nlist;
-    uint32_t* cand = scratch + (size_t)qi * nlist;
-    const bool vec = (nlist & 3u) == 0;  // rows 16-byte aligned
-    // |q|^2
-    float qn = 0.0f;
-    for (uint32_t d = tid; d < dim; d += KR_THREADS) {
-        const float v = qrow[d];
-        qs[d] = v;
-        qn += v * v;
-    }
-    for (int off = 16; off; off >>= 1) qn += __shfl_xor_sync(0xffffffffu, qn, off);
-    if (lane == 0) red_f[warp] = qn;
-    if (tid == 0) ncand_s = 0;
-    __syncthreads();
-    qn = 0.0f;
-    for (int w = 0; w < KR_THREADS / 32; ++w) qn += red_f[w];
-    // one pass over the row: the two smallest a(c) = |q|^2 + |c|^2 - 2 q.c of this
-    // thread's cells, with their indices
-    float m1 = INFINITY, m2 = INFINITY, m3 = INFINITY;
-    uint32_t i1 = 0xFFFFFFFFu, i2 = 0xFFFFFFFFu;
-    auto keep = [&](float a, uint32_t c) {
-        if (a < m3) {
-            if (a < m2) {
-                m3 = m2;
-                if (a < m1) { m2 = m1; i2 = i1; m1 = a; i1 = c; }
-                else { m2 = a; i2 = c; }
-            } else {
-                m3 = a;
-            }
-        }
-    };
-    const float4* d4 = reinterpret_cast<const float4*>(drow);
-    const float4* n4 = reinterpret_cast<const float4*>(cnorm);
-    const uint32_t n4c = nlist / 4;
-    // visit this thread's cells (float4 groups tid, tid + KR_THREADS, ...; scalar rows
-    // when unaligned), KR_UNROLL loads in flight
-    auto visit = [&](auto&& f) {
-        if (vec) {
-            for (uint32_t c0 = tid; c0 < n4c; c0 += KR_THREADS * KR_UNROLL) {
-                float4 d[KR_UNROLL], n[KR_UNROLL];
-#pragma unroll
-                for (int u = 0; u < KR_UNROLL; ++u) {
-                    const uint32_t c = c0 + u * KR_THREADS;
-                    if (c < n4c) { d[u] = __ldcg(d4 + c); n[u] = __ldg(n4 + c); }
-                }
-#pragma unroll
-                for (int u = 0; u < KR_UNROLL; ++u) {
-                    const uint32_t c = c0 + u * KR_THREADS;
-                    if (c >= n4c) continue;
-                    f(qn + n[u].x - 2.0f * d[u].x, 4 * c);
-                    f(qn + n[u].y - 2.0f * d[u].y, 4 * c + 1);
-                    f(qn + n[u].z - 2.0f * d[u].z, 4 * c + 2);
-                    f(qn + n[u].w - 2.0f * d[u].w, 4 * c + 3);
-                }
-            }
-        } else {
-            for (uint32_t c = tid; c < nlist; c += KR_THREADS) f(qn + cnorm[c] - 2.0f * drow[c], c);
-        }
-    };
-    visit(keep);
-    // T: an upper bound of the np-th smallest of the 1024 kept values -- a radix select
-    // of its top 16 bits (two 8-bit passes), T = the upper edge of that 16-bit bucket
-    uint32_t* hist = reinterpret_cast<uint32_t*>(buf);  // 256 bins (aliases buf)
-    const uint32_t k1 = kr_ord(m1), k2 = kr_ord(m2), k3 = kr_ord(m3);
-    uint32_t prefix = 0, want = min(np, (uint32_t)KR_TVALS);
-    for (int pass = 0; pass < 2; ++pass) {
-        const int sh = 24 - 8 * pass;
-        if (tid < 256) hist[tid] = 0;
-        __syncthreads();
-        const uint32_t pm = pass ? prefix >> (sh + 8) : 0;
-        if (!pass || (k1 >> (sh + 8)) == pm) atomicAdd(&hist[(k1 >> sh) & 255u], 1u);
-        if (!pass || (k2 >> (sh + 8)) == pm) atomicAdd(&hist[(k2 >> sh) & 255u], 1u);
-        if (!pass || (k3 >> (sh + 8)) == pm) atomicAdd(&hist[(k3 >> sh) & 255u], 1u);
-        __syncthreads();
-        if (warp == 0) {  // bin holding the want-th key: lane-sums of 8 bins, warp scan
-            uint32_t c8 = 0;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) c8 += hist[lane * 8 + e];
-            uint32_t incl = c8;
-            for (int off = 1; off < 32; off <<= 1) {
-                const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
-                if (lane >= (uint32_t)off) incl += o;
-            }
-            const uint32_t excl = incl - c8;
-            if (excl < want && want <= incl) {
-                uint32_t cum = excl, dg = lane * 8;
-                for (int e = 0; e < 8; ++e) {
-                    if (cum + hist[lane * 8 + e] >= want) { dg = lane * 8 + e; break; }
-                    cum += hist[lane * 8 + e];
-                }
-                red_u[0] = dg;
-                red_u[1] = cum;
-            }
-        }
-        __syncthreads();
-        prefix |= red_u[0] << sh;
-        want -= red_u[1];
-        __syncthreads();  // red_u and hist reused
-    }
-    // T >= the np-th smallest a(c); candidate bound T + 2E (np <= KR_NPMAX <= KR_TVALS)
-    const float T = kr_unord(prefix | 0xFFFFu);
-    const float qnorm = sqrtf(qn);
-    const float E = 4.1e-3f * qnorm * cmax + 4e-5f * (qn + cmax * cmax + 2.0f * qnorm * cmax) + 1e-6f;
-    const float bound = T + 2.0f * E;
-    // candidates: a thread whose third smallest is within the bound may hold more (its
-    // fourth, ...): it revisits its cells -- rare, since the near cells are spread over
-    // the threads, but the CTA waits for it (with two kept values it was the main
-    // barrier stall); otherwise its candidates are among its two smallest
-    if (!(m3 > bound)) {
-        visit([&](float a, uint32_t c) {
-            if (!(a > bound)) cand[atomicAdd(&ncand_s, 1u)] = c;
-        });
-    } else {
-        if (!(m1 > bound)) cand[atomicAdd(&ncand_s, 1u)] = i1;
-        if (!(m2 > bound)) cand[atomicAdd(&ncand_s, 1u)] = i2;
-    }
-    __syncthreads();
-    const uint32_t ncand = ncand_s;
-    // exact sq_l2 of the candidates, chunk by chunk, merged into the running top-np
-    uint32_t ntop = 0;
-    for (uint32_t c0 = 0; c0 < ncand; c0 += KR_CHUNK) {
-        const uint32_t cn = min((uint32_t)KR_CHUNK, ncand - c0);
-        for (uint32_t i = tid; i < cn; i += KR_THREADS) {
-            const uint32_t cell = cand[c0 + i];
-            const float* crow = cent + (size_t)cell * dim;
-            float acc = 0.0f;
-            if ((dim & 31u) == 0) {  // 8 float4 loads in flight, then the sum in dim order
-                for (uint32_t d0 = 0; d0 < dim; d0 += 32) {
-                    float4 c4[8];
-#pragma unroll
-                    for (int v = 0; v < 8; ++v) c4[v] = __ldg(reinterpret_cast<const float4*>(crow + d0) + v);
-#pragma unroll
-                    for (int v = 0; v < 8; ++v) {
-                        const float cv[4] = {c4[v].x, c4[v].y, c4[v].z, c4[v].w};
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const float t = __fsub_rn(qs[d0 + 4 * v + e], cv[e]);
-                            acc = __fadd_rn(acc, __fmul_rn(t, t));
-                        }
-                    }
-                }
-            } else if ((dim & 3u) == 0) {
-                for (uint32_t d = 0; d < dim; d += 4) {
-                    const float4 c4 = __ldg(reinterpret_cast<const float4*>(crow + d));
-                    const float cv[4] = {c4.x, c4.y, c4.z, c4.w};
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float t = __fsub_rn(qs[d + e], cv[e]);
-                        acc = __fadd_rn(acc, __fmul_rn(t, t));
-                    }
-                }
-            } else {
-                for (uint32_t d = 0; d < dim; ++d) {
-                    const float t = __fsub_rn(qs[d], __ldg(crow + d));
-                    acc = __fadd_rn(acc, __fmul_rn(t, t));
-                }
-            }
-            buf[ntop + i] = ((unsigned long long)__float_as_uint(acc) << 32) | cell;
-        }
-        const uint32_t n = ntop + cn;
-        __syncthreads();
-        if (n <= KR_RANKMAX) {  // rank by counting (keys distinct: the low word is the cell)
-            unsigned long long* out = buf + KR_BUF / 2;
-            for (uint32_t i = tid; i < n; i += KR_THREADS) {
-                const unsigned long long ki = buf[i];
-                uint32_t rank = 0;
-                for (uint32_t j = 0; j < n; ++j) rank += buf[j] < ki;
-                if (rank < np) out[rank] = ki;
-            }
-            __syncthreads();
-            for (uint32_t i = tid; i < min(n, np); i += KR_THREADS) buf[i] = out[i];
-            __syncthreads();
-            ntop = min(n, np);
-            continue;
-        }
-        uint32_t P = 1;
-        while (P < n) P <<= 1;
-        for (uint32_t i = n + tid; i < P; i += KR_THREADS) buf[i] = ~0ull;
-        __syncthreads();
-        for (uint32_t size = 2; size <= P; size <<= 1)
-            for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-                for (uint32_t i = tid; i < P / 2; i += KR_THREADS) {
-                    const uint32_t pos = 2 * i - (i & (stride - 1));
-                    const bool asc = (pos & size) == 0;
-                    const unsigned long long x = buf[pos], y = buf[pos + stride];
-                    if ((x > y) == asc) { buf[pos] = y; buf[pos + stride] = x; }
-                }
-                __syncthreads();
-            }
-        ntop = min(n, np);
-    }
-    for (uint32_t i = tid; i < np; i += KR_THREADS) probe_keys[(size_t)qi * np + i] = i < ntop ? buf[i] : ~0ull;
-    if (tid == 0) probe_counts[qi] = ntop;
-}
-
-void launch_coarse_refine(const float* q, uint32_t nq, uint32_t dim, const float* dots, const float* cnorm, float cmax,
-                          const float* cent, uint32_t nlist, uint32_t np, uint32_t* scratch,
-                          unsigned long long* probe_keys, uint32_t* probe_counts, cudaStream_t s) {
-    if (nq == 0) return;
-    const size_t smem = (size_t)KR_BUF * 8 + (size_t)dim * 4;
-    set_max_smem((const void*)coarse_refine_kernel, smem);
-    coarse_refine_kernel<<<nq, KR_THREADS, smem, s>>>(q, dim, dots, cnorm, cmax, cent, nlist, np, scratch, probe_keys,
-                                                      probe_counts);
     count_launch();
 }
 

@@ -31,9 +31,6 @@ constexpr int DSUB = 16;               // every configuration: 128/8 and 256/16
 #ifndef POLY_SEED_BLOCKS  // K2s seed sample: runs of 256 codes (0 = no seed kernel)
 #define POLY_SEED_BLOCKS 128
 #endif
-#ifndef POLY_COARSE_GEMM  // 1: enumerate_cells via TF32 dots + exact re-rank (K5r)
-#define POLY_COARSE_GEMM 1
-#endif
 #ifndef POLY_PROD_SPIN_NS
 #define POLY_PROD_SPIN_NS 0
 #endif
@@ -307,13 +304,16 @@ void launch_seed_compact(const unsigned long long* keys, const uint32_t* counts,
 // IVF (kernels_ivf.cu)
 void launch_coarse_keys(const float* q, uint32_t nq, uint32_t dim, const float* cent, uint32_t nlist,
                         unsigned long long* keys, cudaStream_t s);
-// K5r: exact enumerate_cells from TF32 dots (dots[q * nlist + c] ~ q.c) + exact re-rank; np <= coarse_refine_npmax()
-uint32_t coarse_refine_npmax();
-void launch_coarse_refine(const float* q, uint32_t nq, uint32_t dim, const float* dots, const float* cnorm, float cmax,
-                          const float* cent, uint32_t nlist, uint32_t np, uint32_t* scratch,
-                          unsigned long long* probe_keys, uint32_t* probe_counts, cudaStream_t s);
-void launch_coarse_select(const float* q, uint32_t nq, uint32_t dim, const float* cent, uint32_t nlist, uint32_t np,
-                          uint32_t slices, unsigned long long* out_keys, uint32_t* out_counts, cudaStream_t s);
+// K5t + K5q (kernels_coarse.cu): enumerate_cells on the tensor cores, exact, np <= coarse_rank_npmax()
+uint32_t coarse_tc_tiles(uint32_t nlist);
+uint32_t coarse_rank_npmax();
+void launch_coarse_pack(const float* cent, uint32_t nlist, uint32_t dim, float* packed, float* cnorm_pad,
+                        cudaStream_t s);
+void launch_coarse_tc(const float* q, uint32_t nq, uint32_t dim, const float* packed, const float* cnorm_pad,
+                      uint32_t nlist, int num_sms, float4* grp, cudaStream_t s);
+void launch_coarse_rank(const float* q, uint32_t nq, uint32_t dim, const float4* grp, uint32_t nlist, float cmax,
+                        const float* cent, uint32_t np, uint32_t* scratch, unsigned long long* probe_keys,
+                        uint32_t* probe_counts, cudaStream_t s);
 // K1r over the probes [p_lo, p_hi) of every query (items q * nprobe + p)
 void launch_residual_lut(const float* queries, uint32_t nq, uint32_t dim, uint32_t m,
                          const unsigned long long* probe_keys, uint32_t nprobe, uint32_t p_lo, uint32_t p_hi,

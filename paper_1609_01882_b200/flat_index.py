@@ -189,13 +189,13 @@ class FlatIndex:
                                            int(normalize)))
 
     # ---- search (flat_index.hpp:121-126)
-    def search_batch(self, queries, params: SearchParams, stats: SearchStats | None = None):
+    def search_batch(self, queries, params: SearchParams, stats: SearchStats | None = None, out=None):
         """Returns (ids [nq,k] int64, scores [nq,k] fp32, counts [nq] uint32)."""
         q = np.ascontiguousarray(queries, np.float32).reshape(-1, self._pq.dim)
         nq, k = q.shape[0], int(params.k)
-        ids = np.empty((nq, k), np.int64)
-        scores = np.empty((nq, k), np.float32)
-        counts = np.empty(nq, np.uint32)
+        if out is None:  # out: preallocated (e.g. pinned) ids [nq,k] int64, scores [nq,k] fp32, counts [nq] uint32
+            out = (np.empty((nq, k), np.int64), np.empty((nq, k), np.float32), np.empty(nq, np.uint32))
+        ids, scores, counts = out
         st = SearchStatsC()
         _check(lib.poly_b200_search_batch(self._h, _p(q), nq, C.byref(params.c()), _p(ids), _p(scores), _p(counts),
                                           C.byref(st)))

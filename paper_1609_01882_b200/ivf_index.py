@@ -87,18 +87,24 @@ class IVFIndex:
         _check(lib.poly_b200_ivf_get_lists(self._h, _p(off), _p(codes), _p(ids)))
         return off, codes, ids
 
+    def list_offsets(self):
+        """CSR offsets [nlist+1] of the inverted lists (builds the lists if adds are pending)."""
+        off = np.empty(self.nlist + 1, np.uint64)
+        _check(lib.poly_b200_ivf_get_lists(self._h, _p(off), None, None))
+        return off
+
     def probes(self, queries, nprobe):
         q = np.ascontiguousarray(queries, np.float32).reshape(-1, self._pq.dim)
         out = np.empty((q.shape[0], nprobe), np.uint32)
         _check(lib.poly_b200_ivf_probes(self._h, _p(q), q.shape[0], nprobe, _p(out)))
         return out
 
-    def search(self, queries, params: CoarseParams, stats: SearchStats | None = None):
+    def search(self, queries, params: CoarseParams, stats: SearchStats | None = None, out=None):
         q = np.ascontiguousarray(queries, np.float32).reshape(-1, self._pq.dim)
         nq, k = q.shape[0], int(params.k)
-        ids = np.empty((nq, k), np.int64)
-        scores = np.empty((nq, k), np.float32)
-        counts = np.empty(nq, np.uint32)
+        if out is None:  # out: preallocated (e.g. pinned) ids [nq,k] int64, scores [nq,k] fp32, counts [nq] uint32
+            out = (np.empty((nq, k), np.int64), np.empty((nq, k), np.float32), np.empty(nq, np.uint32))
+        ids, scores, counts = out
         st = SearchStatsC()
         _check(lib.poly_b200_ivf_search(self._h, _p(q), nq, C.byref(params.c()), _p(ids), _p(scores), _p(counts),
                                         C.byref(st)))
@@ -120,6 +126,25 @@ class IVFIndex:
         if stats is not None:
             stats.scanned += st.scanned
             stats.survivors += st.survivors
+
+    def cells(self, cells):
+        """CSR of the given cells' lists: (off [len+1] uint64, codes [off[-1], cb] uint8, ids int64)."""
+        cells = np.ascontiguousarray(cells, np.uint32)
+        off = np.empty(len(cells) + 1, np.uint64)
+        _check(lib.poly_b200_ivf_get_cells(self._h, _p(cells), len(cells), _p(off), None, None))
+        codes = np.empty((int(off[-1]), self._pq.code_bytes()), np.uint8)
+        ids = np.empty(int(off[-1]), np.int64)
+        _check(lib.poly_b200_ivf_get_cells(self._h, _p(cells), len(cells), _p(off), _p(codes), _p(ids)))
+        return off, codes, ids
+
+    def profile_enable(self, on: bool = True):
+        _check(lib.poly_b200_ivf_profile_enable(self._h, int(on)))
+
+    def profile_read(self):
+        """(summed K6 list-scan milliseconds, K6 launches) since the last read."""
+        ms, n = C.c_double(0), C.c_uint64(0)
+        _check(lib.poly_b200_ivf_profile_read(self._h, C.byref(ms), C.byref(n)))
+        return float(ms.value), int(n.value)
 
     def debug_set_list_capacity(self, cap: int):
         _check(lib.poly_b200_ivf_debug_set_list_capacity(self._h, int(cap)))

@@ -52,6 +52,23 @@ __global__ void lds_gather_kernel(float* out, int iters) {
     if (acc == -1.f) out[0] = acc;
 }
 
+// packed FP32: add.rn.f32x2 (FADD2), 8 independent chains per thread
+__global__ void f32x2_kernel(const float* __restrict__ in, float* out, int iters) {
+    unsigned long long a[8], b;
+    const float x = in[threadIdx.x & 255], y = in[(threadIdx.x + 1) & 255];
+    asm("mov.b64 %0, {%1,%2};" : "=l"(b) : "f"(x), "f"(y));
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm("mov.b64 %0, {%1,%2};" : "=l"(a[i]) : "f"(x + i), "f"(y - i));
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(a[i]) : "l"(b));
+    }
+    unsigned long long s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s ^= a[i];
+    if (s == 0x1234567ull) out[0] = 1.f;
+}
+
 int main() {
     cudaDeviceProp p; CK(cudaGetDeviceProperties(&p, 0));
     int clk = 0; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
@@ -74,6 +91,11 @@ int main() {
         cudaEventElapsedTime(&ms, e0, e1);
         ops = (double)blocks * threads * iters * 8 * 2;
         printf("{\"bench\":\"lop+iadd\",\"ms\":%.3f,\"ops_per_s\":%.4e,\"ops_per_clk_sm_at_maxclk\":%.2f}\n", ms, ops / (ms * 1e-3),
+               ops / (ms * 1e-3) / (p.multiProcessorCount * (clk * 1e3)));
+        cudaEventRecord(e0); f32x2_kernel<<<blocks, threads>>>(reinterpret_cast<const float*>(d_in), d_f, iters); cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
+        cudaEventElapsedTime(&ms, e0, e1);
+        ops = (double)blocks * threads * iters * 8 * 2;  // two fp32 adds per FADD2
+        printf("{\"bench\":\"f32x2_add\",\"ms\":%.3f,\"fp32_ops_per_s\":%.4e,\"fp32_ops_per_clk_sm_at_maxclk\":%.2f}\n", ms, ops / (ms * 1e-3),
                ops / (ms * 1e-3) / (p.multiProcessorCount * (clk * 1e3)));
         cudaEventRecord(e0); lds_gather_kernel<<<blocks, threads>>>(d_f, iters / 4); cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
         cudaEventElapsedTime(&ms, e0, e1);
