@@ -219,6 +219,14 @@ int poly_b200_ivf_add_codes(poly_b200_ivf* ivf, const uint32_t* cells, const uin
  * any output may be NULL. */
 int poly_b200_ivf_get_lists(poly_b200_ivf* ivf, uint64_t* off, uint8_t* codes, int64_t* ids);
 
+/* Inverted-list file: save writes the PQ tables, coarse
+ * centroids, CSR offsets, residual codes and int64 ids as checksummed sections; load
+ * creates an index on `device` from such a file.  Errors: POLY_B200_IO (open/write),
+ * POLY_B200_FORMAT (magic, section layout, shape), POLY_B200_VERSION, POLY_B200_CORRUPT
+ * (checksum, truncation, offsets) -- the poly::errc classes (common.hpp:13-22). */
+int poly_b200_ivf_save(poly_b200_ivf* ivf, const char* path);
+int poly_b200_ivf_load(const char* path, int device, poly_b200_ivf** out);
+
 /* enumerate_cells for host queries: cells (nq x nprobe). */
 int poly_b200_ivf_probes(poly_b200_ivf* ivf, const float* queries, uint64_t nq, uint32_t nprobe, uint32_t* cells);
 

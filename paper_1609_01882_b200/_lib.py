@@ -64,6 +64,8 @@ def _load():
     L.poly_b200_debug_set_list_capacity.argtypes = [_P, _u32]
     L.poly_b200_debug_rescued.argtypes = [_P, C.POINTER(_u32)]
     L.poly_b200_ivf_debug_set_list_capacity.argtypes = [_P, _u32]
+    L.poly_b200_ivf_save.argtypes = [_P, C.c_char_p]
+    L.poly_b200_ivf_load.argtypes = [C.c_char_p, _i32, C.POINTER(_P)]
     L.poly_b200_ivf_get_cells.argtypes = [_P, _P, _u32, _P, _P, _P]
     L.poly_b200_ivf_profile_enable.argtypes = [_P, _i32]
     L.poly_b200_ivf_profile_read.argtypes = [_P, C.POINTER(_f64), C.POINTER(_u64)]
@@ -104,7 +106,8 @@ EXPORTS = [
     "poly_b200_add", "poly_b200_add_codes", "poly_b200_search_batch", "poly_b200_search_batch_device",
     "poly_b200_search_batch_device_ex", "poly_b200_ivf_search_device_ex", "poly_b200_debug_set_list_capacity",
     "poly_b200_debug_rescued", "poly_b200_ivf_debug_set_list_capacity", "poly_b200_ivf_debug_rescued",
-    "poly_b200_ivf_get_cells", "poly_b200_ivf_profile_enable", "poly_b200_ivf_profile_read",
+    "poly_b200_ivf_get_cells", "poly_b200_ivf_profile_enable", "poly_b200_ivf_profile_read", "poly_b200_ivf_save",
+    "poly_b200_ivf_load",
     "poly_b200_calibrate_threshold", "poly_b200_with_assignments", "poly_b200_get_codes",
     "poly_b200_search_keys_device", "poly_b200_merge_keys_device", "poly_b200_add_synthetic",
     "poly_b200_gen_points_device", "poly_b200_debug_lut", "poly_b200_debug_counts", "poly_b200_profile_enable", "poly_b200_profile_read",

@@ -7,6 +7,9 @@
 // list scans over probes [0,1), [1,4), [4,16), ... with the k-th key of the
 // candidates so far (K3) seeding each next round's threshold -> K3 top-k.
 #include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
 #include <mutex>
 #include <vector>
 
@@ -1015,6 +1018,154 @@ int poly_b200_ivf_search(poly_b200_ivf* iv, const float* queries, uint64_t nq, c
         if (out_counts) CK(cudaMemcpyAsync(out_counts, iv->d_ocnt, nq * 4, cudaMemcpyDeviceToHost, s));
         if (p->k && iv->n) read_stats(iv, mode, stats, s);
         else CK(cudaStreamSynchronize(s));
+    });
+}
+
+// ---- inverted-list file: a sectioned little-endian binary
+// header { magic "POLYIVF\0", u32 version, u32 m, u32 dbits, u32 dim, u32 nlist, u32 0,
+// u64 n }, then sections { char tag[8], u64 bytes, u64 fnv1a64(payload), payload } in the
+// order PQCODEBK (m x 256 x dsub fp32), PQPERMS_ (m x 256 u16), COARSE__ (nlist x dim
+// fp32), LISTOFF_ ((nlist + 1) u64), CODES___ (n x m u8, list order), IDS_____ (n i64).
+// Errors use poly::errc (common.hpp:13-22): io, format, version, corrupt.
+static const char kIvfMagic[8] = {'P', 'O', 'L', 'Y', 'I', 'V', 'F', '\0'};
+static const uint32_t kIvfVersion = 1;
+
+static uint64_t fnv1a(uint64_t h, const void* p, size_t n) {
+    const uint8_t* b = static_cast<const uint8_t*>(p);
+    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 0x100000001B3ull;
+    return h;
+}
+
+struct FileCloser {
+    void operator()(FILE* f) const { if (f) fclose(f); }
+};
+
+int poly_b200_ivf_save(poly_b200_ivf* iv, const char* path) {
+    return guard([&] {
+        require(iv && path, POLY_B200_INVALID_ARGUMENT, "null arguments");
+        std::lock_guard<std::mutex> lk(iv->mu);
+        DeviceGuard dg(iv->device);
+        rebuild_lists(iv);
+        std::unique_ptr<FILE, FileCloser> f(fopen(path, "wb"));
+        require(f != nullptr, POLY_B200_IO, std::string("cannot open ") + path + " for writing");
+        auto put = [&](const void* p, size_t n) {
+            require(n == 0 || fwrite(p, 1, n, f.get()) == n, POLY_B200_IO, "write failed");
+        };
+        const uint32_t hdr[6] = {kIvfVersion, iv->m, 8u, iv->dim, iv->nlist, 0u};
+        put(kIvfMagic, 8);
+        put(hdr, sizeof(hdr));
+        put(&iv->n, 8);
+        auto section = [&](const char* tag, const void* p, uint64_t bytes) {
+            const uint64_t h = fnv1a(0xCBF29CE484222325ull, p, bytes);
+            put(tag, 8);
+            put(&bytes, 8);
+            put(&h, 8);
+            put(p, bytes);
+        };
+        section("PQCODEBK", iv->h_codebooks.data(), iv->h_codebooks.size() * 4);
+        section("PQPERMS_", iv->h_perms.data(), iv->h_perms.size() * 2);
+        section("COARSE__", iv->h_coarse.data(), iv->h_coarse.size() * 4);
+        section("LISTOFF_", iv->h_off.data(), iv->h_off.size() * 8);
+        // codes and ids stream from the device in chunks; the checksum runs over the chunks
+        const uint64_t chunk = 1ull << 24;
+        std::vector<uint8_t> buf;
+        auto stream_section = [&](const char* tag, uint64_t elem, auto&& fill) {
+            const uint64_t bytes = iv->n * elem;
+            // checksum pass first (the header precedes the payload)
+            uint64_t h = 0xCBF29CE484222325ull;
+            for (uint64_t i = 0; i < iv->n; i += chunk) {
+                const uint64_t c = std::min(chunk, iv->n - i);
+                buf.resize(c * elem);
+                fill(i, c, buf.data());
+                h = fnv1a(h, buf.data(), c * elem);
+            }
+            put(tag, 8);
+            put(&bytes, 8);
+            put(&h, 8);
+            for (uint64_t i = 0; i < iv->n; i += chunk) {
+                const uint64_t c = std::min(chunk, iv->n - i);
+                buf.resize(c * elem);
+                fill(i, c, buf.data());
+                put(buf.data(), c * elem);
+            }
+        };
+        stream_section("CODES___", iv->cb, [&](uint64_t i, uint64_t c, uint8_t* dst) {
+            CK(cudaMemcpy(dst, iv->d_codes_list + i * iv->cb, c * iv->cb, cudaMemcpyDeviceToHost));
+        });
+        std::vector<int64_t> r2id;
+        if (iv->idm.d_rank_to_id && iv->n) {
+            r2id.resize(iv->n);
+            CK(cudaMemcpy(r2id.data(), iv->idm.d_rank_to_id, iv->n * 8, cudaMemcpyDeviceToHost));
+        }
+        std::vector<uint32_t> low;
+        stream_section("IDS_____", 8, [&](uint64_t i, uint64_t c, uint8_t* dst) {
+            low.resize(c);
+            CK(cudaMemcpy(low.data(), iv->d_low_list + i, c * 4, cudaMemcpyDeviceToHost));
+            int64_t* o = reinterpret_cast<int64_t*>(dst);
+            for (uint64_t j = 0; j < c; ++j) o[j] = r2id.empty() ? (int64_t)low[j] : r2id[low[j]];
+        });
+        require(fflush(f.get()) == 0, POLY_B200_IO, "write failed");
+    });
+}
+
+int poly_b200_ivf_load(const char* path, int device, poly_b200_ivf** out) {
+    return guard([&] {
+        require(path && out, POLY_B200_INVALID_ARGUMENT, "null arguments");
+        std::unique_ptr<FILE, FileCloser> f(fopen(path, "rb"));
+        require(f != nullptr, POLY_B200_IO, std::string("cannot open ") + path);
+        auto get = [&](void* p, size_t n) {
+            require(n == 0 || fread(p, 1, n, f.get()) == n, POLY_B200_CORRUPT, "truncated IVF list file");
+        };
+        char magic[8];
+        uint32_t hdr[6];
+        uint64_t n = 0;
+        require(fread(magic, 1, 8, f.get()) == 8 && std::memcmp(magic, kIvfMagic, 8) == 0, POLY_B200_FORMAT,
+                "not an IVF list file (bad magic)");
+        get(hdr, sizeof(hdr));
+        require(hdr[0] == kIvfVersion, POLY_B200_VERSION, "unsupported IVF list file version " + std::to_string(hdr[0]));
+        get(&n, 8);
+        const uint32_t m = hdr[1], dbits = hdr[2], dim = hdr[3], nlist = hdr[4];
+        require(dbits == 8 && (m == 8 || m == 16) && dim == 16 * m && nlist > 0, POLY_B200_FORMAT,
+                "IVF list file shape not supported on the GPU path");
+        auto section = [&](const char* tag, uint64_t want, void* p) {
+            char t[8];
+            uint64_t bytes = 0, h = 0;
+            get(t, 8);
+            require(std::memcmp(t, tag, 8) == 0, POLY_B200_FORMAT, std::string("expected section ") + std::string(tag, 8));
+            get(&bytes, 8);
+            get(&h, 8);
+            require(bytes == want, POLY_B200_FORMAT, std::string("section ") + std::string(tag, 8) + " has the wrong size");
+            get(p, bytes);
+            require(fnv1a(0xCBF29CE484222325ull, p, bytes) == h, POLY_B200_CORRUPT,
+                    std::string("checksum mismatch in section ") + std::string(tag, 8));
+        };
+        std::vector<float> cb((size_t)m * 256 * pb::DSUB), coarse((size_t)nlist * dim);
+        std::vector<uint16_t> perms((size_t)m * 256);
+        std::vector<uint64_t> off((size_t)nlist + 1);
+        section("PQCODEBK", cb.size() * 4, cb.data());
+        section("PQPERMS_", perms.size() * 2, perms.data());
+        section("COARSE__", coarse.size() * 4, coarse.data());
+        section("LISTOFF_", off.size() * 8, off.data());
+        require(off[0] == 0 && off[nlist] == n, POLY_B200_CORRUPT, "list offsets do not cover the codes");
+        for (uint32_t c = 0; c < nlist; ++c) require(off[c] <= off[c + 1], POLY_B200_CORRUPT, "list offsets decrease");
+        std::vector<uint8_t> codes(n * m);
+        std::vector<int64_t> ids(n);
+        section("CODES___", codes.size(), codes.data());
+        section("IDS_____", ids.size() * 8, ids.data());
+        const poly_b200_pq_desc pq{m, dbits, dim, cb.data(), perms.data()};
+        poly_b200_ivf* iv = nullptr;
+        int rc = poly_b200_ivf_create(&pq, coarse.data(), nlist, device, &iv);
+        if (rc != POLY_B200_OK) throw Error(rc, g_err);
+        std::vector<uint32_t> cells(n);
+        for (uint32_t c = 0; c < nlist; ++c)
+            for (uint64_t i = off[c]; i < off[c + 1]; ++i) cells[i] = c;
+        rc = poly_b200_ivf_add_codes(iv, cells.data(), codes.data(), ids.data(), n);
+        if (rc != POLY_B200_OK) {
+            const std::string msg = g_err;
+            poly_b200_ivf_destroy(iv);
+            throw Error(rc, msg);
+        }
+        *out = iv;
     });
 }
 

@@ -193,8 +193,9 @@ void launch_rescue(const ScanArgs& a, int strategy, uint32_t m, uint32_t* rcount
     }
 }
 
-// IVF (K6x): one CTA per flagged query re-scans every visited probe (np_eff[q]) with
-// that probe's residual LUT and query code, and rewrites the query's candidate list.
+// IVF (K6x): persistent CTAs; each takes the flagged queries q = blockIdx.x (mod gridDim.x)
+// and re-scans every visited probe (np_eff[q]) with that probe's residual LUT and query
+// code, rewriting the query's candidate list.
 template <int M, int STRAT>
 __global__ void __launch_bounds__(RS_THREADS) ivf_rescue_kernel(const IvfScanArgs a, const uint32_t* __restrict__ np_eff,
                                                                 uint32_t k) {
@@ -207,8 +208,9 @@ __global__ void __launch_bounds__(RS_THREADS) ivf_rescue_kernel(const IvfScanArg
                reinterpret_cast<unsigned long long*>(rs_smem + M * KSUB * 4) + RS_BUF, &cnt, hist, &prefix, &want,
                &bound};
     constexpr bool USE_LUT = (STRAT == DUAL || STRAT == ADC);
-    const uint32_t q = blockIdx.x;
-    if (!a.ovq[q]) return;
+    for (uint32_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
+    if (!__ldcg(a.ovq + q)) continue;  // uniform across the CTA
+    __syncthreads();
     if (threadIdx.x == 0) {
         cnt = 0;
         bound = a.thr[q];
@@ -242,6 +244,7 @@ __global__ void __launch_bounds__(RS_THREADS) ivf_rescue_kernel(const IvfScanArg
     const uint32_t n = min(cnt, a.cap);
     for (uint32_t i = threadIdx.x; i < n; i += RS_THREADS) a.cand[(size_t)q * a.cap + i] = st.buf[i];
     if (threadIdx.x == 0) a.ccount[q] = n;
+    }
 }
 
 template <int M, int STRAT>
@@ -249,7 +252,10 @@ static void launch_ivf_rescue_m(const IvfScanArgs& a, const uint32_t* np_eff, ui
     const size_t smem = (size_t)M * KSUB * 4 + 2 * (size_t)RS_BUF * 8;
     auto kfn = ivf_rescue_kernel<M, STRAT>;
     set_max_smem((const void*)kfn, smem);
-    kfn<<<a.nq, RS_THREADS, smem, s>>>(a, np_eff, k);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    kfn<<<std::min<uint32_t>(a.nq, (uint32_t)sms), RS_THREADS, smem, s>>>(a, np_eff, k);
     count_launch();
 }
 

@@ -33,14 +33,30 @@ class CoarseParams:
 class IVFIndex:
     """Inverted file over residual polysemous codes on one B200."""
 
-    def __init__(self, pq: ProductQuantizer, coarse, device: int = 0):
+    def __init__(self, pq: ProductQuantizer, coarse, device: int = 0, _handle=None):
         self._pq = pq
+        self.device = device
         self.coarse = np.ascontiguousarray(coarse, np.float32).reshape(-1, pq.dim)
         self.nlist = self.coarse.shape[0]
+        if _handle is not None:
+            self._h = _handle
+            return
         d = PqDesc(pq.m, pq.dbits, pq.dim, _p(pq.codebooks), _p(pq.perms))
         h = C.c_void_p()
         _check(lib.poly_b200_ivf_create(C.byref(d), _p(self.coarse), self.nlist, device, C.byref(h)))
         self._h = h
+
+    # ---- inverted-list file (DESIGN.md "IVF list file"; layout in ivf_format.py)
+    def save(self, path):
+        _check(lib.poly_b200_ivf_save(self._h, str(path).encode()))
+
+    @classmethod
+    def load(cls, path, device: int = 0):
+        from .ivf_format import read_header_tables
+        h = C.c_void_p()
+        _check(lib.poly_b200_ivf_load(str(path).encode(), device, C.byref(h)))
+        m, dim, codebooks, perms, coarse = read_header_tables(path)
+        return cls(ProductQuantizer(m, 8, dim, codebooks, perms), coarse, device, _handle=h)
 
     def __del__(self):
         h = getattr(self, "_h", None)
