@@ -643,6 +643,7 @@ def run_ivf(args, rank, world, local):
     ivf, pq = build_ivf(args, pb, torch, local, row0, row1, coarse, centers, False)
     setup_s = time.time() - t
     nq, B, k, M = c["nq"], args.batch, args.k, c["m"]
+    ivf.set_batch(B)  # one internal batch per step: the cell-major scan groups the step's queries per list
     dq = torch.empty((nq, c["dim"]), dtype=torch.float32, device="cuda")
     pb.gen_points_device(centers, SEED, 3, 0, nq, dq, device=local)
     stream = torch.cuda.current_stream()
@@ -786,6 +787,7 @@ def run_knn(args, rank, world, local):
     setup_s = time.time() - t
     row0, row1 = shard_range(args.n, world, rank)   # this rank's query rows (cfg4 shards the query set)
     k, B, M = args.k, args.batch, c["m"]
+    ivf.set_batch(B)
     p = pb.CoarseParams(pb.Strategy.dual, k, args.ht, args.nprobe, 0)
     p1 = pb.CoarseParams(pb.Strategy.dual, k + 1, args.ht, args.nprobe, 0)
     stream = torch.cuda.current_stream()

@@ -283,6 +283,15 @@ int poly_b200_ivf_get_cells(poly_b200_ivf* ivf, const uint32_t* cells, uint32_t 
 int poly_b200_ivf_profile_enable(poly_b200_ivf* ivf, int enable);
 int poly_b200_ivf_profile_read(poly_b200_ivf* ivf, double* scan_ms, uint64_t* scan_launches);
 
+/* Queries per internal batch (default 2048).  A larger batch groups more (query, probe)
+ * pairs on each inverted list, so the cell-major list scan reads a list once for more
+ * queries (codes reused across the group), at the cost of scratch memory that grows
+ * with the batch (probe keys, residual LUTs, candidate lists).  Setting it waits for
+ * outstanding searches and frees the batch-sized scratch; no reference equivalent
+ * (search_coarse SPEC.md:382-390 takes one query at a time). */
+int poly_b200_ivf_set_batch(poly_b200_ivf* ivf, uint32_t queries_per_batch);
+uint32_t poly_b200_ivf_batch(const poly_b200_ivf* ivf);
+
 int poly_b200_ivf_debug_set_list_capacity(poly_b200_ivf* ivf, uint32_t cap);
 int poly_b200_ivf_debug_rescued(poly_b200_ivf* ivf, uint32_t* n_rescued);
 
@@ -293,6 +302,29 @@ int poly_b200_ivf_debug_rescued(poly_b200_ivf* ivf, uint32_t* n_rescued);
 int poly_b200_ivf_knn_graph_device(poly_b200_ivf* ivf, const float* d_x, uint64_t n, int64_t id0,
                                    const poly_b200_ivf_params* params, int64_t* d_out_ids, float* d_out_scores,
                                    uint32_t* d_out_counts, void* stream);
+
+/* ---- one FlatIndex over several GPUs of one process (SURVEY.md sec. 8(b) create(pq, n_gpus))
+ * The drop-in for a FlatIndex whose database is sharded across the GPUs of a node,
+ * driven by one host process (no torch.distributed): `devices` lists the CUDA
+ * ordinals, one shard each (an ordinal may repeat: several shards on one GPU).
+ * add / add_codes (flat_index.hpp:115-119) split every call's rows into n_devices
+ * contiguous parts, part g to shard g, each row keeping its global id (NULL ids =
+ * size() + i).  search_batch (flat_index.hpp:124-126) runs every shard concurrently
+ * on its own device, copies the per-shard top-k lists to devices[0] over peer memory
+ * and merges them there in (score, id) order: the result equals the single-index
+ * search over the union of the shards.  Statistics are summed over the shards. */
+typedef struct poly_b200_sharded poly_b200_sharded;
+int poly_b200_sharded_create(const poly_b200_pq_desc* pq, const int* devices, uint32_t n_devices,
+                             poly_b200_sharded** out);
+int poly_b200_sharded_destroy(poly_b200_sharded* index);
+uint64_t poly_b200_sharded_size(const poly_b200_sharded* index);
+uint32_t poly_b200_sharded_count(const poly_b200_sharded* index);
+int poly_b200_sharded_shard_size(const poly_b200_sharded* index, uint32_t shard, uint64_t* n);
+int poly_b200_sharded_add(poly_b200_sharded* index, const float* x, uint64_t n, const int64_t* ids);
+int poly_b200_sharded_add_codes(poly_b200_sharded* index, const uint8_t* codes, const int64_t* ids, uint64_t n);
+int poly_b200_sharded_search_batch(poly_b200_sharded* index, const float* queries, uint64_t nq,
+                                   const poly_b200_search_params* params, int64_t* out_ids, float* out_scores,
+                                   uint32_t* out_counts, poly_b200_search_stats* stats);
 
 /* Number of kernel launches this library has issued so far (for bench.py). */
 uint64_t poly_b200_launch_count(void);

@@ -193,4 +193,64 @@ private:
     poly_b200_index* h_ = nullptr;
 };
 
+/// FlatIndex over several GPUs of this process (poly_b200_sharded_*): one shard per
+/// entry of `devices`; add / add_codes split their rows across the shards, search
+/// merges the per-shard top-k on devices[0].  Same results as FlatIndex over the union.
+class ShardedFlatIndex {
+public:
+    ShardedFlatIndex(ProductQuantizer pq, const std::vector<int>& devices) : pq_(std::move(pq)) {
+        poly_b200_pq_desc d{pq_.m, pq_.dbits, pq_.dim, pq_.codebooks.data(), pq_.perms.data()};
+        check(poly_b200_sharded_create(&d, devices.data(), static_cast<std::uint32_t>(devices.size()), &h_));
+    }
+    ShardedFlatIndex(const ShardedFlatIndex&) = delete;
+    ShardedFlatIndex& operator=(const ShardedFlatIndex&) = delete;
+    ~ShardedFlatIndex() { poly_b200_sharded_destroy(h_); }
+
+    const ProductQuantizer& pq() const { return pq_; }
+    std::size_t size() const { return poly_b200_sharded_size(h_); }
+    std::size_t shards() const { return poly_b200_sharded_count(h_); }
+
+    void add(const VectorSet& x, unsigned /*threads*/ = 0) {
+        if (x.dim != pq_.dim) throw error(errc::invalid_argument, "encode dimension mismatch");
+        check(poly_b200_sharded_add(h_, x.data.data(), x.size(), x.ids.empty() ? nullptr : x.ids.data()));
+    }
+    void add_codes(const std::uint8_t* codes, const std::int64_t* ids, std::size_t n) {
+        check(poly_b200_sharded_add_codes(h_, codes, ids, n));
+    }
+
+    std::vector<Neighbor> search(const float* query, const SearchParams& params, SearchStats* stats = nullptr) const {
+        return std::move(run(query, 1, params, stats)[0]);
+    }
+    std::vector<std::vector<Neighbor>> search_batch(const VectorSet& queries, const SearchParams& params,
+                                                    unsigned /*threads*/ = 0,
+                                                    SearchStats* total_stats = nullptr) const {
+        if (queries.dim != pq_.dim) throw error(errc::invalid_argument, "query dimension mismatch");
+        return run(queries.data.data(), queries.size(), params, total_stats);
+    }
+
+private:
+    std::vector<std::vector<Neighbor>> run(const float* q, std::size_t nq, const SearchParams& p,
+                                           SearchStats* stats) const {
+        const poly_b200_search_params cp{static_cast<std::int32_t>(p.strategy), p.k, p.tau};
+        std::vector<std::int64_t> ids(nq * p.k);
+        std::vector<float> scores(nq * p.k);
+        std::vector<std::uint32_t> counts(nq);
+        poly_b200_search_stats st{0, 0};
+        check(poly_b200_sharded_search_batch(h_, q, nq, &cp, ids.data(), scores.data(), counts.data(), &st));
+        if (stats) {
+            stats->scanned += st.scanned;
+            stats->survivors += st.survivors;
+        }
+        std::vector<std::vector<Neighbor>> out(nq);
+        for (std::size_t i = 0; i < nq; ++i) {
+            out[i].resize(counts[i]);
+            for (std::uint32_t r = 0; r < counts[i]; ++r) out[i][r] = {ids[i * p.k + r], scores[i * p.k + r]};
+        }
+        return out;
+    }
+
+    ProductQuantizer pq_;
+    poly_b200_sharded* h_ = nullptr;
+};
+
 }  // namespace poly_b200

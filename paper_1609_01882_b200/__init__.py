@@ -6,9 +6,9 @@ over the C ABI of libpoly_b200.so (include/poly_b200.h); hand-written sm_100a
 kernels in csrc/.  See DESIGN.md.
 """
 from .flat_index import (Errc, FlatIndex, Neighbor, PolyError, ProductQuantizer, SearchParams, SearchStats,
-                         Strategy, gen_points_device, launch_count, strategy_from_string, to_string)
+                         ShardedFlatIndex, Strategy, gen_points_device, launch_count, strategy_from_string, to_string)
 
 from .ivf_index import CoarseParams, IVFIndex
 
 __all__ = ["CoarseParams", "IVFIndex", "Errc", "FlatIndex", "Neighbor", "PolyError", "ProductQuantizer", "SearchParams", "SearchStats",
-           "Strategy", "gen_points_device", "launch_count", "strategy_from_string", "to_string"]
+           "ShardedFlatIndex", "Strategy", "gen_points_device", "launch_count", "strategy_from_string", "to_string"]

@@ -64,6 +64,20 @@ def _load():
     L.poly_b200_debug_set_list_capacity.argtypes = [_P, _u32]
     L.poly_b200_debug_rescued.argtypes = [_P, C.POINTER(_u32)]
     L.poly_b200_ivf_debug_set_list_capacity.argtypes = [_P, _u32]
+    L.poly_b200_sharded_create.argtypes = [C.POINTER(PqDesc), _P, _u32, C.POINTER(_P)]
+    L.poly_b200_sharded_destroy.argtypes = [_P]
+    L.poly_b200_sharded_size.argtypes = [_P]
+    L.poly_b200_sharded_size.restype = _u64
+    L.poly_b200_sharded_count.argtypes = [_P]
+    L.poly_b200_sharded_count.restype = _u32
+    L.poly_b200_sharded_shard_size.argtypes = [_P, _u32, C.POINTER(_u64)]
+    L.poly_b200_sharded_add.argtypes = [_P, _P, _u64, _P]
+    L.poly_b200_sharded_add_codes.argtypes = [_P, _P, _P, _u64]
+    L.poly_b200_sharded_search_batch.argtypes = [_P, _P, _u64, C.POINTER(SearchParamsC), _P, _P, _P,
+                                                 C.POINTER(SearchStatsC)]
+    L.poly_b200_ivf_set_batch.argtypes = [_P, _u32]
+    L.poly_b200_ivf_batch.argtypes = [_P]
+    L.poly_b200_ivf_batch.restype = _u32
     L.poly_b200_ivf_save.argtypes = [_P, C.c_char_p]
     L.poly_b200_ivf_load.argtypes = [C.c_char_p, _i32, C.POINTER(_P)]
     L.poly_b200_ivf_get_cells.argtypes = [_P, _P, _u32, _P, _P, _P]
@@ -107,7 +121,10 @@ EXPORTS = [
     "poly_b200_search_batch_device_ex", "poly_b200_ivf_search_device_ex", "poly_b200_debug_set_list_capacity",
     "poly_b200_debug_rescued", "poly_b200_ivf_debug_set_list_capacity", "poly_b200_ivf_debug_rescued",
     "poly_b200_ivf_get_cells", "poly_b200_ivf_profile_enable", "poly_b200_ivf_profile_read", "poly_b200_ivf_save",
-    "poly_b200_ivf_load",
+    "poly_b200_ivf_load", "poly_b200_ivf_set_batch", "poly_b200_ivf_batch",
+    "poly_b200_sharded_create", "poly_b200_sharded_destroy", "poly_b200_sharded_size", "poly_b200_sharded_count",
+    "poly_b200_sharded_shard_size", "poly_b200_sharded_add", "poly_b200_sharded_add_codes",
+    "poly_b200_sharded_search_batch",
     "poly_b200_calibrate_threshold", "poly_b200_with_assignments", "poly_b200_get_codes",
     "poly_b200_search_keys_device", "poly_b200_merge_keys_device", "poly_b200_add_synthetic",
     "poly_b200_gen_points_device", "poly_b200_debug_lut", "poly_b200_debug_counts", "poly_b200_profile_enable", "poly_b200_profile_read",

@@ -51,10 +51,11 @@ struct poly_b200_ivf {
     uint64_t max_list = 0;
 
     // search scratch
-    unsigned long long* ckeys = nullptr;  // K5 (nprobe > 1024): IVF_NQB x nlist exact keys (lazy)
+    uint32_t nqb = IVF_NQB;               // queries per batch (poly_b200_ivf_set_batch)
+    unsigned long long* ckeys = nullptr;  // K5 (nprobe > 1024): nqb x nlist exact keys (lazy)
     uint32_t* nl_counts = nullptr;         // K3 counts of K5: nlist per query
     float4* grp = nullptr;                 // K5t: per (group of 128 cells, query) kept values
-    uint32_t* rank_scratch = nullptr;      // K5q: per-query candidate cells (IVF_NQB x nlist)
+    uint32_t* rank_scratch = nullptr;      // K5q: per-query candidate cells (nqb x nlist)
     unsigned long long* probe_keys = nullptr;
     uint32_t* probe_counts = nullptr;
     uint32_t* np_eff = nullptr;
@@ -63,6 +64,11 @@ struct poly_b200_ivf {
     uint32_t scratch_nprobe = 0;
     uint4* items[2] = {nullptr, nullptr};  // K6 work lists of the two rounds
     uint64_t items_cap[2] = {0, 0};
+    // K6g (cell-major list scan): per-cell counts / cursors, cell-sorted items, units
+    uint32_t* cw_ccnt = nullptr;
+    uint32_t* cw_sorted = nullptr;
+    uint4* cw_units = nullptr;
+    uint64_t cw_units_cap = 0, cw_sorted_cap = 0;
     float* lutp = nullptr;
     uint8_t* qcodes = nullptr;
     unsigned long long* cand = nullptr;
@@ -133,6 +139,18 @@ constexpr uint64_t IVF_R1_CODES = POLY_IVF_R1_CODES;  // ... and at least this m
 #endif
 constexpr uint32_t IVF_CHUNK = POLY_IVF_CHUNK;    // K6 round-1 work item: 1024 list rows (K6 scans it in 128-row warp blocks)
 constexpr uint32_t IVF_CHUNK2 = POLY_IVF_CHUNK2;  // round 2: longer items (fewer LUT loads per code)
+#ifndef POLY_IVF_CELL  // 1: K6g cell-major list scan (codes read once per group of queries probing a cell)
+#define POLY_IVF_CELL 1
+#endif
+#ifndef POLY_IVF_CELL_ROWS0
+#define POLY_IVF_CELL_ROWS0 2048
+#endif
+#ifndef POLY_IVF_CELL_ROWS1
+#define POLY_IVF_CELL_ROWS1 4096
+#endif
+constexpr bool IVF_CELL = POLY_IVF_CELL != 0;
+constexpr uint32_t IVF_CELL_ROWS0 = POLY_IVF_CELL_ROWS0;  // K6g unit rows, round 1
+constexpr uint32_t IVF_CELL_ROWS1 = POLY_IVF_CELL_ROWS1;  // round 2
 
 __global__ void fill_u32(uint32_t* p, uint64_t n, uint32_t v) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
@@ -211,19 +229,19 @@ void rebuild_lists(poly_b200_ivf* iv) {
 
 void ensure_ivf_scratch(poly_b200_ivf* iv, uint32_t nprobe, uint32_t k) {
     if (!iv->np_eff) {
-        iv->grp = dalloc<float4>((size_t)IVF_NQB * 2 * pb::coarse_tc_tiles(iv->nlist));
-        iv->rank_scratch = dalloc<uint32_t>((size_t)IVF_NQB * iv->nlist);
-        iv->np_eff = dalloc<uint32_t>(IVF_NQB);
-        iv->split = dalloc<uint32_t>(IVF_NQB);
-        iv->scanned = dalloc<unsigned long long>(IVF_NQB);
-        iv->ctrl = dalloc<uint32_t>(IVF_NQB + 32);
-        iv->thr = dalloc<unsigned long long>(IVF_NQB);
-        iv->kcounts = dalloc<uint32_t>(IVF_NQB);
+        iv->grp = dalloc<float4>((size_t)iv->nqb * 2 * pb::coarse_tc_tiles(iv->nlist));
+        iv->rank_scratch = dalloc<uint32_t>((size_t)iv->nqb * iv->nlist);
+        iv->np_eff = dalloc<uint32_t>(iv->nqb);
+        iv->split = dalloc<uint32_t>(iv->nqb);
+        iv->scanned = dalloc<unsigned long long>(iv->nqb);
+        iv->ctrl = dalloc<uint32_t>(iv->nqb + 32);
+        iv->thr = dalloc<unsigned long long>(iv->nqb);
+        iv->kcounts = dalloc<uint32_t>(iv->nqb);
         iv->surv_total = dalloc<unsigned long long>(1);
         iv->scan_total = dalloc<unsigned long long>(1);
-        iv->ovq = dalloc<uint32_t>(IVF_NQB);
-        iv->surv_q = dalloc<unsigned long long>(IVF_NQB);
-        iv->hash_q = dalloc<unsigned long long>(IVF_NQB);
+        iv->ovq = dalloc<uint32_t>(iv->nqb);
+        iv->surv_q = dalloc<unsigned long long>(iv->nqb);
+        iv->hash_q = dalloc<unsigned long long>(iv->nqb);
         iv->sticky_overflow = dalloc<uint32_t>(1);
         CK(cudaMallocHost(&iv->h_overflow, sizeof(uint32_t)));
         *iv->h_overflow = 0;
@@ -235,35 +253,58 @@ void ensure_ivf_scratch(poly_b200_ivf* iv, uint32_t nprobe, uint32_t k) {
         dfree(iv->lutp);
         dfree(iv->qcodes);
         iv->scratch_nprobe = nprobe;
-        iv->probe_keys = dalloc<unsigned long long>((size_t)IVF_NQB * nprobe);
-        iv->probe_counts = dalloc<uint32_t>(IVF_NQB);
-        iv->lutp = dalloc<float>((size_t)IVF_NQB * nprobe * iv->m * 256);
-        iv->qcodes = dalloc<uint8_t>((size_t)IVF_NQB * nprobe * iv->cb);
+        iv->probe_keys = dalloc<unsigned long long>((size_t)iv->nqb * nprobe);
+        iv->probe_counts = dalloc<uint32_t>(iv->nqb);
+        iv->lutp = dalloc<float>((size_t)iv->nqb * nprobe * iv->m * 256);
+        iv->qcodes = dalloc<uint8_t>((size_t)iv->nqb * nprobe * iv->cb);
     }
-    // work-list bounds per query: round 1 <= r1 probes -> <= r1 + r1 * max_list / CHUNK items;
-    // round 2 <= np + min(n, np * max_list) / CHUNK2 items
     const uint64_t r1 = std::min<uint64_t>(nprobe, IVF_R1_MAX);
-    const uint64_t need[2] = {
-        (uint64_t)IVF_NQB * (r1 + (r1 * iv->max_list + IVF_CHUNK - 1) / IVF_CHUNK),
-        (uint64_t)IVF_NQB * (nprobe + r1 + (std::min<uint64_t>(iv->n, nprobe * iv->max_list) + IVF_CHUNK2 - 1) / IVF_CHUNK2)};
-    for (int r = 0; r < 2; ++r)
-        if (iv->items_cap[r] < need[r]) {
-            require(need[r] < (1ull << 32), POLY_B200_INVALID_ARGUMENT, "IVF work list too large");
-            dfree(iv->items[r]);
-            iv->items_cap[r] = need[r];
-            iv->items[r] = dalloc<uint4>(need[r]);
+    if (IVF_CELL) {
+        // K6g units of a round: sum over cells of ceil(cnt / G) * ceil(len / R)
+        //   <= scanned / (G R) + n / R + items / G + min(nlist, items) + 1, scanned <= nqb * min(n, np * max_list)
+        const uint64_t items = (uint64_t)iv->nqb * nprobe, G = pb::cell_scan_group(iv->m);
+        const uint64_t R = std::min<uint32_t>(IVF_CELL_ROWS0, IVF_CELL_ROWS1);
+        const uint64_t scanned = (uint64_t)iv->nqb * std::min<uint64_t>(iv->n, nprobe * iv->max_list);
+        const uint64_t need = scanned / (G * R) + iv->n / R + items / G + std::min<uint64_t>(iv->nlist, items) + 16;
+        require(need < (1ull << 32) && items < (1ull << 32), POLY_B200_INVALID_ARGUMENT, "IVF work list too large");
+        if (!iv->cw_ccnt) iv->cw_ccnt = dalloc<uint32_t>(iv->nlist);
+        if (iv->cw_sorted_cap < items) {
+            dfree(iv->cw_sorted);
+            iv->cw_sorted_cap = items;
+            iv->cw_sorted = dalloc<uint32_t>(items);
         }
-    uint32_t cap = (uint32_t)std::max<uint64_t>(131072, 4 * iv->max_list);
+        if (iv->cw_units_cap < need) {
+            dfree(iv->cw_units);
+            iv->cw_units_cap = need;
+            iv->cw_units = dalloc<uint4>(need);
+        }
+    } else {
+        // work-list bounds per query: round 1 <= r1 probes -> <= r1 + r1 * max_list / CHUNK items;
+        // round 2 <= np + min(n, np * max_list) / CHUNK2 items
+        const uint64_t need[2] = {
+            (uint64_t)iv->nqb * (r1 + (r1 * iv->max_list + IVF_CHUNK - 1) / IVF_CHUNK),
+            (uint64_t)iv->nqb * (nprobe + r1 + (std::min<uint64_t>(iv->n, nprobe * iv->max_list) + IVF_CHUNK2 - 1) / IVF_CHUNK2)};
+        for (int r = 0; r < 2; ++r)
+            if (iv->items_cap[r] < need[r]) {
+                require(need[r] < (1ull << 32), POLY_B200_INVALID_ARGUMENT, "IVF work list too large");
+                dfree(iv->items[r]);
+                iv->items_cap[r] = need[r];
+                iv->items[r] = dalloc<uint4>(need[r]);
+            }
+    }
+    // round 1 runs without a bound: its <= r1 probes' survivors must fit (round 2 is bounded
+    // by round 1's k-th key; a list that still fills up is re-ranked by the rescue scan)
+    uint32_t cap = (uint32_t)std::max<uint64_t>(131072, r1 * iv->max_list + k);
     if (iv->cap_override) cap = std::max<uint32_t>(iv->cap_override, k);
     if (iv->cand_cap != cap) {
         dfree(iv->cand);
         iv->cand_cap = cap;
-        iv->cand = dalloc<unsigned long long>((size_t)IVF_NQB * cap);
+        iv->cand = dalloc<unsigned long long>((size_t)iv->nqb * cap);
     }
     if (iv->keys_k < k) {
         dfree(iv->keys);
         iv->keys_k = k;
-        iv->keys = dalloc<unsigned long long>((size_t)IVF_NQB * k);
+        iv->keys = dalloc<unsigned long long>((size_t)iv->nqb * k);
     }
 }
 
@@ -302,9 +343,9 @@ void enumerate_cells(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, uint32_t
         return;
     }
     if (!iv->ckeys) {
-        iv->ckeys = dalloc<unsigned long long>((size_t)IVF_NQB * iv->nlist);
-        iv->nl_counts = dalloc<uint32_t>(IVF_NQB);
-        fill_u32<<<1, 256, 0, s>>>(iv->nl_counts, IVF_NQB, iv->nlist);
+        iv->ckeys = dalloc<unsigned long long>((size_t)iv->nqb * iv->nlist);
+        iv->nl_counts = dalloc<uint32_t>(iv->nqb);
+        fill_u32<<<1, 256, 0, s>>>(iv->nl_counts, iv->nqb, iv->nlist);
         pb::count_launch();
     }
     pb::launch_coarse_keys(d_q, nqb, iv->dim, iv->d_coarse, iv->nlist, iv->ckeys, s);
@@ -320,27 +361,27 @@ void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_
     const uint32_t np = std::min(p->nprobe, iv->nlist);
     int strategy = p->strategy;
     if (strategy == pb::DUAL && p->tau >= iv->code_bits()) strategy = pb::ADC;  // SPEC.md:388 boundary
-    CK(cudaMemsetAsync(iv->ctrl, 0, (IVF_NQB + 32) * 4, s));
-    CK(cudaMemsetAsync(iv->ovq, 0, IVF_NQB * 4, s));
-    CK(cudaMemsetAsync(iv->thr, 0xFF, IVF_NQB * 8, s));
+    CK(cudaMemsetAsync(iv->ctrl, 0, (iv->nqb + 32) * 4, s));
+    CK(cudaMemsetAsync(iv->ovq, 0, iv->nqb * 4, s));
+    CK(cudaMemsetAsync(iv->thr, 0xFF, iv->nqb * 8, s));
     const bool perq = d_surv || d_hash;
     if (perq) {
-        CK(cudaMemsetAsync(iv->surv_q, 0, IVF_NQB * 8, s));
-        CK(cudaMemsetAsync(iv->hash_q, 0, IVF_NQB * 8, s));
+        CK(cudaMemsetAsync(iv->surv_q, 0, iv->nqb * 8, s));
+        CK(cudaMemsetAsync(iv->hash_q, 0, iv->nqb * 8, s));
     }
     if (d_probes_in)  // probes computed elsewhere (the coarse quantization split by query over ranks)
         CK(cudaMemcpyAsync(iv->probe_keys, d_probes_in, (size_t)nqb * np * 8, cudaMemcpyDeviceToDevice, s));
     else
         enumerate_cells(iv, d_q, nqb, np, s);
     pb::IvfWork w{};
-    w.items[0] = iv->items[0];
-    w.items[1] = iv->items[1];
-    w.nitems = iv->ctrl + IVF_NQB + 3;
+    w.items[0] = IVF_CELL ? nullptr : iv->items[0];  // K6g plans its own work (cw_plan)
+    w.items[1] = IVF_CELL ? nullptr : iv->items[1];
+    w.nitems = iv->ctrl + iv->nqb + 3;
     w.cap[0] = (uint32_t)iv->items_cap[0];
     w.cap[1] = (uint32_t)iv->items_cap[1];
     w.chunk[0] = IVF_CHUNK;
     w.chunk[1] = IVF_CHUNK2;
-    w.overflow = iv->ctrl + IVF_NQB;
+    w.overflow = iv->ctrl + iv->nqb;
     pb::launch_ivf_probe_count(iv->probe_keys, nqb, np, iv->d_off, p->cap, iv->np_eff, iv->scanned, s, iv->split,
                                IVF_R1_CODES, IVF_R1_MAX, w);
     add_u64<<<1, 256, 0, s>>>(iv->scanned, nqb, iv->scan_total);
@@ -383,11 +424,32 @@ void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_
     // 1024-row chunks; its exact k-th key (K3) bounds round 2, the remaining probes
     const uint32_t rounds = np <= 1 ? 1 : 2;  // one probe: round 1 sees everything
     for (uint32_t round = 0; round < rounds; ++round) {
+        pb::CellWork cw{};
+        if (IVF_CELL) {  // group the round's (query, probe) items by cell
+            cw.probe_keys = iv->probe_keys;
+            cw.nq = nqb;
+            cw.nprobe = np;
+            cw.np_eff = iv->np_eff;
+            cw.split = rounds > 1 ? iv->split : nullptr;
+            cw.round = round;
+            cw.ccnt = iv->cw_ccnt;
+            cw.sorted = iv->cw_sorted;
+            cw.units = iv->cw_units;
+            cw.units_cap = (uint32_t)iv->cw_units_cap;
+            cw.nunits = iv->ctrl + iv->nqb + 5 + round;
+            cw.work = iv->ctrl + iv->nqb + 7 + round;
+            cw.overflow = iv->ctrl + iv->nqb;
+            cw.g = pb::cell_scan_group(iv->m);
+            cw.rows = round ? IVF_CELL_ROWS1 : IVF_CELL_ROWS0;
+            CK(cudaMemsetAsync(iv->cw_ccnt, 0, (size_t)iv->nlist * 4, s));
+            pb::launch_cell_plan(cw, iv->d_off, iv->nlist, s);
+        } else {
+            a.items = iv->items[round];
+            a.nitems = w.nitems + round;
+            a.items_cap = w.cap[round];
+            a.work = iv->ctrl + iv->nqb + 1 + round;
+        }
         if (round == 1 && side) CK(cudaStreamWaitEvent(s, iv->ev_join, 0));
-        a.items = iv->items[round];
-        a.nitems = w.nitems + round;
-        a.items_cap = w.cap[round];
-        a.work = iv->ctrl + IVF_NQB + 1 + round;
         cudaEvent_t e1 = nullptr;
         if (iv->profiling) {
             if (iv->prof_used == iv->prof_events.size()) {
@@ -399,7 +461,8 @@ void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_
             CK(cudaEventRecord(iv->prof_events[iv->prof_used].first, s));
             e1 = iv->prof_events[iv->prof_used++].second;
         }
-        pb::launch_ivf_scan(a, strategy, iv->m, iv->num_sms, s);
+        if (IVF_CELL) pb::launch_ivf_cell_scan(a, cw, strategy, iv->m, iv->num_sms, s);
+        else pb::launch_ivf_scan(a, strategy, iv->m, iv->num_sms, s);
         if (e1) CK(cudaEventRecord(e1, s));
         // a query whose list overflowed (in either round) is re-ranked exactly over all its
         // visited probes (no-op for the others)
@@ -408,7 +471,7 @@ void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_
         if (round == 0 && np > 1)  // bound round 2; keep only round 1's top-k as candidates
             pb::launch_seed_compact(iv->keys, iv->kcounts, nqb, k, iv->thr, iv->cand, iv->cand_cap, iv->ctrl, s);
     }
-    pb::launch_or_flag(iv->sticky_overflow, iv->ctrl + IVF_NQB, s);
+    pb::launch_or_flag(iv->sticky_overflow, iv->ctrl + iv->nqb, s);
     if (perq) {
         if (d_surv) CK(cudaMemcpyAsync(d_surv, iv->surv_q, (size_t)nqb * 8, cudaMemcpyDeviceToDevice, s));
         if (d_hash) CK(cudaMemcpyAsync(d_hash, iv->hash_q, (size_t)nqb * 8, cudaMemcpyDeviceToDevice, s));
@@ -446,8 +509,8 @@ int device_search(poly_b200_ivf* iv, const float* d_q, uint64_t nq, const poly_b
     CK(cudaMemsetAsync(iv->surv_total, 0, 8, s));
     CK(cudaMemsetAsync(iv->scan_total, 0, 8, s));
     CK(cudaMemsetAsync(iv->sticky_overflow, 0, 4, s));
-    for (uint64_t b0 = 0; b0 < nq; b0 += IVF_NQB) {
-        const uint32_t nqb = (uint32_t)std::min<uint64_t>(IVF_NQB, nq - b0);
+    for (uint64_t b0 = 0; b0 < nq; b0 += iv->nqb) {
+        const uint32_t nqb = (uint32_t)std::min<uint64_t>(iv->nqb, nq - b0);
         const uint64_t* pr = d_probes ? d_probes + b0 * std::min(p->nprobe, iv->nlist) : nullptr;
         uint64_t* sv = d_surv ? d_surv + b0 : nullptr;
         uint64_t* hv = d_hash ? d_hash + b0 : nullptr;
@@ -592,7 +655,7 @@ int poly_b200_ivf_destroy(poly_b200_ivf* iv) {
                             (void*)iv->d_oid, (void*)iv->d_osc, (void*)iv->d_ocnt,
                             (void*)iv->knn_ids, (void*)iv->knn_sc, (void*)iv->knn_cnt, (void*)iv->d_cnorm, (void*)iv->items[0],
                             (void*)iv->d_cpacked, (void*)iv->grp, (void*)iv->rank_scratch,
-                            (void*)iv->items[1]})
+                            (void*)iv->items[1], (void*)iv->cw_ccnt, (void*)iv->cw_sorted, (void*)iv->cw_units})
                 dfree(p);
             if (iv->h_overflow) cudaFreeHost(iv->h_overflow);
             for (auto& pe : iv->prof_events) {
@@ -783,6 +846,43 @@ int poly_b200_ivf_get_cells(poly_b200_ivf* iv, const uint32_t* cells, uint32_t n
     });
 }
 
+int poly_b200_ivf_set_batch(poly_b200_ivf* iv, uint32_t nqb) {
+    return guard([&] {
+        require(iv != nullptr, POLY_B200_INVALID_ARGUMENT, "null index");
+        require(nqb >= 1 && nqb <= (1u << 20), POLY_B200_INVALID_ARGUMENT, "batch must be in [1, 2^20]");
+        std::lock_guard<std::mutex> lk(iv->mu);
+        DeviceGuard dg(iv->device);
+        if (nqb == iv->nqb) return;
+        check_pending(iv, true);
+        CK(cudaStreamSynchronize(iv->stream));
+        CK(cudaStreamSynchronize(iv->side));
+        CK(cudaDeviceSynchronize());  // callers' streams may still read the scratch
+        // every buffer sized by the batch is reallocated lazily at the next search
+        for (void** pp : {(void**)&iv->ckeys, (void**)&iv->nl_counts, (void**)&iv->grp, (void**)&iv->rank_scratch,
+                          (void**)&iv->probe_keys, (void**)&iv->probe_counts, (void**)&iv->np_eff, (void**)&iv->split,
+                          (void**)&iv->scanned, (void**)&iv->items[0], (void**)&iv->items[1], (void**)&iv->lutp,
+                          (void**)&iv->qcodes, (void**)&iv->cand, (void**)&iv->ctrl, (void**)&iv->thr,
+                          (void**)&iv->keys, (void**)&iv->kcounts, (void**)&iv->surv_total, (void**)&iv->scan_total,
+                          (void**)&iv->ovq, (void**)&iv->surv_q, (void**)&iv->hash_q, (void**)&iv->sticky_overflow,
+                          (void**)&iv->cw_sorted, (void**)&iv->cw_units}) {
+            dfree(*pp);
+            *pp = nullptr;
+        }
+        if (iv->h_overflow) cudaFreeHost(iv->h_overflow);
+        iv->h_overflow = nullptr;
+        if (iv->done_ev) cudaEventDestroy(iv->done_ev);
+        iv->done_ev = nullptr;
+        iv->scratch_nprobe = 0;
+        iv->items_cap[0] = iv->items_cap[1] = 0;
+        iv->cw_units_cap = iv->cw_sorted_cap = 0;
+        iv->cand_cap = 0;
+        iv->keys_k = 0;
+        iv->nqb = nqb;
+    });
+}
+
+uint32_t poly_b200_ivf_batch(const poly_b200_ivf* iv) { return iv ? iv->nqb : 0; }
+
 int poly_b200_ivf_debug_set_list_capacity(poly_b200_ivf* iv, uint32_t cap) {
     return guard([&] {
         require(iv != nullptr, POLY_B200_INVALID_ARGUMENT, "null index");
@@ -798,8 +898,8 @@ int poly_b200_ivf_debug_rescued(poly_b200_ivf* iv, uint32_t* n) {
         DeviceGuard dg(iv->device);
         require(iv->ovq != nullptr, POLY_B200_STATE, "no search has run");
         CK(cudaDeviceSynchronize());
-        std::vector<uint32_t> ovq(IVF_NQB);
-        CK(cudaMemcpy(ovq.data(), iv->ovq, IVF_NQB * 4, cudaMemcpyDeviceToHost));
+        std::vector<uint32_t> ovq(iv->nqb);
+        CK(cudaMemcpy(ovq.data(), iv->ovq, iv->nqb * 4, cudaMemcpyDeviceToHost));
         *n = 0;
         for (uint32_t v : ovq) *n += v != 0;
     });
@@ -815,11 +915,11 @@ int poly_b200_ivf_probes(poly_b200_ivf* iv, const float* queries, uint64_t nq, u
         ensure_ivf_scratch(iv, nprobe, 1);
         cudaStream_t s = iv->stream;
         float* d_q = dalloc<float>(std::max<uint64_t>(nq, 1) * iv->dim);
-        uint32_t* d_c = dalloc<uint32_t>((size_t)IVF_NQB * nprobe);
+        uint32_t* d_c = dalloc<uint32_t>((size_t)iv->nqb * nprobe);
         cudaError_t e = cudaSuccess;
         if (nq) e = cudaMemcpyAsync(d_q, queries, nq * iv->dim * 4, cudaMemcpyHostToDevice, s);
-        for (uint64_t b0 = 0; b0 < nq && e == cudaSuccess; b0 += IVF_NQB) {
-            const uint32_t nqb = (uint32_t)std::min<uint64_t>(IVF_NQB, nq - b0);
+        for (uint64_t b0 = 0; b0 < nq && e == cudaSuccess; b0 += iv->nqb) {
+            const uint32_t nqb = (uint32_t)std::min<uint64_t>(iv->nqb, nq - b0);
             enumerate_cells(iv, d_q + b0 * iv->dim, nqb, nprobe, s);
             probes_to_cells<<<64, 256, 0, s>>>(iv->probe_keys, (uint64_t)nqb * nprobe, d_c);
             pb::count_launch();
@@ -913,8 +1013,8 @@ int poly_b200_ivf_probe_keys_device(poly_b200_ivf* iv, const float* d_q, uint64_
         if (nq == 0) return;
         rebuild_lists(iv);
         ensure_ivf_scratch(iv, np, 1);
-        for (uint64_t b0 = 0; b0 < nq; b0 += IVF_NQB) {
-            const uint32_t nqb = (uint32_t)std::min<uint64_t>(IVF_NQB, nq - b0);
+        for (uint64_t b0 = 0; b0 < nq; b0 += iv->nqb) {
+            const uint32_t nqb = (uint32_t)std::min<uint64_t>(iv->nqb, nq - b0);
             enumerate_cells(iv, d_q + b0 * iv->dim, nqb, np, s);
             CK(cudaMemcpyAsync(d_probe_keys + b0 * np, iv->probe_keys, (size_t)nqb * np * 8, cudaMemcpyDeviceToDevice,
                                s));
@@ -934,8 +1034,8 @@ int poly_b200_ivf_merge_keys_device(poly_b200_ivf* iv, const uint64_t* d_keys, c
         DeviceGuard dg(iv->device);
         cudaStream_t s = (cudaStream_t)stream;
         ensure_ivf_scratch(iv, 1, k);
-        for (uint64_t b0 = 0; b0 < nq; b0 += IVF_NQB) {
-            const uint32_t nqb = (uint32_t)std::min<uint64_t>(IVF_NQB, nq - b0);
+        for (uint64_t b0 = 0; b0 < nq; b0 += iv->nqb) {
+            const uint32_t nqb = (uint32_t)std::min<uint64_t>(iv->nqb, nq - b0);
             // parts x nq x k layout; keys carry the global id, so no id table is needed
             pb::launch_topk(reinterpret_cast<const unsigned long long*>(d_keys) + b0 * k, d_counts + b0, k, parts,
                             nq * k, nq, nqb, k, iv->keys, iv->kcounts, s);
@@ -958,7 +1058,7 @@ int poly_b200_ivf_knn_graph_device(poly_b200_ivf* iv, const float* d_x, uint64_t
         cudaStream_t s = (cudaStream_t)stream;
         poly_b200_ivf_params p1 = *p;
         p1.k = p->k + 1;
-        const uint64_t step = 64 * IVF_NQB;
+        const uint64_t step = 64 * iv->nqb;
         if (iv->knn_rows < std::min(step, n) || iv->knn_k1 < p1.k) {
             cudaStreamSynchronize(s);
             dfree(iv->knn_ids);

@@ -272,6 +272,79 @@ class FlatIndex:
         return FlatIndex(pq, self.device, _handle=h)
 
 
+class ShardedFlatIndex:
+    """One poly::FlatIndex over several GPUs of this process (SURVEY.md sec. 8(b)).
+
+    ``devices`` lists one CUDA ordinal per shard (an ordinal may repeat).  Each
+    add / add_codes call splits its rows into len(devices) contiguous parts, one
+    per shard, ids kept global; search_batch runs every shard concurrently and
+    merges the per-shard top-k lists on devices[0] (peer copies + an n-way
+    (score, id) merge kernel): the results equal FlatIndex over the union.
+    """
+
+    def __init__(self, pq: ProductQuantizer, devices):
+        self._pq = pq
+        self.devices = [int(d) for d in devices]
+        d = PqDesc(pq.m, pq.dbits, pq.dim, _p(pq.codebooks), _p(pq.perms))
+        dev = (C.c_int * len(self.devices))(*self.devices)
+        h = C.c_void_p()
+        _check(lib.poly_b200_sharded_create(C.byref(d), dev, len(self.devices), C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.poly_b200_sharded_destroy(h)
+            self._h = None
+
+    def pq(self):
+        return self._pq
+
+    def size(self) -> int:
+        return int(lib.poly_b200_sharded_size(self._h))
+
+    def __len__(self):
+        return self.size()
+
+    def shard_sizes(self):
+        out = []
+        for g in range(int(lib.poly_b200_sharded_count(self._h))):
+            n = C.c_uint64(0)
+            _check(lib.poly_b200_sharded_shard_size(self._h, g, C.byref(n)))
+            out.append(int(n.value))
+        return out
+
+    def add(self, x, ids=None):
+        x = np.ascontiguousarray(x, np.float32)
+        if x.ndim != 2 or x.shape[1] != self._pq.dim:
+            raise PolyError(Errc.invalid_argument, "encode dimension mismatch")
+        ids = None if ids is None else np.ascontiguousarray(ids, np.int64)
+        _check(lib.poly_b200_sharded_add(self._h, _p(x), x.shape[0], _p(ids)))
+
+    def add_codes(self, codes, ids=None):
+        codes = np.ascontiguousarray(codes, np.uint8)
+        n = codes.shape[0] if codes.ndim == 2 else codes.size // self._pq.code_bytes()
+        ids = None if ids is None else np.ascontiguousarray(ids, np.int64)
+        _check(lib.poly_b200_sharded_add_codes(self._h, _p(codes), _p(ids), n))
+
+    def search_batch(self, queries, params: SearchParams, stats: SearchStats | None = None):
+        """Returns (ids [nq,k] int64, scores [nq,k] fp32, counts [nq] uint32)."""
+        q = np.ascontiguousarray(queries, np.float32).reshape(-1, self._pq.dim)
+        nq, k = q.shape[0], int(params.k)
+        ids, scores, counts = np.empty((nq, k), np.int64), np.empty((nq, k), np.float32), np.empty(nq, np.uint32)
+        st = SearchStatsC()
+        _check(lib.poly_b200_sharded_search_batch(self._h, _p(q), nq, C.byref(params.c()), _p(ids), _p(scores),
+                                                  _p(counts), C.byref(st)))
+        if stats is not None:
+            stats.scanned += st.scanned
+            stats.survivors += st.survivors
+        return ids, scores, counts
+
+    def search(self, query, params: SearchParams, stats: SearchStats | None = None):
+        ids, scores, counts = self.search_batch(np.asarray(query, np.float32).reshape(1, -1), params, stats)
+        return [Neighbor(int(ids[0, i]), float(scores[0, i])) for i in range(int(counts[0]))]
+
+
 def debug_lut(index: FlatIndex, queries):
     """K1 only: (stored-field LUTs [nq,m,256], query codes [nq,code_bytes]) from the GPU."""
     q = np.ascontiguousarray(queries, np.float32).reshape(-1, index.pq().dim)

@@ -162,6 +162,14 @@ class IVFIndex:
         _check(lib.poly_b200_ivf_profile_read(self._h, C.byref(ms), C.byref(n)))
         return float(ms.value), int(n.value)
 
+    def set_batch(self, queries_per_batch: int):
+        """Queries per internal batch (default 2048); larger batches share list reads."""
+        _check(lib.poly_b200_ivf_set_batch(self._h, int(queries_per_batch)))
+
+    @property
+    def batch(self) -> int:
+        return int(lib.poly_b200_ivf_batch(self._h))
+
     def debug_set_list_capacity(self, cap: int):
         _check(lib.poly_b200_ivf_debug_set_list_capacity(self._h, int(cap)))
 

@@ -397,8 +397,12 @@ def test_randomized_ivf_against_oracle(pb, gi, seed):
     strategy = ["dual", "dual", "adc", "binary", "disidx"][seed % 5]
     tau = int(rng.integers(0, 65)) if strategy == "dual" else 64
     cap = int(rng.choice([0, 0, 300]))
+    batch = int(rng.choice([7, 64, 5000])) if seed % 4 == 3 else None  # queries per internal batch
     pq = gi["pq"]
     ix = pb.IVFIndex(pb.ProductQuantizer(8, 8, 128, gi["codebooks"], gi["perms"]), coarse)
+    if batch:
+        ix.set_batch(batch)
+        assert ix.batch == batch
     if n:
         ix.add(base, ids=ids)
         lists, _ = oracle.ivf_build(pq, base, coarse, ids=ids)
@@ -421,7 +425,7 @@ def test_randomized_ivf_against_oracle(pb, gi, seed):
         assert np.array_equal(sv.cpu().numpy().view(np.uint64), osv), (nlist, n, nq, nprobe, k, tau, cap)
         assert np.array_equal(sh.cpu().numpy().view(np.uint64), osh), (nlist, n, nq, nprobe, k, tau, cap)
         assert np.array_equal(d[0].cpu().numpy(), oi)
-    ctx = (nlist, n, nq, nprobe, k, strategy, tau, cap)
+    ctx = (nlist, n, nq, nprobe, k, strategy, tau, cap, batch)
     assert np.array_equal(ix.probes(queries, nprobe), opr), ctx
     assert np.array_equal(gi_, oi), ctx
     assert np.array_equal(_bits(gsc), _bits(osc)), ctx

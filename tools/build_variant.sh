@@ -6,9 +6,9 @@ name=$1; shift
 cd "$(dirname "$0")/.."
 out=tools/lib12/$name; mkdir -p $out
 F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude $*"
-for s in capi capi_ivf kernels_encode kernels_scan kernels_topk kernels_ivf; do
+for s in $(python3 -c "import sys; sys.path.insert(0, 'paper_1609_01882_b200'); import build; print(' '.join(x[:-3] for x in build.SOURCES))"); do
   /usr/local/cuda/bin/nvcc $F -c paper_1609_01882_b200/csrc/$s.cu -o $out/$s.o &
 done
 wait
-/usr/local/cuda/bin/nvcc -shared -gencode arch=compute_100a,code=sm_100a $out/*.o -o tools/lib12/$name.so -lcudart -lcublas
+/usr/local/cuda/bin/nvcc -shared -gencode arch=compute_100a,code=sm_100a $out/*.o -o tools/lib12/$name.so -lcudart
 echo tools/lib12/$name.so

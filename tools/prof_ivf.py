@@ -1,5 +1,5 @@
 """IVF search driver for ncu launch lists: sampled 65,536-cell coarse quantizer,
-N codes built on the GPU, one 256-query batch searched `reps` times."""
+N codes built on the GPU, one query batch (--nq) searched `reps` times."""
 import argparse, os, sys, time
 import numpy as np
 import torch
@@ -11,12 +11,15 @@ ap.add_argument('--n', type=int, default=20_000_000)
 ap.add_argument('--nprobe', type=int, default=16)
 ap.add_argument('--reps', type=int, default=2)
 ap.add_argument('--nq', type=int, default=256)
+ap.add_argument('--batch', type=int, default=0)
 args = ap.parse_args()
 z = np.load('tests/golden/pq_ivf65536_d128_m8.npz')
 pq = pb.ProductQuantizer(8, 8, 128, z['codebooks'], z['perms'])
 centers = synth.gen_centers(160901882, 1000, 128)
 coarse = synth.gen_points(160901882, 1, 0, 65536, centers)
 ivf = pb.IVFIndex(pq, coarse)
+if args.batch:
+    ivf.set_batch(args.batch)
 torch.backends.cuda.matmul.allow_tf32 = True
 dc = torch.from_numpy(coarse).cuda(); cn = (dc * dc).sum(1)
 x = torch.empty((1 << 20, 128), device='cuda'); cells = torch.empty(1 << 20, dtype=torch.int32, device='cuda')
