@@ -64,11 +64,6 @@ struct poly_b200_ivf {
     uint32_t scratch_nprobe = 0;
     uint4* items[2] = {nullptr, nullptr};  // K6 work lists of the two rounds
     uint64_t items_cap[2] = {0, 0};
-    // K6g (cell-major list scan): per-cell counts / cursors, cell-sorted items, units
-    uint32_t* cw_ccnt = nullptr;
-    uint32_t* cw_sorted = nullptr;
-    uint4* cw_units = nullptr;
-    uint64_t cw_units_cap = 0, cw_sorted_cap = 0;
     float* lutp = nullptr;
     uint8_t* qcodes = nullptr;
     unsigned long long* cand = nullptr;
@@ -139,18 +134,6 @@ constexpr uint64_t IVF_R1_CODES = POLY_IVF_R1_CODES;  // ... and at least this m
 #endif
 constexpr uint32_t IVF_CHUNK = POLY_IVF_CHUNK;    // K6 round-1 work item: 1024 list rows (K6 scans it in 128-row warp blocks)
 constexpr uint32_t IVF_CHUNK2 = POLY_IVF_CHUNK2;  // round 2: longer items (fewer LUT loads per code)
-#ifndef POLY_IVF_CELL  // 1: K6g cell-major list scan (codes read once per group of queries probing a cell)
-#define POLY_IVF_CELL 1
-#endif
-#ifndef POLY_IVF_CELL_ROWS0
-#define POLY_IVF_CELL_ROWS0 2048
-#endif
-#ifndef POLY_IVF_CELL_ROWS1
-#define POLY_IVF_CELL_ROWS1 4096
-#endif
-constexpr bool IVF_CELL = POLY_IVF_CELL != 0;
-constexpr uint32_t IVF_CELL_ROWS0 = POLY_IVF_CELL_ROWS0;  // K6g unit rows, round 1
-constexpr uint32_t IVF_CELL_ROWS1 = POLY_IVF_CELL_ROWS1;  // round 2
 
 __global__ void fill_u32(uint32_t* p, uint64_t n, uint32_t v) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
@@ -259,39 +242,18 @@ void ensure_ivf_scratch(poly_b200_ivf* iv, uint32_t nprobe, uint32_t k) {
         iv->qcodes = dalloc<uint8_t>((size_t)iv->nqb * nprobe * iv->cb);
     }
     const uint64_t r1 = std::min<uint64_t>(nprobe, IVF_R1_MAX);
-    if (IVF_CELL) {
-        // K6g units of a round: sum over cells of ceil(cnt / G) * ceil(len / R)
-        //   <= scanned / (G R) + n / R + items / G + min(nlist, items) + 1, scanned <= nqb * min(n, np * max_list)
-        const uint64_t items = (uint64_t)iv->nqb * nprobe, G = pb::cell_scan_group(iv->m);
-        const uint64_t R = std::min<uint32_t>(IVF_CELL_ROWS0, IVF_CELL_ROWS1);
-        const uint64_t scanned = (uint64_t)iv->nqb * std::min<uint64_t>(iv->n, nprobe * iv->max_list);
-        const uint64_t need = scanned / (G * R) + iv->n / R + items / G + std::min<uint64_t>(iv->nlist, items) + 16;
-        require(need < (1ull << 32) && items < (1ull << 32), POLY_B200_INVALID_ARGUMENT, "IVF work list too large");
-        if (!iv->cw_ccnt) iv->cw_ccnt = dalloc<uint32_t>(iv->nlist);
-        if (iv->cw_sorted_cap < items) {
-            dfree(iv->cw_sorted);
-            iv->cw_sorted_cap = items;
-            iv->cw_sorted = dalloc<uint32_t>(items);
+    // work-list bounds per query: round 1 <= r1 probes -> <= r1 + r1 * max_list / CHUNK items;
+    // round 2 <= np + min(n, np * max_list) / CHUNK2 items
+    const uint64_t need[2] = {
+        (uint64_t)iv->nqb * (r1 + (r1 * iv->max_list + IVF_CHUNK - 1) / IVF_CHUNK),
+        (uint64_t)iv->nqb * (nprobe + r1 + (std::min<uint64_t>(iv->n, nprobe * iv->max_list) + IVF_CHUNK2 - 1) / IVF_CHUNK2)};
+    for (int r = 0; r < 2; ++r)
+        if (iv->items_cap[r] < need[r]) {
+            require(need[r] < (1ull << 32), POLY_B200_INVALID_ARGUMENT, "IVF work list too large");
+            dfree(iv->items[r]);
+            iv->items_cap[r] = need[r];
+            iv->items[r] = dalloc<uint4>(need[r]);
         }
-        if (iv->cw_units_cap < need) {
-            dfree(iv->cw_units);
-            iv->cw_units_cap = need;
-            iv->cw_units = dalloc<uint4>(need);
-        }
-    } else {
-        // work-list bounds per query: round 1 <= r1 probes -> <= r1 + r1 * max_list / CHUNK items;
-        // round 2 <= np + min(n, np * max_list) / CHUNK2 items
-        const uint64_t need[2] = {
-            (uint64_t)iv->nqb * (r1 + (r1 * iv->max_list + IVF_CHUNK - 1) / IVF_CHUNK),
-            (uint64_t)iv->nqb * (nprobe + r1 + (std::min<uint64_t>(iv->n, nprobe * iv->max_list) + IVF_CHUNK2 - 1) / IVF_CHUNK2)};
-        for (int r = 0; r < 2; ++r)
-            if (iv->items_cap[r] < need[r]) {
-                require(need[r] < (1ull << 32), POLY_B200_INVALID_ARGUMENT, "IVF work list too large");
-                dfree(iv->items[r]);
-                iv->items_cap[r] = need[r];
-                iv->items[r] = dalloc<uint4>(need[r]);
-            }
-    }
     // round 1 runs without a bound: its <= r1 probes' survivors must fit (round 2 is bounded
     // by round 1's k-th key; a list that still fills up is re-ranked by the rescue scan)
     uint32_t cap = (uint32_t)std::max<uint64_t>(131072, r1 * iv->max_list + k);
@@ -374,8 +336,8 @@ void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_
     else
         enumerate_cells(iv, d_q, nqb, np, s);
     pb::IvfWork w{};
-    w.items[0] = IVF_CELL ? nullptr : iv->items[0];  // K6g plans its own work (cw_plan)
-    w.items[1] = IVF_CELL ? nullptr : iv->items[1];
+    w.items[0] = iv->items[0];
+    w.items[1] = iv->items[1];
     w.nitems = iv->ctrl + iv->nqb + 3;
     w.cap[0] = (uint32_t)iv->items_cap[0];
     w.cap[1] = (uint32_t)iv->items_cap[1];
@@ -424,31 +386,10 @@ void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_
     // 1024-row chunks; its exact k-th key (K3) bounds round 2, the remaining probes
     const uint32_t rounds = np <= 1 ? 1 : 2;  // one probe: round 1 sees everything
     for (uint32_t round = 0; round < rounds; ++round) {
-        pb::CellWork cw{};
-        if (IVF_CELL) {  // group the round's (query, probe) items by cell
-            cw.probe_keys = iv->probe_keys;
-            cw.nq = nqb;
-            cw.nprobe = np;
-            cw.np_eff = iv->np_eff;
-            cw.split = rounds > 1 ? iv->split : nullptr;
-            cw.round = round;
-            cw.ccnt = iv->cw_ccnt;
-            cw.sorted = iv->cw_sorted;
-            cw.units = iv->cw_units;
-            cw.units_cap = (uint32_t)iv->cw_units_cap;
-            cw.nunits = iv->ctrl + iv->nqb + 5 + round;
-            cw.work = iv->ctrl + iv->nqb + 7 + round;
-            cw.overflow = iv->ctrl + iv->nqb;
-            cw.g = pb::cell_scan_group(iv->m);
-            cw.rows = round ? IVF_CELL_ROWS1 : IVF_CELL_ROWS0;
-            CK(cudaMemsetAsync(iv->cw_ccnt, 0, (size_t)iv->nlist * 4, s));
-            pb::launch_cell_plan(cw, iv->d_off, iv->nlist, s);
-        } else {
-            a.items = iv->items[round];
-            a.nitems = w.nitems + round;
-            a.items_cap = w.cap[round];
-            a.work = iv->ctrl + iv->nqb + 1 + round;
-        }
+        a.items = iv->items[round];
+        a.nitems = w.nitems + round;
+        a.items_cap = w.cap[round];
+        a.work = iv->ctrl + iv->nqb + 1 + round;
         if (round == 1 && side) CK(cudaStreamWaitEvent(s, iv->ev_join, 0));
         cudaEvent_t e1 = nullptr;
         if (iv->profiling) {
@@ -461,8 +402,7 @@ void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_
             CK(cudaEventRecord(iv->prof_events[iv->prof_used].first, s));
             e1 = iv->prof_events[iv->prof_used++].second;
         }
-        if (IVF_CELL) pb::launch_ivf_cell_scan(a, cw, strategy, iv->m, iv->num_sms, s);
-        else pb::launch_ivf_scan(a, strategy, iv->m, iv->num_sms, s);
+        pb::launch_ivf_scan(a, strategy, iv->m, iv->num_sms, s);
         if (e1) CK(cudaEventRecord(e1, s));
         // a query whose list overflowed (in either round) is re-ranked exactly over all its
         // visited probes (no-op for the others)
@@ -655,7 +595,7 @@ int poly_b200_ivf_destroy(poly_b200_ivf* iv) {
                             (void*)iv->d_oid, (void*)iv->d_osc, (void*)iv->d_ocnt,
                             (void*)iv->knn_ids, (void*)iv->knn_sc, (void*)iv->knn_cnt, (void*)iv->d_cnorm, (void*)iv->items[0],
                             (void*)iv->d_cpacked, (void*)iv->grp, (void*)iv->rank_scratch,
-                            (void*)iv->items[1], (void*)iv->cw_ccnt, (void*)iv->cw_sorted, (void*)iv->cw_units})
+                            (void*)iv->items[1]})
                 dfree(p);
             if (iv->h_overflow) cudaFreeHost(iv->h_overflow);
             for (auto& pe : iv->prof_events) {
@@ -863,8 +803,7 @@ int poly_b200_ivf_set_batch(poly_b200_ivf* iv, uint32_t nqb) {
                           (void**)&iv->scanned, (void**)&iv->items[0], (void**)&iv->items[1], (void**)&iv->lutp,
                           (void**)&iv->qcodes, (void**)&iv->cand, (void**)&iv->ctrl, (void**)&iv->thr,
                           (void**)&iv->keys, (void**)&iv->kcounts, (void**)&iv->surv_total, (void**)&iv->scan_total,
-                          (void**)&iv->ovq, (void**)&iv->surv_q, (void**)&iv->hash_q, (void**)&iv->sticky_overflow,
-                          (void**)&iv->cw_sorted, (void**)&iv->cw_units}) {
+                          (void**)&iv->ovq, (void**)&iv->surv_q, (void**)&iv->hash_q, (void**)&iv->sticky_overflow}) {
             dfree(*pp);
             *pp = nullptr;
         }
@@ -874,7 +813,6 @@ int poly_b200_ivf_set_batch(poly_b200_ivf* iv, uint32_t nqb) {
         iv->done_ev = nullptr;
         iv->scratch_nprobe = 0;
         iv->items_cap[0] = iv->items_cap[1] = 0;
-        iv->cw_units_cap = iv->cw_sorted_cap = 0;
         iv->cand_cap = 0;
         iv->keys_k = 0;
         iv->nqb = nqb;

@@ -11,11 +11,7 @@
 //   K1r residual_lut_quad_kernel  per (query, probe): r = q - c_cell, then
 //                            compute_lut / permuted_lut / encode on r
 //                            (pq.cpp:29-45,91-119), packed f32x2, bit-exact.
-//   K6  ivf_scan_kernel      per work item (query, probe, row range), one CTA: stream
-//                            the cell's (residual code, id) list, Hamming filter
-//                            against the item's query code, ADC from the item's LUT
-//                            in shared memory, candidate keys appended to the
-//                            query's list.
+//   K6  (kernels_ivf_scan.cu) the list scan over the probed cells.
 //   assign_kernel            build: nearest coarse cell by sq_l2 (strict <).
 #include <type_traits>
 
@@ -331,188 +327,7 @@ void launch_ivf_probe_count(const unsigned long long* probe_keys, uint32_t nq, u
     count_launch();
 }
 
-// ------------------------------------------------------------------ K6
-#ifndef POLY_K6_WARPS
-#define POLY_K6_WARPS 4  // A/B at 2048 queries: 8 -> 4 warps per CTA (16 CTAs per SM) +5% / +8% (nprobe 16 / 64), cfg4 +9%
-#endif
-constexpr int K6_WARPS = POLY_K6_WARPS;
-
-// Survivor-queue accesses through 32-bit shared-window addresses (the generic
-// pointers made ptxas rebuild the window base per access at the 32-register cap).
-__device__ __forceinline__ void k6_sts(uint32_t a, const uint2& c) {
-    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(c.x), "r"(c.y) : "memory");
-}
-__device__ __forceinline__ void k6_sts(uint32_t a, const uint4& c) {
-    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(c.x), "r"(c.y), "r"(c.z), "r"(c.w) : "memory");
-}
-__device__ __forceinline__ void k6_sts(uint32_t a, uint32_t v) {
-    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
-__device__ __forceinline__ void k6_lds(uint32_t a, uint2& c) {
-    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(c.x), "=r"(c.y) : "r"(a) : "memory");
-}
-__device__ __forceinline__ void k6_lds(uint32_t a, uint4& c) {
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(c.x), "=r"(c.y), "=r"(c.z), "=r"(c.w) : "r"(a) : "memory");
-}
-__device__ __forceinline__ void k6_lds(uint32_t a, uint32_t& v) {
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
-}
-
-// Work items (query, probe, chunk of the probed cell's list) are fetched
-// dynamically; the K6_WARPS warps of a CTA split the chunk and share the item's LUT
-// in shared memory.  Each warp compacts its filter survivors with a ballot into
-// its own queue and drains 32 at a time (ADC with early exit, candidate test).
-template <int M, int STRAT, bool PERQ>
-#ifndef POLY_K6_MINB
-#define POLY_K6_MINB 8  // m = 8: 64 warps per SM, <= 32 registers (m = 16: 40 warps)
-#endif
-__global__ void __launch_bounds__(K6_WARPS * 32, (M == 8 ? POLY_K6_MINB : 5) * (8 / K6_WARPS)) ivf_scan_kernel(const IvfScanArgs a) {
-    using C = typename CodeT<M>::T;
-    extern __shared__ __align__(16) uint8_t k6_smem[];
-    float* L = reinterpret_cast<float*>(k6_smem);  // M x 256 floats
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // this warp's survivor queue: 64 codes, then 64 positions (shared-window addresses)
-    const uint32_t qcs = smem_u32(k6_smem + (size_t)M * KSUB * 4 + warp * 64 * (sizeof(C) + 4));
-    const uint32_t qps = qcs + 64 * sizeof(C);
-    const uint32_t lt = (1u << lane) - 1u, tau = a.tau;
-    const uint32_t nitems = min(*a.nitems, a.items_cap);
-    uint32_t surv_total = 0;
-    __shared__ uint32_t item_s;
-    for (;;) {
-        __syncthreads();
-        if (threadIdx.x == 0) item_s = atomicAdd(a.work, 1u);
-        __syncthreads();
-        const uint32_t it = item_s;
-        if (it >= nitems) break;
-        const uint4 w = a.items[it];  // (query, probe, row0, row1)
-        const uint32_t qi = w.x;
-        const size_t item = (size_t)qi * a.nprobe + w.y;
-        const uint32_t cell = (uint32_t)a.probe_keys[item];
-        const uint64_t beg = a.off[cell] + w.z, end = a.off[cell] + w.w;  // the item's rows
-        const float4* src = reinterpret_cast<const float4*>(a.lutp + item * M * KSUB);
-        for (int i = threadIdx.x; i < M * KSUB / 4; i += K6_WARPS * 32) reinterpret_cast<float4*>(L)[i] = src[i];
-        const C qc = reinterpret_cast<const C*>(a.qcodes)[item];
-        const unsigned long long thr = __ldcg(a.thr + qi);
-        __syncthreads();
-        uint32_t qn = 0;
-        auto candidate = [&](float score, uint32_t pos) {
-            const uint32_t sb = __float_as_uint(score);
-            if (sb <= (uint32_t)(thr >> 32)) {
-                const unsigned long long key = ((unsigned long long)sb << 32) | __ldg(a.low + pos);
-                if (key < thr) {
-                    const uint32_t slot = atomicAdd(&a.ccount[qi], 1u);
-                    if (slot < a.cap) a.cand[(size_t)qi * a.cap + slot] = key;
-                    else a.ovq[qi] = 1u;  // list full: the rescue scan re-ranks this query exactly
-                }
-            }
-        };
-        auto drain = [&](uint32_t cnt) {
-            __syncwarp();
-            if ((uint32_t)lane < cnt) {
-                C cc;
-                uint32_t pp;
-                k6_lds(qcs + lane * (uint32_t)sizeof(C), cc);
-                k6_lds(qps + 4u * lane, pp);
-                candidate(adc_bounded<M>(L, cc, (uint32_t)(thr >> 32)), pp);
-            }
-            __syncwarp();
-        };
-        // warp w scans rows 128*w + ..., stride 128 * K6_WARPS, of the item's rows
-        // [beg, end) (32-bit offsets)
-        const C* ci = reinterpret_cast<const C*>(a.codes) + beg;
-        const uint32_t n = (uint32_t)(end - beg), pos0 = (uint32_t)beg;
-        auto block = [&](uint32_t r0) {
-            C c[4];
-            bool in[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t r = r0 + u * 32 + lane;
-                in[u] = r < n;
-                if (in[u]) c[u] = __ldcs(ci + r);  // streamed once: evict-first
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t pos = pos0 + r0 + u * 32 + lane;
-                if constexpr (STRAT == DUAL) {
-                    const bool pass = in[u] && ham(c[u], qc) <= tau;
-                    if constexpr (PERQ) {  // stats mode: per-query survivor count and id hash
-                        if (pass) {
-                            atomicAdd(a.surv_q + qi, 1ull);
-                            atomicAdd(a.hash_q + qi, (unsigned long long)mix64(__ldg(a.low + pos)));
-                        }
-                    }
-                    const uint32_t bal = __ballot_sync(0xffffffffu, pass);
-                    if (bal) {
-                        if (pass) {
-                            const uint32_t at = qn + __popc(bal & lt);
-                            k6_sts(qcs + at * (uint32_t)sizeof(C), c[u]);
-                            k6_sts(qps + 4u * at, pos);
-                        }
-                        qn += __popc(bal);
-                        surv_total += __popc(bal);
-                        if (qn >= 32) {
-                            drain(32);
-                            qn -= 32;
-                            if ((uint32_t)lane < qn) {  // carry the overflow to the queue head
-                                C cc;
-                                uint32_t pp;
-                                k6_lds(qcs + (32u + lane) * (uint32_t)sizeof(C), cc);
-                                k6_lds(qps + 4u * (32u + lane), pp);
-                                k6_sts(qcs + lane * (uint32_t)sizeof(C), cc);
-                                k6_sts(qps + 4u * lane, pp);
-                            }
-                            __syncwarp();
-                        }
-                    }
-                } else if (in[u]) {
-                    if constexpr (PERQ && STRAT == ADC) {  // dual at tau = code_bits: every code survives
-                        atomicAdd(a.surv_q + qi, 1ull);
-                        atomicAdd(a.hash_q + qi, (unsigned long long)mix64(__ldg(a.low + pos)));
-                    }
-                    float score;
-                    if constexpr (STRAT == ADC) score = adc_bounded<M>(L, c[u], (uint32_t)(thr >> 32));
-                    else if constexpr (STRAT == BINARY) score = (float)ham(c[u], qc);
-                    else score = (float)disidx(c[u], qc);
-                    candidate(score, pos);
-                }
-            }
-        };
-        for (uint32_t r0 = warp * 128; r0 < n; r0 += 128 * K6_WARPS) block(r0);
-        if (STRAT == DUAL && qn) drain(qn);
-    }
-    if (STRAT == DUAL && lane == 0 && surv_total) atomicAdd(a.surv_total, (unsigned long long)surv_total);
-}
-
-template <int M, int STRAT>
-static void launch_ivf_one(const IvfScanArgs& a, unsigned grid, cudaStream_t s) {
-    using C = typename CodeT<M>::T;
-    const size_t smem = (size_t)M * KSUB * 4 + (size_t)K6_WARPS * 64 * (sizeof(C) + 4);
-    if (a.surv_q) {
-        set_max_smem((const void*)ivf_scan_kernel<M, STRAT, true>, smem);
-        ivf_scan_kernel<M, STRAT, true><<<grid, K6_WARPS * 32, smem, s>>>(a);
-    } else {
-        set_max_smem((const void*)ivf_scan_kernel<M, STRAT, false>, smem);
-        ivf_scan_kernel<M, STRAT, false><<<grid, K6_WARPS * 32, smem, s>>>(a);
-    }
-}
-
-template <int M>
-static void launch_ivf_m(const IvfScanArgs& a, int strategy, int num_sms, cudaStream_t s) {
-    const unsigned grid = (unsigned)num_sms * (M == 8 ? 8 : 5) * (8 / K6_WARPS);  // ~14 KB (m=8) / ~26 KB (m=16) smem per 8-warp CTA
-    switch (strategy) {
-        case DUAL: launch_ivf_one<M, DUAL>(a, grid, s); break;
-        case ADC: launch_ivf_one<M, ADC>(a, grid, s); break;
-        case BINARY: launch_ivf_one<M, BINARY>(a, grid, s); break;
-        default: launch_ivf_one<M, DISIDX>(a, grid, s); break;
-    }
-    count_launch();
-}
-
-void launch_ivf_scan(const IvfScanArgs& a, int strategy, uint32_t m, int num_sms, cudaStream_t s) {
-    if (a.nq == 0) return;
-    if (m == 8) launch_ivf_m<8>(a, strategy, num_sms, s);
-    else launch_ivf_m<16>(a, strategy, num_sms, s);
-}
+// K6 (the list scan) is in kernels_ivf_scan.cu.
 
 // ------------------------------------------------------------------ build
 // Nearest coarse cell of each vector (sq_l2, strict <, ties -> lowest cell);

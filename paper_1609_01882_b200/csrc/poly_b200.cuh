@@ -121,24 +121,6 @@ struct IvfWork {
     uint32_t* overflow;
 };
 
-// Cell-major work of one K6g round (kernels_ivf_cell.cu): the round's (query, probe)
-// items grouped by cell; a unit is (cell | n_g << 24, first cell-sorted slot, r0, r1).
-struct CellWork {
-    const unsigned long long* probe_keys;  // nq x nprobe
-    uint32_t nq, nprobe;
-    const uint32_t* np_eff;   // probes visited per query
-    const uint32_t* split;    // round-1 probes per query (null: one round covers [0, np_eff))
-    uint32_t round;
-    uint32_t* ccnt;           // nlist: item counts, then scatter cursors
-    uint32_t* sorted;         // items (q * nprobe + p) in cell order
-    uint4* units;
-    uint32_t units_cap;
-    uint32_t* nunits;         // written by the plan
-    uint32_t* work;           // K6g's dynamic unit counter (zeroed)
-    uint32_t* overflow;
-    uint32_t g, rows;         // items per group, rows per unit
-};
-
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -341,11 +323,6 @@ void launch_ivf_probe_count(const unsigned long long* probe_keys, uint32_t nq, u
                             uint64_t cap, uint32_t* np_eff, unsigned long long* scanned, cudaStream_t s,
                             uint32_t* split, uint64_t r1_codes, uint32_t r1_max, const IvfWork& w);
 void launch_ivf_scan(const IvfScanArgs& a, int strategy, uint32_t m, int num_sms, cudaStream_t s);
-// K6g: cell-major list scan (kernels_ivf_cell.cu); plan = count + scan + scatter of the round's items
-uint32_t cell_scan_group(uint32_t m);
-void launch_cell_plan(const CellWork& w, const uint64_t* off, uint32_t nlist, cudaStream_t s);
-void launch_ivf_cell_scan(const IvfScanArgs& a, const CellWork& w, int strategy, uint32_t m, int num_sms,
-                          cudaStream_t s);
 void launch_assign(const float* x, uint64_t n, uint32_t dim, const float* cent, uint32_t nlist, uint32_t* assign,
                    cudaStream_t s);
 void launch_residual_encode(const float* x, uint64_t n, uint32_t dim, uint32_t m, const float* cent,

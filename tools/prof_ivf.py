@@ -26,9 +26,9 @@ x = torch.empty((1 << 20, 128), device='cuda'); cells = torch.empty(1 << 20, dty
 for r in range(0, args.n, 1 << 20):
     nb = min(1 << 20, args.n - r)
     pb.gen_points_device(centers, 160901882, 2, r, nb, x[:nb])
-    for b in range(0, nb, 8192):
-        xs = x[b:min(b + 8192, nb)]
-        cells[b:b + xs.shape[0]] = torch.argmin(cn[None, :] - 2.0 * (xs @ dc.T), dim=1).to(torch.int32)
+    for b in range(0, nb, 16384):
+        xs = x[b:min(b + 16384, nb)]
+        cells[b:b + xs.shape[0]] = torch.argmin(torch.addmm(cn, xs, dc.T, alpha=-2.0), dim=1).to(torch.int32)
     ivf.add_device(x[:nb], cells[:nb], r)
 q = synth.gen_points(160901882, 3, 0, args.nq, centers)
 p = pb.CoarseParams(pb.Strategy.dual, 100, 26, args.nprobe, 0)
