@@ -10,7 +10,7 @@ distributions -- DESIGN.md "Data"):
   1  flat, 64-bit codes, N = 1e8 (800 MB), nq = 10,000 in batches of 256, ht 24 (28/32)
      -- the default: the configuration the metric is quoted on
   2  IVF 65,536 lists + 64-bit residual codes, N = 1e9 codes over the ranks, nq = 10,000
-     in batches of 2048, nprobe 16 (64 under per_nprobe), ht 26
+     (one step = all 10,000 queries), nprobe 16 (64 under per_nprobe), ht 26
   3  flat, 128-bit codes (m = 16), N = 2e8, ht 56 (48/64/128)
   4  k-NN graph: 1e7 unit vectors, IVF 16,384 + m = 16, nprobe 32, ht 52, k = 10
 
@@ -60,7 +60,7 @@ CONFIGS = {
             pq="pq_d128_m8.npz", cpu_q=1000, cpu_q1=32),
     1: dict(kind="flat", dim=128, ncent=1000, m=8, n=100_000_000, nq=NQ, batch=256, ht=24, per_ht="28,32",
             pq="pq_d128_m8.npz", cpu_q=256, cpu_q1=4),
-    2: dict(kind="ivf", dim=128, ncent=1000, m=8, n=1_000_000_000, nq=NQ, batch=2048, ht=26, nlist=65536,
+    2: dict(kind="ivf", dim=128, ncent=1000, m=8, n=1_000_000_000, nq=NQ, batch=NQ, ht=26, nlist=65536,
             nprobe=16, per_nprobe="64", pq="pq_ivf65536_d128_m8.npz", cpu_q=1000, cpu_q1=64),
     3: dict(kind="flat", dim=256, ncent=4096, m=16, n=200_000_000, nq=NQ, batch=256, ht=56, per_ht="48,64,128",
             pq="pq_d256_m16.npz", cpu_q=64, cpu_q1=2),

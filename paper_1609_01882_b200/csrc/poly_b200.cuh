@@ -16,6 +16,9 @@ constexpr int DSUB = 16;               // every configuration: 128/8 and 256/16
 #ifndef POLY_AFFINE  // 1: group-affine K2 schedule
 #define POLY_AFFINE 1
 #endif
+#ifndef POLY_AFFINE_LEAD  // K2: chunks a query group may run ahead of the slowest one
+#define POLY_AFFINE_LEAD 16
+#endif
 #ifndef POLY_UNITS_PER_CTA  // K2 work units per CTA the unit size aims for (capped by POLY_MAX_TPC)
 #define POLY_UNITS_PER_CTA 16
 #endif
@@ -280,6 +283,8 @@ void launch_gen_points(uint64_t seed, uint32_t stream_id, uint64_t row0, uint64_
 // K2: fused filter + ADC + candidate scan.
 void launch_scan(const ScanArgs& a, int strategy, uint32_t m, bool per_query_stats, int num_sms, cudaStream_t s);
 int scan_queries_per_cta(uint32_t m);
+// K2t: the role-split tensor-core scan for m = 8 dual (kernels_scan_tc.cu)
+void launch_scan_tc(const ScanArgs& a, bool per_query_stats, int num_sms, cudaStream_t s);
 // K2s: thr[q] = min(thr[q], k-th key of a fixed sample + 1); one CTA per query
 void launch_seed_sample(const ScanArgs& a, int strategy, uint32_t m, uint32_t nq, uint32_t seed_blocks, cudaStream_t s);
 
