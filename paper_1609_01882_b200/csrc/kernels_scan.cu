@@ -716,14 +716,9 @@ static void launch_m(const ScanArgs& a, int strategy, bool perq, int num_sms, cu
     }
 }
 
-#ifndef POLY_K2T  // 1: m = 8 dual runs the role-split tensor-core scan (kernels_scan_tc.cu)
-#define POLY_K2T 0
-#endif
-
 void launch_scan(const ScanArgs& a, int strategy, uint32_t m, bool per_query_stats, int num_sms, cudaStream_t s) {
     // Q queries per CTA: Q x m x 1 KB of LUTs must fit next to the tile ring.
-    if (POLY_K2T && POLY_TC && m == 8 && strategy == DUAL) launch_scan_tc(a, per_query_stats, num_sms, s);
-    else if (m == 8) launch_m<8, 16, SCAN_WARPS>(a, strategy, per_query_stats, num_sms, s);
+    if (m == 8) launch_m<8, 16, SCAN_WARPS>(a, strategy, per_query_stats, num_sms, s);
     else launch_m<16, 8, SCAN_WARPS / 2>(a, strategy, per_query_stats, num_sms, s);
 }
 

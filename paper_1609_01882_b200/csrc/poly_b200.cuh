@@ -283,8 +283,6 @@ void launch_gen_points(uint64_t seed, uint32_t stream_id, uint64_t row0, uint64_
 // K2: fused filter + ADC + candidate scan.
 void launch_scan(const ScanArgs& a, int strategy, uint32_t m, bool per_query_stats, int num_sms, cudaStream_t s);
 int scan_queries_per_cta(uint32_t m);
-// K2t: the role-split tensor-core scan for m = 8 dual (kernels_scan_tc.cu)
-void launch_scan_tc(const ScanArgs& a, bool per_query_stats, int num_sms, cudaStream_t s);
 // K2s: thr[q] = min(thr[q], k-th key of a fixed sample + 1); one CTA per query
 void launch_seed_sample(const ScanArgs& a, int strategy, uint32_t m, uint32_t nq, uint32_t seed_blocks, cudaStream_t s);
 
