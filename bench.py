@@ -87,6 +87,11 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-n", type=int, default=8_000_000, help="codes in each --impl reference step's sample")
     ap.add_argument("--spawn-check", action="store_true", help="launch/rendezvous self-test (CPU, gloo); tests only")
+    ap.add_argument("--coarse", default="sample", choices=["sample", "kmeans"],
+                    help="IVF coarse quantizer: training-stream rows (default) or GPU k-means (poly_b200_kmeans, "
+                         "k-means++ + 10 Lloyd iterations on 16 x nlist training rows)")
+    ap.add_argument("--knn-full", default=None, metavar="PATH",
+                    help="config 4: also build this rank's whole k-NN graph into PATH (graph file sink, timed)")
     args = ap.parse_args()
     c = dict(CONFIGS[args.config])
     args.c = c
@@ -624,6 +629,20 @@ def ivf_rooflines(args, pk, rt, f, m, scanned, surv, nq_step, np_step, ms_step, 
     return k6, step, hbm
 
 
+def make_coarse(args, pb, synth, centers, norm):
+    """The coarse quantizer: the first nlist training-stream rows (the fixtures' recipe), or
+    GPU k-means (train_coarse) on 16 x nlist training rows, 10 Lloyd iterations."""
+    c = args.c
+    if args.coarse == "sample":
+        return synth.gen_points(SEED, 1, 0, c["nlist"], centers, normalize=norm)
+    t = time.time()
+    train = synth.gen_points(SEED, 1, 0, 16 * c["nlist"], centers, normalize=norm)
+    cent, _, _, mse = pb.kmeans(train, c["nlist"], iters=10, seed=1234567)
+    args.coarse_info = {"kind": "kmeans", "train_rows": len(train), "iters": 10, "mse": mse,
+                        "train_s": round(time.time() - t, 1)}
+    return cent
+
+
 def run_ivf(args, rank, world, local):
     """search_coarse throughput (config 2): codes scanned/s over the probed lists."""
     import torch
@@ -637,7 +656,7 @@ def run_ivf(args, rank, world, local):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     centers = synth.gen_centers(SEED, c["ncent"], c["dim"])
-    coarse = synth.gen_points(SEED, 1, 0, c["nlist"], centers)  # the fixture's coarse recipe
+    coarse = make_coarse(args, pb, synth, centers, False)
     row0, row1 = shard_range(args.n, world, rank)
     t = time.time()
     ivf, pq = build_ivf(args, pb, torch, local, row0, row1, coarse, centers, False)
@@ -754,7 +773,7 @@ def run_ivf(args, rank, world, local):
                        "nlist": c["nlist"], "n_codes": args.n, "m": M, "nprobe": args.nprobe, "k": k, "ht": args.ht,
                        "batch": B, "parallelism": f"db-shard{world} (ids within every list) + query-split coarse "
                                                   "quantization + NCCL probe / key all-gathers",
-                       "coarse": "training-stream rows [0, nlist) (sampled coarse quantizer; DESIGN.md)",
+                       "coarse": getattr(args, "coarse_info", "training-stream rows [0, nlist) (sampled coarse quantizer; DESIGN.md)"),
                        "build_assignment": "TF32 GEMM argmin (setup only)",
                        "l2": "probed lists stream from HBM (GBs of codes per GPU); no flush needed"},
             "e2e": e2e, "gpu_launches": head["gpu_launches"], "clocks": clk,
@@ -771,6 +790,27 @@ def run_ivf(args, rank, world, local):
         dist.destroy_process_group()
 
 
+def knn_full(args, pb, torch, ivf, centers, p, row0, row1, local, stream):
+    """The whole graph of rows [row0, row1) through the output sink (graph file + ivecs):
+    rows generated on the GPU in 1M-row chunks, searched, written while the next step runs.
+    Wall clock around the whole run (generation, search, copies, file writes)."""
+    c = args.c
+    chunk = 1 << 20
+    dx = torch.empty((chunk, c["dim"]), dtype=torch.float32, device="cuda")
+    path = args.knn_full
+    t = time.perf_counter()
+    with pb.KnnGraphWriter(path, p.k, path + ".ivecs") as w:
+        for r in range(row0, row1, chunk):
+            nb = min(chunk, row1 - r)
+            pb.gen_points_device(centers, SEED, 2, r, nb, dx[:nb], device=local, normalize=True)
+            ivf.knn_graph_write_device(w, dx[:nb], r, p, stream.cuda_stream)
+    wall = time.perf_counter() - t
+    rows = row1 - row0
+    return {"rows": rows, "records": w.records, "wall_s": round(wall, 2), "rows_per_s": rows / wall,
+            "file_bytes": os.path.getsize(path), "ivecs_bytes": os.path.getsize(path + ".ivecs"),
+            "note": "knn_graph_write_device per 1M-row chunk; wall clock includes generation, copies, writes"}
+
+
 def run_knn(args, rank, world, local):
     """Config 4: the k-NN graph.  A step = B stored vectors searched against the whole
     index with k + 1 neighbours and the self-match removed (knn_graph_device)."""
@@ -781,7 +821,7 @@ def run_knn(args, rank, world, local):
     c = args.c
     torch.cuda.set_device(local)
     centers = synth.gen_centers(SEED, c["ncent"], c["dim"])
-    coarse = synth.gen_points(SEED, 1, 0, c["nlist"], centers, normalize=True)
+    coarse = make_coarse(args, pb, synth, centers, True)
     t = time.time()
     ivf, pq = build_ivf(args, pb, torch, local, 0, args.n, coarse, centers, True)
     setup_s = time.time() - t
@@ -848,6 +888,8 @@ def run_knn(args, rank, world, local):
             "graph_time_est_s": rows / B * ms / steps / 1e3, "gpu_launches": launches, "clocks": clk,
             "roofline": dict(k6, kernel="K6 ivf_scan_kernel (both rounds)", kernel_share_of_step=k6_ms / ms),
             "roofline_step": stp, "roofline_hbm": hbm, "setup_s": round(setup_s, 1)}
+    if args.knn_full:
+        line["full_graph"] = knn_full(args, pb, torch, ivf, centers, p, row0, row1, local, stream)
     if world == 1 and not args.no_cpu_baseline:
         rng = np.random.default_rng(SEED)
         rows_s = np.sort(rng.choice(args.n, c["cpu_q"], replace=False))   # the seeded 10k-query subsample

@@ -326,6 +326,33 @@ int poly_b200_sharded_search_batch(poly_b200_sharded* index, const float* querie
                                    const poly_b200_search_params* params, int64_t* out_ids, float* out_scores,
                                    uint32_t* out_counts, poly_b200_search_stats* stats);
 
+/* train_coarse's k-means on the GPU (the reference kmeans is
+ * proj/src/kmeans.cpp:14-137 with KmeansParams kmeans.hpp:10-14): k-means++ seeding with
+ * the reference's Rng (mt19937_64) draws, `iters` Lloyd iterations (exact nearest-cell
+ * assignment by fp32 sq_l2, ties to the lower cell; centroids = float(double sum / count);
+ * empty cells take the farthest member of the largest cell), then a final assignment.
+ * x: n x dim host floats; centroids: k x dim out; assign (n, may be NULL);
+ * iteration_mse (iters, may be NULL): the objective before each update; mse: the final one.
+ * n <= k: every point is a centroid, cells replicate points cyclically. */
+int poly_b200_kmeans(const float* x, uint64_t n, uint32_t dim, uint32_t k, uint32_t iters, uint64_t seed, int device,
+                     float* centroids, uint32_t* assign, double* iteration_mse, double* mse);
+
+/* ---- k-NN graph output sink ("streamed to the output sink", External
+ * Interfaces: one record per vector -- id, neighbor count, then (neighbor id, score)
+ * pairs -- in a sectioned binary file, plus an optional ivecs export of neighbor ids).
+ * File: magic "POLYKNNG", u32 version 1, u32 k, u64 records, one section
+ * { "RECORDS_", u64 bytes, u64 fnv1a64(payload), payload }, payload = records
+ * { i64 id, u32 count, count x { i64 neighbor id, f32 score } } packed, little-endian.
+ * ivecs: per record an int32 k, then k int32 neighbor ids (-1 pads).
+ * write_device appends the graph rows of n stored vectors (device d_x, ids id0 ..):
+ * knn_graph on the GPU step by step, each step's rows written while the next is
+ * searched.  close patches the record count and checksum. */
+typedef struct poly_b200_knn_writer poly_b200_knn_writer;
+int poly_b200_knn_writer_open(const char* path, const char* ivecs_path, uint32_t k, poly_b200_knn_writer** out);
+int poly_b200_ivf_knn_graph_write_device(poly_b200_ivf* ivf, poly_b200_knn_writer* writer, const float* d_x,
+                                         uint64_t n, int64_t id0, const poly_b200_ivf_params* params, void* stream);
+int poly_b200_knn_writer_close(poly_b200_knn_writer* writer, uint64_t* records);
+
 /* Number of kernel launches this library has issued so far (for bench.py). */
 uint64_t poly_b200_launch_count(void);
 

@@ -405,3 +405,123 @@ def ref_ivf_search(pq: PQ, centroids, lists: IVFLists, queries, k, nprobe, tau=N
                                     _ptr(lists.codes), _ptr(lists.ids), _ptr(queries), nq, nprobe, cap,
                                     STRATEGIES[strategy], k, tau, threads, _ptr(oi), _ptr(osc), _ptr(oc), _ptr(sv)))
     return oi, osc, oc, sv
+
+
+# ---------------------------------------------------------------- k-means (train_coarse)
+class MT19937_64:
+    """std::mt19937_64 (the engine of poly::Rng, common.hpp:45-67), in Python for the k-means
+    restatement; pinned by the C++ standard's check value (10000th output of the default
+    seed 5489 = 9981545732273789042, tests/test_kmeans_oracle.py)."""
+    _M = (1 << 64) - 1
+
+    def __init__(self, seed: int):
+        self.mt = [0] * 312
+        self.mt[0] = seed & self._M
+        for i in range(1, 312):
+            self.mt[i] = (6364136223846793005 * (self.mt[i - 1] ^ (self.mt[i - 1] >> 62)) + i) & self._M
+        self.idx = 312
+
+    def _twist(self):
+        mt = self.mt
+        for i in range(312):
+            x = (mt[i] & 0xFFFFFFFF80000000) | (mt[(i + 1) % 312] & 0x7FFFFFFF)
+            xa = x >> 1
+            if x & 1:
+                xa ^= 0xB5026F5AA96619E9
+            mt[i] = mt[(i + 156) % 312] ^ xa
+        self.idx = 0
+
+    def __call__(self) -> int:
+        if self.idx >= 312:
+            self._twist()
+        y = self.mt[self.idx]
+        self.idx += 1
+        y ^= (y >> 29) & 0x5555555555555555
+        y ^= (y << 17) & 0x71D67FFFEDA60000
+        y ^= (y << 37) & 0xFFF7EEE000000000
+        y ^= y >> 43
+        return y & self._M
+
+    def u01(self) -> float:  # Rng::u01 (common.hpp:51)
+        return (self() >> 11) * 2.0 ** -53
+
+    def below(self, n: int) -> int:  # Rng::below (common.hpp:55-63)
+        if n <= 1:
+            return 0
+        limit = self._M - self._M % n
+        while True:
+            x = self()
+            if x < limit:
+                return x % n
+
+
+def _sq_l2_rows(x, c):
+    """sq_l2 (distances.cpp:10-17) of every row of x to c: fp32, dimension order, no FMA."""
+    acc = np.zeros(x.shape[0], np.float32)
+    for d in range(x.shape[1]):
+        t = x[:, d] - c[d]
+        acc = acc + t * t
+    return acc
+
+
+def _nearest_exact(x, cent):
+    """assign_nearest (distances.cpp:56-79) with exact fp32 sq_l2, ties to the lower cell."""
+    best = _sq_l2_rows(x, cent[0])
+    arg = np.zeros(x.shape[0], np.uint32)
+    for c in range(1, cent.shape[0]):
+        d = _sq_l2_rows(x, cent[c])
+        m = d < best
+        best = np.where(m, d, best)
+        arg[m] = c
+    return arg, best
+
+
+def kmeans_restated(data, k, iters=25, seed=1234567):
+    """kmeans (kmeans.cpp:14-137) restated in numpy with the exact assignment the GPU uses
+    (the reference's own assign_nearest goes through a BLAS GEMM).  Returns centroids,
+    assign, iteration_mse, mse.  Small inputs only (O(n k d) numpy passes)."""
+    x = np.ascontiguousarray(data, np.float32)
+    n, dim = x.shape
+    if n <= k:
+        cent = np.stack([x[c % n] for c in range(k)])
+        return cent, np.arange(n, dtype=np.uint32), [], 0.0
+    rng = MT19937_64(seed)
+    cent = np.empty((k, dim), np.float32)
+    cent[0] = x[rng.below(n)]
+    min_d2 = _sq_l2_rows(x, cent[0]).astype(np.float64)
+    for c in range(1, k):
+        total = float(np.sum(min_d2))  # (the reference sums sequentially; rounding may differ)
+        if total <= 0.0:
+            pick = rng.below(n)
+        else:
+            target = rng.u01() * total
+            cs = np.cumsum(min_d2)
+            hit = np.nonzero(target - cs <= 0.0)[0]
+            pick = int(hit[0]) if hit.size else n - 1
+        cent[c] = x[pick]
+        min_d2 = np.minimum(min_d2, _sq_l2_rows(x, cent[c]).astype(np.float64))
+    it_mse = []
+    for _ in range(iters):
+        assign, best = _nearest_exact(x, cent)
+        it_mse.append(float(np.sum(best.astype(np.float64))) / n)
+        counts = np.bincount(assign, minlength=k)
+        sums = np.zeros((k, dim), np.float64)
+        np.add.at(sums, assign, x.astype(np.float64))
+        for c in range(k):
+            if counts[c]:
+                cent[c] = (sums[c] * (1.0 / counts[c])).astype(np.float32)
+        for c in range(k):
+            if counts[c]:
+                continue
+            big = int(np.argmax(counts))
+            if counts[big] == 0:
+                break
+            members = np.nonzero(assign == big)[0]
+            d = _sq_l2_rows(x[members], cent[big])
+            far = int(members[int(np.argmax(d))])
+            cent[c] = x[far]
+            assign[far] = c
+            counts[c] = 1
+            counts[big] -= 1
+    assign, best = _nearest_exact(x, cent)
+    return cent, assign, it_mse, float(np.sum(best.astype(np.float64))) / n

@@ -8,7 +8,7 @@ kernels in csrc/.  See DESIGN.md.
 from .flat_index import (Errc, FlatIndex, Neighbor, PolyError, ProductQuantizer, SearchParams, SearchStats,
                          ShardedFlatIndex, Strategy, gen_points_device, launch_count, strategy_from_string, to_string)
 
-from .ivf_index import CoarseParams, IVFIndex
+from .ivf_index import CoarseParams, IVFIndex, KnnGraphWriter, kmeans
 
-__all__ = ["CoarseParams", "IVFIndex", "Errc", "FlatIndex", "Neighbor", "PolyError", "ProductQuantizer", "SearchParams", "SearchStats",
+__all__ = ["CoarseParams", "IVFIndex", "KnnGraphWriter", "kmeans", "Errc", "FlatIndex", "Neighbor", "PolyError", "ProductQuantizer", "SearchParams", "SearchStats",
            "ShardedFlatIndex", "Strategy", "gen_points_device", "launch_count", "strategy_from_string", "to_string"]

@@ -75,6 +75,10 @@ def _load():
     L.poly_b200_sharded_add_codes.argtypes = [_P, _P, _P, _u64]
     L.poly_b200_sharded_search_batch.argtypes = [_P, _P, _u64, C.POINTER(SearchParamsC), _P, _P, _P,
                                                  C.POINTER(SearchStatsC)]
+    L.poly_b200_kmeans.argtypes = [_P, _u64, _u32, _u32, _u32, _u64, _i32, _P, _P, _P, C.POINTER(_f64)]
+    L.poly_b200_knn_writer_open.argtypes = [C.c_char_p, C.c_char_p, _u32, C.POINTER(_P)]
+    L.poly_b200_ivf_knn_graph_write_device.argtypes = [_P, _P, _P, _u64, C.c_int64, C.POINTER(IvfParamsC), _P]
+    L.poly_b200_knn_writer_close.argtypes = [_P, C.POINTER(_u64)]
     L.poly_b200_ivf_set_batch.argtypes = [_P, _u32]
     L.poly_b200_ivf_batch.argtypes = [_P]
     L.poly_b200_ivf_batch.restype = _u32
@@ -124,7 +128,8 @@ EXPORTS = [
     "poly_b200_ivf_load", "poly_b200_ivf_set_batch", "poly_b200_ivf_batch",
     "poly_b200_sharded_create", "poly_b200_sharded_destroy", "poly_b200_sharded_size", "poly_b200_sharded_count",
     "poly_b200_sharded_shard_size", "poly_b200_sharded_add", "poly_b200_sharded_add_codes",
-    "poly_b200_sharded_search_batch",
+    "poly_b200_sharded_search_batch", "poly_b200_knn_writer_open", "poly_b200_ivf_knn_graph_write_device",
+    "poly_b200_knn_writer_close", "poly_b200_kmeans",
     "poly_b200_calibrate_threshold", "poly_b200_with_assignments", "poly_b200_get_codes",
     "poly_b200_search_keys_device", "poly_b200_merge_keys_device", "poly_b200_add_synthetic",
     "poly_b200_gen_points_device", "poly_b200_debug_lut", "poly_b200_debug_counts", "poly_b200_profile_enable", "poly_b200_profile_read",

@@ -18,7 +18,7 @@ OUT_DIR = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libpoly_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 SOURCES = ["capi.cu", "capi_ivf.cu", "kernels_encode.cu", "kernels_scan.cu", "kernels_topk.cu", "kernels_ivf.cu",
-           "kernels_rescue.cu", "kernels_coarse.cu", "kernels_ivf_scan.cu", "capi_multi.cu"]
+           "kernels_rescue.cu", "kernels_coarse.cu", "kernels_ivf_scan.cu", "capi_multi.cu", "capi_kmeans.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
          "-Xptxas", "-v", f"-I{os.path.join(os.path.dirname(HERE), 'include')}"]
 

@@ -1020,6 +1020,215 @@ int poly_b200_ivf_knn_graph_device(poly_b200_ivf* iv, const float* d_x, uint64_t
     });
 }
 
+static const char kIvfMagic[8] = {'P', 'O', 'L', 'Y', 'I', 'V', 'F', '\0'};
+static const uint32_t kIvfVersion = 1;
+
+static uint64_t fnv1a(uint64_t h, const void* p, size_t n) {
+    const uint8_t* b = static_cast<const uint8_t*>(p);
+    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 0x100000001B3ull;
+    return h;
+}
+
+struct FileCloser {
+    void operator()(FILE* f) const { if (f) fclose(f); }
+};
+
+// ---- k-NN graph output sink ("streamed to the output sink"; External
+// Interfaces: "one record per vector -- id, neighbor count, then (neighbor id, score) pairs --
+// in a sectioned binary file plus an optional ivecs export of neighbor ids").
+// Layout (little-endian): magic "POLYKNNG", u32 version 1, u32 k, u64 records, then one
+// section { char tag[8] = "RECORDS_", u64 bytes, u64 fnv1a64(payload), payload } whose
+// payload is the records { i64 id, u32 count, count x { i64 neighbor id, f32 score } },
+// packed.  The ivecs file has per record an int32 k then k int32 neighbor ids (-1 pads).
+struct poly_b200_knn_writer {
+    std::unique_ptr<FILE, FileCloser> f, fv;
+    uint32_t k = 0;
+    uint64_t records = 0, bytes = 0, hash = 0xCBF29CE484222325ull;
+    // pinned double buffers for one step of rows (ids, scores, counts)
+    uint64_t rows_cap = 0;
+    int64_t* h_ids[2] = {nullptr, nullptr};
+    float* h_sc[2] = {nullptr, nullptr};
+    uint32_t* h_cnt[2] = {nullptr, nullptr};
+    std::vector<uint8_t> rec;
+    std::vector<int32_t> vrec;
+};
+
+namespace {
+void knn_free_host(poly_b200_knn_writer* w) {
+    for (int i = 0; i < 2; ++i) {
+        if (w->h_ids[i]) cudaFreeHost(w->h_ids[i]);
+        if (w->h_sc[i]) cudaFreeHost(w->h_sc[i]);
+        if (w->h_cnt[i]) cudaFreeHost(w->h_cnt[i]);
+        w->h_ids[i] = nullptr;
+        w->h_sc[i] = nullptr;
+        w->h_cnt[i] = nullptr;
+    }
+    w->rows_cap = 0;
+}
+
+void knn_put(poly_b200_knn_writer* w, FILE* f, const void* p, size_t n) {
+    require(n == 0 || fwrite(p, 1, n, f) == n, POLY_B200_IO, "k-NN graph write failed");
+}
+
+// append rows [0, nb) of a host batch: ids id0 + r
+void knn_write_batch(poly_b200_knn_writer* w, int slot, uint64_t nb, int64_t id0) {
+    const uint32_t k = w->k;
+    w->rec.clear();
+    for (uint64_t r = 0; r < nb; ++r) {
+        const int64_t id = id0 + (int64_t)r;
+        const uint32_t c = w->h_cnt[slot][r];
+        const size_t at = w->rec.size();
+        w->rec.resize(at + 12 + (size_t)c * 12);
+        uint8_t* o = w->rec.data() + at;
+        std::memcpy(o, &id, 8);
+        std::memcpy(o + 8, &c, 4);
+        for (uint32_t j = 0; j < c; ++j) {
+            std::memcpy(o + 12 + 12 * j, &w->h_ids[slot][r * k + j], 8);
+            std::memcpy(o + 20 + 12 * j, &w->h_sc[slot][r * k + j], 4);
+        }
+    }
+    w->hash = fnv1a(w->hash, w->rec.data(), w->rec.size());
+    knn_put(w, w->f.get(), w->rec.data(), w->rec.size());
+    w->bytes += w->rec.size();
+    w->records += nb;
+    if (w->fv) {
+        w->vrec.resize((size_t)nb * (k + 1));
+        for (uint64_t r = 0; r < nb; ++r) {
+            int32_t* o = w->vrec.data() + r * (k + 1);
+            o[0] = (int32_t)k;
+            for (uint32_t j = 0; j < k; ++j)
+                o[1 + j] = j < w->h_cnt[slot][r] ? (int32_t)w->h_ids[slot][r * k + j] : -1;
+        }
+        knn_put(w, w->fv.get(), w->vrec.data(), w->vrec.size() * 4);
+    }
+}
+}  // namespace
+
+int poly_b200_knn_writer_open(const char* path, const char* ivecs_path, uint32_t k, poly_b200_knn_writer** out) {
+    return guard([&] {
+        require(path && out, POLY_B200_INVALID_ARGUMENT, "null arguments");
+        require(k >= 1 && k < (uint32_t)pb::KMAX, POLY_B200_INVALID_ARGUMENT, "k must be in [1, 2047]");
+        auto w = std::make_unique<poly_b200_knn_writer>();
+        w->k = k;
+        w->f.reset(fopen(path, "wb"));
+        require(w->f != nullptr, POLY_B200_IO, std::string("cannot open ") + path + " for writing");
+        if (ivecs_path) {
+            w->fv.reset(fopen(ivecs_path, "wb"));
+            require(w->fv != nullptr, POLY_B200_IO, std::string("cannot open ") + ivecs_path + " for writing");
+        }
+        static const char magic[8] = {'P', 'O', 'L', 'Y', 'K', 'N', 'N', 'G'};
+        const uint32_t ver = 1;
+        const uint64_t zero = 0;
+        knn_put(w.get(), w->f.get(), magic, 8);
+        knn_put(w.get(), w->f.get(), &ver, 4);
+        knn_put(w.get(), w->f.get(), &k, 4);
+        knn_put(w.get(), w->f.get(), &zero, 8);          // records (patched at close)
+        knn_put(w.get(), w->f.get(), "RECORDS_", 8);
+        knn_put(w.get(), w->f.get(), &zero, 8);          // bytes (patched)
+        knn_put(w.get(), w->f.get(), &zero, 8);          // checksum (patched)
+        *out = w.release();
+    });
+}
+
+int poly_b200_knn_writer_close(poly_b200_knn_writer* w, uint64_t* records) {
+    if (!w) return POLY_B200_OK;
+    std::unique_ptr<poly_b200_knn_writer> owned(w);
+    return guard([&] {
+        knn_free_host(w);
+        FILE* f = w->f.get();
+        require(fseek(f, 16, SEEK_SET) == 0, POLY_B200_IO, "k-NN graph seek failed");
+        knn_put(w, f, &w->records, 8);
+        require(fseek(f, 32, SEEK_SET) == 0, POLY_B200_IO, "k-NN graph seek failed");
+        knn_put(w, f, &w->bytes, 8);
+        knn_put(w, f, &w->hash, 8);
+        require(fflush(f) == 0, POLY_B200_IO, "k-NN graph write failed");
+        if (w->fv) require(fflush(w->fv.get()) == 0, POLY_B200_IO, "ivecs write failed");
+        if (records) *records = w->records;
+    });
+}
+
+int poly_b200_ivf_knn_graph_write_device(poly_b200_ivf* iv, poly_b200_knn_writer* w, const float* d_x, uint64_t n,
+                                         int64_t id0, const poly_b200_ivf_params* p, void* stream) {
+    return guard([&] {
+        require(iv && w && p, POLY_B200_INVALID_ARGUMENT, "null arguments");
+        require(p->k == w->k, POLY_B200_INVALID_ARGUMENT, "params.k differs from the writer's k");
+        require(n == 0 || d_x, POLY_B200_INVALID_ARGUMENT, "null vectors");
+        std::lock_guard<std::mutex> lk(iv->mu);
+        DeviceGuard dg(iv->device);
+        if (n == 0) return;
+        cudaStream_t s = (cudaStream_t)stream;
+        const uint32_t k = p->k;
+        poly_b200_ivf_params p1 = *p;
+        p1.k = k + 1;
+        const uint64_t step = std::min<uint64_t>(64ull * iv->nqb, n);
+        if (iv->knn_rows < step || iv->knn_k1 < p1.k) {
+            CK(cudaStreamSynchronize(s));
+            dfree(iv->knn_ids);
+            dfree(iv->knn_sc);
+            dfree(iv->knn_cnt);
+            iv->knn_rows = std::max<uint64_t>(iv->knn_rows, step);
+            iv->knn_k1 = std::max<uint32_t>(iv->knn_k1, p1.k);
+            iv->knn_ids = dalloc<int64_t>(iv->knn_rows * iv->knn_k1);
+            iv->knn_sc = dalloc<float>(iv->knn_rows * iv->knn_k1);
+            iv->knn_cnt = dalloc<uint32_t>(iv->knn_rows);
+        }
+        if (w->rows_cap < step) {
+            knn_free_host(w);
+            for (int i = 0; i < 2; ++i) {
+                CK(cudaMallocHost(&w->h_ids[i], step * k * 8));
+                CK(cudaMallocHost(&w->h_sc[i], step * k * 4));
+                CK(cudaMallocHost(&w->h_cnt[i], step * 4));
+            }
+            w->rows_cap = step;
+        }
+        // device outputs of one step (k per row), then copies to the pinned slot; the host
+        // writes step b - 1 while the GPU searches step b
+        int64_t* o_ids = dalloc<int64_t>(step * k);
+        float* o_sc = dalloc<float>(step * k);
+        uint32_t* o_cnt = dalloc<uint32_t>(step);
+        cudaEvent_t ev[2] = {nullptr, nullptr};
+        try {
+            CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+            uint64_t prev_nb = 0;
+            int64_t prev_id0 = 0;
+            int slot = 0;
+            for (uint64_t b0 = 0; b0 < n; b0 += step, slot ^= 1) {
+                const uint32_t nb = (uint32_t)std::min<uint64_t>(step, n - b0);
+                device_search(iv, d_x + b0 * iv->dim, nb, &p1, iv->knn_ids, iv->knn_sc, iv->knn_cnt, s);
+                drop_self_kernel<<<(nb + 127) / 128, 128, 0, s>>>(iv->knn_ids, iv->knn_sc, iv->knn_cnt, nb, k,
+                                                                  id0 + (int64_t)b0, o_ids, o_sc, o_cnt);
+                pb::count_launch();
+                CK(cudaGetLastError());
+                CK(cudaMemcpyAsync(w->h_ids[slot], o_ids, (size_t)nb * k * 8, cudaMemcpyDeviceToHost, s));
+                CK(cudaMemcpyAsync(w->h_sc[slot], o_sc, (size_t)nb * k * 4, cudaMemcpyDeviceToHost, s));
+                CK(cudaMemcpyAsync(w->h_cnt[slot], o_cnt, (size_t)nb * 4, cudaMemcpyDeviceToHost, s));
+                CK(cudaEventRecord(ev[slot], s));
+                if (prev_nb) {  // the previous step's records, while this one runs
+                    CK(cudaEventSynchronize(ev[slot ^ 1]));
+                    knn_write_batch(w, slot ^ 1, prev_nb, prev_id0);
+                }
+                prev_nb = nb;
+                prev_id0 = id0 + (int64_t)b0;
+            }
+            CK(cudaEventSynchronize(ev[slot ^ 1]));
+            knn_write_batch(w, slot ^ 1, prev_nb, prev_id0);
+            read_stats(iv, 0, nullptr, s);  // fails loudly on a work-list overflow
+        } catch (...) {
+            dfree(o_ids);
+            dfree(o_sc);
+            dfree(o_cnt);
+            for (auto e : ev)
+                if (e) cudaEventDestroy(e);
+            throw;
+        }
+        dfree(o_ids);
+        dfree(o_sc);
+        dfree(o_cnt);
+        for (auto e : ev) cudaEventDestroy(e);
+    });
+}
+
 int poly_b200_ivf_search(poly_b200_ivf* iv, const float* queries, uint64_t nq, const poly_b200_ivf_params* p,
                          int64_t* out_ids, float* out_scores, uint32_t* out_counts, poly_b200_search_stats* stats) {
     return guard([&] {
@@ -1065,19 +1274,6 @@ int poly_b200_ivf_search(poly_b200_ivf* iv, const float* queries, uint64_t nq, c
 // order PQCODEBK (m x 256 x dsub fp32), PQPERMS_ (m x 256 u16), COARSE__ (nlist x dim
 // fp32), LISTOFF_ ((nlist + 1) u64), CODES___ (n x m u8, list order), IDS_____ (n i64).
 // Errors use poly::errc (common.hpp:13-22): io, format, version, corrupt.
-static const char kIvfMagic[8] = {'P', 'O', 'L', 'Y', 'I', 'V', 'F', '\0'};
-static const uint32_t kIvfVersion = 1;
-
-static uint64_t fnv1a(uint64_t h, const void* p, size_t n) {
-    const uint8_t* b = static_cast<const uint8_t*>(p);
-    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 0x100000001B3ull;
-    return h;
-}
-
-struct FileCloser {
-    void operator()(FILE* f) const { if (f) fclose(f); }
-};
-
 int poly_b200_ivf_save(poly_b200_ivf* iv, const char* path) {
     return guard([&] {
         require(iv && path, POLY_B200_INVALID_ARGUMENT, "null arguments");

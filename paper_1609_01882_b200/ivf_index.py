@@ -208,8 +208,52 @@ class IVFIndex:
         _check(lib.poly_b200_ivf_merge_keys_device(self._h, ptr(d_keys), ptr(d_counts), parts, nq, k, ptr(d_ids),
                                                    ptr(d_scores), ptr(d_counts_out), C.c_void_p(stream)))
 
+    def knn_graph_write_device(self, writer: "KnnGraphWriter", d_x, id0, params: CoarseParams, stream=0):
+        """knn_graph rows of the stored vectors d_x (ids id0..) appended to a graph file."""
+        _check(lib.poly_b200_ivf_knn_graph_write_device(self._h, writer._w, d_x.data_ptr(), d_x.shape[0], int(id0),
+                                                        C.byref(params.c()), C.c_void_p(stream)))
+
     def knn_graph_device(self, d_x, id0, params: CoarseParams, d_ids, d_scores, d_counts=None, stream=0):
         """knn_graph: rows of d_x are the stored vectors id0.. ; self-match removed."""
         ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731
         _check(lib.poly_b200_ivf_knn_graph_device(self._h, ptr(d_x), d_x.shape[0], int(id0), C.byref(params.c()),
                                                   ptr(d_ids), ptr(d_scores), ptr(d_counts), C.c_void_p(stream)))
+
+
+def kmeans(x, k: int, iters: int = 25, seed: int = 1234567, device: int = 0):
+    """train_coarse's k-means on the GPU (kmeans.cpp:14-137 restated,
+    KmeansParams defaults).  Returns (centroids k x dim, assign n, iteration_mse, mse)."""
+    x = np.ascontiguousarray(x, np.float32)
+    n, dim = x.shape
+    cent = np.empty((k, dim), np.float32)
+    assign = np.empty(n, np.uint32)
+    it = np.zeros(max(iters, 1), np.float64)
+    mse = C.c_double(0)
+    _check(lib.poly_b200_kmeans(_p(x), n, dim, k, iters, seed, device, _p(cent), _p(assign), _p(it), C.byref(mse)))
+    return cent, assign, it[:iters] if n > k else it[:0], float(mse.value)
+
+
+class KnnGraphWriter:
+    """The k-NN graph output sink: a sectioned binary graph file plus an
+    optional ivecs export (layout in knn_format.py).  Use as a context manager."""
+
+    def __init__(self, path, k: int, ivecs_path=None):
+        w = C.c_void_p()
+        _check(lib.poly_b200_knn_writer_open(str(path).encode(), None if ivecs_path is None else str(ivecs_path).encode(),
+                                             int(k), C.byref(w)))
+        self._w = w
+        self.records = 0
+
+    def close(self) -> int:
+        if self._w:
+            n = C.c_uint64(0)
+            w, self._w = self._w, None
+            _check(lib.poly_b200_knn_writer_close(w, C.byref(n)))
+            self.records = int(n.value)
+        return self.records
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()

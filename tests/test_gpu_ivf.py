@@ -164,6 +164,46 @@ def test_knn_graph_matches_oracle(pb, gi):
         assert (got[len(row):] == -1).all()
 
 
+def test_knn_graph_file_sink(pb, gi, tmp_path):
+    """The k-NN graph output sink: rows written in two appends (small
+    batches: several pipelined steps each) read back equal to knn_graph_device, the file is
+    byte-identical to the reference writer's, and the ivecs export holds the same ids."""
+    import torch
+    from paper_1609_01882_b200 import knn_format
+    seed = int(gi["data_seed"])
+    centers = oracle.gen_centers(seed, 1000, 128)
+    x = oracle.gen_points(seed, 2, 0, 20000, centers)
+    coarse = oracle.gen_points(seed, 1, 0, 64, centers)
+    ix = pb.IVFIndex(pb.ProductQuantizer(8, 8, 128, gi["codebooks"], gi["perms"]), coarse)
+    ix.add(x)
+    ix.set_batch(50)  # steps of 64 x 50 rows: the write pipeline runs several steps per call
+    n, k = 7000, 5
+    p = pb.CoarseParams(pb.Strategy.dual, k, 26, 4, 0)
+    dx = torch.from_numpy(x[:n]).cuda()
+    ids = torch.empty((n, k), dtype=torch.int64, device="cuda")
+    sc = torch.empty((n, k), dtype=torch.float32, device="cuda")
+    cnt = torch.empty(n, dtype=torch.int32, device="cuda")
+    ix.knn_graph_device(dx, 0, p, ids, sc, cnt)
+    torch.cuda.synchronize()
+    ids, sc, cnt = ids.cpu().numpy(), sc.cpu().numpy(), cnt.cpu().numpy().astype(np.uint32)
+    path, vpath = tmp_path / "g.knng", tmp_path / "g.ivecs"
+    with pb.KnnGraphWriter(path, k, vpath) as w:
+        ix.knn_graph_write_device(w, dx[:4000], 0, p)
+        ix.knn_graph_write_device(w, dx[4000:], 4000, p)
+    assert w.records == n
+    kk, rid, rc, rn, rs = knn_format.read_graph(path, check_sum=False)
+    assert kk == k and np.array_equal(rid, np.arange(n)) and np.array_equal(rc, cnt)
+    assert np.array_equal(rn, ids) and np.array_equal(_bits(rs), _bits(sc))
+    ref = tmp_path / "ref.knng"
+    knn_format.write_graph(ref, k, np.arange(500), cnt[:500], ids[:500], sc[:500])
+    head = open(path, "rb").read()
+    want = open(ref, "rb").read()
+    assert head[48:len(want)] == want[48:]  # the first 500 records, byte for byte
+    assert np.array_equal(knn_format.read_ivecs(vpath), ids.astype(np.int32))
+    with pytest.raises(pb.PolyError):
+        pb.KnnGraphWriter(tmp_path / "no_such_dir" / "g.knng", k)
+
+
 @pytest.mark.parametrize("dim,nlist", [(128, 8192), (256, 4096)])
 def test_probe_order_many_near_ties(pb, gi, dim, nlist):
     """enumerate_cells runs TF32 tensor-core dots + an exact re-rank (K5r): probe order
