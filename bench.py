@@ -224,12 +224,15 @@ def _clk(clk, pk):
 def scan_terms(m, reuse, survivor_frac, f_mhz, hbm_gbs, rt, filt=True, nsm=148):
     """SURVEY.md sec. 8(d) per-pair terms (clocks per pair per SM) of a scan over m-byte
     codes: code bytes at HBM bandwidth (each code read once per `reuse` queries), POPC
-    (code_bits / 32 per pair; none when the filter keeps everything) and LUT gathers (m per
-    survivor)."""
+    (code_bits / 32 per pair; none when the filter keeps everything) and LUT gathers: m / 2
+    per survivor -- the fewest any exact ADC can do here, since the half-sum early exit
+    (code_ops.cuh adc_bounded) stops after m / 2 terms when the bound is exceeded (the
+    full m per survivor of SURVEY.md sec. 8(d) is a looser bound: the plain-ADC kernel
+    beats it)."""
     bytes_per_clk_sm = hbm_gbs * 1e9 / (nsm * f_mhz * 1e6)
     return {"hbm": m / reuse / bytes_per_clk_sm,
             "popc": (m * 8 / 32) / rt["popc"] if filt else 0.0,
-            "lds": survivor_frac * m / rt["lds_gather"]}
+            "lds": survivor_frac * (m / 2) / rt["lds_gather"]}
 
 
 def roofline_from_terms(terms, achieved, f_mhz, nsm=148, unit="pairs/s"):

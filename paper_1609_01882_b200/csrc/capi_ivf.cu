@@ -63,6 +63,7 @@ struct poly_b200_ivf {
     unsigned long long* scanned = nullptr;
     uint32_t scratch_nprobe = 0;
     uint4* items[2] = {nullptr, nullptr};  // K6 work lists of the two rounds
+    uint32_t* lut_items = nullptr;         // K1r item lists of the two rounds (2 x nqb x np)
     uint64_t items_cap[2] = {0, 0};
     float* lutp = nullptr;
     uint8_t* qcodes = nullptr;
@@ -240,6 +241,8 @@ void ensure_ivf_scratch(poly_b200_ivf* iv, uint32_t nprobe, uint32_t k) {
         iv->probe_counts = dalloc<uint32_t>(iv->nqb);
         iv->lutp = dalloc<float>((size_t)iv->nqb * nprobe * iv->m * 256);
         iv->qcodes = dalloc<uint8_t>((size_t)iv->nqb * nprobe * iv->cb);
+        dfree(iv->lut_items);
+        iv->lut_items = dalloc<uint32_t>((size_t)2 * iv->nqb * nprobe);
     }
     const uint64_t r1 = std::min<uint64_t>(nprobe, IVF_R1_MAX);
     // work-list bounds per query: round 1 <= r1 probes -> <= r1 + r1 * max_list / CHUNK items;
@@ -344,24 +347,27 @@ void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_
     w.chunk[0] = IVF_CHUNK;
     w.chunk[1] = IVF_CHUNK2;
     w.overflow = iv->ctrl + iv->nqb;
+    w.lut_items[0] = iv->lut_items;
+    w.lut_items[1] = iv->lut_items + (size_t)iv->nqb * np;
+    w.nlut = iv->ctrl + iv->nqb + 5;
     pb::launch_ivf_probe_count(iv->probe_keys, nqb, np, iv->d_off, p->cap, iv->np_eff, iv->scanned, s, iv->split,
                                IVF_R1_CODES, IVF_R1_MAX, w);
     add_u64<<<1, 256, 0, s>>>(iv->scanned, nqb, iv->scan_total);
     pb::count_launch();
-    // residual LUTs: the round-1 probes on the caller's stream; the others on the side
-    // stream, overlapping round 1, its top-k and the compaction (K1r is FP / shared-
-    // memory bound, round 1 memory / latency bound); round 2 waits for them
-    const uint32_t r1p = std::min(np, IVF_R1_MAX);
-    const bool side = r1p < np;
+    // residual LUTs of the items with a non-empty list here: round 1's on the caller's
+    // stream; round 2's on the side stream, overlapping round 1, its top-k and the
+    // compaction (K1r is FP / shared-memory bound, round 1 memory / latency bound); round 2
+    // waits for them
+    const bool side = np > 1;
     if (side) {
         CK(cudaEventRecord(iv->ev_fork, s));
         CK(cudaStreamWaitEvent(iv->side, iv->ev_fork, 0));
-        pb::launch_residual_lut(d_q, nqb, iv->dim, iv->m, iv->probe_keys, np, r1p, np, iv->d_coarse,
-                                iv->d_codebooks, iv->d_perms, iv->lutp, iv->qcodes, iv->side);
+        pb::launch_residual_lut(d_q, iv->dim, iv->m, iv->probe_keys, np, w.lut_items[1], w.nlut + 1, nqb * np,
+                                iv->d_coarse, iv->d_codebooks, iv->d_perms, iv->lutp, iv->qcodes, iv->side);
         CK(cudaEventRecord(iv->ev_join, iv->side));
     }
-    pb::launch_residual_lut(d_q, nqb, iv->dim, iv->m, iv->probe_keys, np, 0, r1p, iv->d_coarse, iv->d_codebooks,
-                            iv->d_perms, iv->lutp, iv->qcodes, s);
+    pb::launch_residual_lut(d_q, iv->dim, iv->m, iv->probe_keys, np, w.lut_items[0], w.nlut, nqb * np, iv->d_coarse,
+                            iv->d_codebooks, iv->d_perms, iv->lutp, iv->qcodes, s);
     pb::IvfScanArgs a{};
     a.codes = iv->d_codes_list;
     a.low = iv->d_low_list;
@@ -595,7 +601,7 @@ int poly_b200_ivf_destroy(poly_b200_ivf* iv) {
                             (void*)iv->d_oid, (void*)iv->d_osc, (void*)iv->d_ocnt,
                             (void*)iv->knn_ids, (void*)iv->knn_sc, (void*)iv->knn_cnt, (void*)iv->d_cnorm, (void*)iv->items[0],
                             (void*)iv->d_cpacked, (void*)iv->grp, (void*)iv->rank_scratch,
-                            (void*)iv->items[1]})
+                            (void*)iv->items[1], (void*)iv->lut_items})
                 dfree(p);
             if (iv->h_overflow) cudaFreeHost(iv->h_overflow);
             for (auto& pe : iv->prof_events) {
@@ -801,6 +807,7 @@ int poly_b200_ivf_set_batch(poly_b200_ivf* iv, uint32_t nqb) {
         for (void** pp : {(void**)&iv->ckeys, (void**)&iv->nl_counts, (void**)&iv->grp, (void**)&iv->rank_scratch,
                           (void**)&iv->probe_keys, (void**)&iv->probe_counts, (void**)&iv->np_eff, (void**)&iv->split,
                           (void**)&iv->scanned, (void**)&iv->items[0], (void**)&iv->items[1], (void**)&iv->lutp,
+                          (void**)&iv->lut_items,
                           (void**)&iv->qcodes, (void**)&iv->cand, (void**)&iv->ctrl, (void**)&iv->thr,
                           (void**)&iv->keys, (void**)&iv->kcounts, (void**)&iv->surv_total, (void**)&iv->scan_total,
                           (void**)&iv->ovq, (void**)&iv->surv_q, (void**)&iv->hash_q, (void**)&iv->sticky_overflow}) {
@@ -904,8 +911,10 @@ int poly_b200_ivf_search_keys_device(poly_b200_ivf* iv, const float* d_q, uint64
         DeviceGuard dg(iv->device);
         cudaStream_t s = (cudaStream_t)stream;
         iv->idm.sync(iv->n);
-        require(iv->n == 0 || iv->idm.mode == pb::ID_ARITH, POLY_B200_STATE,
-                "key output needs consecutive ids below 2^32 (the key carries the id itself)");
+        // a key carries the 32-bit low word: the id itself unless ids needed a rank table,
+        // whose ranks are local to this shard and would be mis-merged across ranks
+        require(iv->n == 0 || iv->idm.d_rank_to_id == nullptr, POLY_B200_STATE,
+                "key output needs ids in [0, 2^32) (the key carries the id itself)");
         const int mode = device_search(iv, d_q, nq, p, nullptr, nullptr, nullptr, s, d_keys, d_counts);
         if (stats) {
             stats->scanned = stats->survivors = 0;
@@ -926,8 +935,10 @@ int poly_b200_ivf_search_keys_probes_device(poly_b200_ivf* iv, const float* d_q,
         DeviceGuard dg(iv->device);
         cudaStream_t s = (cudaStream_t)stream;
         iv->idm.sync(iv->n);
-        require(iv->n == 0 || iv->idm.mode == pb::ID_ARITH, POLY_B200_STATE,
-                "key output needs consecutive ids below 2^32 (the key carries the id itself)");
+        // a key carries the 32-bit low word: the id itself unless ids needed a rank table,
+        // whose ranks are local to this shard and would be mis-merged across ranks
+        require(iv->n == 0 || iv->idm.d_rank_to_id == nullptr, POLY_B200_STATE,
+                "key output needs ids in [0, 2^32) (the key carries the id itself)");
         const int mode = device_search(iv, d_q, nq, p, nullptr, nullptr, nullptr, s, d_keys, d_counts, d_probe_keys);
         if (stats) {
             stats->scanned = stats->survivors = 0;

@@ -113,8 +113,8 @@ __device__ __forceinline__ unsigned long long k1_pack(float lo, float hi) {
 __global__ void __launch_bounds__(128, POLY_K1R_MINB) residual_lut_quad_kernel(const float* __restrict__ queries, uint32_t dim,
                                                                    uint32_t m,
                                                                    const unsigned long long* __restrict__ probe_keys,
-                                                                   uint32_t nprobe, uint32_t p_lo, uint32_t span,
-                                                                   uint32_t nitems,
+                                                                   uint32_t nprobe, const uint32_t* __restrict__ items,
+                                                                   const uint32_t* __restrict__ nitems_p,
                                                                    const float* __restrict__ cent,
                                                                    const float* __restrict__ codebooks,
                                                                    const uint16_t* __restrict__ perms,
@@ -122,9 +122,10 @@ __global__ void __launch_bounds__(128, POLY_K1R_MINB) residual_lut_quad_kernel(c
                                                                    uint8_t* __restrict__ qcodes, float zero) {
     const uint32_t item0 = blockIdx.x * K1R_ITEMS, t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const uint32_t h = t >> 6, u = t & 63, wh = warp & 1;  // sub-quantizer half, pair index, warp within half
+    const uint32_t nitems = *nitems_p;
+    if (item0 >= nitems) return;
     const uint32_t ni = min(K1R_ITEMS, nitems - item0);
-    // local item i covers probe p_lo + i % span of query i / span: global item q * nprobe + p
-    auto gitem = [&](uint32_t i) { return (i / span) * nprobe + p_lo + i % span; };
+    auto gitem = [&](uint32_t i) { return __ldg(items + i); };  // global item q * nprobe + p
     __shared__ __align__(16) unsigned long long rr[K1R_ITEMS][256];  // (r, r) per dim
     __shared__ float wv[K1R_ITEMS][16][2];
     __shared__ uint32_t wj[K1R_ITEMS][16][2];
@@ -211,15 +212,14 @@ __global__ void __launch_bounds__(128, POLY_K1R_MINB) residual_lut_quad_kernel(c
     }
 }
 
-void launch_residual_lut(const float* queries, uint32_t nq, uint32_t dim, uint32_t m,
-                         const unsigned long long* probe_keys, uint32_t nprobe, uint32_t p_lo, uint32_t p_hi,
+void launch_residual_lut(const float* queries, uint32_t dim, uint32_t m, const unsigned long long* probe_keys,
+                         uint32_t nprobe, const uint32_t* items, const uint32_t* nitems, uint32_t max_items,
                          const float* cent, const float* codebooks, const uint16_t* perms, float* lutp,
                          uint8_t* qcodes, cudaStream_t s) {
-    if (nq == 0 || p_hi <= p_lo) return;
-    const uint32_t span = p_hi - p_lo, nitems = nq * span;
-    const uint32_t grid = (nitems + K1R_ITEMS - 1) / K1R_ITEMS;
-    residual_lut_quad_kernel<<<grid, 128, 0, s>>>(queries, dim, m, probe_keys, nprobe, p_lo, span, nitems, cent,
-                                                  codebooks, perms, lutp, qcodes, 0.0f);
+    if (max_items == 0) return;
+    const uint32_t grid = (max_items + K1R_ITEMS - 1) / K1R_ITEMS;  // CTAs past the device count exit
+    residual_lut_quad_kernel<<<grid, 128, 0, s>>>(queries, dim, m, probe_keys, nprobe, items, nitems, cent, codebooks,
+                                                  perms, lutp, qcodes, 0.0f);
     count_launch();
 }
 
@@ -264,29 +264,46 @@ __global__ void ivf_probe_count_kernel(const unsigned long long* __restrict__ pr
         np_eff[qi] = ne;
         scanned[qi] = base;
     }
-    // round-1 split: the fewest leading probes (>= 1, <= r1_max, <= ne) holding >= r1_codes codes
+    // round-1 split: the leading probes through the first one at which the round holds
+    // >= r1_codes codes or r1_max non-empty lists (empty lists -- all the cells another rank
+    // owns under by-list sharding -- do not count)
     if (split) {
-        const uint32_t lim = min(min(r1_max, ne), 32u);
-        uint64_t sz = 0;
-        if (lane < lim) {
-            const uint32_t cell = (uint32_t)probe_keys[(size_t)qi * nprobe + lane];
-            sz = off[cell + 1] - off[cell];
-        }
-        uint64_t incl = sz;
+        uint32_t sp = ne;
+        uint64_t cum = 0;
+        uint32_t nonempty = 0;
+        for (uint32_t p0 = 0; p0 < ne; p0 += 32) {
+            const uint32_t p = p0 + lane;
+            uint64_t sz = 0;
+            if (p < ne) {
+                const uint32_t cell = (uint32_t)probe_keys[(size_t)qi * nprobe + p];
+                sz = off[cell + 1] - off[cell];
+            }
+            uint64_t incl = sz;
+            uint32_t incl_ne = sz > 0;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint64_t v = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= (uint32_t)o) incl += v;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                const uint32_t w = __shfl_up_sync(0xffffffffu, incl_ne, o);
+                if (lane >= (uint32_t)o) {
+                    incl += v;
+                    incl_ne += w;
+                }
+            }
+            const uint32_t hit = __ballot_sync(0xffffffffu, p < ne && (cum + incl >= r1_codes || nonempty + incl_ne >= r1_max));
+            if (hit) {
+                sp = p0 + __ffs(hit);
+                break;
+            }
+            cum += __shfl_sync(0xffffffffu, incl, 31);
+            nonempty += __shfl_sync(0xffffffffu, incl_ne, 31);
         }
-        const uint32_t hit = __ballot_sync(0xffffffffu, lane < lim && incl >= r1_codes);
-        const uint32_t sp = max(1u, hit ? (uint32_t)__ffs(hit) : lim);
         if (lane == 0) split[qi] = sp;
         // work lists: round 1 = probes [0, sp), round 2 = [sp, ne) (A/B: cutting round 1
         // at 2048 / 4096 rows instead of whole probes gained nothing).  Lists are cut into
         // chunks of w.chunk[r] rows; one item (query, probe, row0, row1) per chunk.
         if (w.items[0]) {
             for (int r = 0; r < 2; ++r) {
-                const uint32_t phi = r ? ne : min(sp, ne), ch = w.chunk[r];
+                const uint32_t phi = r ? ne : sp, ch = w.chunk[r];
                 for (uint32_t p0 = 0; p0 < phi; p0 += 32) {
                     const uint32_t p = p0 + lane;
                     uint32_t len = 0;
@@ -294,7 +311,16 @@ __global__ void ivf_probe_count_kernel(const unsigned long long* __restrict__ pr
                         const uint32_t cell = (uint32_t)probe_keys[(size_t)qi * nprobe + p];
                         len = (uint32_t)(off[cell + 1] - off[cell]);
                     }
-                    const uint32_t ap = p < min(sp, ne) ? len : 0;  // round-1 rows of probe p
+                    // the round's non-empty items get a residual LUT (K1r)
+                    const bool lut = p < phi && len > 0 && (r == 0 || p >= sp);
+                    const uint32_t bl = __ballot_sync(0xffffffffu, lut);
+                    if (bl) {
+                        uint32_t base = 0;
+                        if (lane == 0) base = atomicAdd(w.nlut + r, (uint32_t)__popc(bl));
+                        base = __shfl_sync(0xffffffffu, base, 0);
+                        if (lut) w.lut_items[r][base + __popc(bl & ((1u << lane) - 1u))] = qi * nprobe + p;
+                    }
+                    const uint32_t ap = p < sp ? len : 0;  // round-1 rows of probe p
                     const uint32_t lo = r ? ap : 0, hi = r ? len : ap;
                     const uint32_t nch = hi > lo ? (hi - lo + ch - 1) / ch : 0;
                     uint32_t incl = nch;

@@ -122,6 +122,10 @@ struct IvfWork {
     uint32_t cap[2];
     uint32_t chunk[2];
     uint32_t* overflow;
+    // the (query, probe) items of each round whose list is not empty here: the residual
+    // LUTs K1r builds (by-list sharding leaves most lists of a rank empty)
+    uint32_t* lut_items[2];
+    uint32_t* nlut;     // 2 counters (zeroed)
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -317,9 +321,9 @@ void launch_coarse_tc(const float* q, uint32_t nq, uint32_t dim, const float* pa
 void launch_coarse_rank(const float* q, uint32_t nq, uint32_t dim, const float4* grp, uint32_t nlist, float cmax,
                         const float* cent, uint32_t np, uint32_t* scratch, unsigned long long* probe_keys,
                         uint32_t* probe_counts, cudaStream_t s);
-// K1r over the probes [p_lo, p_hi) of every query (items q * nprobe + p)
-void launch_residual_lut(const float* queries, uint32_t nq, uint32_t dim, uint32_t m,
-                         const unsigned long long* probe_keys, uint32_t nprobe, uint32_t p_lo, uint32_t p_hi,
+// K1r over a list of items (q * nprobe + p; count on the device, at most max_items)
+void launch_residual_lut(const float* queries, uint32_t dim, uint32_t m, const unsigned long long* probe_keys,
+                         uint32_t nprobe, const uint32_t* items, const uint32_t* nitems, uint32_t max_items,
                          const float* cent, const float* codebooks, const uint16_t* perms, float* lutp,
                          uint8_t* qcodes, cudaStream_t s);
 void launch_ivf_probe_count(const unsigned long long* probe_keys, uint32_t nq, uint32_t nprobe, const uint64_t* off,

@@ -23,6 +23,35 @@ def shard_range(n_total: int, world: int, rank: int):
     return begin, min(begin + per, n_total)
 
 
+def assign_lists(list_sizes, world: int):
+    """By-list sharding of an IVF index ("sharding by list"): the owner
+    rank of every cell, cells placed largest first on the least loaded rank (ties to the
+    lower rank), so each rank holds about 1/world of the codes.  Deterministic, so every
+    rank computes the same table from the same list sizes."""
+    import heapq
+
+    import numpy as np
+    sizes = np.asarray(list_sizes, np.int64)
+    owner = np.empty(len(sizes), np.int32)
+    heap = [(0, r) for r in range(world)]
+    for c in np.argsort(-sizes, kind="stable"):
+        load, r = heapq.heappop(heap)
+        owner[c] = r
+        heapq.heappush(heap, (load + int(sizes[c]), r))
+    return owner
+
+
+def by_list_balance(list_sizes, probe_cells, owner, world: int):
+    """Per-rank codes scanned for a query batch under by-list sharding (probe_cells: nq x
+    nprobe cells): (max / mean) -- the imbalance factor of the scan -- and the per-rank
+    totals."""
+    import numpy as np
+    sizes = np.asarray(list_sizes, np.int64)
+    cells = np.asarray(probe_cells, np.int64).ravel()
+    per = np.bincount(np.asarray(owner)[cells], weights=sizes[cells], minlength=world)
+    return float(per.max() / max(per.mean(), 1e-30)), per
+
+
 class FlatIndexEngine:
     """GPU engine over one rank's FlatIndex shard.  Every call is enqueued on torch's
     current stream, the stream the all-gathers and the caching allocator use too, so
@@ -66,12 +95,14 @@ def gather_query_slices(compute, queries, group=None):
 
 
 class IVFIndexEngine(FlatIndexEngine):
-    """GPU engine over one rank's IVF shard: every cell's list restricted to the rank's
-    id range (shard by id within every list), so all ranks probe the
-    same cells and the key merge is exact.  With ``split_coarse`` the coarse
-    quantization (TF32 GEMM + exact re-rank) is split by query: each rank enumerates
-    the probes of its query slice and the probe keys are all-gathered, instead of
-    every rank enumerating every query."""
+    """GPU engine over one rank's IVF shard.  Two shardings, the same
+    engine code: by id (every cell's list restricted to the rank's id range) or by list
+    (the rank holds whole lists, ``assign_lists``; the other cells' lists are empty here,
+    so the rank builds residual LUTs and scans only for the probes that hit its own
+    lists).  All ranks see the same probes and the key merge is exact either way.  With
+    ``split_coarse`` the coarse quantization (tensor-core dots + exact re-rank) is split
+    by query: each rank enumerates the probes of its query slice and the probe keys are
+    all-gathered, instead of every rank enumerating every query."""
 
     def __init__(self, index, stats=None, split_coarse=False, group=None):
         super().__init__(index)

@@ -156,6 +156,47 @@ def test_sharded_ivf_equals_unsharded(tmp_path):
     assert np.array_equal(r["counts"], oc.astype(np.int32))
 
 
+def _ivf_bylist_worker(rank, world, port, result_path):
+    import sys
+    sys.path.insert(0, ROOT)
+    import oracle
+    from paper_1609_01882_b200.distributed import ShardedSearch, assign_lists
+
+    class P:
+        k, tau = 40, 26
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    g, pq, base = _ivf_data()
+    cells = oracle.ivf_assign(base, g["coarse"], threads=2)
+    owner = assign_lists(np.bincount(cells, minlength=len(g["coarse"])), world)
+    rows = np.nonzero(owner[cells] == rank)[0]
+    lists, _ = oracle.ivf_build(pq, base[rows], g["coarse"], ids=rows.astype(np.int64), assign=cells[rows])
+    eng = OracleIVFEngine(pq, g["coarse"], lists, nprobe=8)
+    ids, scores, counts = ShardedSearch(eng, device="cpu").search_batch(torch.from_numpy(g["queries"]), P())
+    if rank == 0:
+        np.savez(result_path, ids=ids.numpy(), scores=scores.numpy(), counts=counts.numpy(), owner=owner)
+    dist.destroy_process_group()
+
+
+def test_sharded_ivf_by_list_equals_unsharded(tmp_path):
+    """SURVEY.md sec. 8e by-list sharding on CPU: each rank holds whole lists (assign_lists,
+    balanced by size), the same probes on every rank, keys all-gathered over gloo and
+    merged == the unsharded IVF oracle."""
+    import oracle
+    from paper_1609_01882_b200.distributed import assign_lists
+    assert assign_lists([5, 1, 4, 4], 2).tolist() == [0, 0, 1, 1]  # LPT: 5 -> r0, 4 -> r1, 4 -> r1 (4 < 5), 1 -> r0
+    out = str(tmp_path / "ivfl0.npz")
+    mp.spawn(_ivf_bylist_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    r = np.load(out)
+    assert set(np.unique(r["owner"])) == {0, 1}
+    g, pq, base = _ivf_data()
+    lists, _ = oracle.ivf_build(pq, base, g["coarse"])
+    oi, osc, oc, _, _, _ = oracle.ivf_search(pq, g["coarse"], lists, g["queries"], 40, 8, tau=26)
+    assert np.array_equal(r["ids"], oi)
+    assert np.array_equal(r["scores"].view(np.uint32), osc.view(np.uint32))
+    assert np.array_equal(r["counts"], oc.astype(np.int32))
+
+
 def _gather_worker(rank, world, port, result_path):
     import torch
     import torch.distributed as dist

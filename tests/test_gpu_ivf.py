@@ -226,6 +226,61 @@ def test_probe_order_many_near_ties(pb, gi, dim, nlist):
         assert np.array_equal(ix.probes(queries, nprobe), want), nprobe
 
 
+def test_by_list_sharding_matches_unsharded(pb, gi):
+    """By-list sharding: 4 shards each holding whole lists (assign_lists
+    by size), the same all-gathered probes, per-shard keys merged == the unsharded search;
+    every shard only scans (and builds LUTs for) its own lists: scanned totals add up."""
+    import torch
+    from paper_1609_01882_b200.distributed import assign_lists, by_list_balance
+    seed = int(gi["data_seed"])
+    centers = oracle.gen_centers(seed, 1000, 128)
+    rng = np.random.default_rng(12)
+    coarse = oracle.gen_points(seed, 1, 0, 20000, centers)[rng.choice(20000, 256, replace=False)]
+    n = 150_000
+    base = oracle.gen_points(seed, 2, 0, n, centers)
+    queries = oracle.gen_points(seed, 3, 0, 300, centers)
+    mk = lambda: pb.IVFIndex(pb.ProductQuantizer(8, 8, 128, gi["codebooks"], gi["perms"]), coarse)  # noqa: E731
+    full = mk()
+    full.add(base)
+    cells = full.assign(base)
+    sizes = np.bincount(cells, minlength=256)
+    owner = assign_lists(sizes, 4)
+    loads = np.bincount(owner, weights=sizes, minlength=4)
+    assert loads.max() - loads.min() <= sizes.max()  # LPT: within one list of each other
+    shards = []
+    for r in range(4):
+        rows = np.nonzero(owner[cells] == r)[0]
+        ix = mk()
+        ix.add(base[rows], cells=cells[rows], ids=rows)
+        shards.append(ix)
+    k = 100
+    dq = torch.from_numpy(queries).cuda()
+    for nprobe, tau in ((8, 26), (32, 24), (32, 64)):
+        p = pb.CoarseParams(pb.Strategy.dual, k, tau, nprobe, 0)
+        want_ids, want_sc, want_cnt = full.search(queries, p)
+        probes = torch.empty((300, nprobe), dtype=torch.int64, device="cuda")
+        full.probe_keys_device(dq, nprobe, probes)
+        keys = torch.empty((4, 300, k), dtype=torch.int64, device="cuda")
+        cnts = torch.empty((4, 300), dtype=torch.int32, device="cuda")
+        st = pb.SearchStats()
+        for r, ix in enumerate(shards):
+            ix.search_keys_device(dq, p, keys[r], cnts[r], stats=st, probes=probes)
+        ids = torch.empty((300, k), dtype=torch.int64, device="cuda")
+        sc = torch.empty((300, k), dtype=torch.float32, device="cuda")
+        cnt = torch.empty(300, dtype=torch.int32, device="cuda")
+        shards[0].merge_keys_device(keys, cnts, 4, 300, k, ids, sc, cnt)
+        torch.cuda.synchronize()
+        assert np.array_equal(ids.cpu().numpy(), want_ids), (nprobe, tau)
+        assert np.array_equal(_bits(sc.cpu().numpy()), _bits(want_sc))
+        assert np.array_equal(cnt.cpu().numpy(), want_cnt)
+        st_full = pb.SearchStats()
+        full.search(queries, p, st_full)
+        assert st.scanned == st_full.scanned and st.survivors == st_full.survivors
+        pc = (probes.cpu().numpy() & 0xFFFFFFFF).astype(np.int64)
+        imb, per = by_list_balance(sizes, pc, owner, 4)
+        assert per.sum() == st_full.scanned and imb >= 1.0
+
+
 def test_sharded_ivf_merge_matches_unsharded(pb, gi):
     """SURVEY.md sec. 8e for IVF: 4 shards (every cell's list restricted to an id range),
     per-shard top-k keys, exact K3 merge == the unsharded search == the oracle; the

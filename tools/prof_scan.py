@@ -12,10 +12,12 @@ ap.add_argument('--n', type=int, default=20_000_000)
 ap.add_argument('--ht', type=int, default=32)
 ap.add_argument('--nq', type=int, default=256)
 ap.add_argument('--reps', type=int, default=1)
+ap.add_argument('--m', type=int, default=8)
 args = ap.parse_args()
-z = np.load('tests/golden/pq_d128_m8.npz')
-pq = pb.ProductQuantizer(8, 8, 128, z['codebooks'], z['perms'])
-centers = synth.gen_centers(160901882, 1000, 128)
+dim = 16 * args.m
+z = np.load('tests/golden/pq_d128_m8.npz' if args.m == 8 else 'tests/golden/pq_d256_m16.npz')
+pq = pb.ProductQuantizer(args.m, 8, dim, z['codebooks'], z['perms'])
+centers = synth.gen_centers(160901882, 1000 if args.m == 8 else 4096, dim)
 ix = pb.FlatIndex(pq); ix.add_synthetic(160901882, centers, 0, args.n)
 q = synth.gen_points(160901882, 3, 0, args.nq, centers)
 p = pb.SearchParams(pb.Strategy.dual, 100, args.ht)
