@@ -357,11 +357,20 @@ def test_sharded_ivf_merge_matches_unsharded(pb, gi):
         ix.search_keys_device(dq, p, k_in, c_in, probes=pr)
         torch.cuda.synchronize()
         assert torch.equal(k_in, keys[r]) and torch.equal(c_in, cnts[r]), r
-    # non-consecutive ids cannot be carried in a key
+    # ids outside [0, 2^32) need a rank table, whose ranks are shard-local: rejected
     odd = mk()
-    odd.add(base[:1000], ids=np.arange(1000) * 3)
-    with pytest.raises(pb.PolyError):
+    odd.add(base[:1000], ids=np.arange(1000) * 3 + 2**33)
+    with pytest.raises(pb.PolyError) as e:
         odd.search_keys_device(dq, pb.CoarseParams(pb.Strategy.dual, k, 26, 8, 0), keys[0], cnts[0])
+    assert e.value.code == pb.Errc.state
+    # scattered ids below 2^32 ride in the key (by-list shards hold such ids)
+    sc3 = mk()
+    sc3.add(base[:1000], ids=np.arange(1000) * 3)
+    sc3.search_keys_device(dq, pb.CoarseParams(pb.Strategy.dual, k, 26, 8, 0), keys[0], cnts[0])
+    torch.cuda.synchronize()
+    got = keys[0].cpu().numpy()
+    ok = got != -1
+    assert ok.any() and (((got[ok] & 0xFFFFFFFF) % 3) == 0).all()
 
 
 def test_full_config2_size(pb):
