@@ -90,6 +90,8 @@ def parse():
     ap.add_argument("--coarse", default="sample", choices=["sample", "kmeans"],
                     help="IVF coarse quantizer: training-stream rows (default) or GPU k-means (poly_b200_kmeans, "
                          "k-means++ + 10 Lloyd iterations on 16 x nlist training rows)")
+    ap.add_argument("--ivf-shard", default="id", choices=["id", "list"],
+                    help="multi-GPU IVF (config 2): shard ids within every list, or whole lists (assign_lists)")
     ap.add_argument("--knn-full", default=None, metavar="PATH",
                     help="config 4: also build this rank's whole k-NN graph into PATH (graph file sink, timed)")
     args = ap.parse_args()
@@ -296,7 +298,8 @@ def run_reference(args, rank):
               f"{threads} threads")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u8/f32", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "u8/f32",
+            "data": "synthetic (seeded Gaussian mixture; N(0,1) as Irwin-Hall(12) over splitmix64, DESIGN.md sec. 3)",
             "config": flat_config(args, 1, n_scanned=nsamp), "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample,
                              "cpu": cpu_info(),
@@ -535,7 +538,7 @@ def run_flat(args, rank, world, local):
                     "note": "the non-binding HBM term: each code is read once per 256-query launch"}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "u8/f32", "data": f"synthetic (seeded Gaussian mixture, BASELINE cfg{args.config})",
+            "vs_baseline": None, "dtype": "u8/f32", "data": f"synthetic (seeded Gaussian mixture, BASELINE cfg{args.config}; N(0,1) as Irwin-Hall(12) over splitmix64, DESIGN.md sec. 3)",
             "config": flat_config(args, world), "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             "roofline": roofline, "roofline_hbm": roofline_hbm, "per_ht": per_ht, "setup_s": round(setup_s, 2)}
     if world == 1 and not args.no_cpu_baseline:
@@ -546,6 +549,45 @@ def run_flat(args, rank, world, local):
 
 
 # ------------------------------------------------------------------ IVF (configs 2 and 4)
+def build_ivf_by_list(args, pb, torch, local, rank, world, coarse, centers, norm):
+    """By-list shard of rank: every rank assigns all rows (pass 1: list sizes -> the same
+    assign_lists table everywhere), then keeps the rows of the cells it owns (pass 2),
+    with their global ids."""
+    from paper_1609_01882_b200.distributed import assign_lists
+    c = args.c
+    z = np.load(os.path.join(ROOT, "tests", "golden", c["pq"]))
+    pq = pb.ProductQuantizer(c["m"], 8, c["dim"], z["codebooks"], z["perms"])
+    ivf = pb.IVFIndex(pq, coarse, device=local)
+    torch.backends.cuda.matmul.allow_tf32 = True
+    dc = torch.from_numpy(coarse).cuda()
+    cn = (dc * dc).sum(1)
+    chunk = 1 << 21
+    xbuf = torch.empty((chunk, c["dim"]), dtype=torch.float32, device="cuda")
+    cells = torch.empty(chunk, dtype=torch.int32, device="cuda")
+
+    def chunks():
+        for r in range(0, args.n, chunk):
+            nb = min(chunk, args.n - r)
+            x = xbuf[:nb]
+            pb.gen_points_device(centers, SEED, 2, r, nb, x, device=local, normalize=norm)
+            for b in range(0, nb, 16384):
+                xs = x[b:b + 16384]
+                cells[b:b + xs.shape[0]] = torch.argmin(torch.addmm(cn, xs, dc.T, alpha=-2.0), dim=1).to(torch.int32)
+            yield r, x, cells[:nb]
+
+    hist = torch.zeros(c["nlist"], dtype=torch.int64, device="cuda")
+    for _, _, cl in chunks():
+        hist += torch.bincount(cl.to(torch.int64), minlength=c["nlist"])
+    owner = torch.from_numpy(assign_lists(hist.cpu().numpy(), world).astype(np.int64)).cuda()
+    for r, x, cl in chunks():
+        keep = torch.nonzero(owner[cl.to(torch.int64)] == rank).squeeze(1)
+        if keep.numel():
+            ivf.add_device_ids(x[keep].contiguous(), cl[keep].contiguous(), (keep.cpu().numpy() + r).astype(np.int64))
+    ivf.list_offsets()
+    torch.cuda.synchronize()
+    return ivf, pq
+
+
 def build_ivf(args, pb, torch, local, row0, row1, coarse, centers, norm):
     """GPU build of this rank's rows: generator, nearest-cell assignment (TF32 GEMM argmin
     through torch -- setup, not the measured path), exact residual encoding (C ABI)."""
@@ -662,7 +704,10 @@ def run_ivf(args, rank, world, local):
     coarse = make_coarse(args, pb, synth, centers, False)
     row0, row1 = shard_range(args.n, world, rank)
     t = time.time()
-    ivf, pq = build_ivf(args, pb, torch, local, row0, row1, coarse, centers, False)
+    if args.ivf_shard == "list":
+        ivf, pq = build_ivf_by_list(args, pb, torch, local, rank, world, coarse, centers, False)
+    else:
+        ivf, pq = build_ivf(args, pb, torch, local, row0, row1, coarse, centers, False)
     setup_s = time.time() - t
     nq, B, k, M = c["nq"], args.batch, args.k, c["m"]
     ivf.set_batch(B)  # one internal batch per step: the cell-major scan groups the step's queries per list
@@ -761,6 +806,17 @@ def run_ivf(args, rank, world, local):
     pk, _ = peaks()
     rt = rates()
     f = _clk(clk, pk)
+    # by-list sharding at 8 ranks: per-rank share of the codes a step's
+    # probes scan, cells placed by assign_lists on this index's list sizes (rank 0's shard)
+    from paper_1609_01882_b200.distributed import assign_lists, by_list_balance
+    sizes = np.diff(ivf.list_offsets().astype(np.int64))
+    owner8 = assign_lists(sizes, 8)
+    cells = ivf.probes(dq[:B].cpu().numpy(), args.nprobe).astype(np.int64)
+    imb, per8 = by_list_balance(sizes, cells, owner8, 8)
+    by_list = {"ranks": 8, "scan_imbalance_max_over_mean": round(imb, 4),
+               "list_codes_imbalance": round(float(np.bincount(owner8, weights=sizes, minlength=8).max() /
+                                                   max(sizes.sum() / 8, 1)), 4),
+               "note": "codes the step's probes scan per rank under assign_lists (LPT by list size), max / mean"}
     for nprobe, r in results.items():
         sc_l, sv_l, k6_l, ms_l = r.pop("_local")
         k6, stp, hbm = ivf_rooflines(args, pk, rt, f, M, sc_l, sv_l, B, nprobe, ms_l, k6_l, world)
@@ -769,12 +825,12 @@ def run_ivf(args, rank, world, local):
     head = results[args.nprobe]
     line = {"metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": world, "steps": head["steps"],
             "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "u8/f32", "data": "synthetic (seeded Gaussian mixture, BASELINE cfg2)",
+            "vs_baseline": None, "dtype": "u8/f32", "data": "synthetic (seeded Gaussian mixture, BASELINE cfg2; N(0,1) as Irwin-Hall(12) over splitmix64, DESIGN.md sec. 3)",
             "config": {"workload": f"cfg2 IVF+polysemous: nlist={c['nlist']}, N={args.n} codes over {world} GPU(s), "
                                    f"PQ m={M} on residuals, nq={nq} in batches of {B}, nprobe={args.nprobe}, k={k}, "
                                    f"ht={args.ht}",
                        "nlist": c["nlist"], "n_codes": args.n, "m": M, "nprobe": args.nprobe, "k": k, "ht": args.ht,
-                       "batch": B, "parallelism": f"db-shard{world} (ids within every list) + query-split coarse "
+                       "batch": B, "parallelism": f"db-shard{world} ({'whole lists per rank (assign_lists)' if args.ivf_shard == 'list' else 'ids within every list'}) + query-split coarse "
                                                   "quantization + NCCL probe / key all-gathers",
                        "coarse": getattr(args, "coarse_info", "training-stream rows [0, nlist) (sampled coarse quantizer; DESIGN.md)"),
                        "build_assignment": "TF32 GEMM argmin (setup only)",
@@ -783,6 +839,7 @@ def run_ivf(args, rank, world, local):
             "roofline": dict(head["roofline"], kernel="K6 ivf_scan_kernel (both rounds)",
                              kernel_share_of_step=head["k6_share_of_step"]),
             "roofline_step": head["roofline_step"], "roofline_hbm": head["roofline_hbm"],
+            "by_list_sharding_8": by_list,
             "per_nprobe": {str(kk): {x: v for x, v in r.items() if x not in ("roofline_step", "roofline_hbm")}
                            for kk, r in results.items()},
             "setup_s": round(setup_s, 1)}
@@ -881,7 +938,7 @@ def run_knn(args, rank, world, local):
     rows = row1 - row0
     line = {"metric": METRIC, "value": scanned / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": steps,
             "warmup": args.warmup, "ms_per_step": ms / steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u8/f32", "data": "synthetic (unit-normalised mixture, BASELINE cfg4)",
+            "vs_baseline": None, "dtype": "u8/f32", "data": "synthetic (unit-normalised mixture, BASELINE cfg4; N(0,1) as Irwin-Hall(12) over splitmix64, DESIGN.md sec. 3)",
             "config": {"workload": f"cfg4 k-NN graph: N={args.n} d={c['dim']} unit-normalised, IVF {c['nlist']} + PQ "
                                    f"m={M}, every vector queries the rest, nprobe={args.nprobe}, ht={args.ht}, k={k}",
                        "n_codes": args.n, "nlist": c["nlist"], "m": M, "nprobe": args.nprobe, "k": k,

@@ -210,6 +210,9 @@ int poly_b200_ivf_add(poly_b200_ivf* ivf, const float* x, uint64_t n, const uint
  * id0 .. id0 + n - 1; used by the benchmark's chunked builder. */
 int poly_b200_ivf_add_device(poly_b200_ivf* ivf, const float* d_x, const uint32_t* d_cells, uint64_t n, int64_t id0,
                              void* stream);
+/* Same with explicit host ids (n int64), e.g. a by-list shard's scattered rows. */
+int poly_b200_ivf_add_device_ids(poly_b200_ivf* ivf, const float* d_x, const uint32_t* d_cells, uint64_t n,
+                                 const int64_t* ids, void* stream);
 
 /* Append pre-encoded residual codes with their cells and ids (serialization). */
 int poly_b200_ivf_add_codes(poly_b200_ivf* ivf, const uint32_t* cells, const uint8_t* codes, const int64_t* ids,

@@ -662,6 +662,27 @@ int poly_b200_ivf_add_device(poly_b200_ivf* iv, const float* d_x, const uint32_t
     });
 }
 
+int poly_b200_ivf_add_device_ids(poly_b200_ivf* iv, const float* d_x, const uint32_t* d_cells, uint64_t n,
+                                 const int64_t* ids, void* stream) {
+    return guard([&] {
+        require(iv && (n == 0 || (d_x && d_cells && ids)), POLY_B200_INVALID_ARGUMENT, "null arguments");
+        std::lock_guard<std::mutex> lk(iv->mu);
+        DeviceGuard dg(iv->device);
+        if (n == 0) return;
+        cudaStream_t s = (cudaStream_t)stream;
+        CK(cudaStreamSynchronize(s));
+        grow_ins(iv, iv->n + n);
+        CK(cudaMemcpyAsync(iv->d_cells_ins + iv->n, d_cells, n * 4, cudaMemcpyDeviceToDevice, iv->stream));
+        pb::launch_residual_encode(d_x, n, iv->dim, iv->m, iv->d_coarse, d_cells, iv->d_codebooks, iv->d_perms,
+                                   iv->d_codes_ins + iv->n * iv->cb, iv->stream);
+        CK(cudaStreamSynchronize(iv->stream));
+        CK(cudaGetLastError());
+        iv->idm.append(ids, iv->n, n);
+        iv->n += n;
+        iv->lists_dirty = true;
+    });
+}
+
 int poly_b200_ivf_add(poly_b200_ivf* iv, const float* x, uint64_t n, const uint32_t* cells, const int64_t* ids) {
     return guard([&] {
         require(iv && (n == 0 || x), POLY_B200_INVALID_ARGUMENT, "null arguments");

@@ -257,7 +257,18 @@ void launch_coarse_tc(const float* q, uint32_t nq, uint32_t dim, const float* pa
     const uint32_t ntiles = coarse_tc_tiles(nlist), qtiles = (nq + CT_M - 1) / CT_M;
     uint32_t stages = 0;
     const size_t smem = coarse_tc_smem(dim, &stages);
-    const uint32_t slices = std::max<uint32_t>(1, std::min<uint32_t>(ntiles, (uint32_t)num_sms / qtiles));
+    // grid = slices x query tiles: pick the slice count (each slice >= 8 cell tiles) whose last
+    // wave is fullest -- with 79 query tiles (10,000 queries) one slice would leave 69 SMs idle
+    uint32_t slices = 1;
+    double best = 0.0;
+    for (uint32_t sl = 1; sl <= std::max<uint32_t>(1, std::min<uint32_t>(ntiles / 8, 32)); ++sl) {
+        const uint64_t ctas = (uint64_t)sl * qtiles, waves = (ctas + num_sms - 1) / num_sms;
+        const double eff = (double)ctas / (double)(waves * (uint64_t)num_sms) - 0.002 * sl;  // mild bias to fewer
+        if (eff > best + 1e-9) {
+            best = eff;
+            slices = sl;
+        }
+    }
     set_max_smem((const void*)coarse_tc_kernel, smem);
     coarse_tc_kernel<<<dim3(slices, qtiles), CT_THREADS, smem, s>>>(q, nq, dim, packed, cnorm_pad, ntiles, stages,
                                                                    grp);

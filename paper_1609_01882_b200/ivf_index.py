@@ -88,6 +88,12 @@ class IVFIndex:
         _check(lib.poly_b200_ivf_add_device(self._h, d_x.data_ptr(), d_cells.data_ptr(), d_x.shape[0], int(id0),
                                             C.c_void_p(stream)))
 
+    def add_device_ids(self, d_x, d_cells, ids, stream=0):
+        """add_device with explicit (host, int64) ids."""
+        ids = np.ascontiguousarray(ids, np.int64)
+        _check(lib.poly_b200_ivf_add_device_ids(self._h, d_x.data_ptr(), d_cells.data_ptr(), d_x.shape[0], _p(ids),
+                                                C.c_void_p(stream)))
+
     def add_codes(self, cells, codes, ids=None):
         cells = np.ascontiguousarray(cells, np.uint32)
         codes = np.ascontiguousarray(codes, np.uint8)
