@@ -276,6 +276,21 @@ int poly_b200_ivf_search_keys_probes_device(poly_b200_ivf* ivf, const float* d_q
                                             uint64_t* d_keys, uint32_t* d_counts, void* stream,
                                             poly_b200_search_stats* stats);
 
+/* Two-phase shard search for by-list sharding, one batch (nq <= the
+ * batch size), probes given (all-gathered):
+ *   phase 1: round 1 over each query's FIRST probe only -- empty on every rank but the one
+ *            owning that cell -- writes the local bound (k-th key + 1; all ones = none)
+ *            to d_thr (nq uint64);
+ *   (caller: d_thr <- min over the ranks; any rank's k-th key bounds the global k-th)
+ *   phase 2: round 2 over the other probes under min(local bound, d_thr), then this
+ *            shard's top-k keys as poly_b200_ivf_search_keys_probes_device writes them.
+ * The merged result equals the unsharded search (the bound only prunes keys that cannot
+ * be in the global top-k). */
+int poly_b200_ivf_search_keys_phase_device(poly_b200_ivf* ivf, const float* d_queries, uint64_t nq,
+                                           const poly_b200_ivf_params* params, const uint64_t* d_probe_keys, int phase,
+                                           uint64_t* d_thr, uint64_t* d_keys, uint32_t* d_counts, void* stream,
+                                           poly_b200_search_stats* stats);
+
 /* The lists of selected cells only, CSR in the order of `cells`: off (ncells + 1),
  * codes (off[ncells] x code_bytes), ids; codes / ids may be NULL. */
 int poly_b200_ivf_get_cells(poly_b200_ivf* ivf, const uint32_t* cells, uint32_t ncells, uint64_t* off, uint8_t* codes,

@@ -99,6 +99,8 @@ def _load():
     L.poly_b200_ivf_add.argtypes = [_P, _P, _u64, _P, _P]
     L.poly_b200_ivf_add_device.argtypes = [_P, _P, _P, _u64, C.c_int64, _P]
     L.poly_b200_ivf_add_device_ids.argtypes = [_P, _P, _P, _u64, _P, _P]
+    L.poly_b200_ivf_search_keys_phase_device.argtypes = [_P, _P, _u64, C.POINTER(IvfParamsC), _P, _i32, _P, _P, _P,
+                                                         _P, C.POINTER(SearchStatsC)]
     L.poly_b200_ivf_add_codes.argtypes = [_P, _P, _P, _P, _u64]
     L.poly_b200_ivf_get_lists.argtypes = [_P, _P, _P, _P]
     L.poly_b200_ivf_probes.argtypes = [_P, _P, _u64, _u32, _P]
@@ -131,6 +133,7 @@ EXPORTS = [
     "poly_b200_sharded_shard_size", "poly_b200_sharded_add", "poly_b200_sharded_add_codes",
     "poly_b200_sharded_search_batch", "poly_b200_knn_writer_open", "poly_b200_ivf_knn_graph_write_device",
     "poly_b200_knn_writer_close", "poly_b200_kmeans", "poly_b200_ivf_add_device_ids",
+    "poly_b200_ivf_search_keys_phase_device",
     "poly_b200_calibrate_threshold", "poly_b200_with_assignments", "poly_b200_get_codes",
     "poly_b200_search_keys_device", "poly_b200_merge_keys_device", "poly_b200_add_synthetic",
     "poly_b200_gen_points_device", "poly_b200_debug_lut", "poly_b200_debug_counts", "poly_b200_profile_enable", "poly_b200_profile_read",

@@ -84,6 +84,8 @@ struct poly_b200_ivf {
     uint32_t* h_overflow = nullptr;          // pinned copy, checked at the next call
     cudaEvent_t done_ev = nullptr;
     bool pending_check = false;
+    bool phase_pending = false, phase_empty = false;  // two-phase search state (phase 1 done)
+    uint64_t phase_nq = 0;
     float* d_q = nullptr;
     uint64_t d_q_cap = 0;
     int64_t* d_oid = nullptr;
@@ -318,26 +320,37 @@ void enumerate_cells(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, uint32_t
 }
 
 // One batch of <= 256 queries; outputs through keys_to_ids.
+__global__ void min_u64(unsigned long long* dst, const unsigned long long* src, uint32_t n) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        dst[i] = src[i] < dst[i] ? src[i] : dst[i];
+}
+
+// phase 0: the whole search.  Two-phase form (by-list sharding):
+// phase 1 = round 1 over each query's FIRST probe only (empty here unless this rank owns
+// it), its k-th key + 1 out as d_thr; the caller min-reduces the bounds over the ranks;
+// phase 2 = round 2 (every other probe) under min(local, d_thr), then the final top-k.
 void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_b200_ivf_params* p, int64_t* d_ids,
                   float* d_scores, uint32_t* d_counts, cudaStream_t s, uint64_t* d_keys_out = nullptr,
                   uint32_t* d_kcounts_out = nullptr, const uint64_t* d_probes_in = nullptr, uint64_t* d_surv = nullptr,
-                  uint64_t* d_hash = nullptr) {
+                  uint64_t* d_hash = nullptr, int phase = 0, uint64_t* d_thr = nullptr) {
     const uint32_t k = p->k;
     const uint32_t np = std::min(p->nprobe, iv->nlist);
     int strategy = p->strategy;
     if (strategy == pb::DUAL && p->tau >= iv->code_bits()) strategy = pb::ADC;  // SPEC.md:388 boundary
-    CK(cudaMemsetAsync(iv->ctrl, 0, (iv->nqb + 32) * 4, s));
-    CK(cudaMemsetAsync(iv->ovq, 0, iv->nqb * 4, s));
-    CK(cudaMemsetAsync(iv->thr, 0xFF, iv->nqb * 8, s));
     const bool perq = d_surv || d_hash;
-    if (perq) {
-        CK(cudaMemsetAsync(iv->surv_q, 0, iv->nqb * 8, s));
-        CK(cudaMemsetAsync(iv->hash_q, 0, iv->nqb * 8, s));
+    if (phase != 2) {
+        CK(cudaMemsetAsync(iv->ctrl, 0, (iv->nqb + 32) * 4, s));
+        CK(cudaMemsetAsync(iv->ovq, 0, iv->nqb * 4, s));
+        CK(cudaMemsetAsync(iv->thr, 0xFF, iv->nqb * 8, s));
+        if (perq) {
+            CK(cudaMemsetAsync(iv->surv_q, 0, iv->nqb * 8, s));
+            CK(cudaMemsetAsync(iv->hash_q, 0, iv->nqb * 8, s));
+        }
+        if (d_probes_in)  // probes computed elsewhere (the coarse quantization split by query over ranks)
+            CK(cudaMemcpyAsync(iv->probe_keys, d_probes_in, (size_t)nqb * np * 8, cudaMemcpyDeviceToDevice, s));
+        else
+            enumerate_cells(iv, d_q, nqb, np, s);
     }
-    if (d_probes_in)  // probes computed elsewhere (the coarse quantization split by query over ranks)
-        CK(cudaMemcpyAsync(iv->probe_keys, d_probes_in, (size_t)nqb * np * 8, cudaMemcpyDeviceToDevice, s));
-    else
-        enumerate_cells(iv, d_q, nqb, np, s);
     pb::IvfWork w{};
     w.items[0] = iv->items[0];
     w.items[1] = iv->items[1];
@@ -350,15 +363,17 @@ void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_
     w.lut_items[0] = iv->lut_items;
     w.lut_items[1] = iv->lut_items + (size_t)iv->nqb * np;
     w.nlut = iv->ctrl + iv->nqb + 5;
+    const bool side = np > 1;
+    if (phase != 2) {
+    // two-phase: round 1 = the first probe exactly (>= 0 codes or 1 list reached at probe 0)
     pb::launch_ivf_probe_count(iv->probe_keys, nqb, np, iv->d_off, p->cap, iv->np_eff, iv->scanned, s, iv->split,
-                               IVF_R1_CODES, IVF_R1_MAX, w);
+                               phase == 1 ? 0 : IVF_R1_CODES, phase == 1 ? 1 : IVF_R1_MAX, w);
     add_u64<<<1, 256, 0, s>>>(iv->scanned, nqb, iv->scan_total);
     pb::count_launch();
     // residual LUTs of the items with a non-empty list here: round 1's on the caller's
     // stream; round 2's on the side stream, overlapping round 1, its top-k and the
     // compaction (K1r is FP / shared-memory bound, round 1 memory / latency bound); round 2
     // waits for them
-    const bool side = np > 1;
     if (side) {
         CK(cudaEventRecord(iv->ev_fork, s));
         CK(cudaStreamWaitEvent(iv->side, iv->ev_fork, 0));
@@ -368,6 +383,7 @@ void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_
     }
     pb::launch_residual_lut(d_q, iv->dim, iv->m, iv->probe_keys, np, w.lut_items[0], w.nlut, nqb * np, iv->d_coarse,
                             iv->d_codebooks, iv->d_perms, iv->lutp, iv->qcodes, s);
+    }
     pb::IvfScanArgs a{};
     a.codes = iv->d_codes_list;
     a.low = iv->d_low_list;
@@ -392,6 +408,12 @@ void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_
     // 1024-row chunks; its exact k-th key (K3) bounds round 2, the remaining probes
     const uint32_t rounds = np <= 1 ? 1 : 2;  // one probe: round 1 sees everything
     for (uint32_t round = 0; round < rounds; ++round) {
+        if (phase == 1 && round == 1) break;
+        if (phase == 2 && round == 0) continue;
+        if (phase == 2 && d_thr) {  // the bound min-reduced over the ranks
+            min_u64<<<(nqb + 255) / 256, 256, 0, s>>>(iv->thr, reinterpret_cast<const unsigned long long*>(d_thr), nqb);
+            pb::count_launch();
+        }
         a.items = iv->items[round];
         a.nitems = w.nitems + round;
         a.items_cap = w.cap[round];
@@ -416,6 +438,10 @@ void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_
         pb::launch_topk(iv->cand, iv->ctrl, iv->cand_cap, 1, 0, 0, nqb, k, iv->keys, iv->kcounts, s);
         if (round == 0 && np > 1)  // bound round 2; keep only round 1's top-k as candidates
             pb::launch_seed_compact(iv->keys, iv->kcounts, nqb, k, iv->thr, iv->cand, iv->cand_cap, iv->ctrl, s);
+    }
+    if (phase == 1) {  // the local round-1 bound (all-ones: no bound) for the min-reduce
+        CK(cudaMemcpyAsync(d_thr, iv->thr, (size_t)nqb * 8, cudaMemcpyDeviceToDevice, s));
+        return;
     }
     pb::launch_or_flag(iv->sticky_overflow, iv->ctrl + iv->nqb, s);
     if (perq) {
@@ -964,6 +990,70 @@ int poly_b200_ivf_search_keys_probes_device(poly_b200_ivf* iv, const float* d_q,
         if (stats) {
             stats->scanned = stats->survivors = 0;
             if (nq && iv->n) read_stats(iv, mode, stats, s);
+        }
+    });
+}
+
+int poly_b200_ivf_search_keys_phase_device(poly_b200_ivf* iv, const float* d_q, uint64_t nq,
+                                           const poly_b200_ivf_params* p, const uint64_t* d_probe_keys, int phase,
+                                           uint64_t* d_thr, uint64_t* d_keys, uint32_t* d_counts, void* stream,
+                                           poly_b200_search_stats* stats) {
+    return guard([&] {
+        require(iv != nullptr && p != nullptr, POLY_B200_INVALID_ARGUMENT, "null arguments");
+        require(phase == 1 || phase == 2, POLY_B200_INVALID_ARGUMENT, "phase must be 1 or 2");
+        require(p->k > 0, POLY_B200_INVALID_ARGUMENT, "k must be positive for key output");
+        require(p->cap == 0, POLY_B200_INVALID_ARGUMENT, "CoarseParams.cap > 0 is not supported with sharded lists");
+        require(nq == 0 || (d_q && d_probe_keys && d_thr), POLY_B200_INVALID_ARGUMENT, "null buffers");
+        require(phase == 1 || nq == 0 || (d_keys && d_counts), POLY_B200_INVALID_ARGUMENT, "null outputs");
+        std::lock_guard<std::mutex> lk(iv->mu);
+        DeviceGuard dg(iv->device);
+        validate(iv, p);
+        require(nq <= iv->nqb, POLY_B200_INVALID_ARGUMENT, "two-phase search takes one batch (nq <= the batch size)");
+        cudaStream_t s = (cudaStream_t)stream;
+        iv->idm.sync(iv->n);
+        require(iv->n == 0 || iv->idm.d_rank_to_id == nullptr, POLY_B200_STATE,
+                "key output needs ids in [0, 2^32) (the key carries the id itself)");
+        if (phase == 1) {
+            require(!iv->phase_pending, POLY_B200_STATE, "phase 1 called twice without phase 2");
+            check_pending(iv, false);
+            if (stats) stats->scanned = stats->survivors = 0;
+            iv->phase_pending = true;
+            iv->phase_nq = nq;
+            iv->phase_empty = nq == 0 || iv->n == 0;
+            if (iv->phase_empty) {
+                if (nq) CK(cudaMemsetAsync(d_thr, 0xFF, nq * 8, s));
+                return;
+            }
+            rebuild_lists(iv);
+            ensure_ivf_scratch(iv, std::min(p->nprobe, iv->nlist), p->k);
+            CK(cudaMemsetAsync(iv->surv_total, 0, 8, s));
+            CK(cudaMemsetAsync(iv->scan_total, 0, 8, s));
+            CK(cudaMemsetAsync(iv->sticky_overflow, 0, 4, s));
+            search_batch(iv, d_q, (uint32_t)nq, p, nullptr, nullptr, nullptr, s, nullptr, nullptr, d_probe_keys, nullptr,
+                         nullptr, 1, d_thr);
+            CK(cudaGetLastError());
+            return;
+        }
+        require(iv->phase_pending && iv->phase_nq == nq, POLY_B200_STATE, "phase 2 without a matching phase 1");
+        iv->phase_pending = false;
+        if (iv->phase_empty) {
+            if (nq) {
+                CK(cudaMemsetAsync(d_counts, 0, nq * 4, s));
+                CK(cudaMemsetAsync(d_keys, 0xFF, nq * p->k * 8, s));
+            }
+            if (stats) stats->scanned = stats->survivors = 0;
+            return;
+        }
+        search_batch(iv, d_q, (uint32_t)nq, p, nullptr, nullptr, nullptr, s, d_keys, d_counts, d_probe_keys, nullptr,
+                     nullptr, 2, d_thr);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(iv->h_overflow, iv->sticky_overflow, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(iv->done_ev, s));
+        iv->pending_check = true;
+        if (stats) {
+            stats->scanned = stats->survivors = 0;
+            const int mode = p->strategy == pb::DUAL ? (p->tau >= iv->code_bits() ? 1 : 2) : 0;
+            read_stats(iv, mode, stats, s);
         }
     });
 }

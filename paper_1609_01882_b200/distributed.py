@@ -104,11 +104,12 @@ class IVFIndexEngine(FlatIndexEngine):
     by query: each rank enumerates the probes of its query slice and the probe keys are
     all-gathered, instead of every rank enumerating every query."""
 
-    def __init__(self, index, stats=None, split_coarse=False, group=None):
+    def __init__(self, index, stats=None, split_coarse=False, group=None, by_list=False):
         super().__init__(index)
         self.stats = stats
-        self.split_coarse = split_coarse
+        self.split_coarse = split_coarse or by_list
         self.group = group
+        self.by_list = by_list
 
     def probe_keys(self, queries, nprobe):
         npr = min(int(nprobe), self.index.nlist)
@@ -129,8 +130,24 @@ class IVFIndexEngine(FlatIndexEngine):
             from .flat_index import Errc, PolyError
             raise PolyError(Errc.invalid_argument, "CoarseParams.cap > 0 is not supported with sharded lists")
         probes = self.probe_keys(queries, params.nprobe) if self.split_coarse else None
-        self.index.search_keys_device(queries, params, keys, counts, stream=self._sptr(), stats=self.stats,
-                                      probes=probes)
+        if not self.by_list:
+            self.index.search_keys_device(queries, params, keys, counts, stream=self._sptr(), stats=self.stats,
+                                          probes=probes)
+            return
+        # by-list: round 1 on the owner of each query's first probe, the bounds min-reduced
+        # over the ranks, round 2 everywhere under the global bound (one batch per call)
+        B = self.index.batch
+        for b in range(0, queries.shape[0], B):
+            q, pr = queries[b:b + B], probes[b:b + B]
+            thr = torch.empty(q.shape[0], dtype=torch.int64, device=queries.device)
+            self.index.search_keys_phase_device(q, params, pr, 1, thr, stream=self._sptr())
+            if world > 1:
+                # keys are < 2^63; 'no bound' (all ones = -1 as int64) -> INT64_MAX for the MIN
+                thr = torch.where(thr == -1, torch.full_like(thr, 2**63 - 1), thr)
+                dist.all_reduce(thr, op=dist.ReduceOp.MIN, group=self.group)
+                thr = torch.where(thr == 2**63 - 1, torch.full_like(thr, -1), thr)
+            self.index.search_keys_phase_device(q, params, pr, 2, thr, keys[b:b + B], counts[b:b + B],
+                                                stream=self._sptr(), stats=self.stats)
 
 
 class ShardedSearch:

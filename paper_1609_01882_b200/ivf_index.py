@@ -203,6 +203,20 @@ class IVFIndex:
             stats.scanned += st.scanned
             stats.survivors += st.survivors
 
+    def search_keys_phase_device(self, d_queries, params: CoarseParams, probes, phase, d_thr, d_keys=None,
+                                 d_counts=None, stream=0, stats: SearchStats | None = None):
+        """By-list sharding's two-phase shard search (poly_b200_ivf_search_keys_phase_device):
+        phase 1 writes the local round-1 bound to d_thr (nq uint64 as int64); after the
+        caller's min-reduce, phase 2 reads it and writes this shard's top-k keys."""
+        st = SearchStatsC()
+        ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731
+        _check(lib.poly_b200_ivf_search_keys_phase_device(
+            self._h, d_queries.data_ptr(), d_queries.shape[0], C.byref(params.c()), probes.data_ptr(), int(phase),
+            d_thr.data_ptr(), ptr(d_keys), ptr(d_counts), C.c_void_p(stream), C.byref(st) if stats is not None else None))
+        if stats is not None:
+            stats.scanned += st.scanned
+            stats.survivors += st.survivors
+
     def probe_keys_device(self, d_queries, nprobe, d_out, stream=0):
         """enumerate_cells on the GPU: nq x min(nprobe, nlist) int64 keys (dist bits << 32 | cell)."""
         _check(lib.poly_b200_ivf_probe_keys_device(self._h, d_queries.data_ptr(), d_queries.shape[0], int(nprobe),

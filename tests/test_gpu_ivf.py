@@ -279,6 +279,33 @@ def test_by_list_sharding_matches_unsharded(pb, gi):
         pc = (probes.cpu().numpy() & 0xFFFFFFFF).astype(np.int64)
         imb, per = by_list_balance(sizes, pc, owner, 4)
         assert per.sum() == st_full.scanned and imb >= 1.0
+        # the two-phase protocol: round 1 on the owner of each first probe, bounds min-reduced,
+        # round 2 everywhere under the global bound -- same merged result, fewer candidates
+        thr = torch.empty((4, 300), dtype=torch.int64, device="cuda")
+        for r, ix in enumerate(shards):
+            ix.search_keys_phase_device(dq, p, probes, 1, thr[r])
+        none = torch.full_like(thr[0], 2**63 - 1)
+        g = torch.where(thr == -1, none, thr).min(0).values
+        g = torch.where(g == 2**63 - 1, torch.full_like(g, -1), g)
+        st2 = pb.SearchStats()
+        for r, ix in enumerate(shards):
+            ix.search_keys_phase_device(dq, p, probes, 2, g.clone(), keys[r], cnts[r], stats=st2)
+        shards[0].merge_keys_device(keys, cnts, 4, 300, k, ids, sc, cnt)
+        torch.cuda.synchronize()
+        assert np.array_equal(ids.cpu().numpy(), want_ids), ("2-phase", nprobe, tau)
+        assert np.array_equal(_bits(sc.cpu().numpy()), _bits(want_sc))
+        assert np.array_equal(cnt.cpu().numpy(), want_cnt)
+        assert st2.scanned == st_full.scanned
+    # the engine's by-list path at world size 1 (no process group: no reduce)
+    from paper_1609_01882_b200.distributed import IVFIndexEngine, ShardedSearch
+    p = pb.CoarseParams(pb.Strategy.dual, k, 26, 16, 0)
+    want_ids, want_sc, want_cnt = full.search(queries, p)
+    full.set_batch(128)  # several phase batches
+    ids, sc, cnt = ShardedSearch(IVFIndexEngine(full, by_list=True)).search_batch(dq, p)
+    torch.cuda.synchronize()
+    assert np.array_equal(ids.cpu().numpy(), want_ids) and np.array_equal(cnt.cpu().numpy(), want_cnt)
+    with pytest.raises(pb.PolyError):  # phase 2 without phase 1
+        shards[1].search_keys_phase_device(dq, p, probes[:, :16].contiguous(), 2, g.clone(), keys[1], cnts[1])
 
 
 def test_sharded_ivf_merge_matches_unsharded(pb, gi):
