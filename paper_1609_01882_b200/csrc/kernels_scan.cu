@@ -40,9 +40,6 @@ namespace pb {
 #ifndef POLY_TC  // 1: DUAL's Hamming filter on the tensor cores (int8 tcgen05.mma); 0: POPC
 #define POLY_TC 1
 #endif
-#ifndef POLY_TC_DBIAS  // 1: bias preloaded into the accumulators (two MMAs per 128 codes, not three)
-#define POLY_TC_DBIAS 1
-#endif
 #ifndef POLY_TC16  // 1: the tensor-core filter also for m = 16
 #define POLY_TC16 0
 #endif
@@ -104,10 +101,6 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
     constexpr int QC = 2 * AC + 32;  // columns per quad: A0, A1, D0, D1
     static_assert(!TCF || (W % 4 == 0 && 16 + (W / 4) * QC <= 512), "TMEM budget");
     __shared__ __align__(256) int8_t bw_s[TCF ? 16 * KB : 16];
-    // POLY_TC_DBIAS: the bias 64 (|q| - tau) - 32 is preloaded into the accumulator (one
-    // tcgen05.st per code row) instead of a third MMA per 128 codes: every tcgen05.mma costs
-    // ~70 clk of tensor pipe whatever N is (tools/umma_rate.cu), and 7 quads share the pipe
-    __shared__ __align__(16) int dbias_s[16];
     __shared__ __align__(8) uint64_t qbar_s[W / 4];
     __shared__ uint32_t qcnt_s[W / 4];  // A-row stagings per quad (the 4th of each round issues the MMA)
     __shared__ uint32_t tmem_s;
@@ -256,16 +249,6 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
                         }
                     }
                     bw_s[bw_offset(n, k)] = (int8_t)v;
-                }
-                if (threadIdx.x < 16) {
-                    int v = 1 << 28;  // padding queries never pass (and are masked anyway)
-                    if (threadIdx.x < nqh) {
-                        const uint32_t* qn = qw + (size_t)(q0 + threadIdx.x) * (M / 4);
-                        int pc = 0;
-                        for (int w = 0; w < M / 4; ++w) pc += __popc(__ldg(qn + w));
-                        v = 64 * (pc - (int)tau) - 32;
-                    }
-                    dbias_s[threadIdx.x] = v;
                 }
                 fence_proxy_async_smem();  // generic-proxy writes -> tensor-core reads
             }
@@ -421,21 +404,6 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
                     expand_word(word(c1, 2 * h + 1), x + 8);
                     tmem_st16(A1 + 16 * h, x);
                 }
-#if POLY_TC_DBIAS
-                {  // accumulators start at the bias: D = 64 (h - |q|) + 64 (|q| - tau) - 32
-                    const uint4* bp = reinterpret_cast<const uint4*>(dbias_s);
-#pragma unroll
-                    for (int v = 0; v < 4; ++v) {
-                        const uint4 b4 = bp[v];
-                        x[4 * v] = b4.x;
-                        x[4 * v + 1] = b4.y;
-                        x[4 * v + 2] = b4.z;
-                        x[4 * v + 3] = b4.w;
-                    }
-                    tmem_st16(D0, x);
-                    tmem_st16(D1, x);
-                }
-#endif
                 tmem_wait_st();
                 tc_fence_before();
                 __syncwarp();
@@ -446,11 +414,8 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
                         const uint32_t ac = qa0 + c * AC, dc = qa0 + 2 * AC + 16 * c;
 #pragma unroll
                         for (int kb = 0; kb < NKB - 1; ++kb)
-                            mma_i8_ts(dc, ac + 8 * kb, bdesc0 + (uint64_t)(32 * kb), IDESC_I8_M128_N16,
-                                      POLY_TC_DBIAS ? 1 : kb);
-#if !POLY_TC_DBIAS
+                            mma_i8_ts(dc, ac + 8 * kb, bdesc0 + (uint64_t)(32 * kb), IDESC_I8_M128_N16, kb);
                         mma_i8_ts(dc, tbase, bdesc0 + (uint64_t)(32 * (NKB - 1)), IDESC_I8_M128_N16, 1);
-#endif
                     }
                     tc_commit(&qbar_s[quad]);
                 }
