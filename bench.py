@@ -718,7 +718,9 @@ def run_ivf(args, rank, world, local):
     o_sc = torch.empty((B, k), dtype=torch.float32, device="cuda")
     o_cnt = torch.empty(B, dtype=torch.int32, device="cuda")
     nb = max(1, nq // B)
-    sharded = ShardedSearch(IVFIndexEngine(ivf, split_coarse=True)) if dist else None
+    # keys exchanged all-to-all by query slice: each rank merges 1/world of the queries
+    sharded = ShardedSearch(IVFIndexEngine(ivf, split_coarse=True, by_list=args.ivf_shard == "list"),
+                            exchange="alltoall") if dist else None
 
     def step(i, p, st=None):
         q = dq[(i % nb) * B:][:B]

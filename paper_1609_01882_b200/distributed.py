@@ -151,12 +151,17 @@ class IVFIndexEngine(FlatIndexEngine):
 
 
 class ShardedSearch:
-    """search_batch over all ranks' shards: local scan, all-gather keys, merge."""
+    """search_batch over all ranks' shards: local scan, exchange of the per-shard top-k
+    keys, exact merge.  ``exchange="allgather"``: every rank gathers every shard's keys and
+    merges every query.  ``exchange="alltoall"``: rank r receives every shard's keys for its
+    query slice only (shard_range over the queries), merges that slice, and the merged
+    slices are all-gathered -- W x less key traffic and merge work per rank."""
 
-    def __init__(self, engine, device="cuda", group=None):
+    def __init__(self, engine, device="cuda", group=None, exchange="allgather"):
         self.engine = engine
         self.device = device
         self.group = group
+        self.exchange = exchange
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
 
     def search_batch(self, queries, params, out=None):
@@ -169,6 +174,8 @@ class ShardedSearch:
         keys = torch.empty((nq, k), dtype=torch.int64, device=dev)
         cnt = torch.empty(nq, dtype=torch.int32, device=dev)
         self.engine.search_keys(queries, params, keys, cnt)
+        if self.world > 1 and self.exchange == "alltoall":
+            return self._alltoall(keys, cnt, nq, k, out)
         if self.world == 1:
             keys_all, cnt_all = keys.unsqueeze(0), cnt.unsqueeze(0)
         else:
@@ -180,4 +187,36 @@ class ShardedSearch:
             keys_all = keys_all.view(self.world, nq, k)
             cnt_all = cnt_all.view(self.world, nq)
         self.engine.merge(keys_all, cnt_all, self.world, nq, k, *out)
+        return out
+
+    def _alltoall(self, keys, cnt, nq, k, out):
+        W, dev = self.world, self.device
+        rank = dist.get_rank(self.group)
+        per = (nq + W - 1) // W
+        # send block r = the rows of query slice r, padded to `per` rows (padding: count 0)
+        send_k = torch.full((W * per, k), -1, dtype=torch.int64, device=dev)
+        send_c = torch.zeros(W * per, dtype=torch.int32, device=dev)
+        for r in range(W):
+            b, e = shard_range(nq, W, r)
+            send_k[r * per:r * per + (e - b)] = keys[b:e]
+            send_c[r * per:r * per + (e - b)] = cnt[b:e]
+        recv_k = torch.empty_like(send_k)
+        recv_c = torch.empty_like(send_c)
+        dist.all_to_all_single(recv_k, send_k, group=self.group)
+        dist.all_to_all_single(recv_c, send_c, group=self.group)
+        # recv block s = shard s's keys for this rank's slice: parts x per x k
+        ids_s = torch.empty((per, k), dtype=torch.int64, device=dev)
+        sc_s = torch.empty((per, k), dtype=torch.float32, device=dev)
+        cnt_s = torch.empty(per, dtype=torch.int32, device=dev)
+        self.engine.merge(recv_k.view(W, per, k), recv_c.view(W, per), W, per, k, ids_s, sc_s, cnt_s)
+        ga = [torch.empty((W * per, k), dtype=torch.int64, device=dev),
+              torch.empty((W * per, k), dtype=torch.float32, device=dev),
+              torch.empty(W * per, dtype=torch.int32, device=dev)]
+        for g, x in zip(ga, (ids_s, sc_s, cnt_s)):
+            dist.all_gather_into_tensor(g, x, group=self.group)
+        for r in range(W):
+            b, e = shard_range(nq, W, r)
+            for o, g in zip(out, ga):
+                o[b:e] = g[r * per:r * per + (e - b)]
+        del rank
         return out

@@ -50,7 +50,7 @@ class OracleEngine:
                     scores[q, r] = float("inf")
 
 
-def _worker(rank, world, port, result_path):
+def _worker(rank, world, port, result_path, exchange="allgather"):
     import sys
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -66,7 +66,8 @@ def _worker(rank, world, port, result_path):
     codes = np.repeat(g["codes"][:3000], 2, axis=0)  # ties across the shard boundary
     b, e = shard_range(len(codes), world, rank)
     eng = OracleEngine(pq, codes[b:e], np.arange(b, e, dtype=np.int64))
-    ids, scores, counts = ShardedSearch(eng, device="cpu").search_batch(torch.from_numpy(g["queries"]), P())
+    ids, scores, counts = ShardedSearch(eng, device="cpu", exchange=exchange).search_batch(
+        torch.from_numpy(g["queries"]), P())
     if rank == 0:
         np.savez(result_path, ids=ids.numpy(), scores=scores.numpy(), counts=counts.numpy())
     dist.destroy_process_group()
@@ -80,12 +81,13 @@ def _free_port():
     return port
 
 
-def test_sharded_search_equals_unsharded(tmp_path, pq8, g8):
+@pytest.mark.parametrize("exchange", ["allgather", "alltoall"])
+def test_sharded_search_equals_unsharded(tmp_path, pq8, g8, exchange):
     import oracle
     from paper_1609_01882_b200.distributed import shard_range
     assert [shard_range(10, 3, r) for r in range(3)] == [(0, 4), (4, 8), (8, 10)]
     out = str(tmp_path / "r0.npz")
-    mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), out, exchange), nprocs=2, join=True)
     r = np.load(out)
     codes = np.repeat(g8["codes"][:3000], 2, axis=0)
     oi, osc, oc, _, _ = oracle.search(pq8, codes, g8["queries"], 30, tau=24)

@@ -107,6 +107,10 @@ for r in range(1, W):  # stand-in parts for the merge's cost (same sizes)
     keys[r].copy_(keys[0])
     cnts[r].copy_(cnts[0])
 t_merge = timed(lambda: full.merge_keys_device(keys, cnts, W, nq, k, o[0], o[1], o[2], stream=sp))
+per = (nq + W - 1) // W  # all-to-all exchange: this rank merges its query slice only
+ks = keys[:, :per].contiguous()
+cs = cnts[:, :per].contiguous()
+t_merge_slice = timed(lambda: full.merge_keys_device(ks, cs, W, per, k, o[0], o[1], o[2], stream=sp))
 # collectives per step: probe keys all-gather (nq x nprobe x 8 B), bound all-reduce (nq x 8 B),
 # key + count all-gather (W x nq x (k x 8 + 4) B received per rank)
 bw = a.nvlink_gbs * 1e9
@@ -114,6 +118,12 @@ comm = {"probe_allgather_ms": nq * a.nprobe * 8 / bw * 1e3, "bound_allreduce_ms"
         "key_allgather_ms": W * nq * (k * 8 + 4) / bw * 1e3, "latency_ms": 3 * 0.02}
 t_comm = sum(comm.values())
 per_rank = t_coarse + t_rank + t_merge + t_comm
+# all-to-all exchange (ShardedSearch(exchange="alltoall"), the bench's IVF default): keys of the
+# other slices out, this slice's keys in, merged slices all-gathered
+comm_a2a = {"probe_allgather_ms": comm["probe_allgather_ms"], "bound_allreduce_ms": comm["bound_allreduce_ms"],
+            "key_alltoall_ms": (W - 1) / W * nq * (k * 8 + 4) / bw * 1e3,
+            "result_allgather_ms": (W - 1) / W * nq * (k * 12 + 4) / bw * 1e3, "latency_ms": 4 * 0.02}
+per_rank_a2a = t_coarse + t_rank + t_merge_slice + sum(comm_a2a.values())
 sizes = np.diff(shard.list_offsets().astype(np.int64))
 print(json.dumps({
     "what": f"by-list sharding, rank {R} of {W}, config 2: N={args.n} codes, nq={nq} per step, nprobe={a.nprobe}",
@@ -121,5 +131,9 @@ print(json.dumps({
     "rank": {"coarse_slice_ms": t_coarse, "phase1_plus_phase2_ms": t_rank, "merge_ms": t_merge,
              "scanned": st_r.scanned, "codes_held": int(sizes.sum())},
     "collectives_est": {k2: round(v, 4) for k2, v in comm.items()},
-    "per_rank_step_ms": per_rank, "projected_speedup": t_full / per_rank,
-    "projected_efficiency": t_full / per_rank / W, "setup_s": round(setup, 1)}), flush=True)
+    "allgather": {"per_rank_step_ms": per_rank, "projected_speedup": t_full / per_rank,
+                  "projected_efficiency": t_full / per_rank / W},
+    "alltoall": {"merge_slice_ms": t_merge_slice, "collectives_est": {k2: round(v, 4) for k2, v in comm_a2a.items()},
+                 "per_rank_step_ms": per_rank_a2a, "projected_speedup": t_full / per_rank_a2a,
+                 "projected_efficiency": t_full / per_rank_a2a / W},
+    "setup_s": round(setup, 1)}), flush=True)
