@@ -22,8 +22,11 @@ namespace pb {
 #ifndef POLY_K6_WARPS
 #define POLY_K6_WARPS 4
 #endif
+#ifndef POLY_K6_PREFETCH  // 1: software-pipelined code loads (one block ahead)
+#define POLY_K6_PREFETCH 1
+#endif
 #ifndef POLY_K6_MINB
-#define POLY_K6_MINB 12  // CTAs per SM the register budget is sized for (m = 8, item mode)
+#define POLY_K6_MINB 10  // CTAs per SM the register budget is sized for (m = 8; A/B with the prefetch: 10 > 12, 8)
 #endif
 constexpr int K6W = POLY_K6_WARPS;
 constexpr uint32_t K6_QN = 64;  // queue entries per warp: < 32 carried + one ballot step
@@ -158,13 +161,32 @@ __global__ void __launch_bounds__(K6W * 32, M == 8 ? POLY_K6_MINB : 8) ivf_list_
             }
             __syncwarp();
         };
+#if POLY_K6_PREFETCH
+        // the next block's codes are loaded before this block is filtered and drained
+        C cn[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const uint32_t row = warp * 128u + 32u * v + lane;
+            if (row < n) cn[v] = ld_stream(ci + row);
+        }
+#endif
         for (uint32_t rb = warp * 128u; rb < n; rb += 128u * K6W) {
             C c[4];
+#if POLY_K6_PREFETCH
+#pragma unroll
+            for (int v = 0; v < 4; ++v) c[v] = cn[v];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const uint32_t row = rb + 128u * K6W + 32u * v + lane;
+                if (row < n) cn[v] = ld_stream(ci + row);
+            }
+#else
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
                 const uint32_t row = rb + 32u * v + lane;
                 if (row < n) c[v] = ld_stream(ci + row);
             }
+#endif
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
                 const uint32_t row = rb + 32u * v + lane;

@@ -29,6 +29,9 @@ constexpr uint32_t TK_BUCKETS = 2048;
 #define POLY_TK_RANK 128
 #endif
 constexpr uint32_t TK_RANK = POLY_TK_RANK;  // at most this many keys to order: rank by counting
+#ifndef POLY_TK_SMALLK_KEYS  // keys staged in shared memory when k <= 512
+#define POLY_TK_SMALLK_KEYS 6144  // A/B on config 2 (10,000-query steps): 4096 8.61, 6144 8.37, 8192 8.52 ms; config 1 flat
+#endif
 
 __device__ __forceinline__ void bitonic_sort(unsigned long long* s, uint32_t p) {
     for (uint32_t size = 2; size <= p; size <<= 1) {
@@ -46,7 +49,7 @@ __device__ __forceinline__ void bitonic_sort(unsigned long long* s, uint32_t p) 
 
 // SMEM_KEYS: keys staged in shared memory (more come from L2); SEL_KEYS: the select
 // buffer (>= k + 1).  Two configurations: 8192 / 4096 (104 KB, two CTAs per SM) for
-// any k <= 2048, and 4096 / 1024 (49 KB, four CTAs per SM) for k <= 512.
+// any k <= 2048, and POLY_TK_SMALLK_KEYS (6144) / 1024 (65 KB, three CTAs per SM) for k <= 512.
 template <uint32_t TK_SMEM_KEYS, uint32_t TK_SEL_KEYS>
 __global__ void __launch_bounds__(TK_THREADS) topk_kernel(const unsigned long long* __restrict__ cand,
                                                           const uint32_t* __restrict__ ccount, uint32_t cap,
@@ -217,7 +220,8 @@ void launch_topk(const unsigned long long* cand, const uint32_t* ccount, uint32_
                  uint32_t* out_counts, cudaStream_t s) {
     if (nq == 0 || k == 0) return;
     if (k <= 512)
-        launch_topk_cfg<4096, 1024>(cand, ccount, cap, parts, part_stride, count_stride, nq, k, out_keys, out_counts, s);
+        launch_topk_cfg<POLY_TK_SMALLK_KEYS, 1024>(cand, ccount, cap, parts, part_stride, count_stride, nq, k, out_keys,
+                                                   out_counts, s);
     else
         launch_topk_cfg<8192, 4096>(cand, ccount, cap, parts, part_stride, count_stride, nq, k, out_keys, out_counts, s);
     count_launch();
