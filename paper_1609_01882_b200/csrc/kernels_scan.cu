@@ -34,14 +34,8 @@
 
 namespace pb {
 
-#ifndef POLY_PRODUCER_POLL  // > 0: the producer polls (sleep ns) and refreshes thresholds while it waits
-#define POLY_PRODUCER_POLL 0
-#endif
 #ifndef POLY_TC  // 1: DUAL's Hamming filter on the tensor cores (int8 tcgen05.mma); 0: POPC
 #define POLY_TC 1
-#endif
-#ifndef POLY_TC16  // 1: the tensor-core filter also for m = 16
-#define POLY_TC16 0
 #endif
 #ifndef POLY_RING
 #define POLY_RING 288
@@ -94,7 +88,9 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
     __shared__ uint32_t sel_hist[256];
     __shared__ uint32_t req_head_s;
     // tensor-core filter state: B operand (query weights + bias), per-quad MMA barriers, TMEM base
-    constexpr bool TCF = POLY_TC && STRAT == DUAL && (M == 8 || POLY_TC16);  // m = 16: 8 queries per CTA (A/B in DESIGN)
+    // m = 16 keeps the POPC filter: 8 queries per CTA do not amortise the bit-plane expansion
+    // (A/B in DESIGN.md sec. 5)
+    constexpr bool TCF = POLY_TC && STRAT == DUAL && M == 8;
     constexpr int KB = M * 8 + 32;   // B row bytes: one per code bit + the bias block
     constexpr int NKB = KB / 32;     // K blocks of 32 bytes
     constexpr int AC = 2 * M;        // TMEM columns of one expanded code (M * 8 bytes)
@@ -272,26 +268,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) scan_kernel(const ScanArgs a)
             };
             for (uint32_t j = 0; j < ntile; ++j) {
                 const uint32_t sq_ = seq + j, s = sq_ % STAGES;
-                if (sq_ >= STAGES) {
-#if POLY_PRODUCER_POLL
-                    // while the stage is busy: serve selects, refresh thresholds
-                    for (;;) {
-                        uint32_t ok = lane == 0 ? mbar_test(&empty_bar[s], ((sq_ / STAGES) - 1) & 1u) : 0u;
-                        if (__shfl_sync(0xffffffffu, ok, 0)) break;
-                        serve_selects();
-                        refresh();
-                        __nanosleep(POLY_PRODUCER_POLL);
-                    }
-#else
-                    if (lane == 0) {
-#if POLY_PROD_SPIN_NS > 0
-                        while (!mbar_test(&empty_bar[s], ((sq_ / STAGES) - 1) & 1u)) __nanosleep(POLY_PROD_SPIN_NS);
-#else
-                        mbar_wait(&empty_bar[s], ((sq_ / STAGES) - 1) & 1u);
-#endif
-                    }
-#endif
-                }
+                if (sq_ >= STAGES && lane == 0) mbar_wait(&empty_bar[s], ((sq_ / STAGES) - 1) & 1u);
                 if (lane == 0) {
                     const uint64_t first = (t0 + j) * a.tile_stride * TC;
                     const uint64_t cnt = min((uint64_t)TC, a.n - first);

@@ -34,9 +34,6 @@ constexpr int DSUB = 16;               // every configuration: 128/8 and 256/16
 #ifndef POLY_SEED_BLOCKS  // K2s seed sample: runs of 256 codes (0 = no seed kernel)
 #define POLY_SEED_BLOCKS 128
 #endif
-#ifndef POLY_PROD_SPIN_NS
-#define POLY_PROD_SPIN_NS 0
-#endif
 #ifndef POLY_SPIN_MMA_NS  // K2: backoff of the quad-MMA commit wait
 #define POLY_SPIN_MMA_NS 400
 #endif

@@ -1,0 +1,15 @@
+#!/bin/bash
+# round-2 evidence on HEAD: smoke, every config's bench line, the reference arm, launch lists, ncu of K2
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out/final
+O=gpurun_out/final
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?"
+timeout 900 python bench.py > $O/cfg1.json 2> $O/cfg1.err; echo "cfg1 rc=$?"
+timeout 900 python bench.py --impl reference > $O/ref.json 2> $O/ref.err; echo "ref rc=$?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launch_cfg1.csv python bench.py --steps 2 --warmup 1 --per-ht "" --no-cpu-baseline --no-e2e > $O/ncu1.log 2>&1; echo "ncu1=$?"
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:scan_kernel -c 1 -o $O/k2_cfg1 python tools/prof_scan.py --n 100000000 --ht 24 > $O/ncu2.log 2>&1; echo "ncu2=$?"
+timeout 1500 python bench.py --config 2 --steps 5 > $O/cfg2.json 2> $O/cfg2.err; echo "cfg2 rc=$?"
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file $O/launch_cfg2.csv env BENCH_PROFILE=1 python bench.py --config 2 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --per-nprobe "" > $O/ncu3.log 2>&1; echo "ncu3=$?"
+timeout 600 python bench.py --config 0 > $O/cfg0.json 2> $O/cfg0.err; echo "cfg0 rc=$?"
+timeout 1200 python bench.py --config 3 --steps 5 > $O/cfg3.json 2> $O/cfg3.err; echo "cfg3 rc=$?"
+timeout 1500 python bench.py --config 4 --steps 10 --knn-full /tmp/knn_full.knng > $O/cfg4.json 2> $O/cfg4.err; echo "cfg4 rc=$?"
