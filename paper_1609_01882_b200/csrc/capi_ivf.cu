@@ -137,6 +137,10 @@ constexpr uint64_t IVF_R1_CODES = POLY_IVF_R1_CODES;  // ... and at least this m
 #endif
 constexpr uint32_t IVF_CHUNK = POLY_IVF_CHUNK;    // K6 round-1 work item: 1024 list rows (K6 scans it in 128-row warp blocks)
 constexpr uint32_t IVF_CHUNK2 = POLY_IVF_CHUNK2;  // round 2: longer items (fewer LUT loads per code)
+#ifndef POLY_IVF_SEED_ROWS  // K6s sample: rows of each query's first list (0 = no round-1 seed)
+#define POLY_IVF_SEED_ROWS 2048
+#endif
+constexpr uint32_t IVF_SEED_ROWS = POLY_IVF_SEED_ROWS;
 
 __global__ void fill_u32(uint32_t* p, uint64_t n, uint32_t v) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
@@ -407,6 +411,9 @@ void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_
     // query's leading probes holding >= IVF_R1_CODES codes (at most IVF_R1_MAX probes) in
     // 1024-row chunks; its exact k-th key (K3) bounds round 2, the remaining probes
     const uint32_t rounds = np <= 1 ? 1 : 2;  // one probe: round 1 sees everything
+    // K6s: round 1's own bound from a sample of each query's first list (k <= sample)
+    if (phase != 2 && IVF_SEED_ROWS && k <= IVF_SEED_ROWS / 4)
+        pb::launch_ivf_seed(a, strategy, iv->m, IVF_SEED_ROWS, k, s);
     for (uint32_t round = 0; round < rounds; ++round) {
         if (phase == 1 && round == 1) break;
         if (phase == 2 && round == 0) continue;

@@ -355,6 +355,113 @@ void launch_ivf_probe_count(const unsigned long long* probe_keys, uint32_t nq, u
 
 // K6 (the list scan) is in kernels_ivf_scan.cu.
 
+// ------------------------------------------------------------------ K6s
+// Round-1 seed: a bound for round 1 itself, so that round 1 (which otherwise starts
+// unbounded) appends few candidates.  One CTA per query scores the first `rows` codes of
+// the query's first probed list exactly as K6 does (the item's LUT and query code from
+// K1r) and sets thr[q] = min(thr[q], k-th key + 1) when it found >= k keys: the k-th key
+// of a subset of round 1's codes is >= the k-th key of round 1 and of the final result,
+// so the bound is valid; seed_compact still sets round 2's bound from round 1's exact k-th.
+constexpr uint32_t K6S_THREADS = 256;
+
+template <int M, int STRAT>
+__global__ void __launch_bounds__(K6S_THREADS) ivf_seed_kernel(const IvfScanArgs a, uint32_t rows, uint32_t k) {
+    using C = typename CodeT<M>::T;
+    extern __shared__ __align__(16) uint8_t k6s_smem[];
+    float* L = reinterpret_cast<float*>(k6s_smem);
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(k6s_smem + M * KSUB * 4);
+    __shared__ uint32_t cnt, hist[256], want_s;
+    __shared__ unsigned long long prefix_s;
+    const uint32_t q = blockIdx.x;
+    const size_t item = (size_t)q * a.nprobe;  // the first probe
+    const uint32_t cell = (uint32_t)a.probe_keys[item];
+    const uint64_t beg = a.off[cell];
+    const uint32_t n = (uint32_t)min((uint64_t)rows, a.off[cell + 1] - beg);
+    if (n < k) return;  // fewer codes than k: no bound from this sample
+    if (STRAT == DUAL || STRAT == ADC)
+        for (uint32_t i = threadIdx.x; i < (uint32_t)M * KSUB / 4; i += K6S_THREADS)
+            reinterpret_cast<float4*>(L)[i] = __ldg(reinterpret_cast<const float4*>(a.lutp + item * M * KSUB) + i);
+    const C qc = reinterpret_cast<const C*>(a.qcodes)[item];
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    const C* ci = reinterpret_cast<const C*>(a.codes) + beg;
+    for (uint32_t i = threadIdx.x; i < n; i += K6S_THREADS) {
+        const C code = ci[i];
+        float score;
+        if (strategy_score<M, STRAT>(L, code, qc, a.tau, 0xFFFFFFFFu, score))
+            keys[atomicAdd(&cnt, 1u)] = ((unsigned long long)__float_as_uint(score) << 32) | __ldg(a.low + beg + i);
+    }
+    __syncthreads();
+    const uint32_t nk = cnt;
+    if (nk < k) return;
+    unsigned long long prefix = 0, mask = 0;
+    uint32_t want = k;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+        hist[threadIdx.x] = 0;
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < nk; i += K6S_THREADS) {
+            const unsigned long long v = keys[i];
+            if ((v & mask) == prefix) atomicAdd(&hist[(v >> shift) & 0xFFu], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            const uint32_t lane = threadIdx.x;
+            uint32_t c[8], t = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                c[j] = hist[lane * 8 + j];
+                t += c[j];
+            }
+            uint32_t incl = t;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= (uint32_t)o) incl += x;
+            }
+            const uint32_t excl = incl - t;
+            if (excl < want && want <= incl) {
+                uint32_t r = want - excl;
+                int digit = lane * 8 + 7;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (r <= c[j]) {
+                        digit = lane * 8 + j;
+                        break;
+                    }
+                    r -= c[j];
+                }
+                prefix_s = prefix | ((unsigned long long)digit << shift);
+                want_s = r;
+            }
+        }
+        __syncthreads();
+        prefix = prefix_s;
+        want = want_s;
+        mask |= 0xFFull << shift;
+    }
+    if (threadIdx.x == 0 && prefix + 1 < a.thr[q]) a.thr[q] = prefix + 1;  // prefix = the k-th key
+}
+
+template <int M, int STRAT>
+static void launch_ivf_seed_m(const IvfScanArgs& a, uint32_t rows, uint32_t k, cudaStream_t s) {
+    const size_t smem = (size_t)M * KSUB * 4 + (size_t)rows * 8;
+    auto kfn = ivf_seed_kernel<M, STRAT>;
+    set_max_smem((const void*)kfn, smem);
+    kfn<<<a.nq, K6S_THREADS, smem, s>>>(a, rows, k);
+    count_launch();
+}
+
+void launch_ivf_seed(const IvfScanArgs& a, int strategy, uint32_t m, uint32_t rows, uint32_t k, cudaStream_t s) {
+    if (a.nq == 0 || rows == 0 || k == 0) return;
+    const bool w = m == 16;
+    switch (strategy) {
+        case DUAL: w ? launch_ivf_seed_m<16, DUAL>(a, rows, k, s) : launch_ivf_seed_m<8, DUAL>(a, rows, k, s); break;
+        case ADC: w ? launch_ivf_seed_m<16, ADC>(a, rows, k, s) : launch_ivf_seed_m<8, ADC>(a, rows, k, s); break;
+        case BINARY: w ? launch_ivf_seed_m<16, BINARY>(a, rows, k, s) : launch_ivf_seed_m<8, BINARY>(a, rows, k, s); break;
+        default: w ? launch_ivf_seed_m<16, DISIDX>(a, rows, k, s) : launch_ivf_seed_m<8, DISIDX>(a, rows, k, s); break;
+    }
+}
+
 // ------------------------------------------------------------------ build
 // Nearest coarse cell of each vector (sq_l2, strict <, ties -> lowest cell);
 // cells are staged through shared memory 32 at a time.

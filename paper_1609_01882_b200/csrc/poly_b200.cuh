@@ -327,6 +327,8 @@ void launch_ivf_probe_count(const unsigned long long* probe_keys, uint32_t nq, u
                             uint64_t cap, uint32_t* np_eff, unsigned long long* scanned, cudaStream_t s,
                             uint32_t* split, uint64_t r1_codes, uint32_t r1_max, const IvfWork& w);
 void launch_ivf_scan(const IvfScanArgs& a, int strategy, uint32_t m, int num_sms, cudaStream_t s);
+// K6s: round-1 bound from the first `rows` codes of each query's first probed list
+void launch_ivf_seed(const IvfScanArgs& a, int strategy, uint32_t m, uint32_t rows, uint32_t k, cudaStream_t s);
 void launch_assign(const float* x, uint64_t n, uint32_t dim, const float* cent, uint32_t nlist, uint32_t* assign,
                    cudaStream_t s);
 void launch_residual_encode(const float* x, uint64_t n, uint32_t dim, uint32_t m, const float* cent,
