@@ -180,6 +180,8 @@ void grow_ins(poly_b200_ivf* iv, uint64_t need) {
 void rebuild_lists(poly_b200_ivf* iv) {
     if (!iv->lists_dirty) return;
     cudaStream_t s = iv->stream;
+    // list positions are 32-bit in the K6 work items and the key low words
+    require(iv->n < (1ull << 32), POLY_B200_INVALID_ARGUMENT, "an IVF index holds < 2^32 codes per GPU");
     iv->idm.sync(iv->n);
     dfree(iv->d_codes_list);
     dfree(iv->d_low_list);

@@ -12,6 +12,7 @@ ap.add_argument('--nprobe', type=int, default=16)
 ap.add_argument('--reps', type=int, default=2)
 ap.add_argument('--nq', type=int, default=256)
 ap.add_argument('--batch', type=int, default=0)
+ap.add_argument('--round-stats', action='store_true', help='print the pairs round 1 / round 2 scan')
 args = ap.parse_args()
 z = np.load('tests/golden/pq_ivf65536_d128_m8.npz')
 pq = pb.ProductQuantizer(8, 8, 128, z['codebooks'], z['perms'])
@@ -33,6 +34,15 @@ for r in range(0, args.n, 1 << 20):
 q = synth.gen_points(160901882, 3, 0, args.nq, centers)
 p = pb.CoarseParams(pb.Strategy.dual, 100, 26, args.nprobe, 0)
 ivf.search(q, p)  # warm (allocations)
+if args.round_stats:
+    off = np.asarray(ivf.list_offsets()).astype(np.int64)
+    pr = np.asarray(ivf.probes(q, args.nprobe)).astype(np.int64)
+    sz = off[pr + 1] - off[pr]
+    cum = np.cumsum(sz, 1)
+    first = np.argmax(cum >= 2048, 1)  # round 1 = probes [0, first] (non-empty-list rule aside)
+    r1 = cum[np.arange(len(q)), first]
+    print(f"round stats: list mean {off[-1] / (len(off) - 1):.0f} max {np.diff(off).max()}; first-probe size mean {sz[:, 0].mean():.0f}; "
+          f"round-1 pairs {r1.sum():.3e} ({r1.mean():.0f}/query), all pairs {cum[:, -1].sum():.3e}")
 torch.cuda.synchronize()
 torch.cuda.profiler.start()  # ncu --profile-from-start off: only the searches below
 for i in range(args.reps):

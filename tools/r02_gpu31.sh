@@ -1,0 +1,15 @@
+#!/bin/bash
+# K6 ring-queue rewrite: IVF parity + survivor tests, A/B against the previous K6 (tools/lib12/base.so) on the config-2 shape
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out/g31
+O=gpurun_out/g31
+timeout 1500 python -m pytest tests/test_gpu_ivf.py tests/test_gpu_survivors.py -x -q > $O/pytest.log 2>&1; echo "tests rc=$?"; tail -3 $O/pytest.log
+for n in base new; do
+  L=tools/lib12/$n.so; [ $n = new ] && L=paper_1609_01882_b200/libpoly_b200.so
+  for np in 16 64; do
+    POLY_B200_LIB=$L timeout 600 python tools/prof_ivf.py --n 400000000 --nq 10000 --batch 10000 --reps 3 --nprobe $np 2>&1 | tail -1 | sed "s/^/$n np$np: /"
+  done
+done
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file $O/launch_4e8_new.csv python tools/prof_ivf.py --n 400000000 --nq 10000 --batch 10000 --reps 1 > $O/ncu.log 2>&1; echo "ncu rc=$?"
+python tools/launches.py $O/launch_4e8_new.csv
+timeout 900 ncu --set full --import-source on --clock-control none --profile-from-start off -k regex:ivf_list_scan -s 1 -c 1 -o $O/k6_ring python tools/prof_ivf.py --n 400000000 --nq 10000 --batch 10000 --reps 1 > $O/ncu2.log 2>&1; echo "ncu2 rc=$?"
