@@ -38,6 +38,7 @@ constexpr int CT_STAGE = CT_N * CT_KC * 4;  // 32 KB
 constexpr int CT_EPI_WARPS = 8;        // two per TMEM lane quadrant, one per 128-cell group
 constexpr int CT_THREADS = (2 + CT_EPI_WARPS) * 32;
 constexpr int CT_GROUP = 128;          // cells per kept-value group
+constexpr float CT_PAD_NORM = 3.0e38f;  // |c|^2 of a pad cell: above every real a', finite under the index packing
 
 // tcgen05 kind::tf32 instruction descriptor: D fp32, A/B tf32, both K-major, N = 256, M = 128
 constexpr uint32_t IDESC_TF32_M128_N256 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(CT_N >> 3) << 17) |
@@ -76,7 +77,7 @@ __device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar) {
 
 // ---------------------------------------------------------------- packing (index creation)
 // packed[t][s] = the 32 KB shared-memory image of cells [256 t, 256 t + 256) x dims
-// [32 s, 32 s + 32); cnorm_pad[c] = |c|^2 (any rounding: E covers it), +inf for pad cells.
+// [32 s, 32 s + 32); cnorm_pad[c] = |c|^2 (any rounding: E covers it), CT_PAD_NORM for pad cells.
 __global__ void coarse_pack_kernel(const float* __restrict__ cent, uint32_t nlist, uint32_t dim, uint32_t ntiles,
                                    float* __restrict__ packed, float* __restrict__ cnorm_pad) {
     const uint32_t nchunk = dim / CT_KC;
@@ -97,7 +98,7 @@ __global__ void coarse_pack_kernel(const float* __restrict__ cent, uint32_t nlis
         float acc = 0.f;
         if (c < nlist)
             for (uint32_t d = 0; d < dim; ++d) acc = __fmaf_rn(cent[c * dim + d], cent[c * dim + d], acc);
-        cnorm_pad[c] = c < nlist ? acc : __int_as_float(0x7f800000);
+        cnorm_pad[c] = c < nlist ? acc : CT_PAD_NORM;
     }
 }
 
@@ -202,8 +203,11 @@ __global__ void __launch_bounds__(CT_THREADS, 1) coarse_tc_kernel(const float* _
             tc_fence_after();
             const uint32_t tile = t0 + u;
             const float* cn = cnorm_pad + (size_t)tile * CT_N + half * CT_GROUP;
+            // Branch-free selection: the cell's index within the group rides in the low 7 mantissa
+            // bits of a' (a relative perturbation <= 2^-16, covered by K5q's error bound E), so the
+            // three smallest packed values -- four min/max per value, merged two values at a time --
+            // carry their cells along and are always distinct.  Pad cells have |c|^2 = 3e38 (finite: no NaN from the packing).
             float m1 = __int_as_float(0x7f800000), m2 = m1, m3 = m1;
-            uint32_t i1 = 0xFFFFu, i2 = 0xFFFFu;
 #pragma unroll 1
             for (uint32_t c0 = 0; c0 < CT_GROUP; c0 += 32) {
                 float d[32];
@@ -214,21 +218,22 @@ __global__ void __launch_bounds__(CT_THREADS, 1) coarse_tc_kernel(const float* _
                     const float4 n4v = __ldg(reinterpret_cast<const float4*>(cn + c0) + j4);  // uniform: broadcast
                     const float nv[4] = {n4v.x, n4v.y, n4v.z, n4v.w};
 #pragma unroll
-                    for (uint32_t e = 0; e < 4; ++e) {
+                    for (uint32_t e = 0; e < 4; e += 2) {
+                        // two packed values at a time: the three smallest of {m1 <= m2 <= m3} U {lo <= hi}
                         const uint32_t j = c0 + 4 * j4 + e;
                         const float a = __fmaf_rn(-2.0f, d[4 * j4 + e], nv[e]);
-                        if (a < m3) {
-                            if (a < m2) {
-                                m3 = m2;
-                                if (a < m1) { m2 = m1; i2 = i1; m1 = a; i1 = j; }
-                                else { m2 = a; i2 = j; }
-                            } else {
-                                m3 = a;
-                            }
-                        }
+                        const float b = __fmaf_rn(-2.0f, d[4 * j4 + e + 1], nv[e + 1]);
+                        const float ap = __uint_as_float((__float_as_uint(a) & ~(CT_GROUP - 1u)) | j);
+                        const float bp = __uint_as_float((__float_as_uint(b) & ~(CT_GROUP - 1u)) | (j + 1u));
+                        const float lo = fminf(ap, bp), hi = fmaxf(ap, bp);
+                        const float x = fmaxf(m1, lo);
+                        m3 = fminf(fminf(m3, fmaxf(m2, lo)), fmaxf(m1, hi));
+                        m2 = fminf(fminf(m2, x), hi);
+                        m1 = fminf(m1, lo);
                     }
                 }
             }
+            const uint32_t i1 = __float_as_uint(m1) & (CT_GROUP - 1u), i2 = __float_as_uint(m2) & (CT_GROUP - 1u);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cta(&tempty[buf]);
@@ -384,7 +389,9 @@ __global__ void __launch_bounds__(CR_THREADS, 2) coarse_rank_kernel(const float*
     // threads (groups) hold fewer than np values when ngroups * 3 < np: no bound
     const float T = np > nkept ? __int_as_float(0x7f800000) : cr_unord(prefix | 0xFFFFu);
     const float qnorm = sqrtf(qn);
-    const float E = 4.2e-3f * qnorm * cmax + (float)dim * 4e-7f * (qn + cmax * cmax + 2.0f * qnorm * cmax) + 1e-6f;
+    // + K5t's index packing: the low 7 mantissa bits of a' are replaced, |a'| <= |c|^2 + 2 |q| |c|
+    const float E = 4.2e-3f * qnorm * cmax + (float)dim * 4e-7f * (qn + cmax * cmax + 2.0f * qnorm * cmax) + 1e-6f +
+                    1.7e-5f * (cmax * cmax + 2.0f * qnorm * cmax);
     const float bound = T + 2.0f * E;
     if (!(m3 > bound)) {  // every cell of this thread's groups is a candidate
         for (uint32_t g = tid; g < ngroups; g += CR_THREADS)

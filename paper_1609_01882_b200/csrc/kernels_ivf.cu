@@ -300,16 +300,18 @@ __global__ void ivf_probe_count_kernel(const unsigned long long* __restrict__ pr
         if (lane == 0) split[qi] = sp;
         // work lists: round 1 = probes [0, sp), round 2 = [sp, ne) (A/B: cutting round 1
         // at 2048 / 4096 rows instead of whole probes gained nothing).  Lists are cut into
-        // chunks of w.chunk[r] rows; one item (query, probe, row0, row1) per chunk.
+        // chunks of w.chunk[r] rows; one item (query, probe, first list position, rows) per chunk.
         if (w.items[0]) {
             for (int r = 0; r < 2; ++r) {
                 const uint32_t phi = r ? ne : sp, ch = w.chunk[r];
                 for (uint32_t p0 = 0; p0 < phi; p0 += 32) {
                     const uint32_t p = p0 + lane;
-                    uint32_t len = 0;
+                    uint32_t len = 0, pos = 0;  // the list's length and first position (< 2^32 codes per GPU)
                     if (p < phi) {
                         const uint32_t cell = (uint32_t)probe_keys[(size_t)qi * nprobe + p];
-                        len = (uint32_t)(off[cell + 1] - off[cell]);
+                        const uint64_t o0 = off[cell];
+                        len = (uint32_t)(off[cell + 1] - o0);
+                        pos = (uint32_t)o0;
                     }
                     // the round's non-empty items get a residual LUT (K1r)
                     const bool lut = p < phi && len > 0 && (r == 0 || p >= sp);
@@ -335,7 +337,7 @@ __global__ void ivf_probe_count_kernel(const unsigned long long* __restrict__ pr
                     at = __shfl_sync(0xffffffffu, at, 0) + incl - nch;
                     for (uint32_t c = 0; c < nch; ++c)
                         if (at + c < w.cap[r])
-                            w.items[r][at + c] = make_uint4(qi, p, lo + c * ch, min(hi, lo + (c + 1) * ch));
+                            w.items[r][at + c] = make_uint4(qi, p, pos + lo + c * ch, min(hi, lo + (c + 1) * ch) - (lo + c * ch));
                         else
                             atomicOr(w.overflow, 1u);
                 }

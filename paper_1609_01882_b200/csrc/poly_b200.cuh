@@ -107,8 +107,8 @@ struct IvfScanArgs {
     unsigned long long* surv_total;
     unsigned long long* surv_q;           // per-query survivor counts and hashes (stats mode; else null)
     unsigned long long* hash_q;
-    const uint4* items;      // work items (query, probe, row0, row1): rows [row0, row1) of the
-    const uint32_t* nitems;  // probed cell's list; built by the probe-count kernel
+    const uint4* items;      // work items (query, probe, pos, rows): `rows` codes from list-order position
+    const uint32_t* nitems;  // `pos` (a chunk of the probed cell's list); built by the probe-count kernel
     uint32_t items_cap;
 };
 
