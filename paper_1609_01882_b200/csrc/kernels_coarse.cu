@@ -225,15 +225,11 @@ __global__ void __launch_bounds__(CT_THREADS, 1) coarse_tc_kernel(const float* _
                         const float b = __fmaf_rn(-2.0f, d[4 * j4 + e + 1], nv[e + 1]);
                         const float ap = __uint_as_float((__float_as_uint(a) & ~(CT_GROUP - 1u)) | j);
                         const float bp = __uint_as_float((__float_as_uint(b) & ~(CT_GROUP - 1u)) | (j + 1u));
-#ifdef POLY_K5T_DBG_NOEPI  // timing experiment only: one min per two values
-                        m1 = fminf(fminf(m1, ap), bp);
-#else
                         const float lo = fminf(ap, bp), hi = fmaxf(ap, bp);
                         const float x = fmaxf(m1, lo);
                         m3 = fminf(fminf(m3, fmaxf(m2, lo)), fmaxf(m1, hi));
                         m2 = fminf(fminf(m2, x), hi);
                         m1 = fminf(m1, lo);
-#endif
                     }
                 }
             }
