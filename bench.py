@@ -838,7 +838,7 @@ def run_ivf(args, rank, world, local):
                        "build_assignment": "TF32 GEMM argmin (setup only)",
                        "l2": "probed lists stream from HBM (GBs of codes per GPU); no flush needed"},
             "e2e": e2e, "gpu_launches": head["gpu_launches"], "clocks": clk,
-            "roofline": dict(head["roofline"], kernel="K6 ivf_scan_kernel (both rounds)",
+            "roofline": dict(head["roofline"], kernel="K6 ivf_list_scan_kernel (both rounds)",
                              kernel_share_of_step=head["k6_share_of_step"]),
             "roofline_step": head["roofline_step"], "roofline_hbm": head["roofline_hbm"],
             "by_list_sharding_8": by_list,
@@ -948,7 +948,7 @@ def run_knn(args, rank, world, local):
                        "l2": "160 MB of list codes stream through L2 per step; no flush"},
             "scanned_per_query": scanned / (steps * B), "survivor_frac": surv / max(scanned, 1),
             "graph_time_est_s": rows / B * ms / steps / 1e3, "gpu_launches": launches, "clocks": clk,
-            "roofline": dict(k6, kernel="K6 ivf_scan_kernel (both rounds)", kernel_share_of_step=k6_ms / ms),
+            "roofline": dict(k6, kernel="K6 ivf_list_scan_kernel (both rounds)", kernel_share_of_step=k6_ms / ms),
             "roofline_step": stp, "roofline_hbm": hbm, "setup_s": round(setup_s, 1)}
     if args.knn_full:
         line["full_graph"] = knn_full(args, pb, torch, ivf, centers, p, row0, row1, local, stream)

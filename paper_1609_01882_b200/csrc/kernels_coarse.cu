@@ -33,8 +33,15 @@ namespace pb {
 
 constexpr int CT_M = 128;              // queries per tile (TMEM lanes)
 constexpr int CT_N = 256;              // cells per tile (TMEM columns per accumulator)
-constexpr int CT_KC = 32;              // dims per pipeline stage
-constexpr int CT_STAGE = CT_N * CT_KC * 4;  // 32 KB
+#ifndef POLY_CT_KC
+#define POLY_CT_KC 32
+#endif
+#ifndef POLY_CT_SMEM  // dynamic shared memory budget of K5t (A + the B stages)
+#define POLY_CT_SMEM (225 * 1024)
+#endif
+constexpr int CT_KC = POLY_CT_KC;       // dims per pipeline stage
+constexpr int CT_STAGE = CT_N * CT_KC * 4;  // 32 KB at 32 dims
+constexpr int CT_MAX_STAGES = 16;
 constexpr int CT_EPI_WARPS = 8;        // two per TMEM lane quadrant, one per 128-cell group
 constexpr int CT_THREADS = (2 + CT_EPI_WARPS) * 32;
 constexpr int CT_GROUP = 128;          // cells per kept-value group
@@ -120,7 +127,7 @@ __global__ void __launch_bounds__(CT_THREADS, 1) coarse_tc_kernel(const float* _
                                                                   const float* __restrict__ cnorm_pad, uint32_t ntiles,
                                                                   uint32_t stages, float4* __restrict__ grp) {
     extern __shared__ __align__(1024) uint8_t ct_smem[];
-    __shared__ __align__(8) uint64_t full_bar[8], empty_bar[8], tfull[2], tempty[2];
+    __shared__ __align__(8) uint64_t full_bar[CT_MAX_STAGES], empty_bar[CT_MAX_STAGES], tfull[2], tempty[2];
     __shared__ uint32_t tmem_s;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t S = gridDim.x, s = blockIdx.x, qt = blockIdx.y;
@@ -251,7 +258,8 @@ __global__ void __launch_bounds__(CT_THREADS, 1) coarse_tc_kernel(const float* _
 
 size_t coarse_tc_smem(uint32_t dim, uint32_t* stages) {
     const size_t a = (size_t)CT_M * dim * 4;
-    uint32_t st = (uint32_t)std::min<size_t>(4, (200 * 1024 - a) / CT_STAGE);
+    // as many stages as fit: the main loop is bound by the bulk copies' latency, i.e. by the bytes in flight
+    uint32_t st = (uint32_t)std::min<size_t>(CT_MAX_STAGES, ((size_t)POLY_CT_SMEM - a) / CT_STAGE);
     if (stages) *stages = st;
     return a + (size_t)st * CT_STAGE;
 }
