@@ -1,15 +1,16 @@
 #!/bin/bash
-# Round evidence: GPU tests, bench lines of every config, IVF launch lists.
-mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pt_all.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pt_all.log
-timeout 600 python bench.py > gpurun_out/bench_cfg1.json 2> gpurun_out/bench_cfg1.err; echo "cfg1 rc=$?"
-timeout 900 python bench.py --config 2 > gpurun_out/bench_cfg2.json 2> gpurun_out/bench_cfg2.err; echo "cfg2 rc=$?"
-timeout 900 python bench.py --config 4 > gpurun_out/bench_cfg4.json 2> gpurun_out/bench_cfg4.err; echo "cfg4 rc=$?"
-timeout 900 python bench.py --config 3 --no-cpu-baseline > gpurun_out/bench_cfg3.json 2> gpurun_out/bench_cfg3.err; echo "cfg3 rc=$?"
-for np in 16 64; do
-  ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
-      --log-file gpurun_out/ivf_cfg2_b1024_np${np}_launches.csv \
-      python tools/prof_ivf.py --n 125000000 --nq 1024 --reps 1 --nprobe $np > /dev/null 2>&1
-done
-python tools/launches.py gpurun_out/ivf_cfg2_b1024_np*_launches.csv
-for c in 1 2 4 3; do tail -1 gpurun_out/bench_cfg$c.json | cut -c1-400; done
+# Round evidence on HEAD: smoke, the GPU suite, every config's bench line, the reference arm, launch lists
+# (gpurun -- bash tools/round_evidence.sh; the outputs are copied to profiles/ by hand)
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out/evidence
+O=gpurun_out/evidence
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?"
+timeout 1800 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.txt 2>&1; echo "pytest rc=$?"; tail -2 $O/pytest_gpu.txt
+timeout 900 python bench.py > $O/cfg1.json 2> $O/cfg1.err; echo "cfg1 rc=$?"
+timeout 900 python bench.py --impl reference > $O/ref.json 2> $O/ref.err; echo "ref rc=$?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launch_cfg1.csv python bench.py --steps 2 --warmup 1 --per-ht "" --no-cpu-baseline --no-e2e > $O/ncu1.log 2>&1; echo "ncu1=$?"
+timeout 1500 python bench.py --config 2 --steps 5 > $O/cfg2.json 2> $O/cfg2.err; echo "cfg2 rc=$?"
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file $O/launch_cfg2.csv env BENCH_PROFILE=1 python bench.py --config 2 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --per-nprobe "" > $O/ncu3.log 2>&1; echo "ncu3=$?"
+timeout 600 python bench.py --config 0 > $O/cfg0.json 2> $O/cfg0.err; echo "cfg0 rc=$?"
+timeout 1200 python bench.py --config 3 --steps 5 > $O/cfg3.json 2> $O/cfg3.err; echo "cfg3 rc=$?"
+timeout 1500 python bench.py --config 4 --steps 10 --knn-full /tmp/knn_full.knng > $O/cfg4.json 2> $O/cfg4.err; echo "cfg4 rc=$?"
