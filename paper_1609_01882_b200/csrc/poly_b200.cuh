@@ -52,9 +52,8 @@ constexpr int STAGES = POLY_STAGES;          // bulk-copy ring depth
 #define POLY_SCAN_WARPS 28
 #endif
 constexpr int SCAN_WARPS = POLY_SCAN_WARPS;  // K2 consumer warps (plus one TMA producer warp)
-constexpr int BS = 4096;               // candidate block size for threshold selects
+constexpr int BS = 4096;               // candidate list capacity unit: a list holds >= 32 * BS keys per query
 constexpr int KMAX = 2048;             // largest supported k
-constexpr int QCAP = 64;               // per-warp survivor queue entries
 constexpr int MAXREQ = 32;             // pending threshold selects per CTA (ring)
 constexpr uint64_t KEY_INF = ~0ull;
 
