@@ -102,6 +102,14 @@ __device__ __forceinline__ unsigned long long k1_pack(float lo, float hi) {
     asm("mov.b64 %0, {%1,%2};" : "=l"(v) : "f"(lo), "f"(hi));
     return v;
 }
+// A packed pair that stays packed: the result of an FADD2 with a runtime -0.0 pair (x + -0.0 == x for
+// every x).  ptxas rematerialises a plain mov.b64 pack at every use -- two MOVs per packed operand,
+// 0.6 MOV per FP op in the term loop -- but keeps an arithmetic result in its register pair.
+__device__ __forceinline__ unsigned long long k1_pack_once(float lo, float hi, unsigned long long nzz) {
+    unsigned long long v;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(v) : "l"(k1_pack(lo, hi)), "l"(nzz));
+    return v;
+}
 
 // K1r, two centroid pairs per thread: the 128 threads cover two sub-quantizers at a
 // time (thread t: sq 2s + (t >> 6), pairs (u, u + 128) and (u + 64, u + 192), u = t & 63),
@@ -137,7 +145,7 @@ __global__ void __launch_bounds__(128, POLY_K1R_MINB) residual_lut_quad_kernel(c
         rr[it][d] = k1_pack(r, r);
     }
     __syncthreads();
-    const unsigned long long zz = k1_pack(zero, zero);
+    const unsigned long long zz = k1_pack(zero, zero), nzz = k1_pack(-zero, -zero);
     const uint32_t ja = u, jb = u + 128, jc = u + 64, jd = u + 192;  // pair 0 = (ja, jb), pair 1 = (jc, jd)
     for (uint32_t s2 = 0; s2 < m / 2; ++s2) {
         const uint32_t sq = 2 * s2 + h;
@@ -149,10 +157,10 @@ __global__ void __launch_bounds__(128, POLY_K1R_MINB) residual_lut_quad_kernel(c
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
             const float4 a = __ldg(ca + v), b = __ldg(cb + v), c = __ldg(cc_ + v), d = __ldg(cd + v);
-            p0[4 * v + 0] = k1_pack(a.x, b.x); p1[4 * v + 0] = k1_pack(c.x, d.x);
-            p0[4 * v + 1] = k1_pack(a.y, b.y); p1[4 * v + 1] = k1_pack(c.y, d.y);
-            p0[4 * v + 2] = k1_pack(a.z, b.z); p1[4 * v + 2] = k1_pack(c.z, d.z);
-            p0[4 * v + 3] = k1_pack(a.w, b.w); p1[4 * v + 3] = k1_pack(c.w, d.w);
+            p0[4 * v + 0] = k1_pack_once(a.x, b.x, nzz); p1[4 * v + 0] = k1_pack_once(c.x, d.x, nzz);
+            p0[4 * v + 1] = k1_pack_once(a.y, b.y, nzz); p1[4 * v + 1] = k1_pack_once(c.y, d.y, nzz);
+            p0[4 * v + 2] = k1_pack_once(a.z, b.z, nzz); p1[4 * v + 2] = k1_pack_once(c.z, d.z, nzz);
+            p0[4 * v + 3] = k1_pack_once(a.w, b.w, nzz); p1[4 * v + 3] = k1_pack_once(c.w, d.w, nzz);
         }
         unsigned long long acc0[K1R_ITEMS], acc1[K1R_ITEMS];
 #pragma unroll

@@ -122,6 +122,11 @@ __global__ void __launch_bounds__(RS_THREADS) rescue_scan_kernel(const ScanArgs 
                &bound};
     constexpr bool USE_LUT = (STRAT == DUAL || STRAT == ADC);
     const uint64_t lo = a.n * blockIdx.x / gridDim.x, hi = a.n * (blockIdx.x + 1) / gridDim.x;
+    {  // the common case -- no query overflowed -- costs one parallel pass over the flags
+        uint32_t any = 0;
+        for (uint32_t q = threadIdx.x; q < a.nqb; q += RS_THREADS) any |= __ldcg(a.ovq + q);
+        if (!__syncthreads_or((int)any)) return;
+    }
     for (uint32_t q = 0; q < a.nqb; ++q) {
         if (!__ldcg(a.ovq + q)) continue;  // uniform across the CTA
         __syncthreads();
@@ -208,6 +213,12 @@ __global__ void __launch_bounds__(RS_THREADS) ivf_rescue_kernel(const IvfScanArg
                reinterpret_cast<unsigned long long*>(rs_smem + M * KSUB * 4) + RS_BUF, &cnt, hist, &prefix, &want,
                &bound};
     constexpr bool USE_LUT = (STRAT == DUAL || STRAT == ADC);
+    {  // the common case -- none of this CTA's queries overflowed -- costs one parallel pass over their flags
+        uint32_t any = 0;
+        for (uint64_t q = blockIdx.x + (uint64_t)threadIdx.x * gridDim.x; q < a.nq; q += (uint64_t)RS_THREADS * gridDim.x)
+            any |= __ldcg(a.ovq + q);
+        if (!__syncthreads_or((int)any)) return;
+    }
     for (uint32_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
     if (!__ldcg(a.ovq + q)) continue;  // uniform across the CTA
     __syncthreads();

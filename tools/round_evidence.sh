@@ -14,3 +14,8 @@ timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --profile
 timeout 600 python bench.py --config 0 > $O/cfg0.json 2> $O/cfg0.err; echo "cfg0 rc=$?"
 timeout 1200 python bench.py --config 3 --steps 5 > $O/cfg3.json 2> $O/cfg3.err; echo "cfg3 rc=$?"
 timeout 1500 python bench.py --config 4 --steps 10 --knn-full /tmp/knn_full.knng > $O/cfg4.json 2> $O/cfg4.err; echo "cfg4 rc=$?"
+# launch lists of the other configs; the 8-rank by-list emulation (config 2, 1e9 codes, rank 0 measured on this GPU)
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file $O/launch_cfg4.csv env BENCH_PROFILE=1 python bench.py --config 4 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $O/ncu4.log 2>&1; echo "ncu4=$?"
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file $O/launch_cfg3.csv env BENCH_PROFILE=1 python bench.py --config 3 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --per-ht "" > $O/ncu3.log 2>&1; echo "ncu3=$?"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file $O/launch_cfg0.csv env BENCH_PROFILE=1 python bench.py --config 0 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --per-ht "" > $O/ncu0.log 2>&1; echo "ncu0=$?"
+timeout 2400 python tools/emulate_bylist.py > $O/emulate_bylist_rank0of8.json 2> $O/emulate.err; echo "emulate rc=$?"; tail -1 $O/emulate_bylist_rank0of8.json | cut -c1-600
