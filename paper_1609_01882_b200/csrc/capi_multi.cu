@@ -6,10 +6,11 @@
 // each row keeping its global id (FlatIndex ids, flat_index.hpp:40).  A search
 // runs the single-device path (K1 -> K2s -> K2 -> K3) on every shard
 // concurrently, one host thread per shard, each on its own device and stream;
-// the per-shard top-k lists (ascending (score, id)) are copied
-// to the first device over peer memory (NVLink on a B200 node) and merged
-// there by K3m, an n-way merge per query in (score, id) order -- exact for
-// arbitrary int64 ids, since the shards hold disjoint rows.  This is the
+// the per-shard top-k lists (ascending (score, id)) are merged on
+// the first device by K3g, which reads them in place over peer memory (NVLink on
+// a B200 node): gather and merge in one kernel, exact for arbitrary int64 ids
+// since the shards hold disjoint rows (peer copies + K3m, an n-way merge per
+// query, when a device cannot load from a peer or k is large).  This is the
 // single-process counterpart of distributed.ShardedSearch (one rank per GPU,
 // NCCL all-gather); both merge the same lists.
 #include <algorithm>
@@ -67,11 +68,86 @@ __global__ void merge_sorted_kernel(const int64_t* __restrict__ ids, const float
     }
 }
 
+// K3g: gather + merge in one kernel.  The shards' top-k lists are read where they lie -- on the
+// shards' own devices, through peer memory (NVLink P2P loads; plain loads for a shard on this
+// device) -- so there is no copy step between the shard searches and the merge.  One warp per
+// query: coalesced loads stage the query's `parts` sorted lists in shared memory, then every
+// entry finds its rank in the union by binary searches in the other lists ((score, id) order:
+// ids are distinct across shards, so the ranks are a permutation) and the entries of rank < k
+// are written out.
+constexpr uint32_t GM_PARTS = 64, GM_WARPS = 4;
+struct GatherSrc {
+    const int64_t* ids[GM_PARTS];
+    const float* sc[GM_PARTS];
+    const uint32_t* cnt[GM_PARTS];
+};
+
+__device__ __forceinline__ bool gm_less(float s, int64_t id, float s2, int64_t id2) {
+    return s < s2 || (s == s2 && id < id2);
+}
+
+__global__ void __launch_bounds__(GM_WARPS * 32) gather_merge_kernel(const GatherSrc src, uint32_t parts, uint32_t nq,
+                                                                      uint32_t k, int64_t* __restrict__ out_ids,
+                                                                      float* __restrict__ out_sc,
+                                                                      uint32_t* __restrict__ out_cnt) {
+    extern __shared__ __align__(16) uint8_t gm_smem[];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t q = blockIdx.x * GM_WARPS + warp;
+    if (q >= nq) return;  // warps are independent: no CTA barrier below
+    const size_t per_warp = (((size_t)parts * k * 12 + 15) & ~(size_t)15) + (size_t)GM_PARTS * 4;  // as the host sizes it
+    int64_t* s_id = reinterpret_cast<int64_t*>(gm_smem + warp * per_warp);
+    float* s_sc = reinterpret_cast<float*>(s_id + (size_t)parts * k);
+    uint32_t* s_cnt = reinterpret_cast<uint32_t*>(gm_smem + warp * per_warp + (((size_t)parts * k * 12 + 15) & ~(size_t)15));
+    for (uint32_t p = lane; p < parts; p += 32) s_cnt[p] = min(src.cnt[p][q], k);
+    __syncwarp();
+    uint32_t total = 0;
+    for (uint32_t p = 0; p < parts; ++p) {
+        const uint32_t c = s_cnt[p];
+        total += c;
+        const int64_t* gi = src.ids[p] + (size_t)q * k;
+        const float* gs = src.sc[p] + (size_t)q * k;
+        for (uint32_t i = lane; i < c; i += 32) {
+            s_id[p * k + i] = gi[i];
+            s_sc[p * k + i] = gs[i];
+        }
+    }
+    __syncwarp();
+    for (uint32_t p = 0; p < parts; ++p) {
+        const uint32_t c = s_cnt[p];
+        for (uint32_t i = lane; i < c; i += 32) {
+            const float s = s_sc[p * k + i];
+            const int64_t id = s_id[p * k + i];
+            uint32_t rank = i;
+            for (uint32_t p2 = 0; p2 < parts && rank < k; ++p2) {
+                if (p2 == p) continue;
+                uint32_t lo = 0, hi = s_cnt[p2];  // entries of list p2 before (s, id)
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (gm_less(s_sc[p2 * k + mid], s_id[p2 * k + mid], s, id)) lo = mid + 1;
+                    else hi = mid;
+                }
+                rank += lo;
+            }
+            if (rank < k) {
+                out_ids[(size_t)q * k + rank] = id;
+                out_sc[(size_t)q * k + rank] = s;
+            }
+        }
+    }
+    const uint32_t w = min(total, k);
+    if (lane == 0 && out_cnt) out_cnt[q] = w;
+    for (uint32_t r = w + lane; r < k; r += 32) {
+        out_ids[(size_t)q * k + r] = -1;
+        out_sc[(size_t)q * k + r] = __int_as_float(0x7f800000);
+    }
+}
+
 }  // namespace pb
 
 struct poly_b200_sharded {
     std::vector<int> devices;
     std::vector<poly_b200_index*> shards;
+    std::vector<char> direct;  // shard g's buffers are loadable from devices[0] (same device or peer access enabled)
     uint32_t m = 0, dim = 0, cb = 0, code_bits = 0;
     uint64_t n = 0;
     // per-shard device staging (queries in, top-k out) on the shard's device
@@ -203,7 +279,8 @@ int poly_b200_sharded_create(const poly_b200_pq_desc* pq, const int* devices, ui
                 CK(cudaStreamCreateWithFlags(&h->st[g].stream, cudaStreamNonBlocking));
                 CK(cudaEventCreateWithFlags(&h->st[g].done, cudaEventDisableTiming));
             }
-            // peer access lets the gathers below go device to device over NVLink
+            // peer access lets K3g load the shards' lists from devices[0] over NVLink
+            h->direct.assign(n_devices, 1);
             for (uint32_t g = 1; g < n_devices; ++g) {
                 if (devices[g] == devices[0]) continue;
                 int can = 0;
@@ -214,6 +291,7 @@ int poly_b200_sharded_create(const poly_b200_pq_desc* pq, const int* devices, ui
                     if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
                     else CK(e);
                 }
+                h->direct[g] = (char)(can != 0);
             }
         } catch (...) {
             poly_b200_sharded_destroy(h.release());
@@ -326,19 +404,36 @@ int poly_b200_sharded_search_batch(poly_b200_sharded* h, const float* queries, u
                                                   s.stream, stats ? &sst[g] : nullptr));
             CK(cudaEventRecord(s.done, s.stream));
         });
-        // gather the P lists on devices[0] (peer copies) and merge them there
+        // merge on devices[0].  K3g reads the shards' lists in place over peer memory when every
+        // shard is loadable from devices[0] and a query's lists fit a warp's shared memory; otherwise
+        // the lists are gathered with peer copies first and merged by K3m.
         DeviceGuard dg(h->devices[0]);
         cudaStream_t s0 = h->st[0].stream;
-        for (size_t g = 0; g < P; ++g) {
-            auto& s = h->st[g];
-            CK(cudaStreamWaitEvent(s0, s.done, 0));
-            const size_t off = g * nq * k;
-            CK(cudaMemcpyPeerAsync(h->g_ids + off, h->devices[0], s.d_ids, h->devices[g], nq * k * 8, s0));
-            CK(cudaMemcpyPeerAsync(h->g_sc + off, h->devices[0], s.d_sc, h->devices[g], nq * k * 4, s0));
-            CK(cudaMemcpyPeerAsync(h->g_cnt + g * nq, h->devices[0], s.d_cnt, h->devices[g], nq * 4, s0));
+        for (size_t g = 0; g < P; ++g) CK(cudaStreamWaitEvent(s0, h->st[g].done, 0));
+        const size_t gm_warp = ((P * (size_t)k * 12 + 15) & ~(size_t)15) + (size_t)pb::GM_PARTS * 4, gm_smem = gm_warp * pb::GM_WARPS;
+        bool fused = P <= pb::GM_PARTS && gm_smem <= 200 * 1024;
+        for (size_t g = 0; g < P; ++g) fused = fused && h->direct[g];
+        if (fused) {
+            pb::GatherSrc src{};
+            for (size_t g = 0; g < P; ++g) {
+                src.ids[g] = h->st[g].d_ids;
+                src.sc[g] = h->st[g].d_sc;
+                src.cnt[g] = h->st[g].d_cnt;
+            }
+            CK(cudaFuncSetAttribute(pb::gather_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gm_smem));
+            pb::gather_merge_kernel<<<(unsigned)((nq + pb::GM_WARPS - 1) / pb::GM_WARPS), pb::GM_WARPS * 32, gm_smem, s0>>>(
+                src, (uint32_t)P, (uint32_t)nq, k, h->o_ids, h->o_sc, h->o_cnt);
+        } else {
+            for (size_t g = 0; g < P; ++g) {
+                auto& s = h->st[g];
+                const size_t off = g * nq * k;
+                CK(cudaMemcpyPeerAsync(h->g_ids + off, h->devices[0], s.d_ids, h->devices[g], nq * k * 8, s0));
+                CK(cudaMemcpyPeerAsync(h->g_sc + off, h->devices[0], s.d_sc, h->devices[g], nq * k * 4, s0));
+                CK(cudaMemcpyPeerAsync(h->g_cnt + g * nq, h->devices[0], s.d_cnt, h->devices[g], nq * 4, s0));
+            }
+            pb::merge_sorted_kernel<<<(unsigned)((nq + 127) / 128), 128, 0, s0>>>(
+                h->g_ids, h->g_sc, h->g_cnt, (uint32_t)P, (uint32_t)nq, k, h->o_ids, h->o_sc, h->o_cnt);
         }
-        pb::merge_sorted_kernel<<<(unsigned)((nq + 127) / 128), 128, 0, s0>>>(
-            h->g_ids, h->g_sc, h->g_cnt, (uint32_t)P, (uint32_t)nq, k, h->o_ids, h->o_sc, h->o_cnt);
         pb::count_launch();
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(out_ids, h->o_ids, nq * k * 8, cudaMemcpyDeviceToHost, s0));
