@@ -328,8 +328,9 @@ int poly_b200_ivf_knn_graph_device(poly_b200_ivf* ivf, const float* d_x, uint64_
  * add / add_codes (flat_index.hpp:115-119) split every call's rows into n_devices
  * contiguous parts, part g to shard g, each row keeping its global id (NULL ids =
  * size() + i).  search_batch (flat_index.hpp:124-126) runs every shard concurrently
- * on its own device, copies the per-shard top-k lists to devices[0] over peer memory
- * and merges them there in (score, id) order: the result equals the single-index
+ * on its own device and merges the per-shard top-k lists on devices[0] in (score, id)
+ * order, reading them in place over peer memory (one gather + merge kernel; peer copies
+ * first when a device cannot load from a peer): the result equals the single-index
  * search over the union of the shards.  Statistics are summed over the shards. */
 typedef struct poly_b200_sharded poly_b200_sharded;
 int poly_b200_sharded_create(const poly_b200_pq_desc* pq, const int* devices, uint32_t n_devices,
