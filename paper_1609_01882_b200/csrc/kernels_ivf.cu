@@ -116,7 +116,7 @@ __device__ __forceinline__ unsigned long long k1_pack_once(float lo, float hi, u
 // so each shared-memory load of a residual pair feeds 12 packed FP ops instead of 6
 // (the pair kernel's shared-memory pipe was 93% busy).
 #ifndef POLY_K1R_MINB
-#define POLY_K1R_MINB 4
+#define POLY_K1R_MINB 5  // 94 registers, 5 CTAs per SM (A/B on config 4: 4 -> 686, 5 -> 659, 6 -> 702 us)
 #endif
 __global__ void __launch_bounds__(128, POLY_K1R_MINB) residual_lut_quad_kernel(const float* __restrict__ queries, uint32_t dim,
                                                                    uint32_t m,
