@@ -90,6 +90,7 @@ void launch_coarse_keys(const float* q, uint32_t nq, uint32_t dim, const float* 
 #define POLY_K1R_ITEMS 8
 #endif
 constexpr uint32_t K1R_ITEMS = POLY_K1R_ITEMS;
+static_assert(K1R_ITEMS * 16 <= 128, "K1r writes the items' query codes with one thread per (item, sub-quantizer)");
 
 // K1r, centroid pairs: thread t owns centroids t and t + 128 as one packed f32x2
 // lane pair, so each (item, dim) term is FADD2 (r - c), FFMA2 (t * t + z, z a
