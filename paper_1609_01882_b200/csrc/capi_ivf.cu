@@ -265,9 +265,13 @@ void ensure_ivf_scratch(poly_b200_ivf* iv, uint32_t nprobe, uint32_t k) {
             iv->items_cap[r] = need[r];
             iv->items[r] = dalloc<uint4>(need[r]);
         }
-    // round 1 runs without a bound: its <= r1 probes' survivors must fit (round 2 is bounded
-    // by round 1's k-th key; a list that still fills up is re-ranked by the rescue scan)
-    uint32_t cap = (uint32_t)std::max<uint64_t>(131072, r1 * iv->max_list + k);
+    // Round 2 is bounded by round 1's k-th key.  Round 1 is bounded by the K6s seed when it runs
+    // (k <= IVF_SEED_ROWS / 4): 131,072 keys then hold its candidates with a wide margin.  Without the
+    // seed round 1 has no bound and its <= r1 probes' survivors must fit.  A list that still fills up
+    // (a query whose seed found fewer than k keys and whose next list is huge) is re-ranked by the
+    // exact rescue scan.
+    const bool seeded = IVF_SEED_ROWS && k <= IVF_SEED_ROWS / 4;
+    uint32_t cap = (uint32_t)std::max<uint64_t>(131072, seeded ? 4ull * k : r1 * iv->max_list + k);
     if (iv->cap_override) cap = std::max<uint32_t>(iv->cap_override, k);
     if (iv->cand_cap != cap) {
         dfree(iv->cand);
