@@ -930,6 +930,35 @@ def run_knn(args, rank, world, local):
     ms = e0.elapsed_time(e1)
     k6_ms, _ = ivf.profile_read()
     ivf.profile_enable(False)
+    # ---- e2e (N = 1): every step's rows come in from pinned host memory and its neighbours,
+    # scores and counts go back out, around the same public call
+    e2e = None
+    if not args.no_e2e and world == 1:
+        h_rows = torch.empty((nrows, c["dim"]), dtype=torch.float32).pin_memory()
+        h_rows.copy_(dx)
+        d_in = torch.empty((B, c["dim"]), dtype=torch.float32, device="cuda")
+        h_ids = torch.empty((B, k), dtype=torch.int64).pin_memory()
+        h_sc = torch.empty((B, k), dtype=torch.float32).pin_memory()
+        h_cnt = torch.empty(B, dtype=torch.int32).pin_memory()
+
+        def e2e_step(i):
+            d_in.copy_(h_rows[i * B:(i + 1) * B], non_blocking=True)
+            ivf.knn_graph_device(d_in, row0 + i * B, p, o_ids, o_sc, o_cnt, stream.cuda_stream)
+            h_ids.copy_(o_ids, non_blocking=True)
+            h_sc.copy_(o_sc, non_blocking=True)
+            h_cnt.copy_(o_cnt, non_blocking=True)
+            stream.synchronize()
+
+        for i in range(args.warmup):
+            e2e_step(i)
+        t = time.perf_counter()
+        for i in range(args.warmup, args.warmup + steps):
+            e2e_step(i)
+        e2e_ms = (time.perf_counter() - t) * 1e3
+        e2e = {"value": scanned / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": B * c["dim"] * 4,
+               "d2h_bytes_per_step": B * k * 12 + B * 4, "ms_per_step": e2e_ms / steps,
+               "via": "poly_b200_ivf_knn_graph_device; the step's rows copied in from pinned host memory and its "
+                      "ids / scores / counts copied out, synchronised every step"}
     if rank != 0:
         return
     pk, _ = peaks()
@@ -947,7 +976,7 @@ def run_knn(args, rank, world, local):
                        "ht": args.ht, "queries_per_step": B,
                        "l2": "160 MB of list codes stream through L2 per step; no flush"},
             "scanned_per_query": scanned / (steps * B), "survivor_frac": surv / max(scanned, 1),
-            "graph_time_est_s": rows / B * ms / steps / 1e3, "gpu_launches": launches, "clocks": clk,
+            "graph_time_est_s": rows / B * ms / steps / 1e3, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             "roofline": dict(k6, kernel="K6 ivf_list_scan_kernel (both rounds)", kernel_share_of_step=k6_ms / ms),
             "roofline_step": stp, "roofline_hbm": hbm, "setup_s": round(setup_s, 1)}
     if args.knn_full:
