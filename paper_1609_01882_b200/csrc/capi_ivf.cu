@@ -133,9 +133,9 @@ constexpr uint64_t IVF_R1_CODES = POLY_IVF_R1_CODES;  // ... and at least this m
 #define POLY_IVF_CHUNK2 4096
 #endif
 #ifndef POLY_IVF_CHUNK
-#define POLY_IVF_CHUNK 1024
+#define POLY_IVF_CHUNK 4096
 #endif
-constexpr uint32_t IVF_CHUNK = POLY_IVF_CHUNK;    // K6 round-1 work item: 1024 list rows (K6 scans it in 128-row warp blocks)
+constexpr uint32_t IVF_CHUNK = POLY_IVF_CHUNK;    // K6 round-1 work item: rows of a list (A/B with the unit pipeline: 512 / 1024 / 2048 / 4096 / 8192 rows -> 924 / 760 / 676 / 665 / 695 us)
 constexpr uint32_t IVF_CHUNK2 = POLY_IVF_CHUNK2;  // round 2: longer items (fewer LUT loads per code)
 #ifndef POLY_IVF_SEED_ROWS  // K6s sample: rows of each query's first list (0 = no round-1 seed)
 #define POLY_IVF_SEED_ROWS 2048
@@ -415,7 +415,7 @@ void search_batch(poly_b200_ivf* iv, const float* d_q, uint32_t nqb, const poly_
     a.hash_q = perq && p->strategy == pb::DUAL ? iv->hash_q : nullptr;
     // two rounds over the work lists built by the probe-count kernel: round 1 scans each
     // query's leading probes holding >= IVF_R1_CODES codes (at most IVF_R1_MAX probes) in
-    // 1024-row chunks; its exact k-th key (K3) bounds round 2, the remaining probes
+    // IVF_CHUNK-row chunks; its exact k-th key (K3) bounds round 2, the remaining probes
     const uint32_t rounds = np <= 1 ? 1 : 2;  // one probe: round 1 sees everything
     // K6s: round 1's own bound from a sample of each query's first list (k <= sample)
     if (phase != 2 && IVF_SEED_ROWS && k <= IVF_SEED_ROWS / 4)
